@@ -1,0 +1,214 @@
+"""ORACLE -- test infrastructure only.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (its
+``cpu_baseline`` leg and ``--impl reference``) may import this module.  The
+product path (``paper_2111_06868_b200``) never imports it and shares no code
+with it; the only common dependency is the input generator package
+``hq_inputs`` (which holds no method arithmetic).
+
+Contents, each following the passage cited:
+
+* ``apply_gate`` / ``simulate`` -- the plain fp64 gate-by-gate apply of
+  ``sv_oracle.c``.
+* ``norm`` -- ||psi||_2 (reading C13).
+* ``embed_dense`` -- the 2^n x 2^n matrix of one gate written out from its
+  definition M[i][i'] = U[r(i)][r(i')] if i, i' agree off the target bits,
+  else 0 (brute-force pin P7, n <= 10).
+* ``kron_embed_adjacent`` -- textbook kron(I, U, I) for ascending adjacent
+  qubits (independent check of ``embed_dense``).
+* ``circuit_matrix`` -- product of embedded gate matrices in application
+  order.
+* ``tensordot_apply`` -- the paper's own einsum engine idea (P:644-648,
+  pin P8): numpy.tensordot on a (2,)*n array, axis j = qubit j.
+* ``compress`` / ``fused_gates`` -- the greedy fusion rule, reading C7 of
+  PAPER P:499-504 (worked example P:510-529), and the fused matrix
+  U_group = U_last ... U_first embedded on the ascending support (P:493-494,
+  readings C8, C9).
+
+Parity pins for every function live in ``tests/test_oracle_pins.py``.
+"""
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "sv_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+
+def build_oracle(force=False):
+    """Compile sv_oracle.c (plain C, OpenMP, no FMA contraction)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-ffp-contract=off",
+                               "-fno-fast-math", "-shared", "-fPIC", "-o", _LIB, _SRC])
+    return _LIB
+
+
+def _get():
+    global _lib
+    if _lib is None:
+        build_oracle()
+        lib = ctypes.CDLL(_LIB)
+        lib.oracle_apply.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
+                                     ctypes.c_void_p, ctypes.c_int]
+        lib.oracle_apply.restype = ctypes.c_int
+        lib.oracle_norm.argtypes = [ctypes.c_void_p, ctypes.c_int]
+        lib.oracle_norm.restype = ctypes.c_double
+        lib.oracle_init_basis.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_uint64]
+        lib.oracle_init_basis.restype = None
+        lib.oracle_set_threads.argtypes = [ctypes.c_int]
+        lib.oracle_max_threads.restype = ctypes.c_int
+        _lib = lib
+    return _lib
+
+
+def set_threads(t):
+    _get().oracle_set_threads(int(t))
+
+
+def max_threads():
+    return int(_get().oracle_max_threads())
+
+
+class OracleError(RuntimeError):
+    pass
+
+
+def _nqubits(psi):
+    N = psi.shape[0]
+    n = N.bit_length() - 1
+    if 1 << n != N:
+        raise OracleError("length is not a power of two")
+    return n
+
+
+def apply_gate(psi, U, qubits):
+    """In place: psi <- (U embedded on qubits) psi.  psi is complex128 1-D."""
+    assert psi.dtype == np.complex128 and psi.flags.c_contiguous
+    n = _nqubits(psi)
+    U = np.ascontiguousarray(U, dtype=np.complex128)
+    k = len(qubits)
+    if U.shape != (2 ** k, 2 ** k):
+        raise OracleError("matrix shape does not match arity")
+    q = np.ascontiguousarray(qubits, dtype=np.int32)
+    rc = _get().oracle_apply(psi.ctypes.data, n, U.ctypes.data, q.ctypes.data, k)
+    if rc != 0:
+        raise OracleError("oracle_apply failed with code %d" % rc)
+    return psi
+
+
+def init_basis(n, x=0):
+    psi = np.empty(2 ** n, dtype=np.complex128)
+    _get().oracle_init_basis(psi.ctypes.data, n, int(x))
+    return psi
+
+
+def simulate(n, gates, psi0=None, x=0):
+    """Apply ``gates`` (leftmost first) to psi0 (copied) or |x>."""
+    psi = init_basis(n, x) if psi0 is None else np.array(psi0, dtype=np.complex128, copy=True)
+    for g in gates:
+        apply_gate(psi, g.U if hasattr(g, "U") else g[1], g.qubits if hasattr(g, "qubits") else g[0])
+    return psi
+
+
+def norm(psi):
+    psi = np.ascontiguousarray(psi, dtype=np.complex128)
+    return float(_get().oracle_norm(psi.ctypes.data, _nqubits(psi)))
+
+
+# ---------------------------------------------------------------- brute force
+
+def embed_dense(n, U, qubits):
+    """M[i][i'] = U[r(i)][r(i')] when i and i' agree off the target bits,
+    else 0; r(i) = sum_j bit_(n-1-q_j)(i) 2^(k-1-j)."""
+    k = len(qubits)
+    idx = np.arange(2 ** n, dtype=np.int64)
+    r = np.zeros_like(idx)
+    mask = 0
+    for j, q in enumerate(qubits):
+        b = n - 1 - q
+        r |= ((idx >> b) & 1) << (k - 1 - j)
+        mask |= 1 << b
+    rest = idx & ~mask
+    same = rest[:, None] == rest[None, :]
+    return np.where(same, np.asarray(U)[r[:, None], r[None, :]], 0).astype(np.complex128)
+
+
+def kron_embed_adjacent(n, U, q0):
+    """Textbook kron(I_{2^q0}, U, I_{2^(n-q0-k)}) for qubits q0..q0+k-1 in
+    ascending order, qubit 0 being the leftmost Kronecker factor (C1)."""
+    k = int(np.log2(np.asarray(U).shape[0]))
+    return np.kron(np.kron(np.eye(2 ** q0), U), np.eye(2 ** (n - q0 - k)))
+
+
+def circuit_matrix(n, gates):
+    """Product of embedded gate matrices in application order."""
+    M = np.eye(2 ** n, dtype=np.complex128)
+    for g in gates:
+        M = embed_dense(n, g.U, g.qubits) @ M
+    return M
+
+
+def tensordot_apply(psi, U, qubits):
+    """numpy.tensordot engine (pin P8): psi as (2,)*n with axis j
+    = qubit j; U as (2,)*2k with output axes first."""
+    n = _nqubits(psi)
+    k = len(qubits)
+    T = np.asarray(psi).reshape((2,) * n)
+    Ut = np.asarray(U).reshape((2,) * (2 * k))
+    out = np.tensordot(Ut, T, axes=(list(range(k, 2 * k)), list(qubits)))
+    out = np.moveaxis(out, list(range(k)), list(qubits))
+    return np.ascontiguousarray(out).reshape(-1)
+
+
+# ---------------------------------------------------------------- compress
+
+def compress(gates, kmax):
+    """Greedy fusion into groups of support <= kmax (rule C7):
+    gate g joins the earliest-created group G with |supp(G) u supp(g)| <= kmax
+    such that no non-member gate between G's first member and g touches a
+    qubit of g; otherwise it opens a new group.  Groups are returned in
+    first-member order as lists of gate indices."""
+    for g in gates:
+        if len(g.qubits) > kmax:
+            raise OracleError("GateTooWide")
+    groups = []           # each: dict(first, members(list), support(set), mset)
+    for i, g in enumerate(gates):
+        qs = set(g.qubits)
+        placed = False
+        for G in groups:
+            if len(G["support"] | qs) > kmax:
+                continue
+            blocked = False
+            for j in range(G["first"] + 1, i):
+                if j not in G["mset"] and qs & set(gates[j].qubits):
+                    blocked = True
+                    break
+            if blocked:
+                continue
+            G["members"].append(i)
+            G["mset"].add(i)
+            G["support"] |= qs
+            placed = True
+            break
+        if not placed:
+            groups.append({"first": i, "members": [i], "mset": {i}, "support": set(qs)})
+    return [G["members"] for G in groups]
+
+
+def fused_gates(gates, kmax):
+    """Fused gate list: (ascending support, U_last ... U_first embedded on it)
+    (P:493-494 to_matrix_gate; readings C8, C9)."""
+    out = []
+    for members in compress(gates, kmax):
+        support = sorted(set().union(*[set(gates[i].qubits) for i in members]))
+        pos = {q: j for j, q in enumerate(support)}
+        m = len(support)
+        M = np.eye(2 ** m, dtype=np.complex128)
+        for i in members:
+            M = embed_dense(m, gates[i].U, [pos[q] for q in gates[i].qubits]) @ M
+        out.append((tuple(support), M))
+    return out

@@ -1,0 +1,310 @@
+"""Pins of the CPU oracle against things other than itself (SURVEY §8(c) pins).
+
+Each test names the pin and the passage it follows.  None of them imports the
+product path.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+from hq_inputs import (SQRT_X, SQRT_Y, SQRT_W, H, X, Y, CX, SWAP, CCX, fsim,
+                       cphase, cr_m, Gate, sycamore_circuit, random_circuit,
+                       haar_unitary, random_state, integer_state,
+                       permutation_matrix)
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _golden(name):
+    rows = []
+    with open(os.path.join(GOLDEN, name)) as f:
+        for line in f:
+            line = line.strip()
+            if line and not line.startswith("#"):
+                rows.append(line.split())
+    return rows
+
+
+# ---------------------------------------------------------------- P1 (C1)
+def test_P1_grover_listing_pins_bit_order():
+    """Grover gate on qubits [1,2] of the uniform 3-qubit
+    state.  The oracle psi -= 2 P_0 psi on qubits (1,2) is U = diag(-1,1,1,1)."""
+    psi = np.ones(8, dtype=np.complex128) / np.sqrt(8)
+    O.apply_gate(psi, np.diag([-1, 1, 1, 1]).astype(np.complex128), [1, 2])
+    for bits, val in _golden("grover_P403-422.txt"):
+        i = int(bits, 2)
+        assert abs(psi[i].imag) < 1e-15
+        assert abs(psi[i].real - float(val)) < 1e-6, bits
+
+
+# ---------------------------------------------------------------- P2 (C7/C8)
+def test_P2_compress_worked_example():
+    """CPHASE on all pairs of 5 qubits, max_n_qubits=3."""
+    gates = [Gate("CPHASE", (q1, q2), cphase(1.0)) for q1 in range(5) for q2 in range(q1 + 1, 5)]
+    fused = O.fused_gates(gates, 3)
+    want = [tuple(int(x) for x in row) for row in _golden("compress_P510-529.txt")]
+    assert [f[0] for f in fused] == want
+    # and the fused circuit reproduces the original (C9)
+    psi0 = random_state(5, 7)
+    a = O.simulate(5, gates, psi0)
+    b = O.simulate(5, [Gate("F", q, U) for q, U in fused], psi0)
+    assert np.linalg.norm(a - b) < 1e-13
+
+
+def test_C7_lenient_rule_counterexample_is_avoided():
+    """[(0,1),(2,3),(0,1),(1,2)] with k_max=3.  The strict
+    rule must keep the replay exact."""
+    rng = np.random.default_rng(3)
+    gates = [Gate("U", q, haar_unitary(2, rng)) for q in [(0, 1), (2, 3), (0, 1), (1, 2)]]
+    psi0 = random_state(4, 1)
+    a = O.simulate(4, gates, psi0)
+    fused = O.fused_gates(gates, 3)
+    b = O.simulate(4, [Gate("F", q, U) for q, U in fused], psi0)
+    assert np.linalg.norm(a - b) < 1e-13
+    for grp in O.compress(gates, 3):
+        assert grp == sorted(grp)
+
+
+@pytest.mark.parametrize("kmax", [2, 3, 4, 5, 6])
+def test_fusion_preserves_state(kmax):
+    """Fusion is associativity: fused == unfused to 1e-12."""
+    n = 12
+    gates = sycamore_circuit(n, 10, seed=0)
+    psi0 = random_state(n, 11)
+    a = O.simulate(n, gates, psi0)
+    fused = O.fused_gates(gates, kmax)
+    assert all(len(q) <= kmax for q, _ in fused)
+    b = O.simulate(n, [Gate("F", q, U) for q, U in fused], psi0)
+    assert np.linalg.norm(a - b) < 1e-12
+
+
+def test_fusion_random_circuits():
+    for seed in range(4):
+        gates = random_circuit(7, 40, seed, kmax=3)
+        psi0 = random_state(7, seed)
+        a = O.simulate(7, gates, psi0)
+        for kmax in (3, 4, 5):
+            fused = O.fused_gates(gates, kmax)
+            b = O.simulate(7, [Gate("F", q, U) for q, U in fused], psi0)
+            assert np.linalg.norm(a - b) < 1e-12
+
+
+# ---------------------------------------------------------------- P3-P5 closed forms
+@pytest.mark.parametrize("n", list(range(1, 13)))
+def test_P3_hadamard_uniform(n):
+    psi = O.simulate(n, [Gate("H", (q,), H) for q in range(n)])
+    assert np.allclose(psi, 2 ** (-n / 2), atol=1e-14, rtol=0)
+
+
+@pytest.mark.parametrize("n", [2, 5, 9])
+def test_P4_ghz(n):
+    gates = [Gate("H", (0,), H)] + [Gate("CX", (j, j + 1), CX) for j in range(n - 1)]
+    psi = O.simulate(n, gates)
+    nz = np.flatnonzero(np.abs(psi) > 1e-14)
+    assert list(nz) == [0, 2 ** n - 1]
+    assert np.allclose(psi[nz], 1 / np.sqrt(2), atol=1e-15)
+
+
+def _qft_gates(n):
+    gates = []
+    for j in range(n):
+        gates.append(Gate("H", (j,), H))
+        for l in range(j + 1, n):
+            gates.append(Gate("CR", (l, j), cr_m(l - j + 1)))
+    for j in range(n // 2):
+        gates.append(Gate("SWAP", (j, n - 1 - j), SWAP))
+    return gates
+
+
+@pytest.mark.parametrize("x", [0, 1, 6, 19, 31])
+def test_P5_qft_phases(x):
+    """QFT|x> = 2^(-n/2) sum_y e^{2 pi i x y / 2^n} |y> (closed form)."""
+    n = 5
+    psi = O.simulate(n, _qft_gates(n), x=x)
+    y = np.arange(2 ** n)
+    want = np.exp(2j * np.pi * x * y / 2 ** n) / 2 ** (n / 2)
+    assert np.max(np.abs(psi - want)) < 1e-14
+
+
+# ---------------------------------------------------------------- P6 invariants
+def test_P6_norm_preserved():
+    n = 12
+    gates = random_circuit(n, 200, seed=5, kmax=3)
+    psi = O.simulate(n, gates)
+    assert abs(O.norm(psi) - 1.0) < 1e-10
+
+
+def test_norm_closed_form():
+    psi = np.zeros(4, dtype=np.complex128)
+    psi[1] = 3.0
+    psi[2] = 4.0j
+    assert O.norm(psi) == 5.0
+    v = random_state(10, 3, normalize=False)
+    assert abs(O.norm(v) - np.linalg.norm(v)) < 1e-12 * np.linalg.norm(v)
+
+
+def test_P12_identity_and_linearity():
+    n = 6
+    a = random_state(n, 1)
+    b = O.simulate(n, [Gate("I", (1, 4, 2), np.eye(8, dtype=np.complex128))], a)
+    assert np.array_equal(a, b)
+    U = haar_unitary(3, np.random.default_rng(0))
+    p1, p2 = random_state(n, 2), random_state(n, 3)
+    al, be = 0.3 - 0.2j, -1.1 + 0.5j
+    lhs = O.simulate(n, [Gate("U", (5, 0, 3), U)], al * p1 + be * p2)
+    rhs = al * O.simulate(n, [Gate("U", (5, 0, 3), U)], p1) + be * O.simulate(n, [Gate("U", (5, 0, 3), U)], p2)
+    assert np.max(np.abs(lhs - rhs)) < 1e-12
+
+
+# ---------------------------------------------------------------- P7 brute force
+def test_embed_dense_matches_textbook_kron():
+    rng = np.random.default_rng(0)
+    for n in (3, 5, 7):
+        for k in (1, 2, 3):
+            for q0 in range(0, n - k + 1):
+                U = haar_unitary(k, rng)
+                A = O.embed_dense(n, U, list(range(q0, q0 + k)))
+                B = O.kron_embed_adjacent(n, U, q0)
+                assert np.array_equal(A, B)
+
+
+def test_circuit_matrix_cx_triple_is_swap():
+    """[CX(0,1), CX(1,0), CX(0,1)] -> SWAP."""
+    g = [Gate("CX", (0, 1), CX), Gate("CX", (1, 0), CX), Gate("CX", (0, 1), CX)]
+    assert np.array_equal(O.circuit_matrix(2, g), SWAP)
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5, 6])
+def test_P7_oracle_vs_dense(k):
+    rng = np.random.default_rng(100 + k)
+    n = 8
+    for trial in range(3):
+        U = haar_unitary(k, rng)
+        qs = [int(q) for q in rng.choice(n, size=k, replace=False)]
+        psi = random_state(n, trial)
+        want = O.embed_dense(n, U, qs) @ psi
+        got = O.apply_gate(psi.copy(), U, qs)
+        assert np.max(np.abs(got - want)) < 1e-14
+
+
+def test_P7_circuit_vs_dense_matrix():
+    """6-qubit 50-gate circuit vs circuit_matrix (1e-8; we use 1e-12)."""
+    n = 6
+    gates = random_circuit(n, 50, seed=9, kmax=3)
+    psi0 = random_state(n, 4)
+    assert np.max(np.abs(O.simulate(n, gates, psi0) - O.circuit_matrix(n, gates) @ psi0)) < 1e-12
+
+
+# ---------------------------------------------------------------- P8 tensordot
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5, 6])
+def test_P8_tensordot(k):
+    rng = np.random.default_rng(7 + k)
+    n = 14
+    U = haar_unitary(k, rng)
+    qs = [int(q) for q in rng.choice(n, size=k, replace=False)]
+    psi = random_state(n, k)
+    want = O.tensordot_apply(psi, U, qs)
+    got = O.apply_gate(psi.copy(), U, qs)
+    assert np.max(np.abs(got - want)) < 1e-14
+
+
+# ---------------------------------------------------------------- C2 / C3
+def test_C2_matrix_acts_on_column_vectors():
+    """sqrt(Y)|0> = |+>; the transpose would give |->."""
+    psi = O.simulate(1, [Gate("SY", (0,), SQRT_Y)])
+    assert np.allclose(psi, [1 / np.sqrt(2), 1 / np.sqrt(2)], atol=1e-16)
+
+
+def test_C2_kron_order_on_targets():
+    """kron(A, B) on (a, b) == A on a then B on b (qubits[0] = MSB of U)."""
+    rng = np.random.default_rng(1)
+    A, B = haar_unitary(1, rng), haar_unitary(1, rng)
+    n = 4
+    psi = random_state(n, 5)
+    lhs = O.simulate(n, [Gate("AB", (2, 0), np.kron(A, B))], psi)
+    rhs = O.simulate(n, [Gate("A", (2,), A), Gate("B", (0,), B)], psi)
+    assert np.max(np.abs(lhs - rhs)) < 1e-15
+
+
+def test_C3_target_order_matters():
+    rng = np.random.default_rng(2)
+    U = haar_unitary(2, rng)
+    psi = random_state(5, 6)
+    a = O.simulate(5, [Gate("U", (1, 3), U)], psi)
+    b = O.simulate(5, [Gate("U", (3, 1), SWAP @ U @ SWAP)], psi)
+    c = O.simulate(5, [Gate("U", (3, 1), U)], psi)
+    assert np.max(np.abs(a - b)) < 1e-15
+    assert np.max(np.abs(a - c)) > 1e-3
+
+
+def test_C11_permutation_on_integer_state_is_exact():
+    """Reversible gates map |x> to |f(x)> computed by host bit operations."""
+    n = 6
+    psi = integer_state(n, 0)
+    perm = [3, 0, 7, 1, 6, 2, 5, 4]
+    qs = (4, 0, 2)
+    got = O.apply_gate(psi.copy(), permutation_matrix(perm), qs)
+    want = np.empty_like(psi)
+    for i in range(2 ** n):
+        c = 0
+        for j, q in enumerate(qs):
+            c |= ((i >> (n - 1 - q)) & 1) << (2 - j)
+        r = perm[c]
+        o = i
+        for j, q in enumerate(qs):
+            b = n - 1 - q
+            o = (o & ~(1 << b)) | (((r >> (2 - j)) & 1) << b)
+        want[o] = psi[i]
+    assert np.array_equal(got, want)
+
+
+def test_P15_determinism_across_threads():
+    n = 16
+    gates = random_circuit(n, 30, seed=1, kmax=4)
+    psi0 = random_state(n, 0)
+    O.set_threads(1)
+    a = O.simulate(n, gates, psi0)
+    na = O.norm(a)
+    O.set_threads(4)
+    b = O.simulate(n, gates, psi0)
+    nb = O.norm(b)
+    O.set_threads(os.cpu_count() or 1)
+    assert np.array_equal(a, b) and na == nb
+
+
+def test_oracle_rejects_bad_gates():
+    psi = O.init_basis(3)
+    with pytest.raises(O.OracleError):
+        O.apply_gate(psi, np.eye(4), [0, 0])
+    with pytest.raises(O.OracleError):
+        O.apply_gate(psi, np.eye(2), [3])
+    with pytest.raises(O.OracleError):
+        O.apply_gate(psi, np.eye(4), [0])
+
+
+# ---------------------------------------------------------------- inputs (C15, C16, C18)
+def test_C15_gate_definitions():
+    for U in (SQRT_X, SQRT_Y, SQRT_W, fsim()):
+        assert np.allclose(U @ U.conj().T, np.eye(U.shape[0]), atol=1e-15)
+    assert np.allclose(SQRT_X @ SQRT_X, -1j * X, atol=1e-15)
+    W = (X + Y) / np.sqrt(2)
+    ev, V = np.linalg.eigh(W)
+    expw = V @ np.diag(np.exp(-1j * np.pi / 4 * ev)) @ V.conj().T
+    assert np.allclose(SQRT_W, expw, atol=1e-15)
+    assert np.allclose(CCX @ CCX, np.eye(8))
+
+
+@pytest.mark.parametrize("n,cycles,count", [(12, 10, 163), (30, 20, 845), (34, 20, 960), (36, 24, 1224)])
+def test_C16_generator_gate_counts(n, cycles, count):
+    gates = sycamore_circuit(n, cycles, seed=0)
+    assert len(gates) == count
+    assert sum(len(g.qubits) == 1 for g in gates) == n * cycles
+
+
+def test_C18_haar_unitary():
+    rng = np.random.default_rng(0)
+    for k in range(1, 7):
+        U = haar_unitary(k, rng)
+        assert np.max(np.abs(U @ U.conj().T - np.eye(2 ** k))) < 1e-14
