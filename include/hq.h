@@ -1,0 +1,246 @@
+/*
+ * hq.h -- C ABI of the B200-native HybridQ state-vector core.
+ *
+ * What it computes (the one hot path of HybridQ, arXiv 2111.06868):
+ *   apply a dense, possibly fused, k-qubit gate matrix U (2^k x 2^k complex,
+ *   1 <= k <= 6) to a 2^n complex amplitude vector on an arbitrary ordered
+ *   set of target qubits -- the "matrix-vector multiplication of quantum
+ *   states ... similar syntax of numpy.dot" of PAPER.md P:87-91, implemented
+ *   there as the C++/AVX core of P:641-656 (SPEC.md S:238-246 apply_matrix,
+ *   S:274-282 simulate_statevector).  Gates are fused on the host by the
+ *   greedy planner of P:499-504 (utils.compress) before they reach the GPU.
+ *
+ * Conventions:
+ *   - Amplitude index: qubit q is bit n-1-q (qubit 0 = most significant bit).
+ *     Reading C1, pinned by the Grover listing P:403-422.
+ *   - Matrices: 2*4^k doubles, interleaved (re, im), row-major; qubits[0] is
+ *     the most significant bit of U's row/column index; psi' = U psi.
+ *     Reading C2.  Target order matters (C3).  U need not be
+ *     unitary (C4): no renormalisation happens inside apply.
+ *   - Host amplitude buffers: interleaved complex in the state dtype
+ *     (HQ_C64: 2 x float32, HQ_C128: 2 x float64), LOGICAL order (C14)
+ *     whatever permutation the library uses internally.
+ *
+ * Ownership and threading:
+ *   - The library owns all device memory it allocates, its streams and its
+ *     NCCL communicators.  hq_state_create_from_buffers() borrows caller
+ *     memory (e.g. torch tensors) that must outlive the state.
+ *   - Every pointer argument is borrowed for the duration of the call only;
+ *     matrices are copied (and rounded once, fp64 -> dtype, round-to-nearest)
+ *     before the call returns.
+ *   - Mutating calls are asynchronous and stream-ordered on the state's
+ *     stream(s); hq_norm, hq_get_amplitudes, hq_sync synchronise.
+ *   - A state is exclusively owned during mutation and is not thread-safe
+ *     (SPEC S:295).
+ *
+ * Errors: every call returns hq_status; HQ_OK == 0.  No exception crosses the
+ * ABI.  Arguments are validated before any device work is enqueued, so on an
+ * argument error the state is unchanged.  hq_last_error() returns a
+ * thread-local human-readable message for the last failing call.
+ */
+#ifndef HQ_H
+#define HQ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum hq_status {
+    HQ_OK = 0,
+    HQ_ERR_ARG = 1,         /* NULL pointer, bad n / dtype / count / kmax        */
+    HQ_ERR_NGPUS = 2,       /* ngpus not a power of two, too many, n - log2 G < 6 */
+    HQ_ERR_OOM = 3,         /* device or pinned host allocation failed           */
+    HQ_ERR_CUDA = 4,        /* a CUDA runtime call failed (message in last_error) */
+    HQ_ERR_NCCL = 5,        /* an NCCL call failed                               */
+    HQ_ERR_QUBIT = 6,       /* target qubit not in [0, n)          */
+    HQ_ERR_DUP_QUBIT = 7,   /* repeated target qubit  ("distinct")    */
+    HQ_ERR_K = 8,           /* k < 1, k > 6, k > local qubits, or k > kmax       */
+    HQ_ERR_RANGE = 9,       /* basis index / amplitude range outside 2^n         */
+    HQ_ERR_STATE = 10,      /* operation not valid for this state (e.g. mode)    */
+    HQ_ERR_NO_DEVICE = 11   /* no CUDA device: the library has no CPU fallback   */
+} hq_status;
+
+typedef enum hq_dtype {
+    HQ_C64 = 0,   /* complex64: FP32 storage; FP32 FMA (k<=4), 3xTF32 tcgen05 (k=5,6) */
+    HQ_C128 = 1   /* complex128: FP64 storage and FP64 FMA                            */
+} hq_dtype;
+
+/* Opaque state: the 2^n amplitudes, sharded over G = 2^m ranks on the top m
+ * physical bits, plus the logical->physical qubit map pi. */
+typedef struct hq_state hq_state;
+
+/* A (possibly fused) gate: k targets, qubits[0..k-1] valid, U = 2*4^k doubles
+ * (interleaved, row-major).  U is borrowed for the duration of the call. */
+typedef struct hq_gate {
+    int32_t k;
+    int32_t qubits[6];
+    const double *U;
+} hq_gate;
+
+/* A circuit uploaded once to the device(s) and replayable (compile once, run
+ * many): scheduled op stream + device-resident matrices. */
+typedef struct hq_circuit hq_circuit;
+
+typedef struct hq_stats {
+    uint64_t passes;          /* apply kernels launched (all shards)              */
+    uint64_t remaps;          /* global<->local qubit swaps (all-to-all exchanges) */
+    uint64_t permutes;        /* local bit-permutation passes                      */
+    uint64_t kernel_launches; /* all library kernels launched on this rank         */
+    uint64_t hbm_bytes;       /* algorithmic HBM bytes of those kernels (this rank) */
+    uint64_t link_bytes;      /* bytes sent to peers by remaps (this rank)         */
+} hq_stats;
+
+/* ------------------------------------------------------------------ create */
+
+/* Single-process state on ngpus devices (0..ngpus-1 of the current process).
+ * ngpus = 1: the current CUDA device.  ngpus > 1: one shard per device, NCCL
+ * communicator from ncclCommInitAll.  Requires ngpus a power of two <= the
+ * visible device count and n - log2(ngpus) >= 6 (so any k<=6 gate can be made
+ * local).  n in [1, 40].  The state is NOT initialised: call
+ * hq_state_init_basis or hq_set_amplitudes.
+ * Errors: HQ_ERR_ARG, HQ_ERR_NGPUS, HQ_ERR_OOM, HQ_ERR_CUDA, HQ_ERR_NCCL,
+ * HQ_ERR_NO_DEVICE. */
+hq_status hq_state_create(int n, hq_dtype dtype, int ngpus, hq_state **out);
+
+/* One process per GPU (torchrun): this process holds shard `rank` of
+ * `world_size` (a power of two) on CUDA device `device`.  nccl_id points to
+ * the 128-byte ncclUniqueId produced by hq_nccl_unique_id() on rank 0 and
+ * broadcast by the caller (e.g. torch.distributed); it may be NULL when
+ * world_size == 1.  Collective: every rank must call it. */
+hq_status hq_state_create_rank(int n, hq_dtype dtype, int world_size, int rank,
+                               int device, const void *nccl_id, hq_state **out);
+
+/* Writes a fresh 128-byte ncclUniqueId into out128. */
+hq_status hq_nccl_unique_id(void *out128);
+
+/* Test mode: G = nshards (power of two) "virtual" shards as separate buffers
+ * on ONE device, remaps done by device-to-device copies on one stream.  Same
+ * scheduler, same pi map and same kernels as the multi-GPU path; used to check
+ * the distribution logic bit-exactly on a single GPU. */
+hq_status hq_state_create_virtual(int n, hq_dtype dtype, int nshards, hq_state **out);
+
+/* Borrowed-memory variant of the 1-GPU state (e.g. torch.empty buffers):
+ * psi = 2^n amplitudes in dtype (16-byte aligned), stream = a cudaStream_t (or
+ * NULL for the legacy default stream).  Memory must outlive the state. */
+hq_status hq_state_create_from_buffers(int n, hq_dtype dtype, void *psi_device,
+                                       void *stream, hq_state **out);
+
+/* Frees everything the library owns.  NULL is accepted. */
+hq_status hq_state_destroy(hq_state *s);
+
+/* Replace the stream used for shard 0 of this process (caller-owned
+ * cudaStream_t; must outlive its use).  Synchronises the old stream first. */
+hq_status hq_state_set_stream(hq_state *s, void *stream);
+
+/* n, dtype, world size G, ranks held by this process, first rank held. */
+hq_status hq_state_info(const hq_state *s, int *n, int *dtype, int *world,
+                        int *local_shards, int *first_rank);
+
+/* ------------------------------------------------------------------ state */
+
+/* psi = |x>: x read with qubit 0 as the most significant bit (C1).
+ * x >= 2^n -> HQ_ERR_RANGE.  (SPEC S:229-236.) */
+hq_status hq_state_init_basis(hq_state *s, uint64_t x);
+
+/* Copy `count` amplitudes starting at LOGICAL index `first` into host_out
+ * (interleaved, state dtype).  Synchronises.  In a multi-rank state each rank
+ * writes only the amplitudes it owns and leaves the others untouched; call
+ * hq_gather_amplitudes-style logic at the caller if needed.
+ * Range outside [0, 2^n) -> HQ_ERR_RANGE.  (SPEC S:241.) */
+hq_status hq_get_amplitudes(hq_state *s, uint64_t first, uint64_t count, void *host_out);
+
+/* Inverse of hq_get_amplitudes: explicit-array initial state.
+ * Each rank takes the amplitudes it owns from host_in. */
+hq_status hq_set_amplitudes(hq_state *s, uint64_t first, uint64_t count, const void *host_in);
+
+/* ||psi||_2 (not squared; reading C13), FP64 accumulation for both dtypes,
+ * reduced over all ranks.  Synchronises.  (SPEC S:221.) */
+hq_status hq_norm(hq_state *s, double *out);
+
+/* ------------------------------------------------------------------ apply */
+
+/* psi <- (U embedded on qubits) psi.
+ * U: 2*4^k doubles (interleaved, row-major, qubits[0] = MSB of U's index).
+ * Errors (state unchanged): HQ_ERR_ARG (NULL), HQ_ERR_K (k<1, k>6, k > n - m),
+ * HQ_ERR_QUBIT, HQ_ERR_DUP_QUBIT.  If a target is a global (rank) qubit the
+ * library first remaps (all-to-all) so that every target is local. */
+hq_status hq_apply_matrix(hq_state *s, const double *U, const int32_t *qubits, int k);
+
+/* Apply an (already fused) gate list in order, leftmost first.
+ * All gates are validated before any work is enqueued.  Remaps are scheduled
+ * here with next-use (Belady) lookahead over the whole list. */
+hq_status hq_apply_circuit(hq_state *s, const hq_gate *gates, size_t ngates);
+
+/* Compile once, run many: validate + schedule + upload matrices of `gates`
+ * for state s (the circuit is bound to s's layout: n, dtype, G).  Running it
+ * applies exactly what hq_apply_circuit(s, gates, ngates) would. */
+hq_status hq_circuit_create(hq_state *s, const hq_gate *gates, size_t ngates,
+                            hq_circuit **out);
+hq_status hq_circuit_run(hq_state *s, hq_circuit *c);
+/* passes, remaps and local permutes in the compiled op stream. */
+hq_status hq_circuit_info(const hq_circuit *c, uint64_t *passes, uint64_t *remaps,
+                          uint64_t *permutes);
+hq_status hq_circuit_destroy(hq_circuit *c);
+
+/* ------------------------------------------------------------------ planner */
+
+/* Greedy gate fusion (PAPER P:499-504 `compress` + P:493-494
+ * `to_matrix_gate`; reading C7): gate g joins the earliest-created group G
+ * with |supp(G) u supp(g)| <= kmax such that no non-member gate between G's
+ * first member and g touches a qubit of g; otherwise it opens a new group.
+ * Groups are emitted in first-member order; each fused gate acts on its
+ * ascending support with U = U_last ... U_first (fp64).
+ * kmax in [1, 6] and >= every input arity, else HQ_ERR_K.
+ * *out is allocated by the library (free with hq_free_gates). */
+hq_status hq_fuse(const hq_gate *in, size_t ngates, int kmax, hq_gate **out, size_t *nout);
+hq_status hq_free_gates(hq_gate *gates, size_t ngates);
+
+/* Grouping only: group_of[i] = index (first-member order) of the fused group
+ * of input gate i; *ngroups = number of groups.  group_of has ngates slots. */
+hq_status hq_fuse_plan(const hq_gate *in, size_t ngates, int kmax, int32_t *group_of,
+                       size_t *ngroups);
+
+/* Host-only view of the distributed schedule (for tests): for an n-qubit
+ * state on G = 2^m ranks, the op stream hq_apply_circuit would execute.
+ * ops[i] = {kind, gate, nbits, bits[12]}:
+ *   kind 0 APPLY  : gate index `gate`, bits[0..k-1] = physical target bits of
+ *                   qubits[0..k-1];
+ *   kind 1 REMAP  : swap global bit bits[2i] with local bit bits[2i+1],
+ *                   i < nbits (all-to-all among 2^nbits ranks);
+ *   kind 2 PERMUTE: local bit swap bits[2i] <-> bits[2i+1], i < nbits.
+ * pi_out (n entries, may be NULL) receives the final logical->physical map. */
+typedef struct hq_op {
+    int32_t kind;
+    int32_t gate;
+    int32_t nbits;
+    int32_t bits[12];
+} hq_op;
+hq_status hq_schedule(int n, int m, const hq_gate *gates, size_t ngates,
+                      hq_op **ops, size_t *nops, int32_t *pi_out);
+hq_status hq_free_ops(hq_op *ops);
+
+/* ------------------------------------------------------------------ diagnostics */
+
+/* Thread-local message for the last failing call on this thread ("" if none). */
+const char *hq_last_error(void);
+/* Block until all work enqueued on the state's streams has completed. */
+hq_status hq_sync(hq_state *s);
+hq_status hq_stats_get(const hq_state *s, hq_stats *out);
+hq_status hq_stats_reset(hq_state *s);
+/* Per-launch timing of apply kernels with CUDA events on the launching
+ * stream (off by default).  hq_kernel_times synchronises and returns, for the
+ * launches since profiling was enabled / last read: count, total and max
+ * milliseconds, and algorithmic bytes (2 x shard bytes per pass). */
+hq_status hq_profile_enable(hq_state *s, int on);
+hq_status hq_kernel_times(hq_state *s, uint64_t *count, double *total_ms,
+                          double *max_ms, uint64_t *bytes);
+/* Library version string. */
+const char *hq_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HQ_H */

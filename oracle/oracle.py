@@ -176,17 +176,16 @@ def compress(gates, kmax):
         if len(g.qubits) > kmax:
             raise OracleError("GateTooWide")
     groups = []           # each: dict(first, members(list), support(set), mset)
+    touch = {}            # qubit -> indices of the gates (so far) that touch it
     for i, g in enumerate(gates):
         qs = set(g.qubits)
         placed = False
         for G in groups:
             if len(G["support"] | qs) > kmax:
                 continue
-            blocked = False
-            for j in range(G["first"] + 1, i):
-                if j not in G["mset"] and qs & set(gates[j].qubits):
-                    blocked = True
-                    break
+            # non-member gates between G's first member and g touching g's qubits
+            blocked = any(G["first"] < j < i and j not in G["mset"]
+                          for q in qs for j in touch.get(q, ()))
             if blocked:
                 continue
             G["members"].append(i)
@@ -196,6 +195,8 @@ def compress(gates, kmax):
             break
         if not placed:
             groups.append({"first": i, "members": [i], "mset": {i}, "support": set(qs)})
+        for q in qs:
+            touch.setdefault(q, []).append(i)
     return [G["members"] for G in groups]
 
 

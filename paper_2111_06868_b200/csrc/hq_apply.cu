@@ -1,0 +1,521 @@
+// SIMT apply kernels (sm_100a) and the small state kernels (init, norm,
+// permute, gather/scatter).
+//
+// The operation: for every
+// outer index o in [0, 2^(n_l-k)) take the gather set of 2^k amplitudes whose
+// index agrees with o off the k target bits, and replace it by U times it.
+// Each pass streams the whole shard through HBM once (read + write), so the
+// kernels are built for bandwidth:
+//
+//  * apply_reg<R,K,T0,KL>  (k <= 4): each warp owns 32 lanes x 2^|R| amplitudes.
+//    Lanes cover physical bits [LB, LB+5) with 16-byte vectors (c64: two
+//    amplitudes per vector, bit 0 in-thread; c128: one), so every load/store
+//    instruction of a warp is a fully coalesced 512-byte access.  Target bits
+//    above the lane range are register bits (direct loads at stride 2^p).
+//    Targets inside the lane range are moved into registers with warp shuffles
+//    (a lane-bit <-> register-bit transpose against a spare high bit), which
+//    is the GPU counterpart of the paper's "qubits are swapped to fully exploit
+//    AVX instructions".  U travels in the kernel's parameter space
+//    (constant bank), so every complex MAC is 4 FFMA/DFMA with a constant
+//    operand and no load instruction.
+//  * apply_gen<R,K> (any k <= 6, any placement, small n): one thread per
+//    gather set, U from global memory (L1 broadcast).  Correctness fallback.
+//
+// Canonical target order: the host permutes U so that U-index bit i <-> the
+// i-th smallest physical target bit (exact: a permutation of rows/columns).
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstring>
+#include <type_traits>
+
+#include "hq_internal.h"
+
+namespace hq {
+
+template <typename R> struct C2;
+template <> struct C2<float> { using T = float2; };
+template <> struct C2<double> { using T = double2; };
+
+__device__ __forceinline__ uint64_t insert_zero(uint64_t x, int s) {
+    const uint64_t lo = x & ((1ull << s) - 1);
+    return ((x >> s) << (s + 1)) | lo;
+}
+
+// ------------------------------------------------------------------ fast SIMT kernel
+
+struct RegParams {
+    uint64_t voff[32];   // offset (in 16-byte vectors) of each register vector
+    uint64_t nunits;     // number of threads with work (= 32 * warps)
+    int S[6];            // ascending insertion positions in warp space (count K-T0)
+    int la[5];           // lane bit (0..4) of each lane target, canonical order
+};
+
+template <typename R, int K> struct UParam {
+    typename C2<R>::T u[1 << K][1 << K];
+};
+
+template <typename R, int K, int T0, int KL>
+__global__ void __launch_bounds__(128)
+apply_reg(typename C2<R>::T *__restrict__ psi, const __grid_constant__ RegParams P,
+          const __grid_constant__ UParam<R, K> U) {
+    using V = typename C2<R>::T;
+    constexpr int VEC = std::is_same<R, float>::value ? 2 : 1;   // amplitudes per 16 B
+    constexpr int NB0 = (VEC == 2 && !T0) ? 1 : 0;              // bit 0 as non-target register bit
+    constexpr int NR = 1 << (K + NB0);                           // amplitudes per thread
+    constexpr int P0 = T0 ? 0 : K;                               // register bit holding phys bit 0 (c64)
+    constexpr int NV = NR / VEC;                                 // 16-byte vectors per thread
+    constexpr int NS = K - T0;                                   // register phys bits above lanes
+
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (tid >= P.nunits) return;
+    const int lane = threadIdx.x & 31;
+    uint64_t w = tid >> 5;
+#pragma unroll
+    for (int i = 0; i < NS; ++i) w = insert_zero(w, P.S[i]);
+    const uint64_t base = (w << 5) | (uint64_t)lane;             // in 16-byte vectors
+
+    V x[NR];
+    if constexpr (VEC == 2) {
+        const float4 *src = reinterpret_cast<const float4 *>(psi);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            // register index with bit P0 cleared, built from v
+            const int j0 = ((v >> P0) << (P0 + 1)) | (v & ((1 << P0) - 1));
+            const int j1 = j0 | (1 << P0);
+            const float4 t = src[base + P.voff[v]];
+            x[j0] = make_float2(t.x, t.y);
+            x[j1] = make_float2(t.z, t.w);
+        }
+    } else {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) x[v] = psi[base + P.voff[v]];
+    }
+
+    // lane-target transposes: lane bit la[i] <-> register bit T0+i
+#pragma unroll
+    for (int i = 0; i < KL; ++i) {
+        const int la = P.la[i];
+        const bool hi = (lane >> la) & 1;
+        const int e = T0 + i;
+#pragma unroll
+        for (int j0 = 0; j0 < NR; ++j0) {
+            if (j0 & (1 << e)) continue;
+            const int j1 = j0 | (1 << e);
+            V snd;
+            snd.x = hi ? x[j0].x : x[j1].x;
+            snd.y = hi ? x[j0].y : x[j1].y;
+            V rcv;
+            rcv.x = __shfl_xor_sync(0xffffffffu, snd.x, 1 << la);
+            rcv.y = __shfl_xor_sync(0xffffffffu, snd.y, 1 << la);
+            if (hi) x[j0] = rcv; else x[j1] = rcv;
+        }
+    }
+
+    // w = U v for each gather set held by the thread
+#pragma unroll
+    for (int s = 0; s < (1 << NB0); ++s) {
+        V out[1 << K];
+#pragma unroll
+        for (int r = 0; r < (1 << K); ++r) {
+            R ar = 0, ai = 0;
+#pragma unroll
+            for (int c = 0; c < (1 << K); ++c) {
+                const V u = U.u[r][c];
+                const V v = x[c | (s << K)];
+                ar = fma(u.x, v.x, ar);
+                ar = fma(-u.y, v.y, ar);
+                ai = fma(u.x, v.y, ai);
+                ai = fma(u.y, v.x, ai);
+            }
+            out[r].x = ar;
+            out[r].y = ai;
+        }
+#pragma unroll
+        for (int r = 0; r < (1 << K); ++r) x[r | (s << K)] = out[r];
+    }
+
+    // undo the transposes (each is an involution), in reverse order
+#pragma unroll
+    for (int i = KL - 1; i >= 0; --i) {
+        const int la = P.la[i];
+        const bool hi = (lane >> la) & 1;
+        const int e = T0 + i;
+#pragma unroll
+        for (int j0 = 0; j0 < NR; ++j0) {
+            if (j0 & (1 << e)) continue;
+            const int j1 = j0 | (1 << e);
+            V snd;
+            snd.x = hi ? x[j0].x : x[j1].x;
+            snd.y = hi ? x[j0].y : x[j1].y;
+            V rcv;
+            rcv.x = __shfl_xor_sync(0xffffffffu, snd.x, 1 << la);
+            rcv.y = __shfl_xor_sync(0xffffffffu, snd.y, 1 << la);
+            if (hi) x[j0] = rcv; else x[j1] = rcv;
+        }
+    }
+
+    if constexpr (VEC == 2) {
+        float4 *dst = reinterpret_cast<float4 *>(psi);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            const int j0 = ((v >> P0) << (P0 + 1)) | (v & ((1 << P0) - 1));
+            const int j1 = j0 | (1 << P0);
+            dst[base + P.voff[v]] = make_float4(x[j0].x, x[j0].y, x[j1].x, x[j1].y);
+        }
+    } else {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) psi[base + P.voff[v]] = x[v];
+    }
+}
+
+// ------------------------------------------------------------------ generic kernel
+
+struct GenParams {
+    uint64_t off[64];    // amplitude offset of U-index c (canonical order)
+    uint64_t nsets;      // 2^(n_l - k)
+    int s[6];            // ascending target bits
+};
+
+template <typename R, int K>
+__global__ void __launch_bounds__(128)
+apply_gen(typename C2<R>::T *__restrict__ psi, const __grid_constant__ GenParams P,
+          const typename C2<R>::T *__restrict__ Ud) {
+    using V = typename C2<R>::T;
+    constexpr int D = 1 << K;
+    for (uint64_t o = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; o < P.nsets;
+         o += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t base = o;
+#pragma unroll
+        for (int j = 0; j < K; ++j) base = insert_zero(base, P.s[j]);
+        V v[D];
+#pragma unroll
+        for (int c = 0; c < D; ++c) v[c] = psi[base + P.off[c]];
+        for (int r = 0; r < D; ++r) {
+            R ar = 0, ai = 0;
+#pragma unroll
+            for (int c = 0; c < D; ++c) {
+                const V u = __ldg(&Ud[r * D + c]);
+                ar = fma(u.x, v[c].x, ar);
+                ar = fma(-u.y, v[c].y, ar);
+                ai = fma(u.x, v[c].y, ai);
+                ai = fma(u.y, v[c].x, ai);
+            }
+            V w;
+            w.x = ar;
+            w.y = ai;
+            psi[base + P.off[r]] = w;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ dispatch
+
+namespace {
+
+constexpr int kThreads = 128;
+
+template <typename R, int K, int T0, int KL>
+cudaError_t launch_reg_t(void *psi, const RegParams &P, const void *host_U, cudaStream_t st) {
+    UParam<R, K> U;
+    memcpy(&U, host_U, sizeof(U));
+    const uint64_t blocks = (P.nunits + kThreads - 1) / kThreads;
+    apply_reg<R, K, T0, KL><<<(unsigned)blocks, kThreads, 0, st>>>(
+        reinterpret_cast<typename C2<R>::T *>(psi), P, U);
+    return cudaGetLastError();
+}
+
+template <typename R, int K, int T0>
+cudaError_t launch_reg_kl(int KL, void *psi, const RegParams &P, const void *hU, cudaStream_t st) {
+    switch (KL) {
+        case 0: return launch_reg_t<R, K, T0, 0>(psi, P, hU, st);
+        case 1: if constexpr (K - T0 >= 1) return launch_reg_t<R, K, T0, 1>(psi, P, hU, st); break;
+        case 2: if constexpr (K - T0 >= 2) return launch_reg_t<R, K, T0, 2>(psi, P, hU, st); break;
+        case 3: if constexpr (K - T0 >= 3) return launch_reg_t<R, K, T0, 3>(psi, P, hU, st); break;
+        case 4: if constexpr (K - T0 >= 4) return launch_reg_t<R, K, T0, 4>(psi, P, hU, st); break;
+        default: break;
+    }
+    return cudaErrorInvalidValue;
+}
+
+template <typename R, int K>
+cudaError_t launch_reg_k(int T0, int KL, void *psi, const RegParams &P, const void *hU,
+                         cudaStream_t st) {
+    if constexpr (std::is_same<R, float>::value) {
+        if (T0) return launch_reg_kl<R, K, 1>(KL, psi, P, hU, st);
+    }
+    return launch_reg_kl<R, K, 0>(KL, psi, P, hU, st);
+}
+
+template <typename R>
+cudaError_t launch_gen(int K, void *psi, const GenParams &P, const void *dU, cudaStream_t st) {
+    using V = typename C2<R>::T;
+    uint64_t blocks = (P.nsets + kThreads - 1) / kThreads;
+    if (blocks > 148ull * 64) blocks = 148ull * 64;
+    if (blocks == 0) blocks = 1;
+    V *p = reinterpret_cast<V *>(psi);
+    const V *u = reinterpret_cast<const V *>(dU);
+    switch (K) {
+        case 1: apply_gen<R, 1><<<(unsigned)blocks, kThreads, 0, st>>>(p, P, u); break;
+        case 2: apply_gen<R, 2><<<(unsigned)blocks, kThreads, 0, st>>>(p, P, u); break;
+        case 3: apply_gen<R, 3><<<(unsigned)blocks, kThreads, 0, st>>>(p, P, u); break;
+        case 4: apply_gen<R, 4><<<(unsigned)blocks, kThreads, 0, st>>>(p, P, u); break;
+        case 5: apply_gen<R, 5><<<(unsigned)blocks, kThreads, 0, st>>>(p, P, u); break;
+        case 6: apply_gen<R, 6><<<(unsigned)blocks, kThreads, 0, st>>>(p, P, u); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+// Plan the register kernel for this placement; returns false if it does not
+// apply (then the generic kernel runs).
+bool plan_reg(int dtype, const ApplyDesc &d, RegParams &P, int &T0, int &KL) {
+    const int K = d.k;
+    if (K > 4) return false;
+    const int LB = dtype == HQ_C64 ? 1 : 0;
+    const int lane_lo = LB, lane_hi = LB + 5;      // lane bits [lane_lo, lane_hi)
+    T0 = (dtype == HQ_C64 && d.p[0] == 0) ? 1 : 0;
+    KL = 0;
+    for (int i = T0; i < K; ++i)
+        if (d.p[i] < lane_hi) ++KL;
+    // register physical bits (besides bit 0 for c64): extras + high targets
+    const int used = lane_hi + (K - T0);
+    if (d.n_local - used < 8) return false;       // too small to fill a GPU
+    // extras: lowest KL physical bits >= lane_hi that are not targets
+    int extras[5], ne = 0;
+    for (int b = lane_hi; ne < KL && b < d.n_local; ++b) {
+        bool tgt = false;
+        for (int i = 0; i < K; ++i) tgt |= d.p[i] == b;
+        if (!tgt) extras[ne++] = b;
+    }
+    if (ne < KL) return false;
+    // register bit -> physical bit (load-phase meaning)
+    int regphys[7];
+    int nreg = 0;
+    if (T0) regphys[nreg++] = 0;
+    for (int i = 0; i < KL; ++i) regphys[nreg++] = extras[i];
+    for (int i = T0 + KL; i < K; ++i) regphys[nreg++] = d.p[i];
+    const int NB0 = (dtype == HQ_C64 && !T0) ? 1 : 0;
+    if (NB0) regphys[nreg++] = 0;                 // register bit K
+    const int P0 = T0 ? 0 : K;
+    // vector offsets: registers with the bit-0 register cleared
+    const int NR = 1 << (K + NB0);
+    const int VEC = dtype == HQ_C64 ? 2 : 1;
+    for (int v = 0; v < NR / VEC; ++v) {
+        int j0 = v;
+        if (VEC == 2) j0 = ((v >> P0) << (P0 + 1)) | (v & ((1 << P0) - 1));
+        uint64_t off = 0;
+        for (int b = 0; b < nreg; ++b)
+            if ((j0 >> b) & 1) off |= 1ull << (regphys[b] - LB);
+        P.voff[v] = off;
+    }
+    // warp-space insertion positions: register phys bits other than bit 0
+    int S[6], ns = 0;
+    for (int b = 0; b < nreg; ++b)
+        if (regphys[b] >= lane_hi) S[ns++] = regphys[b] - lane_hi;
+    // sort ascending
+    for (int i = 1; i < ns; ++i) {
+        int x = S[i], j = i - 1;
+        while (j >= 0 && S[j] > x) { S[j + 1] = S[j]; --j; }
+        S[j + 1] = x;
+    }
+    if (ns != K - T0) return false;
+    for (int i = 0; i < ns; ++i) P.S[i] = S[i];
+    for (int i = 0; i < KL; ++i) P.la[i] = d.p[T0 + i] - LB;
+    const int nvbits = d.n_local - LB;           // vector-index bits
+    P.nunits = 1ull << (nvbits - ns);              // threads = 32 lanes x warps
+    return true;
+}
+
+}  // namespace
+
+int launch_apply(int dtype, void *psi, const ApplyDesc &d, const void *host_U, const void *dev_U,
+                 void *stream, int *launches) {
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    RegParams rp;
+    int T0 = 0, KL = 0;
+    cudaError_t e;
+    if (host_U && plan_reg(dtype, d, rp, T0, KL)) {
+        if (dtype == HQ_C64) {
+            switch (d.k) {
+                case 1: e = launch_reg_k<float, 1>(T0, KL, psi, rp, host_U, st); break;
+                case 2: e = launch_reg_k<float, 2>(T0, KL, psi, rp, host_U, st); break;
+                case 3: e = launch_reg_k<float, 3>(T0, KL, psi, rp, host_U, st); break;
+                default: e = launch_reg_k<float, 4>(T0, KL, psi, rp, host_U, st); break;
+            }
+        } else {
+            switch (d.k) {
+                case 1: e = launch_reg_k<double, 1>(0, KL, psi, rp, host_U, st); break;
+                case 2: e = launch_reg_k<double, 2>(0, KL, psi, rp, host_U, st); break;
+                case 3: e = launch_reg_k<double, 3>(0, KL, psi, rp, host_U, st); break;
+                default: e = launch_reg_k<double, 4>(0, KL, psi, rp, host_U, st); break;
+            }
+        }
+    } else {
+        GenParams gp;
+        for (int c = 0; c < (1 << d.k); ++c) {
+            uint64_t o = 0;
+            for (int i = 0; i < d.k; ++i)
+                if ((c >> i) & 1) o |= 1ull << d.p[i];
+            gp.off[c] = o;
+        }
+        for (int i = 0; i < d.k; ++i) gp.s[i] = d.p[i];
+        gp.nsets = 1ull << (d.n_local - d.k);
+        if (!dev_U) return (int)cudaErrorInvalidValue;
+        e = dtype == HQ_C64 ? launch_gen<float>(d.k, psi, gp, dev_U, st)
+                            : launch_gen<double>(d.k, psi, gp, dev_U, st);
+    }
+    if (launches) ++*launches;
+    return (int)e;
+}
+
+bool apply_needs_dev_U(int dtype, const ApplyDesc &d) {
+    RegParams rp;
+    int T0, KL;
+    return !plan_reg(dtype, d, rp, T0, KL);
+}
+
+// ------------------------------------------------------------------ small kernels
+
+template <typename V>
+__global__ void set_one_kernel(V *psi, int64_t idx) {
+    V one;
+    one.x = 1;
+    one.y = 0;
+    psi[idx] = one;
+}
+
+int launch_init_basis(int dtype, void *psi, uint64_t n_amps, int64_t idx, void *stream) {
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const size_t es = dtype == HQ_C64 ? 8 : 16;
+    cudaError_t e = cudaMemsetAsync(psi, 0, es * n_amps, st);
+    if (e != cudaSuccess) return (int)e;
+    if (idx >= 0) {
+        if (dtype == HQ_C64) set_one_kernel<float2><<<1, 1, 0, st>>>((float2 *)psi, idx);
+        else set_one_kernel<double2><<<1, 1, 0, st>>>((double2 *)psi, idx);
+        e = cudaGetLastError();
+    }
+    return (int)e;
+}
+
+template <typename V>
+__global__ void __launch_bounds__(256) norm_partial_kernel(const V *__restrict__ psi, uint64_t n,
+                                                           double *__restrict__ part) {
+    double acc = 0.0;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const V v = psi[i];
+        acc += (double)v.x * (double)v.x + (double)v.y * (double)v.y;
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    __shared__ double red[8];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+        part[blockIdx.x] = t;
+    }
+}
+
+int launch_norm_partials(int dtype, const void *psi, uint64_t n_amps, double *dev_partial,
+                         int max_blocks, void *stream, int *nblocks_out) {
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    uint64_t blocks = (n_amps + 255) / 256;
+    if (blocks > (uint64_t)max_blocks) blocks = max_blocks;
+    if (blocks == 0) blocks = 1;
+    if (dtype == HQ_C64)
+        norm_partial_kernel<float2><<<(unsigned)blocks, 256, 0, st>>>((const float2 *)psi, n_amps, dev_partial);
+    else
+        norm_partial_kernel<double2><<<(unsigned)blocks, 256, 0, st>>>((const double2 *)psi, n_amps, dev_partial);
+    *nblocks_out = (int)blocks;
+    return (int)cudaGetLastError();
+}
+
+struct PermParams {
+    int npairs;
+    int a[6];
+    int b[6];
+};
+
+template <typename V>
+__global__ void permute_kernel(const V *__restrict__ src, V *__restrict__ dst, uint64_t n,
+                               const __grid_constant__ PermParams P) {
+    for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n;
+         x += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t y = x;
+        for (int i = 0; i < P.npairs; ++i) {
+            const uint64_t ba = (x >> P.a[i]) & 1, bb = (x >> P.b[i]) & 1;
+            y &= ~((1ull << P.a[i]) | (1ull << P.b[i]));
+            y |= (ba << P.b[i]) | (bb << P.a[i]);
+        }
+        dst[y] = src[x];
+    }
+}
+
+int launch_permute(int dtype, const void *src, void *dst, uint64_t n_amps, int npairs, const int *a,
+                   const int *b, void *stream) {
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    PermParams P;
+    P.npairs = npairs;
+    for (int i = 0; i < npairs && i < 6; ++i) { P.a[i] = a[i]; P.b[i] = b[i]; }
+    uint64_t blocks = (n_amps + 255) / 256;
+    if (blocks > 148ull * 32) blocks = 148ull * 32;
+    if (dtype == HQ_C64)
+        permute_kernel<float2><<<(unsigned)blocks, 256, 0, st>>>((const float2 *)src, (float2 *)dst, n_amps, P);
+    else
+        permute_kernel<double2><<<(unsigned)blocks, 256, 0, st>>>((const double2 *)src, (double2 *)dst, n_amps, P);
+    return (int)cudaGetLastError();
+}
+
+struct MapParams {
+    int bitmap[64];
+    int n, n_local, rank;
+};
+
+template <typename V, bool GATHER>
+__global__ void gather_scatter_kernel(V *psi, V *buf, uint64_t first, uint64_t count,
+                                      const __grid_constant__ MapParams P) {
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < count;
+         j += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = first + j;
+        uint64_t phys = 0;
+        for (int b = 0; b < P.n; ++b) phys |= ((i >> b) & 1) << P.bitmap[b];
+        if ((int)(phys >> P.n_local) != P.rank) continue;
+        const uint64_t off = phys & ((1ull << P.n_local) - 1);
+        if (GATHER) buf[j] = psi[off];
+        else psi[off] = buf[j];
+    }
+}
+
+static int launch_gs(bool gather, int dtype, void *psi, void *buf, uint64_t first, uint64_t count,
+                     int n, int n_local, const int *bitmap, int my_rank, void *stream) {
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    MapParams P;
+    for (int b = 0; b < n; ++b) P.bitmap[b] = bitmap[b];
+    P.n = n;
+    P.n_local = n_local;
+    P.rank = my_rank;
+    uint64_t blocks = (count + 255) / 256;
+    if (blocks > 148ull * 32) blocks = 148ull * 32;
+    if (blocks == 0) return 0;
+    if (dtype == HQ_C64) {
+        if (gather) gather_scatter_kernel<float2, true><<<(unsigned)blocks, 256, 0, st>>>((float2 *)psi, (float2 *)buf, first, count, P);
+        else gather_scatter_kernel<float2, false><<<(unsigned)blocks, 256, 0, st>>>((float2 *)psi, (float2 *)buf, first, count, P);
+    } else {
+        if (gather) gather_scatter_kernel<double2, true><<<(unsigned)blocks, 256, 0, st>>>((double2 *)psi, (double2 *)buf, first, count, P);
+        else gather_scatter_kernel<double2, false><<<(unsigned)blocks, 256, 0, st>>>((double2 *)psi, (double2 *)buf, first, count, P);
+    }
+    return (int)cudaGetLastError();
+}
+
+int launch_gather(int dtype, const void *psi, void *dst, uint64_t first, uint64_t count, int n,
+                  int n_local, const int *bitmap, int my_rank, void *stream) {
+    return launch_gs(true, dtype, const_cast<void *>(psi), dst, first, count, n, n_local, bitmap, my_rank, stream);
+}
+
+int launch_scatter(int dtype, void *psi, const void *src, uint64_t first, uint64_t count, int n,
+                   int n_local, const int *bitmap, int my_rank, void *stream) {
+    return launch_gs(false, dtype, psi, const_cast<void *>(src), first, count, n, n_local, bitmap, my_rank, stream);
+}
+
+}  // namespace hq

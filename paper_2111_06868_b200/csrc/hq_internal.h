@@ -1,0 +1,92 @@
+// Internal declarations shared by the host runtime (.cpp) and the kernels (.cu).
+// Product code only: nothing here is shared with oracle/.
+#pragma once
+
+#include <cstdint>
+#include <cstddef>
+#include <string>
+#include <vector>
+
+#include "hq.h"
+
+namespace hq {
+
+// ------------------------------------------------------------------ errors
+hq_status set_error(hq_status st, const char *fmt, ...);
+void clear_error();
+
+// ------------------------------------------------------------------ planner (hq_plan.cpp)
+struct GateRef {            // validated view of an hq_gate
+    int k;
+    int q[6];
+    const double *U;        // 2*4^k doubles
+};
+
+// Greedy fusion (reading C7).  group_of[i] = group index in first-member order.
+// Returns number of groups.
+size_t fuse_groups(const std::vector<GateRef> &g, int kmax, std::vector<int32_t> &group_of);
+
+// Build fused gates: ascending support, U = U_last...U_first (fp64, interleaved).
+struct FusedGate {
+    int k;
+    int q[6];
+    std::vector<double> U;  // 2*4^k
+};
+void fuse_build(const std::vector<GateRef> &g, int kmax, std::vector<FusedGate> &out);
+
+// Distributed schedule (hq_schedule semantics).  pi: logical->physical, in/out.
+enum OpKind { OP_APPLY = 0, OP_REMAP = 1, OP_PERMUTE = 2 };
+struct Op {
+    int kind;
+    int gate;
+    int nbits;
+    int bits[12];
+};
+void schedule(int n, int m, const std::vector<GateRef> &g, std::vector<int> &pi,
+              std::vector<Op> &ops);
+
+// ------------------------------------------------------------------ kernels (hq_apply.cu)
+// Target description handed to the kernel launchers: k physical bit
+// positions in CANONICAL order (ascending), and U already permuted so that
+// U-index bit i <-> canonical target i (LSB first).  U in the state dtype.
+struct ApplyDesc {
+    int k;
+    int p[6];               // ascending physical bit positions (< n_local)
+    int n_local;
+};
+
+// Device-side matrix: U in dtype, row-major, interleaved, 4^k complex.
+// host_U (dtype, same layout) is also given so small matrices travel in the
+// kernel's parameter space; dev_U may be null if host path suffices.
+struct KernelStatus {
+    int launches;
+};
+
+// Launch one apply pass on `psi` (2^n_local amplitudes).  Returns cudaError_t
+// as int.  stream is a cudaStream_t.
+int launch_apply(int dtype, void *psi, const ApplyDesc &d, const void *host_U,
+                 const void *dev_U, void *stream, int *launches);
+
+// Whether launch_apply needs dev_U (true when U cannot travel as a kernel
+// parameter for this (dtype, k, placement)).
+bool apply_needs_dev_U(int dtype, const ApplyDesc &d);
+
+// psi = 0, then psi[idx] = 1 if idx >= 0.
+int launch_init_basis(int dtype, void *psi, uint64_t n_amps, int64_t idx, void *stream);
+// partial sums of |psi|^2 into dev_partial[0..nblocks), returns nblocks used.
+int launch_norm_partials(int dtype, const void *psi, uint64_t n_amps, double *dev_partial,
+                         int max_blocks, void *stream, int *nblocks_out);
+// out-of-place local bit permutation: dst[perm(x)] = src[x] where perm swaps
+// bit a[i] <-> b[i] for i < npairs.
+int launch_permute(int dtype, const void *src, void *dst, uint64_t n_amps, int npairs,
+                   const int *a, const int *b, void *stream);
+// gather: dst[j] = psi[phys(first + j)] for the amplitudes this shard owns;
+// phys() maps logical index -> physical index by the bit map `bitmap`
+// (bitmap[logical_bit] = physical_bit, n entries), returns only those with
+// rank == my_rank (others left untouched in dst, mask written as 0/1).
+int launch_gather(int dtype, const void *psi, void *dst, uint64_t first, uint64_t count,
+                  int n, int n_local, const int *bitmap, int my_rank, void *stream);
+int launch_scatter(int dtype, void *psi, const void *src, uint64_t first, uint64_t count,
+                   int n, int n_local, const int *bitmap, int my_rank, void *stream);
+
+}  // namespace hq

@@ -1,0 +1,339 @@
+// Host planner: greedy gate fusion and the distributed (global-qubit) schedule.
+//
+// Fusion follows PAPER.md P:499-504 (utils.compress: "Compress gates in
+// circuit so that gates in the new circuit will not have more than
+// max_n_qubits qubits ... larger gates may better exploit vectorization") and
+// P:493-494 (to_matrix_gate), with the grouping rule of DESIGN.md reading C7
+// (SPEC S:166-174 made sound):  gate g joins the earliest-created group G
+// with |supp(G) u supp(g)| <= kmax such that no non-member gate between G's
+// first member and g touches a qubit of g; otherwise it opens a new group.
+// Worked example: P:510-529 (supports (0,1,2),(0,3,4),(1,3,4),(2,3,4)).
+//
+// The schedule implements the state-vector distribution the paper only
+// plans: amplitudes are sharded on the top m physical
+// bits; a gate with a global target is preceded by a REMAP that swaps global
+// bits with the top local bits (an all-to-all), choosing which logical qubits
+// to evict by furthest next use (Belady).  The paper's own idea is the same
+// swap applied to the least-significant qubits for AVX.
+#include <algorithm>
+#include <cstring>
+#include <limits>
+#include <new>
+
+#include "hq_internal.h"
+
+namespace hq {
+
+static inline uint64_t qmask(const GateRef &g) {
+    uint64_t m = 0;
+    for (int j = 0; j < g.k; ++j) m |= 1ull << g.q[j];
+    return m;
+}
+
+size_t fuse_groups(const std::vector<GateRef> &g, int kmax, std::vector<int32_t> &group_of) {
+    const size_t N = g.size();
+    group_of.assign(N, -1);
+    struct Group { size_t first; uint64_t support; };
+    std::vector<Group> groups;
+    // history[q] = indices of gates touching qubit q, ascending
+    std::vector<std::vector<uint32_t>> history(64);
+    for (size_t i = 0; i < N; ++i) {
+        const uint64_t Q = qmask(g[i]);
+        int chosen = -1;
+        for (size_t G = 0; G < groups.size() && chosen < 0; ++G) {
+            if (__builtin_popcountll(groups[G].support | Q) > kmax) continue;
+            bool blocked = false;
+            for (int j = 0; j < g[i].k && !blocked; ++j) {
+                const auto &h = history[g[i].q[j]];
+                // walk back over gates touching this qubit that come after G.first
+                for (size_t t = h.size(); t-- > 0;) {
+                    if (h[t] <= groups[G].first) break;
+                    if (group_of[h[t]] != (int32_t)G) { blocked = true; break; }
+                }
+            }
+            if (!blocked) chosen = (int)G;
+        }
+        if (chosen < 0) {
+            chosen = (int)groups.size();
+            groups.push_back({i, 0});
+        }
+        groups[chosen].support |= Q;
+        group_of[i] = chosen;
+        for (int j = 0; j < g[i].k; ++j) history[g[i].q[j]].push_back((uint32_t)i);
+    }
+    return groups.size();
+}
+
+// Embed member U (on qubits q, k) into the m-qubit ascending support `sup`:
+// E[i][i'] = U[r(i)][r(i')] if i, i' agree off the member's bits, else 0,
+// with support position j <-> index bit m-1-j (qubit order of C1 restricted
+// to the support).  Then M <- E * M.
+static void left_multiply_embedded(std::vector<double> &M, int m, const int *sup,
+                                   const GateRef &gt) {
+    const int D = 1 << m;
+    int bitpos[6];
+    for (int j = 0; j < gt.k; ++j) {
+        int pos = -1;
+        for (int s = 0; s < m; ++s) if (sup[s] == gt.q[j]) pos = s;
+        bitpos[j] = m - 1 - pos;
+    }
+    uint32_t mask = 0;
+    for (int j = 0; j < gt.k; ++j) mask |= 1u << bitpos[j];
+    const int d = 1 << gt.k;
+    std::vector<int> r(D);
+    for (int i = 0; i < D; ++i) {
+        int v = 0;
+        for (int j = 0; j < gt.k; ++j) v |= ((i >> bitpos[j]) & 1) << (gt.k - 1 - j);
+        r[i] = v;
+    }
+    std::vector<double> out((size_t)2 * D * D, 0.0);
+    // out = E * M;  E[i][l] nonzero only when (i & ~mask) == (l & ~mask)
+    for (int i = 0; i < D; ++i) {
+        const int rest = i & ~mask;
+        for (int c = 0; c < d; ++c) {
+            // l = rest with member bits set from c
+            int l = rest;
+            for (int j = 0; j < gt.k; ++j)
+                if ((c >> (gt.k - 1 - j)) & 1) l |= 1 << bitpos[j];
+            const double er = gt.U[2 * (r[i] * d + r[l])];
+            const double ei = gt.U[2 * (r[i] * d + r[l]) + 1];
+            if (er == 0.0 && ei == 0.0) continue;
+            const double *Ml = &M[(size_t)2 * l * D];
+            double *Oi = &out[(size_t)2 * i * D];
+            for (int col = 0; col < D; ++col) {
+                const double mr = Ml[2 * col], mi = Ml[2 * col + 1];
+                Oi[2 * col] += er * mr - ei * mi;
+                Oi[2 * col + 1] += er * mi + ei * mr;
+            }
+        }
+    }
+    M.swap(out);
+}
+
+void fuse_build(const std::vector<GateRef> &g, int kmax, std::vector<FusedGate> &out) {
+    std::vector<int32_t> group_of;
+    const size_t ng = fuse_groups(g, kmax, group_of);
+    std::vector<std::vector<size_t>> members(ng);
+    for (size_t i = 0; i < g.size(); ++i) members[group_of[i]].push_back(i);
+    out.clear();
+    out.resize(ng);
+    for (size_t G = 0; G < ng; ++G) {
+        uint64_t sm = 0;
+        for (size_t i : members[G]) sm |= qmask(g[i]);
+        FusedGate &f = out[G];
+        f.k = 0;
+        for (int q = 0; q < 64; ++q) if ((sm >> q) & 1) f.q[f.k++] = q;
+        const int D = 1 << f.k;
+        f.U.assign((size_t)2 * D * D, 0.0);
+        for (int i = 0; i < D; ++i) f.U[(size_t)2 * (i * D + i)] = 1.0;
+        for (size_t i : members[G]) left_multiply_embedded(f.U, f.k, f.q, g[i]);
+    }
+}
+
+// ------------------------------------------------------------------ schedule
+
+void schedule(int n, int m, const std::vector<GateRef> &g, std::vector<int> &pi,
+              std::vector<Op> &ops) {
+    const int nl = n - m;
+    if ((int)pi.size() != n) {
+        pi.resize(n);
+        for (int q = 0; q < n; ++q) pi[q] = n - 1 - q;     // logical q <-> bit n-1-q (C1)
+    }
+    std::vector<int> inv(n);
+    for (int q = 0; q < n; ++q) inv[pi[q]] = q;
+    ops.clear();
+    // next_use[i][q] computed lazily: for each qubit, list of gate indices using it
+    std::vector<std::vector<uint32_t>> uses(n);
+    for (size_t i = 0; i < g.size(); ++i)
+        for (int j = 0; j < g[i].k; ++j) uses[g[i].q[j]].push_back((uint32_t)i);
+    std::vector<size_t> cursor(n, 0);
+    auto next_use = [&](int q, size_t after) -> size_t {
+        auto &u = uses[q];
+        size_t &c = cursor[q];
+        while (c < u.size() && u[c] <= after) ++c;
+        return c < u.size() ? u[c] : std::numeric_limits<size_t>::max();
+    };
+    for (size_t i = 0; i < g.size(); ++i) {
+        const GateRef &gt = g[i];
+        if (m > 0) {
+            uint64_t Q = qmask(gt);
+            int need[6], nneed = 0;
+            for (int j = 0; j < gt.k; ++j)
+                if (pi[gt.q[j]] >= nl) need[nneed++] = gt.q[j];
+            if (nneed > 0) {
+                // choose evictees: local logical qubits not in Q, furthest next use;
+                // ties broken toward higher physical bit (fewer permutes).
+                std::vector<std::pair<size_t, int>> cand;   // (next use, -physbit)
+                for (int p = 0; p < nl; ++p) {
+                    const int q = inv[p];
+                    if ((Q >> q) & 1) continue;
+                    cand.push_back({next_use(q, i), p});
+                }
+                std::sort(cand.begin(), cand.end(), [](const auto &a, const auto &b) {
+                    if (a.first != b.first) return a.first > b.first;
+                    return a.second > b.second;
+                });
+                int ev[6];
+                for (int t = 0; t < nneed; ++t) ev[t] = inv[cand[t].second];
+                // bring evictees to the top nneed local bits [nl-nneed, nl)
+                Op perm{OP_PERMUTE, -1, 0, {0}};
+                // evictees already in the top slots stay; others swap into free top slots
+                bool in_top[6] = {false, false, false, false, false, false};
+                int slot_used[6] = {0, 0, 0, 0, 0, 0};
+                for (int t = 0; t < nneed; ++t) {
+                    const int p = pi[ev[t]];
+                    if (p >= nl - nneed) { in_top[t] = true; slot_used[p - (nl - nneed)] = 1; }
+                }
+                for (int t = 0; t < nneed; ++t) {
+                    if (in_top[t]) continue;
+                    int s = 0;
+                    while (slot_used[s]) ++s;
+                    slot_used[s] = 1;
+                    const int a = pi[ev[t]], b = nl - nneed + s;
+                    perm.bits[2 * perm.nbits] = a;
+                    perm.bits[2 * perm.nbits + 1] = b;
+                    perm.nbits++;
+                    const int qa = inv[a], qb = inv[b];
+                    std::swap(pi[qa], pi[qb]);
+                    inv[a] = qb; inv[b] = qa;
+                }
+                if (perm.nbits > 0) ops.push_back(perm);
+                // swap global bits of `need` with the top local bits; pair the
+                // lowest global bit with the lowest top-local bit, etc.
+                int gb[6];
+                for (int t = 0; t < nneed; ++t) gb[t] = pi[need[t]];
+                std::sort(gb, gb + nneed);
+                Op rem{OP_REMAP, -1, nneed, {0}};
+                for (int t = 0; t < nneed; ++t) {
+                    const int a = gb[t], b = nl - nneed + t;
+                    rem.bits[2 * t] = a;
+                    rem.bits[2 * t + 1] = b;
+                    const int qa = inv[a], qb = inv[b];
+                    std::swap(pi[qa], pi[qb]);
+                    inv[a] = qb; inv[b] = qa;
+                }
+                ops.push_back(rem);
+            }
+        }
+        Op ap{OP_APPLY, (int)i, gt.k, {0}};
+        for (int j = 0; j < gt.k; ++j) ap.bits[j] = pi[gt.q[j]];
+        ops.push_back(ap);
+    }
+}
+
+}  // namespace hq
+
+// ------------------------------------------------------------------ C ABI
+
+using namespace hq;
+
+static hq_status to_refs(const hq_gate *in, size_t ng, int n, std::vector<GateRef> &out) {
+    out.resize(ng);
+    for (size_t i = 0; i < ng; ++i) {
+        const hq_gate &x = in[i];
+        if (x.k < 1 || x.k > 6) return set_error(HQ_ERR_K, "gate %zu: k=%d not in [1,6]", i, x.k);
+        if (!x.U) return set_error(HQ_ERR_ARG, "gate %zu: U is NULL", i);
+        GateRef &r = out[i];
+        r.k = x.k;
+        r.U = x.U;
+        for (int j = 0; j < x.k; ++j) {
+            const int q = x.qubits[j];
+            if (q < 0 || q >= n) return set_error(HQ_ERR_QUBIT, "gate %zu: qubit %d not in [0,%d)", i, q, n);
+            for (int l = 0; l < j; ++l)
+                if (x.qubits[l] == q) return set_error(HQ_ERR_DUP_QUBIT, "gate %zu: repeated qubit %d", i, q);
+            r.q[j] = q;
+        }
+    }
+    return HQ_OK;
+}
+
+extern "C" hq_status hq_fuse_plan(const hq_gate *in, size_t ngates, int kmax, int32_t *group_of,
+                                  size_t *ngroups) {
+    clear_error();
+    if ((!in && ngates) || !ngroups || (!group_of && ngates)) return set_error(HQ_ERR_ARG, "NULL argument");
+    if (kmax < 1 || kmax > 6) return set_error(HQ_ERR_K, "kmax=%d not in [1,6]", kmax);
+    std::vector<GateRef> refs;
+    hq_status st = to_refs(in, ngates, 64, refs);
+    if (st) return st;
+    for (size_t i = 0; i < ngates; ++i)
+        if (refs[i].k > kmax) return set_error(HQ_ERR_K, "gate %zu wider (%d) than kmax=%d", i, refs[i].k, kmax);
+    std::vector<int32_t> go;
+    *ngroups = fuse_groups(refs, kmax, go);
+    if (ngates) std::memcpy(group_of, go.data(), sizeof(int32_t) * ngates);
+    return HQ_OK;
+}
+
+extern "C" hq_status hq_fuse(const hq_gate *in, size_t ngates, int kmax, hq_gate **out,
+                             size_t *nout) {
+    clear_error();
+    if ((!in && ngates) || !out || !nout) return set_error(HQ_ERR_ARG, "NULL argument");
+    if (kmax < 1 || kmax > 6) return set_error(HQ_ERR_K, "kmax=%d not in [1,6]", kmax);
+    std::vector<GateRef> refs;
+    hq_status st = to_refs(in, ngates, 64, refs);
+    if (st) return st;
+    for (size_t i = 0; i < ngates; ++i)
+        if (refs[i].k > kmax) return set_error(HQ_ERR_K, "gate %zu wider (%d) than kmax=%d", i, refs[i].k, kmax);
+    std::vector<FusedGate> fused;
+    try {
+        fuse_build(refs, kmax, fused);
+    } catch (const std::bad_alloc &) {
+        return set_error(HQ_ERR_OOM, "host allocation failed in hq_fuse");
+    }
+    hq_gate *arr = new (std::nothrow) hq_gate[fused.size() ? fused.size() : 1];
+    if (!arr) return set_error(HQ_ERR_OOM, "host allocation failed");
+    for (size_t G = 0; G < fused.size(); ++G) {
+        arr[G].k = fused[G].k;
+        for (int j = 0; j < 6; ++j) arr[G].qubits[j] = j < fused[G].k ? fused[G].q[j] : -1;
+        double *U = new (std::nothrow) double[fused[G].U.size()];
+        if (!U) {
+            for (size_t t = 0; t < G; ++t) delete[] arr[t].U;
+            delete[] arr;
+            return set_error(HQ_ERR_OOM, "host allocation failed");
+        }
+        std::memcpy(U, fused[G].U.data(), sizeof(double) * fused[G].U.size());
+        arr[G].U = U;
+    }
+    *out = arr;
+    *nout = fused.size();
+    return HQ_OK;
+}
+
+extern "C" hq_status hq_free_gates(hq_gate *gates, size_t ngates) {
+    if (!gates) return HQ_OK;
+    for (size_t i = 0; i < ngates; ++i) delete[] gates[i].U;
+    delete[] gates;
+    return HQ_OK;
+}
+
+extern "C" hq_status hq_schedule(int n, int m, const hq_gate *gates, size_t ngates, hq_op **ops,
+                                 size_t *nops, int32_t *pi_out) {
+    clear_error();
+    if ((!gates && ngates) || !ops || !nops) return set_error(HQ_ERR_ARG, "NULL argument");
+    if (n < 1 || n > 63 || m < 0 || m > 16) return set_error(HQ_ERR_ARG, "bad n=%d / m=%d", n, m);
+    if (m > 0 && n - m < 6) return set_error(HQ_ERR_NGPUS, "n - m = %d < 6", n - m);
+    std::vector<GateRef> refs;
+    hq_status st = to_refs(gates, ngates, n, refs);
+    if (st) return st;
+    for (size_t i = 0; i < ngates; ++i)
+        if (refs[i].k > n - m) return set_error(HQ_ERR_K, "gate %zu: k=%d > local qubits %d", i, refs[i].k, n - m);
+    std::vector<int> pi;
+    std::vector<Op> v;
+    schedule(n, m, refs, pi, v);
+    hq_op *arr = new (std::nothrow) hq_op[v.size() ? v.size() : 1];
+    if (!arr) return set_error(HQ_ERR_OOM, "host allocation failed");
+    for (size_t i = 0; i < v.size(); ++i) {
+        arr[i].kind = v[i].kind;
+        arr[i].gate = v[i].gate;
+        arr[i].nbits = v[i].nbits;
+        for (int t = 0; t < 12; ++t) arr[i].bits[t] = v[i].bits[t];
+    }
+    *ops = arr;
+    *nops = v.size();
+    if (pi_out) for (int q = 0; q < n; ++q) pi_out[q] = pi[q];
+    return HQ_OK;
+}
+
+extern "C" hq_status hq_free_ops(hq_op *ops) {
+    delete[] ops;
+    return HQ_OK;
+}

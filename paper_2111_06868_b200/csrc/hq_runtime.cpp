@@ -1,0 +1,959 @@
+// C-ABI runtime: state objects, validation, the op-stream executor (apply /
+// remap / permute), norm and amplitude I/O.  See include/hq.h for the
+// contract of every exported function.
+//
+// Layout in HBM: each rank r holds physical indices
+// [r 2^(n_l), (r+1) 2^(n_l)) of the 2^n amplitudes as one contiguous array of
+// interleaved complex (float2 for HQ_C64, double2 for HQ_C128), 256-byte
+// aligned.  The logical->physical qubit map pi starts as q -> n-1-q (so the
+// physical index equals the logical index, reading C1) and changes only when
+// the distributed schedule remaps global qubits.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <new>
+#include <vector>
+
+#include "hq_internal.h"
+
+namespace hq {
+
+static thread_local std::string g_err;
+
+hq_status set_error(hq_status st, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+
+void clear_error() { g_err.clear(); }
+
+}  // namespace hq
+
+using namespace hq;
+
+#define CUDA_TRY(expr)                                                                  \
+    do {                                                                                \
+        cudaError_t _e = (expr);                                                        \
+        if (_e != cudaSuccess)                                                          \
+            return set_error(_e == cudaErrorMemoryAllocation ? HQ_ERR_OOM : HQ_ERR_CUDA, \
+                             "%s: %s (%s:%d)", #expr, cudaGetErrorString(_e), __FILE__,  \
+                             __LINE__);                                                 \
+    } while (0)
+
+#define NCCL_TRY(expr)                                                                   \
+    do {                                                                                 \
+        ncclResult_t _r = (expr);                                                        \
+        if (_r != ncclSuccess)                                                           \
+            return set_error(HQ_ERR_NCCL, "%s: %s (%s:%d)", #expr, ncclGetErrorString(_r), \
+                             __FILE__, __LINE__);                                        \
+    } while (0)
+
+enum Mode { MODE_SINGLE = 0, MODE_RANK = 1, MODE_VIRTUAL = 2, MODE_MULTI = 3 };
+
+// Device staging area for gate matrices (generic kernels read U from HBM).
+struct Arena {
+    char *dev = nullptr;
+    char *host = nullptr;   // pinned
+    size_t cap = 0, off = 0;
+};
+
+struct Shard {
+    int device = 0;
+    int rank = 0;
+    void *psi = nullptr;
+    void *buf = nullptr;          // receive / permute scratch (G > 1)
+    bool own_psi = true;
+    bool own_buf = true;
+    cudaStream_t stream = nullptr;
+    bool own_stream = true;
+    ncclComm_t comm = nullptr;
+    double *d_part = nullptr;     // norm partials
+    double *h_part = nullptr;     // pinned
+    Arena arena;
+};
+
+struct ProfEvent {
+    cudaEvent_t a, b;
+    uint64_t bytes;
+};
+
+struct hq_state {
+    int n = 0, m = 0, nl = 0;
+    hq_dtype dtype = HQ_C64;
+    size_t es = 8;
+    int world = 1;
+    int mode = MODE_SINGLE;
+    std::vector<Shard> sh;
+    std::vector<int> pi;          // logical qubit -> physical bit
+    hq_stats stats{};
+    bool profiling = false;
+    std::vector<ProfEvent> prof;  // pending
+    std::vector<cudaEvent_t> ev_pool;
+    uint64_t prof_count = 0;
+    double prof_total = 0, prof_max = 0;
+    uint64_t prof_bytes = 0;
+};
+
+struct hq_circuit {
+    hq_state *owner = nullptr;
+    std::vector<int> pi_start, pi_end;
+    std::vector<Op> ops;
+    std::vector<int> op_uoff;              // per APPLY op: element offset into U buffers
+    std::vector<ApplyDesc> desc;           // per op (APPLY)
+    std::vector<std::vector<char>> host_U; // per APPLY op: canonical U in dtype
+    std::vector<char *> dev_U;             // per shard: all U's
+    uint64_t passes = 0, remaps = 0, permutes = 0;
+};
+
+// ------------------------------------------------------------------ helpers
+
+static int ilog2(int x) {
+    int l = 0;
+    while ((1 << l) < x) ++l;
+    return l;
+}
+
+static hq_status arena_init(Shard &s, size_t cap) {
+    CUDA_TRY(cudaSetDevice(s.device));
+    CUDA_TRY(cudaMalloc((void **)&s.arena.dev, cap));
+    CUDA_TRY(cudaMallocHost((void **)&s.arena.host, cap));
+    s.arena.cap = cap;
+    s.arena.off = 0;
+    return HQ_OK;
+}
+
+// Copy `bytes` of host data to the device arena (stream-ordered); returns the
+// device pointer.  When full, synchronise the stream and restart.
+static hq_status arena_push(Shard &s, const void *src, size_t bytes, void **dev_out) {
+    const size_t a = (bytes + 255) & ~(size_t)255;
+    if (a > s.arena.cap) return set_error(HQ_ERR_ARG, "matrix larger than staging arena");
+    if (s.arena.off + a > s.arena.cap) {
+        CUDA_TRY(cudaStreamSynchronize(s.stream));
+        s.arena.off = 0;
+    }
+    memcpy(s.arena.host + s.arena.off, src, bytes);
+    CUDA_TRY(cudaMemcpyAsync(s.arena.dev + s.arena.off, s.arena.host + s.arena.off, bytes,
+                             cudaMemcpyHostToDevice, s.stream));
+    *dev_out = s.arena.dev + s.arena.off;
+    s.arena.off += a;
+    return HQ_OK;
+}
+
+static hq_status shard_alloc(hq_state *st, Shard &s, bool need_buf, bool make_stream) {
+    CUDA_TRY(cudaSetDevice(s.device));
+    const size_t bytes = st->es << st->nl;
+    if (make_stream) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+        s.own_stream = true;
+    }
+    if (!s.psi) {
+        cudaError_t e = cudaMalloc(&s.psi, bytes);
+        if (e != cudaSuccess) {
+            s.psi = nullptr;
+            return set_error(HQ_ERR_OOM, "cudaMalloc(%zu) for the state shard failed: %s", bytes,
+                             cudaGetErrorString(e));
+        }
+        s.own_psi = true;
+    }
+    if (need_buf && !s.buf) {
+        cudaError_t e = cudaMalloc(&s.buf, bytes);
+        if (e != cudaSuccess) {
+            s.buf = nullptr;
+            return set_error(HQ_ERR_OOM, "cudaMalloc(%zu) for the exchange buffer failed: %s",
+                             bytes, cudaGetErrorString(e));
+        }
+        s.own_buf = true;
+    }
+    CUDA_TRY(cudaMalloc((void **)&s.d_part, sizeof(double) * 148 * 16));
+    CUDA_TRY(cudaMallocHost((void **)&s.h_part, sizeof(double) * 148 * 16));
+    return arena_init(s, (size_t)16 << 20);
+}
+
+static void shard_free(Shard &s) {
+    cudaSetDevice(s.device);
+    if (s.stream) cudaStreamSynchronize(s.stream);
+    if (s.own_psi && s.psi) cudaFree(s.psi);
+    if (s.own_buf && s.buf) cudaFree(s.buf);
+    if (s.d_part) cudaFree(s.d_part);
+    if (s.h_part) cudaFreeHost(s.h_part);
+    if (s.arena.dev) cudaFree(s.arena.dev);
+    if (s.arena.host) cudaFreeHost(s.arena.host);
+    if (s.comm) ncclCommDestroy(s.comm);
+    if (s.own_stream && s.stream) cudaStreamDestroy(s.stream);
+    s = Shard{};
+}
+
+static hq_status check_device() {
+    int cnt = 0;
+    cudaError_t e = cudaGetDeviceCount(&cnt);
+    if (e != cudaSuccess || cnt == 0)
+        return set_error(HQ_ERR_NO_DEVICE,
+                         "no CUDA device visible (%s); this library has no CPU fallback",
+                         e == cudaSuccess ? "count 0" : cudaGetErrorString(e));
+    return HQ_OK;
+}
+
+static hq_state *new_state(int n, hq_dtype dtype, int world) {
+    hq_state *st = new (std::nothrow) hq_state();
+    if (!st) return nullptr;
+    st->n = n;
+    st->dtype = dtype;
+    st->es = dtype == HQ_C64 ? 8 : 16;
+    st->world = world;
+    st->m = ilog2(world);
+    st->nl = n - st->m;
+    st->pi.resize(n);
+    for (int q = 0; q < n; ++q) st->pi[q] = n - 1 - q;
+    return st;
+}
+
+static hq_status validate_common(int n, hq_dtype dtype, int G) {
+    if (n < 1 || n > 40) return set_error(HQ_ERR_ARG, "n=%d not in [1,40]", n);
+    if (dtype != HQ_C64 && dtype != HQ_C128) return set_error(HQ_ERR_ARG, "bad dtype %d", (int)dtype);
+    if (G < 1 || (G & (G - 1))) return set_error(HQ_ERR_NGPUS, "G=%d is not a power of two", G);
+    if (G > 1 && n - ilog2(G) < 6)
+        return set_error(HQ_ERR_NGPUS, "n - log2(G) = %d < 6 local qubits", n - ilog2(G));
+    return HQ_OK;
+}
+
+// ------------------------------------------------------------------ create / destroy
+
+extern "C" hq_status hq_state_create(int n, hq_dtype dtype, int ngpus, hq_state **out) {
+    clear_error();
+    if (!out) return set_error(HQ_ERR_ARG, "out is NULL");
+    *out = nullptr;
+    hq_status rc = validate_common(n, dtype, ngpus);
+    if (rc) return rc;
+    if ((rc = check_device())) return rc;
+    int cnt = 0;
+    CUDA_TRY(cudaGetDeviceCount(&cnt));
+    if (ngpus > cnt) return set_error(HQ_ERR_NGPUS, "ngpus=%d > %d visible devices", ngpus, cnt);
+    hq_state *st = new_state(n, dtype, ngpus);
+    if (!st) return set_error(HQ_ERR_OOM, "host allocation failed");
+    st->mode = ngpus == 1 ? MODE_SINGLE : MODE_MULTI;
+    st->sh.resize(ngpus);
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (int r = 0; r < ngpus; ++r) {
+        st->sh[r].device = ngpus == 1 ? cur : r;
+        st->sh[r].rank = r;
+        if ((rc = shard_alloc(st, st->sh[r], ngpus > 1, true))) {
+            for (auto &s : st->sh) shard_free(s);
+            delete st;
+            return rc;
+        }
+    }
+    if (ngpus > 1) {
+        std::vector<ncclComm_t> comms(ngpus);
+        std::vector<int> devs(ngpus);
+        for (int r = 0; r < ngpus; ++r) devs[r] = r;
+        ncclResult_t nr = ncclCommInitAll(comms.data(), ngpus, devs.data());
+        if (nr != ncclSuccess) {
+            for (auto &s : st->sh) shard_free(s);
+            delete st;
+            return set_error(HQ_ERR_NCCL, "ncclCommInitAll: %s", ncclGetErrorString(nr));
+        }
+        for (int r = 0; r < ngpus; ++r) st->sh[r].comm = comms[r];
+    }
+    cudaSetDevice(cur);
+    *out = st;
+    return HQ_OK;
+}
+
+extern "C" hq_status hq_nccl_unique_id(void *out128) {
+    clear_error();
+    if (!out128) return set_error(HQ_ERR_ARG, "out is NULL");
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId id;
+    NCCL_TRY(ncclGetUniqueId(&id));
+    memcpy(out128, &id, sizeof id);
+    return HQ_OK;
+}
+
+extern "C" hq_status hq_state_create_rank(int n, hq_dtype dtype, int world_size, int rank,
+                                          int device, const void *nccl_id, hq_state **out) {
+    clear_error();
+    if (!out) return set_error(HQ_ERR_ARG, "out is NULL");
+    *out = nullptr;
+    hq_status rc = validate_common(n, dtype, world_size);
+    if (rc) return rc;
+    if (rank < 0 || rank >= world_size) return set_error(HQ_ERR_ARG, "rank %d not in [0,%d)", rank, world_size);
+    if (world_size > 1 && !nccl_id) return set_error(HQ_ERR_ARG, "nccl_id is NULL");
+    if ((rc = check_device())) return rc;
+    hq_state *st = new_state(n, dtype, world_size);
+    if (!st) return set_error(HQ_ERR_OOM, "host allocation failed");
+    st->mode = world_size == 1 ? MODE_SINGLE : MODE_RANK;
+    st->sh.resize(1);
+    st->sh[0].device = device;
+    st->sh[0].rank = rank;
+    if ((rc = shard_alloc(st, st->sh[0], world_size > 1, true))) {
+        shard_free(st->sh[0]);
+        delete st;
+        return rc;
+    }
+    if (world_size > 1) {
+        ncclUniqueId id;
+        memcpy(&id, nccl_id, sizeof id);
+        cudaSetDevice(device);
+        ncclResult_t nr = ncclCommInitRank(&st->sh[0].comm, world_size, id, rank);
+        if (nr != ncclSuccess) {
+            shard_free(st->sh[0]);
+            delete st;
+            return set_error(HQ_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(nr));
+        }
+    }
+    *out = st;
+    return HQ_OK;
+}
+
+extern "C" hq_status hq_state_create_virtual(int n, hq_dtype dtype, int nshards, hq_state **out) {
+    clear_error();
+    if (!out) return set_error(HQ_ERR_ARG, "out is NULL");
+    *out = nullptr;
+    hq_status rc = validate_common(n, dtype, nshards);
+    if (rc) return rc;
+    if ((rc = check_device())) return rc;
+    hq_state *st = new_state(n, dtype, nshards);
+    if (!st) return set_error(HQ_ERR_OOM, "host allocation failed");
+    st->mode = MODE_VIRTUAL;
+    st->sh.resize(nshards);
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (int r = 0; r < nshards; ++r) {
+        st->sh[r].device = cur;
+        st->sh[r].rank = r;
+        const bool mk = r == 0;
+        if (!mk) { st->sh[r].stream = st->sh[0].stream; st->sh[r].own_stream = false; }
+        if ((rc = shard_alloc(st, st->sh[r], nshards > 1, mk))) {
+            for (auto &s : st->sh) shard_free(s);
+            delete st;
+            return rc;
+        }
+    }
+    *out = st;
+    return HQ_OK;
+}
+
+extern "C" hq_status hq_state_create_from_buffers(int n, hq_dtype dtype, void *psi_device,
+                                                  void *stream, hq_state **out) {
+    clear_error();
+    if (!out || !psi_device) return set_error(HQ_ERR_ARG, "NULL argument");
+    *out = nullptr;
+    hq_status rc = validate_common(n, dtype, 1);
+    if (rc) return rc;
+    if ((rc = check_device())) return rc;
+    if (((uintptr_t)psi_device) & 15) return set_error(HQ_ERR_ARG, "psi buffer not 16-byte aligned");
+    cudaPointerAttributes at;
+    CUDA_TRY(cudaPointerGetAttributes(&at, psi_device));
+    if (at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged)
+        return set_error(HQ_ERR_ARG, "psi is not device memory");
+    hq_state *st = new_state(n, dtype, 1);
+    if (!st) return set_error(HQ_ERR_OOM, "host allocation failed");
+    st->mode = MODE_SINGLE;
+    st->sh.resize(1);
+    Shard &s = st->sh[0];
+    s.device = at.device;
+    s.psi = psi_device;
+    s.own_psi = false;
+    s.stream = reinterpret_cast<cudaStream_t>(stream);
+    s.own_stream = false;
+    if ((rc = shard_alloc(st, s, false, false))) {
+        shard_free(s);
+        delete st;
+        return rc;
+    }
+    *out = st;
+    return HQ_OK;
+}
+
+extern "C" hq_status hq_state_destroy(hq_state *st) {
+    clear_error();
+    if (!st) return HQ_OK;
+    for (auto &p : st->prof) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
+    for (auto e : st->ev_pool) cudaEventDestroy(e);
+    // virtual shards share shard 0's stream: free others first
+    for (size_t i = st->sh.size(); i-- > 0;) shard_free(st->sh[i]);
+    delete st;
+    return HQ_OK;
+}
+
+extern "C" hq_status hq_state_set_stream(hq_state *st, void *stream) {
+    clear_error();
+    if (!st) return set_error(HQ_ERR_ARG, "state is NULL");
+    if (st->mode == MODE_MULTI) return set_error(HQ_ERR_STATE, "set_stream not supported for multi-device states");
+    Shard &s0 = st->sh[0];
+    CUDA_TRY(cudaSetDevice(s0.device));
+    if (s0.stream) CUDA_TRY(cudaStreamSynchronize(s0.stream));
+    if (s0.own_stream && s0.stream) cudaStreamDestroy(s0.stream);
+    for (auto &s : st->sh) {
+        s.stream = reinterpret_cast<cudaStream_t>(stream);
+        s.own_stream = false;
+    }
+    return HQ_OK;
+}
+
+extern "C" hq_status hq_state_info(const hq_state *st, int *n, int *dtype, int *world,
+                                   int *local_shards, int *first_rank) {
+    clear_error();
+    if (!st) return set_error(HQ_ERR_ARG, "state is NULL");
+    if (n) *n = st->n;
+    if (dtype) *dtype = (int)st->dtype;
+    if (world) *world = st->world;
+    if (local_shards) *local_shards = (int)st->sh.size();
+    if (first_rank) *first_rank = st->sh[0].rank;
+    return HQ_OK;
+}
+
+// ------------------------------------------------------------------ executor
+
+// Canonicalise: sort targets by physical bit ascending and permute U so that
+// U-index bit i <-> i-th smallest target (exact), then round fp64 -> dtype.
+static void canonical_U(hq_dtype dt, const double *U, int k, const int *phys, ApplyDesc &d,
+                        std::vector<char> &out, int nl) {
+    int order[6];
+    for (int j = 0; j < k; ++j) order[j] = j;
+    std::sort(order, order + k, [&](int a, int b) { return phys[a] < phys[b]; });
+    d.k = k;
+    d.n_local = nl;
+    for (int i = 0; i < k; ++i) d.p[i] = phys[order[i]];
+    // canonical bit i corresponds to user target order[i], whose user U bit is k-1-order[i]
+    const int D = 1 << k;
+    std::vector<int> map(D);
+    for (int c = 0; c < D; ++c) {
+        int u = 0;
+        for (int i = 0; i < k; ++i)
+            if ((c >> i) & 1) u |= 1 << (k - 1 - order[i]);
+        map[c] = u;
+    }
+    const size_t es = dt == HQ_C64 ? 8 : 16;
+    out.resize(es * D * D);
+    for (int r = 0; r < D; ++r)
+        for (int c = 0; c < D; ++c) {
+            const double re = U[2 * (map[r] * D + map[c])];
+            const double im = U[2 * (map[r] * D + map[c]) + 1];
+            if (dt == HQ_C64) {
+                float *o = reinterpret_cast<float *>(out.data()) + 2 * (r * D + c);
+                o[0] = (float)re;
+                o[1] = (float)im;
+            } else {
+                double *o = reinterpret_cast<double *>(out.data()) + 2 * (r * D + c);
+                o[0] = re;
+                o[1] = im;
+            }
+        }
+}
+
+static hq_status prof_begin(hq_state *st, Shard &s, ProfEvent &pe) {
+    if (!st->profiling) return HQ_OK;
+    auto take = [&]() {
+        cudaEvent_t e;
+        if (!st->ev_pool.empty()) { e = st->ev_pool.back(); st->ev_pool.pop_back(); }
+        else cudaEventCreate(&e);
+        return e;
+    };
+    pe.a = take();
+    pe.b = take();
+    CUDA_TRY(cudaEventRecord(pe.a, s.stream));
+    return HQ_OK;
+}
+
+static hq_status prof_end(hq_state *st, Shard &s, ProfEvent &pe, uint64_t bytes) {
+    if (!st->profiling) return HQ_OK;
+    CUDA_TRY(cudaEventRecord(pe.b, s.stream));
+    pe.bytes = bytes;
+    st->prof.push_back(pe);
+    return HQ_OK;
+}
+
+static hq_status exec_apply(hq_state *st, Shard &s, const ApplyDesc &d, const void *hU,
+                            const void *dU) {
+    CUDA_TRY(cudaSetDevice(s.device));
+    ProfEvent pe{};
+    hq_status rc = prof_begin(st, s, pe);
+    if (rc) return rc;
+    int launches = 0;
+    int e = launch_apply((int)st->dtype, s.psi, d, hU, dU, s.stream, &launches);
+    if (e != cudaSuccess)
+        return set_error(HQ_ERR_CUDA, "apply kernel launch failed: %s", cudaGetErrorString((cudaError_t)e));
+    const uint64_t bytes = (uint64_t)2 * (st->es << st->nl);
+    if ((rc = prof_end(st, s, pe, bytes))) return rc;
+    st->stats.passes++;
+    st->stats.kernel_launches += launches;
+    st->stats.hbm_bytes += bytes;
+    return HQ_OK;
+}
+
+static hq_status exec_permute(hq_state *st, const Op &op) {
+    int a[6], b[6];
+    for (int i = 0; i < op.nbits; ++i) { a[i] = op.bits[2 * i]; b[i] = op.bits[2 * i + 1]; }
+    for (auto &s : st->sh) {
+        CUDA_TRY(cudaSetDevice(s.device));
+        int e = launch_permute((int)st->dtype, s.psi, s.buf, 1ull << st->nl, op.nbits, a, b, s.stream);
+        if (e != cudaSuccess)
+            return set_error(HQ_ERR_CUDA, "permute launch failed: %s", cudaGetErrorString((cudaError_t)e));
+        std::swap(s.psi, s.buf);
+        std::swap(s.own_psi, s.own_buf);
+        st->stats.kernel_launches++;
+        st->stats.hbm_bytes += (uint64_t)2 * (st->es << st->nl);
+    }
+    st->stats.permutes++;
+    return HQ_OK;
+}
+
+// REMAP: swap global bits g_i with local bits l_i = nl - m' + i (top local
+// bits).  Rank r's chunk t (top m' local bits = t) goes to the peer p whose
+// swapped rank bits equal t, landing in p's chunk whose index is r's swapped
+// rank bits.  Symmetric: for each peer p in the exchange group, send chunk
+// bits(p) and receive into chunk bits(p).
+static hq_status exec_remap(hq_state *st, const Op &op) {
+    const int mp = op.nbits;
+    int gsh[6];
+    for (int i = 0; i < mp; ++i) {
+        gsh[i] = op.bits[2 * i] - st->nl;               // rank bit
+        if (op.bits[2 * i + 1] != st->nl - mp + i)
+            return set_error(HQ_ERR_STATE, "internal: remap local bit is not a top bit");
+    }
+    const uint64_t chunk = 1ull << (st->nl - mp);       // amplitudes per chunk
+    const size_t cbytes = chunk * st->es;
+    auto bits_of = [&](int r) {
+        int t = 0;
+        for (int i = 0; i < mp; ++i) t |= ((r >> gsh[i]) & 1) << i;
+        return t;
+    };
+    auto peer_of = [&](int r, int t) {
+        int p = r;
+        for (int i = 0; i < mp; ++i) p = (p & ~(1 << gsh[i])) | (((t >> i) & 1) << gsh[i]);
+        return p;
+    };
+    if (st->mode == MODE_VIRTUAL) {
+        for (auto &s : st->sh) {
+            for (int t = 0; t < (1 << mp); ++t) {
+                const int p = peer_of(s.rank, t);
+                Shard &d = st->sh[p];
+                char *src = (char *)s.psi + (size_t)t * cbytes;
+                char *dst = (char *)d.buf + (size_t)bits_of(s.rank) * cbytes;
+                CUDA_TRY(cudaMemcpyAsync(dst, src, cbytes, cudaMemcpyDeviceToDevice, s.stream));
+                if (p != s.rank) st->stats.link_bytes += cbytes;
+            }
+        }
+    } else {
+        NCCL_TRY(ncclGroupStart());
+        for (auto &s : st->sh) {
+            cudaSetDevice(s.device);
+            for (int t = 0; t < (1 << mp); ++t) {
+                const int p = peer_of(s.rank, t);
+                char *src = (char *)s.psi + (size_t)t * cbytes;
+                char *dst = (char *)s.buf + (size_t)t * cbytes;   // from p: chunk bits(p) == t
+                if (p == s.rank) {
+                    CUDA_TRY(cudaMemcpyAsync(dst, src, cbytes, cudaMemcpyDeviceToDevice, s.stream));
+                } else {
+                    NCCL_TRY(ncclSend(src, cbytes, ncclChar, p, s.comm, s.stream));
+                    NCCL_TRY(ncclRecv(dst, cbytes, ncclChar, p, s.comm, s.stream));
+                    st->stats.link_bytes += cbytes;
+                }
+            }
+        }
+        NCCL_TRY(ncclGroupEnd());
+    }
+    for (auto &s : st->sh) {
+        std::swap(s.psi, s.buf);
+        std::swap(s.own_psi, s.own_buf);
+    }
+    st->stats.remaps++;
+    return HQ_OK;
+}
+
+static hq_status validate_gates(const hq_state *st, const hq_gate *g, size_t ng,
+                                std::vector<GateRef> &refs) {
+    refs.resize(ng);
+    for (size_t i = 0; i < ng; ++i) {
+        const hq_gate &x = g[i];
+        if (x.k < 1 || x.k > 6) return set_error(HQ_ERR_K, "gate %zu: k=%d not in [1,6]", i, x.k);
+        if (x.k > st->nl)
+            return set_error(HQ_ERR_K, "gate %zu: k=%d > %d local qubits", i, x.k, st->nl);
+        if (!x.U) return set_error(HQ_ERR_ARG, "gate %zu: U is NULL", i);
+        refs[i].k = x.k;
+        refs[i].U = x.U;
+        for (int j = 0; j < x.k; ++j) {
+            const int q = x.qubits[j];
+            if (q < 0 || q >= st->n)
+                return set_error(HQ_ERR_QUBIT, "gate %zu: qubit %d not in [0,%d)", i, q, st->n);
+            for (int l = 0; l < j; ++l)
+                if (x.qubits[l] == q) return set_error(HQ_ERR_DUP_QUBIT, "gate %zu: repeated qubit %d", i, q);
+            refs[i].q[j] = q;
+        }
+    }
+    return HQ_OK;
+}
+
+// Run an op stream with matrices either host-side (converted on the fly and
+// staged through the arena) or precompiled (circuit).
+static hq_status run_ops(hq_state *st, const std::vector<GateRef> &refs, const std::vector<Op> &ops) {
+    std::vector<char> cu;
+    for (const Op &op : ops) {
+        hq_status rc = HQ_OK;
+        if (op.kind == OP_APPLY) {
+            const GateRef &g = refs[op.gate];
+            ApplyDesc d;
+            canonical_U(st->dtype, g.U, g.k, op.bits, d, cu, st->nl);
+            const bool need_dev = apply_needs_dev_U((int)st->dtype, d);
+            for (auto &s : st->sh) {
+                void *dU = nullptr;
+                if (need_dev && (rc = arena_push(s, cu.data(), cu.size(), &dU))) return rc;
+                if ((rc = exec_apply(st, s, d, cu.data(), dU))) return rc;
+            }
+        } else if (op.kind == OP_REMAP) {
+            rc = exec_remap(st, op);
+        } else {
+            rc = exec_permute(st, op);
+        }
+        if (rc) return rc;
+    }
+    return HQ_OK;
+}
+
+extern "C" hq_status hq_apply_matrix(hq_state *st, const double *U, const int32_t *qubits, int k) {
+    clear_error();
+    if (!st || !U || !qubits) return set_error(HQ_ERR_ARG, "NULL argument");
+    if (k < 1 || k > 6) return set_error(HQ_ERR_K, "k=%d not in [1,6]", k);
+    hq_gate g;
+    g.k = k;
+    for (int j = 0; j < 6; ++j) g.qubits[j] = j < k ? qubits[j] : -1;
+    g.U = U;
+    return hq_apply_circuit(st, &g, 1);
+}
+
+extern "C" hq_status hq_apply_circuit(hq_state *st, const hq_gate *gates, size_t ng) {
+    clear_error();
+    if (!st || (!gates && ng)) return set_error(HQ_ERR_ARG, "NULL argument");
+    std::vector<GateRef> refs;
+    hq_status rc = validate_gates(st, gates, ng, refs);
+    if (rc) return rc;
+    std::vector<Op> ops;
+    std::vector<int> pi = st->pi;
+    schedule(st->n, st->m, refs, pi, ops);
+    rc = run_ops(st, refs, ops);
+    if (rc) return rc;
+    st->pi = pi;
+    return HQ_OK;
+}
+
+// ------------------------------------------------------------------ circuits
+
+static hq_status circuit_compile(hq_state *st, hq_circuit *c, const std::vector<GateRef> &refs) {
+    c->pi_start = st->pi;
+    c->pi_end = st->pi;
+    schedule(st->n, st->m, refs, c->pi_end, c->ops);
+    c->desc.assign(c->ops.size(), ApplyDesc{});
+    c->host_U.assign(c->ops.size(), {});
+    c->op_uoff.assign(c->ops.size(), -1);
+    size_t total = 0;
+    c->passes = c->remaps = c->permutes = 0;
+    for (size_t i = 0; i < c->ops.size(); ++i) {
+        const Op &op = c->ops[i];
+        if (op.kind == OP_APPLY) {
+            const GateRef &g = refs[op.gate];
+            canonical_U(st->dtype, g.U, g.k, op.bits, c->desc[i], c->host_U[i], st->nl);
+            c->op_uoff[i] = (int)total;
+            total += (c->host_U[i].size() + 255) & ~(size_t)255;
+            c->passes++;
+        } else if (op.kind == OP_REMAP) {
+            c->remaps++;
+        } else {
+            c->permutes++;
+        }
+    }
+    for (char *p : c->dev_U) if (p) cudaFree(p);
+    c->dev_U.assign(st->sh.size(), nullptr);
+    if (total == 0) return HQ_OK;
+    std::vector<char> blob(total, 0);
+    for (size_t i = 0; i < c->ops.size(); ++i)
+        if (c->op_uoff[i] >= 0) memcpy(blob.data() + c->op_uoff[i], c->host_U[i].data(), c->host_U[i].size());
+    for (size_t r = 0; r < st->sh.size(); ++r) {
+        Shard &s = st->sh[r];
+        if (r > 0 && st->mode == MODE_VIRTUAL) { c->dev_U[r] = nullptr; continue; }
+        CUDA_TRY(cudaSetDevice(s.device));
+        CUDA_TRY(cudaMalloc((void **)&c->dev_U[r], total));
+        CUDA_TRY(cudaMemcpy(c->dev_U[r], blob.data(), total, cudaMemcpyHostToDevice));
+    }
+    return HQ_OK;
+}
+
+extern "C" hq_status hq_circuit_create(hq_state *st, const hq_gate *gates, size_t ng, hq_circuit **out) {
+    clear_error();
+    if (!st || !out || (!gates && ng)) return set_error(HQ_ERR_ARG, "NULL argument");
+    *out = nullptr;
+    std::vector<GateRef> refs;
+    hq_status rc = validate_gates(st, gates, ng, refs);
+    if (rc) return rc;
+    hq_circuit *c = new (std::nothrow) hq_circuit();
+    if (!c) return set_error(HQ_ERR_OOM, "host allocation failed");
+    c->owner = st;
+    if ((rc = circuit_compile(st, c, refs))) {
+        hq_circuit_destroy(c);
+        return rc;
+    }
+    *out = c;
+    return HQ_OK;
+}
+
+extern "C" hq_status hq_circuit_run(hq_state *st, hq_circuit *c) {
+    clear_error();
+    if (!st || !c) return set_error(HQ_ERR_ARG, "NULL argument");
+    if (c->owner != st) return set_error(HQ_ERR_STATE, "circuit was compiled for another state");
+    if (st->pi != c->pi_start)
+        return set_error(HQ_ERR_STATE, "state qubit layout differs from the one the circuit was compiled for");
+    for (size_t i = 0; i < c->ops.size(); ++i) {
+        const Op &op = c->ops[i];
+        hq_status rc = HQ_OK;
+        if (op.kind == OP_APPLY) {
+            for (size_t r = 0; r < st->sh.size(); ++r) {
+                const char *base = c->dev_U[st->mode == MODE_VIRTUAL ? 0 : r];
+                const void *dU = base ? base + c->op_uoff[i] : nullptr;
+                if ((rc = exec_apply(st, st->sh[r], c->desc[i], c->host_U[i].data(), dU))) return rc;
+            }
+        } else if (op.kind == OP_REMAP) {
+            rc = exec_remap(st, op);
+        } else {
+            rc = exec_permute(st, op);
+        }
+        if (rc) return rc;
+    }
+    st->pi = c->pi_end;
+    return HQ_OK;
+}
+
+extern "C" hq_status hq_circuit_info(const hq_circuit *c, uint64_t *passes, uint64_t *remaps,
+                                     uint64_t *permutes) {
+    clear_error();
+    if (!c) return set_error(HQ_ERR_ARG, "NULL circuit");
+    if (passes) *passes = c->passes;
+    if (remaps) *remaps = c->remaps;
+    if (permutes) *permutes = c->permutes;
+    return HQ_OK;
+}
+
+extern "C" hq_status hq_circuit_destroy(hq_circuit *c) {
+    if (!c) return HQ_OK;
+    for (size_t r = 0; r < c->dev_U.size(); ++r)
+        if (c->dev_U[r]) {
+            if (c->owner && r < c->owner->sh.size()) cudaSetDevice(c->owner->sh[r].device);
+            cudaFree(c->dev_U[r]);
+        }
+    delete c;
+    return HQ_OK;
+}
+
+// ------------------------------------------------------------------ state I/O
+
+static bool pi_identity(const hq_state *st) {
+    for (int q = 0; q < st->n; ++q)
+        if (st->pi[q] != st->n - 1 - q) return false;
+    return true;
+}
+
+// physical index of logical index i
+static uint64_t phys_of(const hq_state *st, uint64_t i) {
+    uint64_t p = 0;
+    for (int q = 0; q < st->n; ++q) p |= ((i >> (st->n - 1 - q)) & 1) << st->pi[q];
+    return p;
+}
+
+extern "C" hq_status hq_state_init_basis(hq_state *st, uint64_t x) {
+    clear_error();
+    if (!st) return set_error(HQ_ERR_ARG, "state is NULL");
+    if (st->n < 64 && x >= (1ull << st->n)) return set_error(HQ_ERR_RANGE, "basis index out of range");
+    // the whole state is overwritten: restore the canonical layout q -> n-1-q
+    for (int q = 0; q < st->n; ++q) st->pi[q] = st->n - 1 - q;
+    const uint64_t p = phys_of(st, x);
+    for (auto &s : st->sh) {
+        CUDA_TRY(cudaSetDevice(s.device));
+        const int64_t idx = (int)(p >> st->nl) == s.rank ? (int64_t)(p & ((1ull << st->nl) - 1)) : -1;
+        int e = launch_init_basis((int)st->dtype, s.psi, 1ull << st->nl, idx, s.stream);
+        if (e != cudaSuccess) return set_error(HQ_ERR_CUDA, "init launch: %s", cudaGetErrorString((cudaError_t)e));
+        st->stats.kernel_launches += idx >= 0 ? 1 : 0;
+    }
+    return HQ_OK;
+}
+
+static hq_status range_check(const hq_state *st, uint64_t first, uint64_t count) {
+    const uint64_t N = 1ull << st->n;
+    if (first > N || count > N - first) return set_error(HQ_ERR_RANGE, "amplitude range outside [0, 2^n)");
+    return HQ_OK;
+}
+
+static hq_status io_amplitudes(hq_state *st, uint64_t first, uint64_t count, void *host, bool get) {
+    hq_status rc = range_check(st, first, count);
+    if (rc) return rc;
+    if (count == 0) return HQ_OK;
+    const size_t es = st->es;
+    const bool ident = pi_identity(st);
+    std::vector<int> bitmap(st->n);
+    for (int q = 0; q < st->n; ++q) bitmap[st->n - 1 - q] = st->pi[q];
+    for (auto &s : st->sh) {
+        CUDA_TRY(cudaSetDevice(s.device));
+        if (ident) {
+            // logical == physical: contiguous intersection with this shard
+            const uint64_t lo = (uint64_t)s.rank << st->nl, hi = lo + (1ull << st->nl);
+            const uint64_t a = std::max(first, lo), b = std::min(first + count, hi);
+            if (a >= b) continue;
+            char *h = (char *)host + (a - first) * es;
+            char *d = (char *)s.psi + (a - lo) * es;
+            if (get) CUDA_TRY(cudaMemcpyAsync(h, d, (b - a) * es, cudaMemcpyDeviceToHost, s.stream));
+            else CUDA_TRY(cudaMemcpyAsync(d, h, (b - a) * es, cudaMemcpyHostToDevice, s.stream));
+            CUDA_TRY(cudaStreamSynchronize(s.stream));
+            continue;
+        }
+        // general: gather/scatter through a device temp in slices
+        const uint64_t slice = std::min<uint64_t>(count, 1ull << 24);
+        void *tmp = nullptr;
+        CUDA_TRY(cudaMalloc(&tmp, slice * es));
+        std::vector<char> h(slice * es);
+        for (uint64_t off = 0; off < count; off += slice) {
+            const uint64_t c = std::min(slice, count - off);
+            // which entries are owned by this shard
+            std::vector<uint64_t> own;
+            for (uint64_t j = 0; j < c; ++j)
+                if ((int)(phys_of(st, first + off + j) >> st->nl) == s.rank) own.push_back(j);
+            if (own.empty()) continue;
+            int e;
+            if (get) {
+                e = launch_gather((int)st->dtype, s.psi, tmp, first + off, c, st->n, st->nl, bitmap.data(), s.rank, s.stream);
+                if (e) { cudaFree(tmp); return set_error(HQ_ERR_CUDA, "gather launch failed"); }
+                cudaError_t ce = cudaMemcpyAsync(h.data(), tmp, c * es, cudaMemcpyDeviceToHost, s.stream);
+                if (!ce) ce = cudaStreamSynchronize(s.stream);
+                if (ce) { cudaFree(tmp); return set_error(HQ_ERR_CUDA, "gather copy: %s", cudaGetErrorString(ce)); }
+                for (uint64_t j : own) memcpy((char *)host + (off + j) * es, h.data() + j * es, es);
+            } else {
+                memcpy(h.data(), (const char *)host + off * es, c * es);
+                cudaError_t ce = cudaMemcpyAsync(tmp, h.data(), c * es, cudaMemcpyHostToDevice, s.stream);
+                if (ce) { cudaFree(tmp); return set_error(HQ_ERR_CUDA, "scatter copy: %s", cudaGetErrorString(ce)); }
+                e = launch_scatter((int)st->dtype, s.psi, tmp, first + off, c, st->n, st->nl, bitmap.data(), s.rank, s.stream);
+                if (e) { cudaFree(tmp); return set_error(HQ_ERR_CUDA, "scatter launch failed"); }
+                ce = cudaStreamSynchronize(s.stream);
+                if (ce) { cudaFree(tmp); return set_error(HQ_ERR_CUDA, "scatter: %s", cudaGetErrorString(ce)); }
+            }
+            st->stats.kernel_launches++;
+        }
+        cudaFree(tmp);
+    }
+    return HQ_OK;
+}
+
+extern "C" hq_status hq_get_amplitudes(hq_state *st, uint64_t first, uint64_t count, void *host_out) {
+    clear_error();
+    if (!st || (!host_out && count)) return set_error(HQ_ERR_ARG, "NULL argument");
+    return io_amplitudes(st, first, count, host_out, true);
+}
+
+extern "C" hq_status hq_set_amplitudes(hq_state *st, uint64_t first, uint64_t count, const void *host_in) {
+    clear_error();
+    if (!st || (!host_in && count)) return set_error(HQ_ERR_ARG, "NULL argument");
+    return io_amplitudes(st, first, count, const_cast<void *>(host_in), false);
+}
+
+extern "C" hq_status hq_norm(hq_state *st, double *out) {
+    clear_error();
+    if (!st || !out) return set_error(HQ_ERR_ARG, "NULL argument");
+    double total = 0.0;
+    for (auto &s : st->sh) {
+        CUDA_TRY(cudaSetDevice(s.device));
+        int nb = 0;
+        int e = launch_norm_partials((int)st->dtype, s.psi, 1ull << st->nl, s.d_part, 148 * 16, s.stream, &nb);
+        if (e) return set_error(HQ_ERR_CUDA, "norm launch: %s", cudaGetErrorString((cudaError_t)e));
+        st->stats.kernel_launches++;
+        st->stats.hbm_bytes += st->es << st->nl;
+        CUDA_TRY(cudaMemcpyAsync(s.h_part, s.d_part, sizeof(double) * nb, cudaMemcpyDeviceToHost, s.stream));
+        CUDA_TRY(cudaStreamSynchronize(s.stream));
+        double acc = 0.0;
+        for (int b = 0; b < nb; ++b) acc += s.h_part[b];
+        total += acc;
+    }
+    if (st->mode == MODE_RANK) {
+        Shard &s = st->sh[0];
+        s.h_part[0] = total;
+        CUDA_TRY(cudaMemcpyAsync(s.d_part, s.h_part, sizeof(double), cudaMemcpyHostToDevice, s.stream));
+        NCCL_TRY(ncclAllReduce(s.d_part, s.d_part, 1, ncclDouble, ncclSum, s.comm, s.stream));
+        CUDA_TRY(cudaMemcpyAsync(s.h_part, s.d_part, sizeof(double), cudaMemcpyDeviceToHost, s.stream));
+        CUDA_TRY(cudaStreamSynchronize(s.stream));
+        total = s.h_part[0];
+    }
+    *out = sqrt(total);
+    return HQ_OK;
+}
+
+// ------------------------------------------------------------------ diagnostics
+
+extern "C" const char *hq_last_error(void) { return g_err.c_str(); }
+
+extern "C" hq_status hq_sync(hq_state *st) {
+    clear_error();
+    if (!st) return set_error(HQ_ERR_ARG, "state is NULL");
+    for (auto &s : st->sh) {
+        CUDA_TRY(cudaSetDevice(s.device));
+        CUDA_TRY(cudaStreamSynchronize(s.stream));
+    }
+    return HQ_OK;
+}
+
+extern "C" hq_status hq_stats_get(const hq_state *st, hq_stats *out) {
+    clear_error();
+    if (!st || !out) return set_error(HQ_ERR_ARG, "NULL argument");
+    *out = st->stats;
+    return HQ_OK;
+}
+
+extern "C" hq_status hq_stats_reset(hq_state *st) {
+    clear_error();
+    if (!st) return set_error(HQ_ERR_ARG, "state is NULL");
+    st->stats = hq_stats{};
+    return HQ_OK;
+}
+
+extern "C" hq_status hq_profile_enable(hq_state *st, int on) {
+    clear_error();
+    if (!st) return set_error(HQ_ERR_ARG, "state is NULL");
+    st->profiling = on != 0;
+    return HQ_OK;
+}
+
+extern "C" hq_status hq_kernel_times(hq_state *st, uint64_t *count, double *total_ms, double *max_ms,
+                                     uint64_t *bytes) {
+    clear_error();
+    if (!st) return set_error(HQ_ERR_ARG, "state is NULL");
+    for (auto &p : st->prof) {
+        CUDA_TRY(cudaEventSynchronize(p.b));
+        float ms = 0.f;
+        CUDA_TRY(cudaEventElapsedTime(&ms, p.a, p.b));
+        st->prof_count++;
+        st->prof_total += ms;
+        st->prof_max = std::max(st->prof_max, (double)ms);
+        st->prof_bytes += p.bytes;
+        st->ev_pool.push_back(p.a);
+        st->ev_pool.push_back(p.b);
+    }
+    st->prof.clear();
+    if (count) *count = st->prof_count;
+    if (total_ms) *total_ms = st->prof_total;
+    if (max_ms) *max_ms = st->prof_max;
+    if (bytes) *bytes = st->prof_bytes;
+    st->prof_count = 0;
+    st->prof_total = st->prof_max = 0;
+    st->prof_bytes = 0;
+    return HQ_OK;
+}
+
+extern "C" const char *hq_version(void) { return "hq-b200 0.1 (sm_100a)"; }

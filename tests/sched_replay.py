@@ -1,0 +1,87 @@
+"""Test helper: replay an hq_schedule op stream on CPU shards.
+
+APPLY ops run through the oracle (plain fp64 apply) on the local shard with the
+op's physical target bits; REMAP ops exchange contiguous chunks exactly as
+include/hq.h documents (chunk t of rank r -> peer with swapped rank bits = t,
+landing in chunk bits(r)); PERMUTE ops swap local index bits.  Used by the
+CPU tests of the distribution logic (single process and gloo world_size 2).
+"""
+import numpy as np
+
+import oracle as O
+
+
+def phys_apply(shard, nl, U, phys_bits):
+    """Apply U with qubits[j] at physical bit phys_bits[j] of an nl-bit shard
+    (oracle qubit label of physical bit p is nl-1-p)."""
+    O.apply_gate(shard, U, [nl - 1 - p for p in phys_bits])
+
+
+def permute_bits(shard, pairs):
+    idx = np.arange(shard.size, dtype=np.int64)
+    dst = idx.copy()
+    for a, b in pairs:
+        ba = (idx >> a) & 1
+        bb = (idx >> b) & 1
+        dst &= ~((1 << a) | (1 << b))
+        dst |= (ba << b) | (bb << a)
+    out = np.empty_like(shard)
+    out[dst] = shard
+    return out
+
+
+def remap_chunks(nl, pairs):
+    """Returns (mp, gsh, chunk) for a REMAP op."""
+    mp = len(pairs)
+    gsh = [a - nl for a, _ in pairs]
+    for i, (_, b) in enumerate(pairs):
+        assert b == nl - mp + i, "remap local bit must be a top bit"
+    return mp, gsh, 1 << (nl - mp)
+
+
+def peer_of(r, t, gsh):
+    p = r
+    for i, g in enumerate(gsh):
+        p = (p & ~(1 << g)) | (((t >> i) & 1) << g)
+    return p
+
+
+def bits_of(r, gsh):
+    return sum(((r >> g) & 1) << i for i, g in enumerate(gsh))
+
+
+def replay_all_shards(n, m, gates, ops, psi_logical):
+    """Single-process replay over all 2^m shards; returns the final shards."""
+    nl = n - m
+    G = 1 << m
+    shards = [psi_logical[r << nl:(r + 1) << nl].copy() for r in range(G)]   # pi0 = identity
+    for op in ops:
+        if op["kind"] == "apply":
+            g = gates[op["gate"]]
+            k = len(g.qubits)
+            for s in shards:
+                phys_apply(s, nl, g.U, op["bits"][:k])
+        elif op["kind"] == "permute":
+            pairs = [(op["bits"][2 * i], op["bits"][2 * i + 1]) for i in range(op["nbits"])]
+            shards = [permute_bits(s, pairs) for s in shards]
+        else:
+            pairs = [(op["bits"][2 * i], op["bits"][2 * i + 1]) for i in range(op["nbits"])]
+            mp, gsh, chunk = remap_chunks(nl, pairs)
+            new = [np.empty_like(s) for s in shards]
+            for r in range(G):
+                for t in range(1 << mp):
+                    p = peer_of(r, t, gsh)
+                    c = bits_of(r, gsh)
+                    new[p][c * chunk:(c + 1) * chunk] = shards[r][t * chunk:(t + 1) * chunk]
+            shards = new
+    return shards
+
+
+def to_logical(n, shards, pi):
+    """Physical shards + final pi (logical q -> physical bit) -> logical psi."""
+    phys = np.concatenate(shards)
+    idx = np.arange(1 << n, dtype=np.int64)
+    p = np.zeros_like(idx)
+    for q in range(n):
+        p |= ((idx >> (n - 1 - q)) & 1) << pi[q]
+    return phys[p]

@@ -1,0 +1,160 @@
+"""CPU-side tests of the C-ABI library: it loads, exports every symbol that
+include/hq.h declares, fails loudly without a GPU, and its host logic (fusion
+planner, distributed schedule) matches the oracle.  No compute calls here."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle as O
+from hq_inputs import (Gate, sycamore_circuit, random_circuit, reversible_circuit, cphase,
+                       random_state, haar_unitary)
+import paper_2111_06868_b200 as hq
+from paper_2111_06868_b200 import build as hqbuild
+
+from sched_replay import replay_all_shards, to_logical
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    hqbuild.build()
+
+
+def test_library_exports_every_declared_symbol():
+    header = open(os.path.join(ROOT, "include", "hq.h")).read()
+    header = re.sub(r"/\*.*?\*/", "", header, flags=re.S)
+    declared = set(re.findall(r"\b(hq_[a-z_0-9]+)\s*\(", header))
+    assert len(declared) >= 30
+    L = hq.lib()
+    for name in sorted(declared):
+        assert hasattr(L, name), name
+
+
+def test_no_cpu_fallback():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(hq.HQError) as e:
+        hq.hq_state_create(8, "c64", 1)
+    assert e.value.status == "HQ_ERR_NO_DEVICE"
+
+
+def _groups_from_oracle(gates, kmax):
+    g = O.compress(gates, kmax)
+    out = np.empty(len(gates), dtype=np.int32)
+    for gi, members in enumerate(g):
+        out[members] = gi
+    return out, len(g)
+
+
+def test_fuse_P2_worked_example():
+    """PAPER P:510-529."""
+    gates = [Gate("CPHASE", (q1, q2), cphase(1.0)) for q1 in range(5) for q2 in range(q1 + 1, 5)]
+    fused = hq.hq_fuse(gates, 3)
+    assert [f[0] for f in fused] == [(0, 1, 2), (0, 3, 4), (1, 3, 4), (2, 3, 4)]
+
+
+@pytest.mark.parametrize("kmax", [2, 3, 4, 5, 6])
+@pytest.mark.parametrize("n,cycles,seed", [(12, 10, 0), (12, 10, 3), (30, 20, 1000), (34, 20, 3000)])
+def test_fuse_groups_bit_exact_vs_oracle(n, cycles, seed, kmax):
+    gates = sycamore_circuit(n, cycles, seed)
+    got, ng = hq.hq_fuse_plan(gates, kmax)
+    want, nw = _groups_from_oracle(gates, kmax)
+    assert ng == nw
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_fuse_groups_random_circuits(seed):
+    gates = random_circuit(9, 80, seed, kmax=3)
+    for kmax in (3, 4, 5, 6):
+        got, _ = hq.hq_fuse_plan(gates, kmax)
+        want, _ = _groups_from_oracle(gates, kmax)
+        assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("kmax", [2, 4, 5, 6])
+def test_fused_matrices_vs_oracle(kmax):
+    gates = sycamore_circuit(12, 10, 2)
+    got = hq.hq_fuse(gates, kmax)
+    want = O.fused_gates(gates, kmax)
+    assert len(got) == len(want)
+    for (qg, Ug), (qw, Uw) in zip(got, want):
+        assert qg == qw
+        assert np.max(np.abs(Ug - Uw)) < 1e-13
+
+
+def test_fuse_errors():
+    gates = [Gate("U", (0, 1, 2), np.eye(8))]
+    with pytest.raises(hq.HQError) as e:
+        hq.hq_fuse(gates, 2)
+    assert e.value.status == "HQ_ERR_K"
+    with pytest.raises(hq.HQError) as e:
+        hq.hq_fuse([Gate("U", (1, 1), np.eye(4))], 3)
+    assert e.value.status == "HQ_ERR_DUP_QUBIT"
+    with pytest.raises(hq.HQError) as e:
+        hq.hq_fuse(gates, 7)
+    assert e.value.status == "HQ_ERR_K"
+    assert hq.hq_fuse([], 3) == []
+
+
+# ---------------------------------------------------------------- distributed schedule
+
+@pytest.mark.parametrize("m", [0, 1, 2, 3])
+@pytest.mark.parametrize("kind", ["sycamore", "random"])
+def test_schedule_replay_matches_oracle(m, kind):
+    n = 12
+    if kind == "sycamore":
+        gates = [Gate("F", q, U) for q, U in O.fused_gates(sycamore_circuit(n, 10, 1), 4)]
+    else:
+        gates = random_circuit(n, 60, 5, kmax=4)
+    ops, pi = hq.hq_schedule(n, m, gates)
+    assert sum(o["kind"] == "apply" for o in ops) == len(gates)
+    if m == 0:
+        assert all(o["kind"] == "apply" for o in ops)
+    # every APPLY target is local
+    for o in ops:
+        if o["kind"] == "apply":
+            k = len(gates[o["gate"]].qubits)
+            assert all(b < n - m for b in o["bits"][:k])
+    psi0 = random_state(n, 3)
+    shards = replay_all_shards(n, m, gates, ops, psi0)
+    got = to_logical(n, shards, pi)
+    want = O.simulate(n, gates, psi0)
+    assert np.max(np.abs(got - want)) < 1e-12
+
+
+def test_schedule_reversible_bit_exact():
+    n, m = 10, 2
+    gates = reversible_circuit(n, 80, 4, kmax=3)
+    ops, pi = hq.hq_schedule(n, m, gates)
+    from hq_inputs import integer_state
+    psi0 = integer_state(n, 1)
+    got = to_logical(n, replay_all_shards(n, m, gates, ops, psi0), pi)
+    want = O.simulate(n, gates, psi0)
+    assert np.array_equal(got, want)
+
+
+def test_schedule_remap_counts_34q():
+    """SURVEY Appendix A estimate: R ~ 11 remaps for 34q d20 at k<=5, m=3."""
+    gates = sycamore_circuit(34, 20, 3000)
+    fused = hq.hq_fuse(gates, 5)
+    ops, _ = hq.hq_schedule(34, 3, [Gate("F", q, U) for q, U in fused])
+    passes = sum(o["kind"] == "apply" for o in ops)
+    remaps = sum(o["kind"] == "remap" for o in ops)
+    permutes = sum(o["kind"] == "permute" for o in ops)
+    assert passes == len(fused)
+    assert remaps <= 0.2 * passes
+    print("34q k<=5 m=3: P=%d R=%d permutes=%d" % (passes, remaps, permutes))
+
+
+def test_schedule_errors():
+    with pytest.raises(hq.HQError) as e:
+        hq.hq_schedule(8, 3, [Gate("U", (0,), np.eye(2))])
+    assert e.value.status == "HQ_ERR_NGPUS"
+    with pytest.raises(hq.HQError) as e:
+        hq.hq_schedule(8, 0, [Gate("U", (8,), np.eye(2))])
+    assert e.value.status == "HQ_ERR_QUBIT"

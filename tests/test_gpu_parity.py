@@ -1,0 +1,301 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 CPU oracle.
+
+Tolerances (BASELINE.json north_star): ||psi - psi_ref||_2 <= 1e-4 for complex64
+and <= 1e-10 for complex128; permutation/index logic bit-exact (C11).
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from hq_inputs import (Gate, sycamore_circuit, random_circuit, reversible_circuit,
+                       haar_sweep_gate, haar_unitary, random_state, integer_state,
+                       permutation_matrix, H, CX)
+import paper_2111_06868_b200 as hq
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"c64": 1e-4, "c128": 1e-10}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    from paper_2111_06868_b200 import build
+    build.build()
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+
+
+def _gpu_state(n, dtype, psi0=None, x=0):
+    s = hq.hq_state_create(n, dtype, 1)
+    if psi0 is None:
+        hq.hq_state_init_basis(s, x)
+    else:
+        hq.hq_set_amplitudes(s, psi0)
+    return s
+
+
+def _err(a, b):
+    return float(np.linalg.norm(a.astype(np.complex128) - b))
+
+
+# ---------------------------------------------------------------- worked example / closed forms
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_P1_grover_on_gpu(dtype):
+    s = _gpu_state(3, dtype, np.ones(8) / np.sqrt(8))
+    hq.hq_apply_matrix(s, np.diag([-1, 1, 1, 1]).astype(complex), [1, 2])
+    out = hq.hq_get_amplitudes(s)
+    want = np.full(8, 1 / np.sqrt(8))
+    want[[0, 4]] *= -1
+    assert np.max(np.abs(out - want)) < 1e-6
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_ghz_and_norm(dtype):
+    n = 20
+    s = _gpu_state(n, dtype)
+    hq.hq_apply_circuit(s, [Gate("H", (0,), H)] + [Gate("CX", (j, j + 1), CX) for j in range(n - 1)])
+    out = hq.hq_get_amplitudes(s)
+    nz = np.flatnonzero(np.abs(out) > 1e-6)
+    assert list(nz) == [0, 2 ** n - 1]
+    assert abs(hq.hq_norm(s) - 1.0) < (1e-6 if dtype == "c64" else 1e-13)
+
+
+# ---------------------------------------------------------------- config [0]: 12q d10
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("kmax", [2, 3, 4, 5, 6])
+@pytest.mark.parametrize("seed", [0, 1, 2, 3, 4])
+def test_config0_12q_fused_vs_unfused_oracle(dtype, kmax, seed):
+    n = 12
+    gates = sycamore_circuit(n, 10, seed)
+    want = O.simulate(n, gates)
+    fused = hq.hq_fuse(gates, kmax)
+    s = _gpu_state(n, dtype)
+    hq.hq_apply_circuit(s, fused)
+    got = hq.hq_get_amplitudes(s)
+    assert _err(got, want) <= TOL[dtype]
+
+
+# ---------------------------------------------------------------- single gates, every k, placements
+PLACEMENTS = ["low", "high", "spread", "random0", "random1", "random2"]
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5, 6])
+@pytest.mark.parametrize("placement", PLACEMENTS)
+@pytest.mark.parametrize("n", [11, 20])
+def test_single_gate_all_placements(dtype, k, placement, n):
+    g = haar_sweep_gate(n, k, placement, seed=2000 + k)
+    psi0 = random_state(n, 17)
+    want = O.apply_gate(psi0.copy(), g.U, g.qubits)
+    s = _gpu_state(n, dtype, psi0)
+    hq.hq_apply_matrix(s, g.U, g.qubits)
+    got = hq.hq_get_amplitudes(s)
+    assert _err(got, want) <= TOL[dtype] * 0.1
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5, 6])
+def test_all_target_orders_k(dtype, k):
+    """Every qubit order of targets spread over lane/register bit classes."""
+    n = 18
+    rng = np.random.default_rng(50 + k)
+    psi0 = random_state(n, k)
+    gates = []
+    for t in range(6):
+        qs = tuple(int(q) for q in rng.choice(n, size=k, replace=False))
+        gates.append(Gate("U", qs, haar_unitary(k, rng)))
+    want = O.simulate(n, gates, psi0)
+    s = _gpu_state(n, dtype, psi0)
+    hq.hq_apply_circuit(s, gates)
+    assert _err(hq.hq_get_amplitudes(s), want) <= TOL[dtype]
+
+
+# ---------------------------------------------------------------- bit-exact index logic (C11)
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5, 6])
+def test_permutation_bit_exact(dtype, k):
+    n = 20
+    rng = np.random.default_rng(900 + k)
+    psi0 = integer_state(n, k)
+    gates = []
+    for t in range(5):
+        qs = tuple(int(q) for q in rng.choice(n, size=k, replace=False))
+        gates.append(Gate("P", qs, permutation_matrix([int(p) for p in rng.permutation(2 ** k)])))
+    want = O.simulate(n, gates, psi0)
+    s = _gpu_state(n, dtype, psi0)
+    hq.hq_apply_circuit(s, gates)
+    got = hq.hq_get_amplitudes(s).astype(np.complex128)
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_reversible_circuit_bit_exact(dtype):
+    n = 16
+    gates = reversible_circuit(n, 120, 7, kmax=4)
+    psi0 = integer_state(n, 3)
+    want = O.simulate(n, gates, psi0)
+    s = _gpu_state(n, dtype, psi0)
+    hq.hq_apply_circuit(s, gates)
+    assert np.array_equal(hq.hq_get_amplitudes(s).astype(np.complex128), want)
+
+
+# ---------------------------------------------------------------- edge cases / errors
+def test_errors_leave_state_unchanged():
+    n = 8
+    psi0 = random_state(n, 1)
+    s = _gpu_state(n, "c128", psi0)
+    for qs, U, status in [((0, 0), np.eye(4), "HQ_ERR_DUP_QUBIT"), ((8,), np.eye(2), "HQ_ERR_QUBIT"),
+                          ((0, 1, 2, 3, 4, 5, 6), np.eye(128), "HQ_ERR_K")]:
+        with pytest.raises(hq.HQError) as e:
+            hq.hq_apply_matrix(s, U, qs)
+        assert e.value.status == status
+    with pytest.raises(hq.HQError) as e:
+        hq.hq_apply_circuit(s, [Gate("H", (0,), H), Gate("bad", (9,), H)])
+    assert e.value.status == "HQ_ERR_QUBIT"
+    with pytest.raises(hq.HQError) as e:
+        hq.hq_state_init_basis(s, 1 << n)
+    assert e.value.status == "HQ_ERR_RANGE"
+    assert np.array_equal(hq.hq_get_amplitudes(s), psi0)
+
+
+@pytest.mark.parametrize("n", [1, 2, 5, 6])
+def test_tiny_states(n):
+    rng = np.random.default_rng(n)
+    psi0 = random_state(n, n)
+    gates = []
+    for t in range(10):
+        k = int(rng.integers(1, n + 1))
+        k = min(k, 6)
+        qs = tuple(int(q) for q in rng.choice(n, size=k, replace=False))
+        gates.append(Gate("U", qs, haar_unitary(k, rng)))
+    want = O.simulate(n, gates, psi0)
+    s = _gpu_state(n, "c128", psi0)
+    hq.hq_apply_circuit(s, gates)
+    assert _err(hq.hq_get_amplitudes(s), want) <= 1e-12
+
+
+def test_empty_circuit_and_identity():
+    s = _gpu_state(10, "c64", random_state(10, 2))
+    before = hq.hq_get_amplitudes(s)
+    hq.hq_apply_circuit(s, [])
+    hq.hq_apply_matrix(s, np.eye(16), [3, 1, 7, 9])
+    assert np.array_equal(hq.hq_get_amplitudes(s), before)
+
+
+def test_non_unitary_allowed():
+    """C4: Projection-like U is applied as is, no renormalisation."""
+    psi0 = random_state(6, 3)
+    P0 = np.diag([1, 0]).astype(complex)
+    s = _gpu_state(6, "c128", psi0)
+    hq.hq_apply_matrix(s, P0, [2])
+    want = O.apply_gate(psi0.copy(), P0, [2])
+    assert _err(hq.hq_get_amplitudes(s), want) < 1e-15
+    assert abs(hq.hq_norm(s) - np.linalg.norm(want)) < 1e-14
+
+
+def test_partial_amplitude_ranges():
+    n = 14
+    psi0 = random_state(n, 9)
+    s = _gpu_state(n, "c128", psi0)
+    assert np.array_equal(hq.hq_get_amplitudes(s, 100, 37), psi0[100:137])
+    hq.hq_set_amplitudes(s, np.arange(5) + 1j, first=2 ** n - 5)
+    assert np.array_equal(hq.hq_get_amplitudes(s, 2 ** n - 5, 5), np.arange(5) + 1j)
+    with pytest.raises(hq.HQError):
+        hq.hq_get_amplitudes(s, 2 ** n - 2, 3)
+
+
+# ---------------------------------------------------------------- compiled circuits
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_circuit_create_run_matches_apply(dtype):
+    n = 18
+    gates = hq.hq_fuse(sycamore_circuit(n, 12, 5), 4)
+    s1 = _gpu_state(n, dtype)
+    hq.hq_apply_circuit(s1, gates)
+    s2 = _gpu_state(n, dtype)
+    c = hq.hq_circuit_create(s2, gates)
+    info = hq.hq_circuit_info(c)
+    assert info["passes"] == len(gates) and info["remaps"] == 0
+    hq.hq_circuit_run(s2, c)
+    a, b = hq.hq_get_amplitudes(s1), hq.hq_get_amplitudes(s2)
+    assert np.array_equal(a, b)
+    want = O.simulate(n, [Gate("F", q, U) for q, U in gates])
+    assert _err(b, want) <= TOL[dtype]
+
+
+# ---------------------------------------------------------------- virtual shards (distribution logic on 1 GPU)
+@pytest.mark.parametrize("G", [2, 4, 8])
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_virtual_shards_sycamore(G, dtype):
+    n = 16
+    gates = hq.hq_fuse(sycamore_circuit(n, 12, 6), 4)
+    want = O.simulate(n, [Gate("F", q, U) for q, U in gates])
+    s = hq.hq_state_create_virtual(n, dtype, G)
+    hq.hq_state_init_basis(s, 0)
+    hq.hq_apply_circuit(s, gates)
+    st = hq.hq_stats_get(s)
+    assert st["remaps"] > 0
+    assert _err(hq.hq_get_amplitudes(s), want) <= TOL[dtype]
+    assert abs(hq.hq_norm(s) - 1) < 1e-5
+
+
+@pytest.mark.parametrize("G", [2, 8])
+def test_virtual_shards_reversible_bit_exact(G):
+    n = 14
+    gates = reversible_circuit(n, 100, 11, kmax=4)
+    psi0 = integer_state(n, 5)
+    want = O.simulate(n, gates, psi0)
+    s = hq.hq_state_create_virtual(n, "c64", G)
+    hq.hq_set_amplitudes(s, psi0)
+    hq.hq_apply_circuit(s, gates)
+    assert np.array_equal(hq.hq_get_amplitudes(s).astype(np.complex128), want)
+    # readback of a sub-range through pi^-1
+    assert np.array_equal(hq.hq_get_amplitudes(s, 77, 300).astype(np.complex128), want[77:377])
+
+
+def test_virtual_circuit_rerun_requires_same_layout():
+    n = 14
+    gates = hq.hq_fuse(sycamore_circuit(n, 8, 1), 3)
+    s = hq.hq_state_create_virtual(n, "c128", 4)
+    hq.hq_state_init_basis(s, 0)
+    c = hq.hq_circuit_create(s, gates)
+    hq.hq_circuit_run(s, c)
+    want = O.simulate(n, [Gate("F", q, U) for q, U in gates])
+    assert _err(hq.hq_get_amplitudes(s), want) <= 1e-10
+
+
+# ---------------------------------------------------------------- full size: properties at any n
+@pytest.mark.parametrize("n", [26, 30])
+def test_mirror_circuit_full_size(n):
+    """P9: C then C^dagger returns |0> (c64 tolerance 1e-4)."""
+    gates = sycamore_circuit(n, 20 if n == 30 else 12, 1000)
+    inv = [Gate(g.name + "^-1", g.qubits, g.U.conj().T) for g in reversed(gates)]
+    fused = hq.hq_fuse(gates + inv, 2 if n == 30 else 4)
+    s = _gpu_state(n, "c64")
+    hq.hq_apply_circuit(s, fused)
+    a0 = hq.hq_get_amplitudes(s, 0, 1)[0]
+    nrm = hq.hq_norm(s)
+    # ||psi - |0>||^2 = ||psi||^2 - 2 Re psi_0 + 1
+    dist = np.sqrt(max(nrm ** 2 - 2 * a0.real + 1, 0.0))
+    assert dist <= 1e-4
+
+
+def test_reversible_full_size_bit_exact():
+    """P10: basis state through reversible gates at 30q; f(x) by host bit ops."""
+    n = 30
+    gates = reversible_circuit(n, 60, 99, kmax=4)
+    x = 0x2A5F3C1
+    # host: push the basis index through the permutations
+    y = x
+    for g in gates:
+        k = len(g.qubits)
+        c = 0
+        for j, q in enumerate(g.qubits):
+            c |= ((y >> (n - 1 - q)) & 1) << (k - 1 - j)
+        r = int(np.flatnonzero(np.abs(g.U[:, c]) > 0.5)[0])
+        for j, q in enumerate(g.qubits):
+            b = n - 1 - q
+            y = (y & ~(1 << b)) | (((r >> (k - 1 - j)) & 1) << b)
+    s = _gpu_state(n, "c64", x=x)
+    hq.hq_apply_circuit(s, gates)
+    assert hq.hq_get_amplitudes(s, y, 1)[0] == 1.0
+    assert hq.hq_norm(s) == 1.0
