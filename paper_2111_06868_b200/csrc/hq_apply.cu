@@ -54,16 +54,88 @@ template <typename R, int K> struct UParam {
     typename C2<R>::T u[1 << K][1 << K];
 };
 
-template <typename R, int K, int T0, int KL>
+// Complex multiply-accumulate acc += u * v.  For complex64 this is two packed
+// FFMA2 (fma.rn.f32x2, sm_100) instructions: (ar, ai) += (ur, ur) * (vr, vi)
+// and (ar, ai) += (-ui, ui) * (vi, vr); ptxas folds the broadcast, swap and
+// negation into FFMA2 operand modifiers and takes u from a uniform register.
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b,
+                                                    unsigned long long c) {
+    unsigned long long r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+__device__ __forceinline__ float2 unpk2(unsigned long long r) {
+    float2 o;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(o.x), "=f"(o.y) : "l"(r));
+    return o;
+}
+
+template <int D>
+__device__ __forceinline__ void matvec(const float2 (&u)[D][D], const float2 *v, float2 *out) {
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+        unsigned long long acc = 0ull;
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+            acc = ffma2(pk2(u[r][c].x, u[r][c].x), pk2(v[c].x, v[c].y), acc);
+            acc = ffma2(pk2(-u[r][c].y, u[r][c].y), pk2(v[c].y, v[c].x), acc);
+        }
+        out[r] = unpk2(acc);
+    }
+}
+
+template <int D>
+__device__ __forceinline__ void matvec(const double2 (&u)[D][D], const double2 *v, double2 *out) {
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+        double ar = 0, ai = 0;
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+            ar = fma(u[r][c].x, v[c].x, ar);
+            ar = fma(-u[r][c].y, v[c].y, ar);
+            ai = fma(u[r][c].x, v[c].y, ai);
+            ai = fma(u[r][c].y, v[c].x, ai);
+        }
+        out[r].x = ar;
+        out[r].y = ai;
+    }
+}
+
+// lane bit la <-> register bit e transpose (an involution) over the NR registers
+template <typename V, int NR>
+__device__ __forceinline__ void lane_transpose(V *x, int la, int e, int lane) {
+    const bool hi = (lane >> la) & 1;
+#pragma unroll
+    for (int j0 = 0; j0 < NR; ++j0) {
+        if (j0 & (1 << e)) continue;
+        const int j1 = j0 | (1 << e);
+        V snd;
+        snd.x = hi ? x[j0].x : x[j1].x;
+        snd.y = hi ? x[j0].y : x[j1].y;
+        V rcv;
+        rcv.x = __shfl_xor_sync(0xffffffffu, snd.x, 1 << la);
+        rcv.y = __shfl_xor_sync(0xffffffffu, snd.y, 1 << la);
+        if (hi) x[j0] = rcv; else x[j1] = rcv;
+    }
+}
+
+// VEC = amplitudes per load: 2 (complex64 as float4, physical bit 0 in-thread)
+// or 1 (complex64 as float2 / complex128 as double2).  T0: bit 0 is a target
+// (VEC == 2 only).  KL: number of targets inside the lane bit range.
+template <typename R, int VEC, int K, int T0, int KL>
 __global__ void __launch_bounds__(128)
 apply_reg(typename C2<R>::T *__restrict__ psi, const __grid_constant__ RegParams P,
           const __grid_constant__ UParam<R, K> U) {
     using V = typename C2<R>::T;
-    constexpr int VEC = std::is_same<R, float>::value ? 2 : 1;   // amplitudes per 16 B
     constexpr int NB0 = (VEC == 2 && !T0) ? 1 : 0;              // bit 0 as non-target register bit
     constexpr int NR = 1 << (K + NB0);                           // amplitudes per thread
-    constexpr int P0 = T0 ? 0 : K;                               // register bit holding phys bit 0 (c64)
-    constexpr int NV = NR / VEC;                                 // 16-byte vectors per thread
+    constexpr int P0 = T0 ? 0 : K;                               // register bit holding phys bit 0
+    constexpr int NV = NR / VEC;                                 // loads per thread
     constexpr int NS = K - T0;                                   // register phys bits above lanes
 
     const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -72,14 +144,13 @@ apply_reg(typename C2<R>::T *__restrict__ psi, const __grid_constant__ RegParams
     uint64_t w = tid >> 5;
 #pragma unroll
     for (int i = 0; i < NS; ++i) w = insert_zero(w, P.S[i]);
-    const uint64_t base = (w << 5) | (uint64_t)lane;             // in 16-byte vectors
+    const uint64_t base = (w << 5) | (uint64_t)lane;             // in load units
 
     V x[NR];
     if constexpr (VEC == 2) {
         const float4 *src = reinterpret_cast<const float4 *>(psi);
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
-            // register index with bit P0 cleared, built from v
             const int j0 = ((v >> P0) << (P0 + 1)) | (v & ((1 << P0) - 1));
             const int j1 = j0 | (1 << P0);
             const float4 t = src[base + P.voff[v]];
@@ -91,68 +162,19 @@ apply_reg(typename C2<R>::T *__restrict__ psi, const __grid_constant__ RegParams
         for (int v = 0; v < NV; ++v) x[v] = psi[base + P.voff[v]];
     }
 
-    // lane-target transposes: lane bit la[i] <-> register bit T0+i
 #pragma unroll
-    for (int i = 0; i < KL; ++i) {
-        const int la = P.la[i];
-        const bool hi = (lane >> la) & 1;
-        const int e = T0 + i;
-#pragma unroll
-        for (int j0 = 0; j0 < NR; ++j0) {
-            if (j0 & (1 << e)) continue;
-            const int j1 = j0 | (1 << e);
-            V snd;
-            snd.x = hi ? x[j0].x : x[j1].x;
-            snd.y = hi ? x[j0].y : x[j1].y;
-            V rcv;
-            rcv.x = __shfl_xor_sync(0xffffffffu, snd.x, 1 << la);
-            rcv.y = __shfl_xor_sync(0xffffffffu, snd.y, 1 << la);
-            if (hi) x[j0] = rcv; else x[j1] = rcv;
-        }
-    }
+    for (int i = 0; i < KL; ++i) lane_transpose<V, NR>(x, P.la[i], T0 + i, lane);
 
-    // w = U v for each gather set held by the thread
 #pragma unroll
     for (int s = 0; s < (1 << NB0); ++s) {
         V out[1 << K];
-#pragma unroll
-        for (int r = 0; r < (1 << K); ++r) {
-            R ar = 0, ai = 0;
-#pragma unroll
-            for (int c = 0; c < (1 << K); ++c) {
-                const V u = U.u[r][c];
-                const V v = x[c | (s << K)];
-                ar = fma(u.x, v.x, ar);
-                ar = fma(-u.y, v.y, ar);
-                ai = fma(u.x, v.y, ai);
-                ai = fma(u.y, v.x, ai);
-            }
-            out[r].x = ar;
-            out[r].y = ai;
-        }
+        matvec<1 << K>(U.u, x + (s << K), out);
 #pragma unroll
         for (int r = 0; r < (1 << K); ++r) x[r | (s << K)] = out[r];
     }
 
-    // undo the transposes (each is an involution), in reverse order
 #pragma unroll
-    for (int i = KL - 1; i >= 0; --i) {
-        const int la = P.la[i];
-        const bool hi = (lane >> la) & 1;
-        const int e = T0 + i;
-#pragma unroll
-        for (int j0 = 0; j0 < NR; ++j0) {
-            if (j0 & (1 << e)) continue;
-            const int j1 = j0 | (1 << e);
-            V snd;
-            snd.x = hi ? x[j0].x : x[j1].x;
-            snd.y = hi ? x[j0].y : x[j1].y;
-            V rcv;
-            rcv.x = __shfl_xor_sync(0xffffffffu, snd.x, 1 << la);
-            rcv.y = __shfl_xor_sync(0xffffffffu, snd.y, 1 << la);
-            if (hi) x[j0] = rcv; else x[j1] = rcv;
-        }
-    }
+    for (int i = KL - 1; i >= 0; --i) lane_transpose<V, NR>(x, P.la[i], T0 + i, lane);
 
     if constexpr (VEC == 2) {
         float4 *dst = reinterpret_cast<float4 *>(psi);
@@ -214,36 +236,38 @@ namespace {
 
 constexpr int kThreads = 128;
 
-template <typename R, int K, int T0, int KL>
+template <typename R, int VEC, int K, int T0, int KL>
 cudaError_t launch_reg_t(void *psi, const RegParams &P, const void *host_U, cudaStream_t st) {
     UParam<R, K> U;
     memcpy(&U, host_U, sizeof(U));
     const uint64_t blocks = (P.nunits + kThreads - 1) / kThreads;
-    apply_reg<R, K, T0, KL><<<(unsigned)blocks, kThreads, 0, st>>>(
+    apply_reg<R, VEC, K, T0, KL><<<(unsigned)blocks, kThreads, 0, st>>>(
         reinterpret_cast<typename C2<R>::T *>(psi), P, U);
     return cudaGetLastError();
 }
 
-template <typename R, int K, int T0>
+template <typename R, int VEC, int K, int T0>
 cudaError_t launch_reg_kl(int KL, void *psi, const RegParams &P, const void *hU, cudaStream_t st) {
     switch (KL) {
-        case 0: return launch_reg_t<R, K, T0, 0>(psi, P, hU, st);
-        case 1: if constexpr (K - T0 >= 1) return launch_reg_t<R, K, T0, 1>(psi, P, hU, st); break;
-        case 2: if constexpr (K - T0 >= 2) return launch_reg_t<R, K, T0, 2>(psi, P, hU, st); break;
-        case 3: if constexpr (K - T0 >= 3) return launch_reg_t<R, K, T0, 3>(psi, P, hU, st); break;
-        case 4: if constexpr (K - T0 >= 4) return launch_reg_t<R, K, T0, 4>(psi, P, hU, st); break;
+        case 0: return launch_reg_t<R, VEC, K, T0, 0>(psi, P, hU, st);
+        case 1: if constexpr (K - T0 >= 1) return launch_reg_t<R, VEC, K, T0, 1>(psi, P, hU, st); break;
+        case 2: if constexpr (K - T0 >= 2) return launch_reg_t<R, VEC, K, T0, 2>(psi, P, hU, st); break;
+        case 3: if constexpr (K - T0 >= 3) return launch_reg_t<R, VEC, K, T0, 3>(psi, P, hU, st); break;
+        case 4: if constexpr (K - T0 >= 4) return launch_reg_t<R, VEC, K, T0, 4>(psi, P, hU, st); break;
         default: break;
     }
     return cudaErrorInvalidValue;
 }
 
-template <typename R, int K>
-cudaError_t launch_reg_k(int T0, int KL, void *psi, const RegParams &P, const void *hU,
+template <int K>
+cudaError_t launch_reg_f(int VEC, int T0, int KL, void *psi, const RegParams &P, const void *hU,
                          cudaStream_t st) {
-    if constexpr (std::is_same<R, float>::value) {
-        if (T0) return launch_reg_kl<R, K, 1>(KL, psi, P, hU, st);
+    if (VEC == 2) {
+        if (T0) return launch_reg_kl<float, 2, K, 1>(KL, psi, P, hU, st);
+        if constexpr (K <= 3) return launch_reg_kl<float, 2, K, 0>(KL, psi, P, hU, st);
+        return cudaErrorInvalidValue;
     }
-    return launch_reg_kl<R, K, 0>(KL, psi, P, hU, st);
+    return launch_reg_kl<float, 1, K, 0>(KL, psi, P, hU, st);
 }
 
 template <typename R>
@@ -267,20 +291,22 @@ cudaError_t launch_gen(int K, void *psi, const GenParams &P, const void *dU, cud
 }
 
 // Plan the register kernel for this placement; returns false if it does not
-// apply (then the generic kernel runs).
-bool plan_reg(int dtype, const ApplyDesc &d, RegParams &P, int &T0, int &KL) {
+// apply (then the generic kernel runs).  VEC: 2 for complex64 when bit 0 is a
+// target or k <= 3 (float4 access, two gather sets per thread when bit 0 is
+// not a target), else 1 (float2 / double2 access, one gather set per thread).
+bool plan_reg(int dtype, const ApplyDesc &d, RegParams &P, int &VEC, int &T0, int &KL) {
     const int K = d.k;
     if (K > 4) return false;
-    const int LB = dtype == HQ_C64 ? 1 : 0;
-    const int lane_lo = LB, lane_hi = LB + 5;      // lane bits [lane_lo, lane_hi)
-    T0 = (dtype == HQ_C64 && d.p[0] == 0) ? 1 : 0;
+    const bool t0 = dtype == HQ_C64 && d.p[0] == 0;
+    VEC = (dtype == HQ_C64 && (t0 || K <= 3)) ? 2 : 1;
+    const int LB = VEC == 2 ? 1 : 0;
+    const int lane_hi = LB + 5;                    // lane bits [LB, LB+5)
+    T0 = (VEC == 2 && t0) ? 1 : 0;
     KL = 0;
     for (int i = T0; i < K; ++i)
         if (d.p[i] < lane_hi) ++KL;
-    // register physical bits (besides bit 0 for c64): extras + high targets
     const int used = lane_hi + (K - T0);
     if (d.n_local - used < 8) return false;       // too small to fill a GPU
-    // extras: lowest KL physical bits >= lane_hi that are not targets
     int extras[5], ne = 0;
     for (int b = lane_hi; ne < KL && b < d.n_local; ++b) {
         bool tgt = false;
@@ -294,12 +320,10 @@ bool plan_reg(int dtype, const ApplyDesc &d, RegParams &P, int &T0, int &KL) {
     if (T0) regphys[nreg++] = 0;
     for (int i = 0; i < KL; ++i) regphys[nreg++] = extras[i];
     for (int i = T0 + KL; i < K; ++i) regphys[nreg++] = d.p[i];
-    const int NB0 = (dtype == HQ_C64 && !T0) ? 1 : 0;
+    const int NB0 = (VEC == 2 && !T0) ? 1 : 0;
     if (NB0) regphys[nreg++] = 0;                 // register bit K
     const int P0 = T0 ? 0 : K;
-    // vector offsets: registers with the bit-0 register cleared
     const int NR = 1 << (K + NB0);
-    const int VEC = dtype == HQ_C64 ? 2 : 1;
     for (int v = 0; v < NR / VEC; ++v) {
         int j0 = v;
         if (VEC == 2) j0 = ((v >> P0) << (P0 + 1)) | (v & ((1 << P0) - 1));
@@ -308,11 +332,9 @@ bool plan_reg(int dtype, const ApplyDesc &d, RegParams &P, int &T0, int &KL) {
             if ((j0 >> b) & 1) off |= 1ull << (regphys[b] - LB);
         P.voff[v] = off;
     }
-    // warp-space insertion positions: register phys bits other than bit 0
     int S[6], ns = 0;
     for (int b = 0; b < nreg; ++b)
         if (regphys[b] >= lane_hi) S[ns++] = regphys[b] - lane_hi;
-    // sort ascending
     for (int i = 1; i < ns; ++i) {
         int x = S[i], j = i - 1;
         while (j >= 0 && S[j] > x) { S[j + 1] = S[j]; --j; }
@@ -321,8 +343,7 @@ bool plan_reg(int dtype, const ApplyDesc &d, RegParams &P, int &T0, int &KL) {
     if (ns != K - T0) return false;
     for (int i = 0; i < ns; ++i) P.S[i] = S[i];
     for (int i = 0; i < KL; ++i) P.la[i] = d.p[T0 + i] - LB;
-    const int nvbits = d.n_local - LB;           // vector-index bits
-    P.nunits = 1ull << (nvbits - ns);              // threads = 32 lanes x warps
+    P.nunits = 1ull << (d.n_local - LB - ns);     // threads = 32 lanes x warps
     return true;
 }
 
@@ -332,22 +353,22 @@ int launch_apply(int dtype, void *psi, const ApplyDesc &d, const void *host_U, c
                  void *stream, int *launches) {
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     RegParams rp;
-    int T0 = 0, KL = 0;
+    int VEC = 1, T0 = 0, KL = 0;
     cudaError_t e;
-    if (host_U && plan_reg(dtype, d, rp, T0, KL)) {
+    if (host_U && plan_reg(dtype, d, rp, VEC, T0, KL)) {
         if (dtype == HQ_C64) {
             switch (d.k) {
-                case 1: e = launch_reg_k<float, 1>(T0, KL, psi, rp, host_U, st); break;
-                case 2: e = launch_reg_k<float, 2>(T0, KL, psi, rp, host_U, st); break;
-                case 3: e = launch_reg_k<float, 3>(T0, KL, psi, rp, host_U, st); break;
-                default: e = launch_reg_k<float, 4>(T0, KL, psi, rp, host_U, st); break;
+                case 1: e = launch_reg_f<1>(VEC, T0, KL, psi, rp, host_U, st); break;
+                case 2: e = launch_reg_f<2>(VEC, T0, KL, psi, rp, host_U, st); break;
+                case 3: e = launch_reg_f<3>(VEC, T0, KL, psi, rp, host_U, st); break;
+                default: e = launch_reg_f<4>(VEC, T0, KL, psi, rp, host_U, st); break;
             }
         } else {
             switch (d.k) {
-                case 1: e = launch_reg_k<double, 1>(0, KL, psi, rp, host_U, st); break;
-                case 2: e = launch_reg_k<double, 2>(0, KL, psi, rp, host_U, st); break;
-                case 3: e = launch_reg_k<double, 3>(0, KL, psi, rp, host_U, st); break;
-                default: e = launch_reg_k<double, 4>(0, KL, psi, rp, host_U, st); break;
+                case 1: e = launch_reg_kl<double, 1, 1, 0>(KL, psi, rp, host_U, st); break;
+                case 2: e = launch_reg_kl<double, 1, 2, 0>(KL, psi, rp, host_U, st); break;
+                case 3: e = launch_reg_kl<double, 1, 3, 0>(KL, psi, rp, host_U, st); break;
+                default: e = launch_reg_kl<double, 1, 4, 0>(KL, psi, rp, host_U, st); break;
             }
         }
     } else {
@@ -370,8 +391,8 @@ int launch_apply(int dtype, void *psi, const ApplyDesc &d, const void *host_U, c
 
 bool apply_needs_dev_U(int dtype, const ApplyDesc &d) {
     RegParams rp;
-    int T0, KL;
-    return !plan_reg(dtype, d, rp, T0, KL);
+    int VEC, T0, KL;
+    return !plan_reg(dtype, d, rp, VEC, T0, KL);
 }
 
 // ------------------------------------------------------------------ small kernels
