@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--dtype", default="c64", choices=["c64", "c128"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-layout", action="store_true",
+                    help="keep the default qubit layout instead of hq_plan_layout's")
     return ap.parse_args()
 
 
@@ -233,6 +235,12 @@ def run_hq(args):
         state = hq.hq_state_create(n, args.dtype, 1)
     stream = torch.cuda.Stream(device=local)
     hq.hq_state_set_stream(state, stream.cuda_stream)
+    layout = None
+    if world == 1 and not args.no_layout:
+        t0 = time.perf_counter()
+        layout, cost0, cost1 = hq.hq_plan_layout(n, 0, fused, args.dtype)
+        plan_ms += (time.perf_counter() - t0) * 1e3
+        hq.hq_state_set_layout(state, layout)
     circ = hq.hq_circuit_create(state, fused)
     info = hq.hq_circuit_info(circ)
     P, R = info["passes"], info["remaps"]
@@ -306,6 +314,9 @@ def run_hq(args):
         t0 = time.perf_counter()
         hq.hq_state_init_basis(state, 0)
         fz = hq.hq_fuse(gates, kmax)
+        if layout is not None:
+            hq.hq_state_set_layout(state, hq.hq_plan_layout(n, 0, fz, args.dtype)[0])
+            hq.hq_state_init_basis(state, 0)
         hq.hq_apply_circuit(state, fz)
         nv = hq.hq_norm(state)           # D2H of the result, synchronises
         barrier()
@@ -320,7 +331,9 @@ def run_hq(args):
             e2e_t = float(t.item())
         e2e = {"value": work_bytes / (e2e_t * 1e-3) / 1e9, "unit": "GB/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8 * 148 * 16,
-               "ms_per_step": e2e_t, "api": "hq_state_init_basis + hq_fuse + hq_apply_circuit + hq_norm"}
+               "ms_per_step": e2e_t,
+               "api": "hq_fuse + hq_plan_layout + hq_state_set_layout + hq_state_init_basis + "
+                      "hq_apply_circuit + hq_norm"}
 
     line = {
         "metric": "state-update GB/s", "value": value, "unit": "GB/s", "n_gpus": world,
@@ -333,7 +346,8 @@ def run_hq(args):
                    "passes": P, "remaps": R, "circuit_sha256": circuit_sha256(gates),
                    "state_gib": state_bytes / 2 ** 30,
                    "l2": "no flush: state %.0f GiB >> 126 MB L2" % (state_bytes / 2 ** 30),
-                   "parallelism": "sv-shard%d" % world},
+                   "parallelism": "sv-shard%d" % world,
+                   "layout": "hq_plan_layout" if layout is not None else "default"},
         "circuit_wall_s": ms_per_step / 1e3,
         "per_gpu_gbs": value / world,
         "frac_of_hbm_per_gpu": value / world / peak,

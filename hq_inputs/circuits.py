@@ -101,6 +101,7 @@ def haar_sweep_gate(n, k, placement, seed):
                'high' -> physical bits n-k..n-1, i.e. qubits 0..k-1
                'spread' -> evenly spread over the n bits
                'random<j>' -> k distinct random qubits (seeded by j)
+               'b:<b0>-<b1>-...' -> these physical bits
     Qubit q sits at index bit n-1-q (C1).  Returns a Gate.
     """
     rng = np.random.default_rng(seed)
@@ -111,6 +112,9 @@ def haar_sweep_gate(n, k, placement, seed):
         bits = list(range(n - k, n))
     elif placement == "spread":
         bits = sorted({int(round(i * (n - 1) / max(k - 1, 1))) for i in range(k)})
+        assert len(bits) == k
+    elif placement.startswith("b:"):
+        bits = [int(x) for x in placement[2:].split("-")]
         assert len(bits) == k
     elif placement.startswith("random"):
         j = int(placement[6:] or 0)

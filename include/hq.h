@@ -128,6 +128,18 @@ hq_status hq_state_create_virtual(int n, hq_dtype dtype, int nshards, hq_state *
 hq_status hq_state_create_from_buffers(int n, hq_dtype dtype, void *psi_device,
                                        void *stream, hq_state **out);
 
+/* Qubit layout (the logical->physical bit map pi, pi[q] = physical index bit
+ * of logical qubit q).  The default is pi[q] = n-1-q, i.e. physical index ==
+ * logical index.  A layout is a permutation of [0, n); it changes only where
+ * the amplitudes live in HBM, never what get/set_amplitudes return (always
+ * logical order, C14).  hq_state_set_layout makes the given layout the one
+ * hq_state_init_basis restores; the amplitudes are UNDEFINED after the call
+ * until hq_state_init_basis or a full hq_set_amplitudes.  Single-rank states
+ * only (distributed states start from the default and change by remaps).
+ * Errors: HQ_ERR_ARG (not a permutation), HQ_ERR_STATE (multi-rank). */
+hq_status hq_state_set_layout(hq_state *s, const int32_t *pi);
+hq_status hq_state_get_layout(const hq_state *s, int32_t *pi_out);
+
 /* Frees everything the library owns.  NULL is accepted. */
 hq_status hq_state_destroy(hq_state *s);
 
@@ -221,6 +233,17 @@ typedef struct hq_op {
 hq_status hq_schedule(int n, int m, const hq_gate *gates, size_t ngates,
                       hq_op **ops, size_t *nops, int32_t *pi_out);
 hq_status hq_free_ops(hq_op *ops);
+
+/* Layout planner (the GPU counterpart of the paper's "qubits are swapped to
+ * fully exploit AVX instructions"): a local search over the
+ * logical->physical map of the n-m local qubits that lowers the summed
+ * estimated pass cost of `gates` for dtype (HQ_C64 / HQ_C128).  The cost model
+ * penalises targets in the warp-lane bits of the
+ * SIMT kernel and tensor-core gathers spanning more than 16 8-MB regions.
+ * pi_out receives n entries; cost_before / cost_after (may be NULL) the
+ * model's totals for the default and the returned layout. */
+hq_status hq_plan_layout(int n, int m, int dtype, const hq_gate *gates, size_t ngates,
+                         int32_t *pi_out, double *cost_before, double *cost_after);
 
 /* ------------------------------------------------------------------ diagnostics */
 

@@ -45,6 +45,11 @@ struct Op {
 void schedule(int n, int m, const std::vector<GateRef> &g, std::vector<int> &pi,
               std::vector<Op> &ops);
 
+// Layout planner: logical->physical map of the local qubits minimising the
+// estimated pass cost of `g` (hq_plan_layout).
+double layout_pass_cost(int dtype, int k, const int *bits);
+void plan_layout(int n, int m, int dtype, const std::vector<GateRef> &g, std::vector<int> &pi);
+
 // ------------------------------------------------------------------ kernels (hq_apply.cu)
 // Target description handed to the kernel launchers: k physical bit
 // positions in CANONICAL order (ascending), and U already permuted so that
@@ -70,6 +75,14 @@ int launch_apply(int dtype, void *psi, const ApplyDesc &d, const void *host_U,
 // Whether launch_apply needs dev_U (true when U cannot travel as a kernel
 // parameter for this (dtype, k, placement)).
 bool apply_needs_dev_U(int dtype, const ApplyDesc &d);
+
+// tcgen05 tensor-core path (hq_tc.cu): complex64, k = 5 or 6 (5 is widened to
+// 6 exactly as U (x) I).  tc_prepare builds the device payload (real-embedded
+// A hi/lo, 128 KB) and the kernel parameter block from the canonical fp64 U.
+bool tc_applicable(int dtype, const ApplyDesc &d);
+void tc_prepare(const ApplyDesc &d, const double *Ucanon, std::vector<char> &payload,
+                std::vector<char> &params);
+int tc_launch(void *psi, const void *params, const void *dev_payload, void *stream);
 
 // psi = 0, then psi[idx] = 1 if idx >= 0.
 int launch_init_basis(int dtype, void *psi, uint64_t n_amps, int64_t idx, void *stream);

@@ -17,6 +17,7 @@
 // swap applied to the least-significant qubits for AVX.
 #include <algorithm>
 #include <cstring>
+#include <vector>
 #include <limits>
 #include <new>
 
@@ -221,6 +222,77 @@ void schedule(int n, int m, const std::vector<GateRef> &g, std::vector<int> &pi,
     }
 }
 
+// ------------------------------------------------------------------ layout
+
+// Estimated relative cost of one pass with physical targets `bits` (k of them)
+// for the kernel the executor will pick.  The
+// weights are the measured slowdowns of bench_sweep.py on a B200:
+//   SIMT (k <= 4): each target inside the warp-lane bit range [1, 6) costs a
+//     shuffle transpose (~10% per target at k = 4);
+//   tensor cores (complex64 k = 5, 6): gathers that span more than 16 distinct
+//     8 MB regions (targets at amplitude bit >= 20) fall off a cliff (0.66 ->
+//     0.53 -> 0.19 of HBM for 4, 5, 6 such targets); targets in [0, 6) make
+//     the tile loads less coalesced.
+double layout_pass_cost(int dtype, int k, const int *bits) {
+    double c = 1.0;
+    if (dtype == HQ_C64 && k >= 5) {
+        int hi = 0, lo = 0;
+        for (int j = 0; j < k; ++j) {
+            hi += bits[j] >= 20;
+            lo += bits[j] < 6;
+        }
+        if (hi > 4) c += hi == 5 ? 0.3 : 2.5;
+        c += 0.05 * lo;
+    } else {
+        const int lane_lo = dtype == HQ_C64 ? 1 : 0, lane_hi = lane_lo + 5;
+        for (int j = 0; j < k; ++j)
+            if (bits[j] >= lane_lo && bits[j] < lane_hi) c += 0.08;
+    }
+    return c;
+}
+
+// Local search over the logical->physical map of the n - m local qubits:
+// start from q -> n-1-q and apply any swap of two local positions that lowers
+// the summed pass cost, until no swap helps (deterministic).
+void plan_layout(int n, int m, int dtype, const std::vector<GateRef> &g, std::vector<int> &pi) {
+    pi.resize(n);
+    for (int q = 0; q < n; ++q) pi[q] = n - 1 - q;
+    const int nl = n - m;
+    std::vector<std::vector<int>> uses(n);
+    for (size_t i = 0; i < g.size(); ++i)
+        for (int j = 0; j < g[i].k; ++j) uses[g[i].q[j]].push_back((int)i);
+    auto gate_cost = [&](size_t i) {
+        int b[6];
+        for (int j = 0; j < g[i].k; ++j) b[j] = pi[g[i].q[j]];
+        return layout_pass_cost(dtype, g[i].k, b);
+    };
+    std::vector<int> inv(n);
+    for (int q = 0; q < n; ++q) inv[pi[q]] = q;
+    for (int sweep = 0; sweep < 20; ++sweep) {
+        bool improved = false;
+        for (int a = 0; a < nl; ++a)
+            for (int b = a + 1; b < nl; ++b) {
+                const int qa = inv[a], qb = inv[b];
+                std::vector<int> touched(uses[qa]);
+                touched.insert(touched.end(), uses[qb].begin(), uses[qb].end());
+                std::sort(touched.begin(), touched.end());
+                touched.erase(std::unique(touched.begin(), touched.end()), touched.end());
+                double before = 0, after = 0;
+                for (int i : touched) before += gate_cost(i);
+                std::swap(pi[qa], pi[qb]);
+                for (int i : touched) after += gate_cost(i);
+                if (after < before - 1e-9) {
+                    inv[a] = qb;
+                    inv[b] = qa;
+                    improved = true;
+                } else {
+                    std::swap(pi[qa], pi[qb]);
+                }
+            }
+        if (!improved) break;
+    }
+}
+
 }  // namespace hq
 
 // ------------------------------------------------------------------ C ABI
@@ -330,6 +402,33 @@ extern "C" hq_status hq_schedule(int n, int m, const hq_gate *gates, size_t ngat
     *ops = arr;
     *nops = v.size();
     if (pi_out) for (int q = 0; q < n; ++q) pi_out[q] = pi[q];
+    return HQ_OK;
+}
+
+extern "C" hq_status hq_plan_layout(int n, int m, int dtype, const hq_gate *gates, size_t ngates,
+                                   int32_t *pi_out, double *cost_before, double *cost_after) {
+    clear_error();
+    if ((!gates && ngates) || !pi_out) return set_error(HQ_ERR_ARG, "NULL argument");
+    if (n < 1 || n > 63 || m < 0 || m > 16 || (m > 0 && n - m < 6))
+        return set_error(HQ_ERR_ARG, "bad n=%d / m=%d", n, m);
+    std::vector<GateRef> refs;
+    hq_status st = to_refs(gates, ngates, n, refs);
+    if (st) return st;
+    auto total = [&](const std::vector<int> &pi) {
+        double c = 0;
+        for (auto &gt : refs) {
+            int b[6];
+            for (int j = 0; j < gt.k; ++j) b[j] = pi[gt.q[j]];
+            c += layout_pass_cost(dtype, gt.k, b);
+        }
+        return c;
+    };
+    std::vector<int> pi0(n), pi;
+    for (int q = 0; q < n; ++q) pi0[q] = n - 1 - q;
+    plan_layout(n, m, dtype, refs, pi);
+    if (cost_before) *cost_before = total(pi0);
+    if (cost_after) *cost_after = total(pi);
+    for (int q = 0; q < n; ++q) pi_out[q] = pi[q];
     return HQ_OK;
 }
 

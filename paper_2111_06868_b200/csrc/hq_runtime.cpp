@@ -98,6 +98,7 @@ struct hq_state {
     int mode = MODE_SINGLE;
     std::vector<Shard> sh;
     std::vector<int> pi;          // logical qubit -> physical bit
+    std::vector<int> pi_init;     // layout restored by hq_state_init_basis
     hq_stats stats{};
     bool profiling = false;
     std::vector<ProfEvent> prof;  // pending
@@ -111,10 +112,9 @@ struct hq_circuit {
     hq_state *owner = nullptr;
     std::vector<int> pi_start, pi_end;
     std::vector<Op> ops;
-    std::vector<int> op_uoff;              // per APPLY op: element offset into U buffers
-    std::vector<ApplyDesc> desc;           // per op (APPLY)
-    std::vector<std::vector<char>> host_U; // per APPLY op: canonical U in dtype
-    std::vector<char *> dev_U;             // per shard: all U's
+    std::vector<long long> op_uoff;        // per APPLY op: byte offset of its payload (-1: none)
+    std::vector<struct Prep> prep;         // per op (APPLY)
+    std::vector<char *> dev_U;             // per shard: all payloads
     uint64_t passes = 0, remaps = 0, permutes = 0;
 };
 
@@ -179,7 +179,7 @@ static hq_status shard_alloc(hq_state *st, Shard &s, bool need_buf, bool make_st
     }
     CUDA_TRY(cudaMalloc((void **)&s.d_part, sizeof(double) * 148 * 16));
     CUDA_TRY(cudaMallocHost((void **)&s.h_part, sizeof(double) * 148 * 16));
-    return arena_init(s, (size_t)16 << 20);
+    return arena_init(s, (size_t)64 << 20);
 }
 
 static void shard_free(Shard &s) {
@@ -217,6 +217,7 @@ static hq_state *new_state(int n, hq_dtype dtype, int world) {
     st->nl = n - st->m;
     st->pi.resize(n);
     for (int q = 0; q < n; ++q) st->pi[q] = n - 1 - q;
+    st->pi_init = st->pi;
     return st;
 }
 
@@ -390,6 +391,28 @@ extern "C" hq_status hq_state_destroy(hq_state *st) {
     return HQ_OK;
 }
 
+extern "C" hq_status hq_state_set_layout(hq_state *st, const int32_t *pi) {
+    clear_error();
+    if (!st || !pi) return set_error(HQ_ERR_ARG, "NULL argument");
+    if (st->world > 1) return set_error(HQ_ERR_STATE, "layout can only be chosen for single-rank states");
+    std::vector<int> seen(st->n, 0), v(st->n);
+    for (int q = 0; q < st->n; ++q) {
+        if (pi[q] < 0 || pi[q] >= st->n || seen[pi[q]]++)
+            return set_error(HQ_ERR_ARG, "layout is not a permutation of [0, %d)", st->n);
+        v[q] = pi[q];
+    }
+    st->pi = v;
+    st->pi_init = v;
+    return HQ_OK;
+}
+
+extern "C" hq_status hq_state_get_layout(const hq_state *st, int32_t *pi_out) {
+    clear_error();
+    if (!st || !pi_out) return set_error(HQ_ERR_ARG, "NULL argument");
+    for (int q = 0; q < st->n; ++q) pi_out[q] = st->pi[q];
+    return HQ_OK;
+}
+
 extern "C" hq_status hq_state_set_stream(hq_state *st, void *stream) {
     clear_error();
     if (!st) return set_error(HQ_ERR_ARG, "state is NULL");
@@ -420,9 +443,9 @@ extern "C" hq_status hq_state_info(const hq_state *st, int *n, int *dtype, int *
 // ------------------------------------------------------------------ executor
 
 // Canonicalise: sort targets by physical bit ascending and permute U so that
-// U-index bit i <-> i-th smallest target (exact), then round fp64 -> dtype.
-static void canonical_U(hq_dtype dt, const double *U, int k, const int *phys, ApplyDesc &d,
-                        std::vector<char> &out, int nl) {
+// U-index bit i <-> i-th smallest target (exact), keep it in fp64.
+static void canonical_U64(const double *U, int k, const int *phys, ApplyDesc &d,
+                          std::vector<double> &out, int nl) {
     int order[6];
     for (int j = 0; j < k; ++j) order[j] = j;
     std::sort(order, order + k, [&](int a, int b) { return phys[a] < phys[b]; });
@@ -438,22 +461,45 @@ static void canonical_U(hq_dtype dt, const double *U, int k, const int *phys, Ap
             if ((c >> i) & 1) u |= 1 << (k - 1 - order[i]);
         map[c] = u;
     }
-    const size_t es = dt == HQ_C64 ? 8 : 16;
-    out.resize(es * D * D);
+    out.resize((size_t)2 * D * D);
     for (int r = 0; r < D; ++r)
         for (int c = 0; c < D; ++c) {
-            const double re = U[2 * (map[r] * D + map[c])];
-            const double im = U[2 * (map[r] * D + map[c]) + 1];
-            if (dt == HQ_C64) {
-                float *o = reinterpret_cast<float *>(out.data()) + 2 * (r * D + c);
-                o[0] = (float)re;
-                o[1] = (float)im;
-            } else {
-                double *o = reinterpret_cast<double *>(out.data()) + 2 * (r * D + c);
-                o[0] = re;
-                o[1] = im;
-            }
+            out[2 * (r * D + c)] = U[2 * (map[r] * D + map[c])];
+            out[2 * (r * D + c) + 1] = U[2 * (map[r] * D + map[c]) + 1];
         }
+}
+
+enum { PATH_REG = 0, PATH_GEN = 1, PATH_TC = 2 };
+
+struct Prep {
+    ApplyDesc d;
+    int path = PATH_GEN;
+    std::vector<char> hostU;     // canonical U in the state dtype (RN from fp64)
+    std::vector<char> payload;   // bytes the kernel reads from device memory
+    std::vector<char> params;    // TC parameter block
+};
+
+static void prepare(hq_dtype dt, const double *U, int k, const int *phys, int nl, Prep &p) {
+    std::vector<double> Uc;
+    canonical_U64(U, k, phys, p.d, Uc, nl);
+    const int D = 1 << k;
+    const size_t es = dt == HQ_C64 ? 8 : 16;
+    p.hostU.resize(es * D * D);
+    for (size_t i = 0; i < (size_t)2 * D * D; ++i) {
+        if (dt == HQ_C64) reinterpret_cast<float *>(p.hostU.data())[i] = (float)Uc[i];
+        else reinterpret_cast<double *>(p.hostU.data())[i] = Uc[i];
+    }
+    p.payload.clear();
+    p.params.clear();
+    if (tc_applicable((int)dt, p.d)) {
+        p.path = PATH_TC;
+        tc_prepare(p.d, Uc.data(), p.payload, p.params);
+    } else if (!apply_needs_dev_U((int)dt, p.d)) {
+        p.path = PATH_REG;
+    } else {
+        p.path = PATH_GEN;
+        p.payload = p.hostU;
+    }
 }
 
 static hq_status prof_begin(hq_state *st, Shard &s, ProfEvent &pe) {
@@ -478,14 +524,19 @@ static hq_status prof_end(hq_state *st, Shard &s, ProfEvent &pe, uint64_t bytes)
     return HQ_OK;
 }
 
-static hq_status exec_apply(hq_state *st, Shard &s, const ApplyDesc &d, const void *hU,
-                            const void *dU) {
+static hq_status exec_apply(hq_state *st, Shard &s, const Prep &p, const void *dU) {
     CUDA_TRY(cudaSetDevice(s.device));
     ProfEvent pe{};
     hq_status rc = prof_begin(st, s, pe);
     if (rc) return rc;
     int launches = 0;
-    int e = launch_apply((int)st->dtype, s.psi, d, hU, dU, s.stream, &launches);
+    int e;
+    if (p.path == PATH_TC) {
+        e = tc_launch(s.psi, p.params.data(), dU, s.stream);
+        launches = 1;
+    } else {
+        e = launch_apply((int)st->dtype, s.psi, p.d, p.hostU.data(), dU, s.stream, &launches);
+    }
     if (e != cudaSuccess)
         return set_error(HQ_ERR_CUDA, "apply kernel launch failed: %s", cudaGetErrorString((cudaError_t)e));
     const uint64_t bytes = (uint64_t)2 * (st->es << st->nl);
@@ -602,18 +653,18 @@ static hq_status validate_gates(const hq_state *st, const hq_gate *g, size_t ng,
 // Run an op stream with matrices either host-side (converted on the fly and
 // staged through the arena) or precompiled (circuit).
 static hq_status run_ops(hq_state *st, const std::vector<GateRef> &refs, const std::vector<Op> &ops) {
-    std::vector<char> cu;
+    Prep p;
     for (const Op &op : ops) {
         hq_status rc = HQ_OK;
         if (op.kind == OP_APPLY) {
             const GateRef &g = refs[op.gate];
-            ApplyDesc d;
-            canonical_U(st->dtype, g.U, g.k, op.bits, d, cu, st->nl);
-            const bool need_dev = apply_needs_dev_U((int)st->dtype, d);
-            for (auto &s : st->sh) {
+            prepare(st->dtype, g.U, g.k, op.bits, st->nl, p);
+            for (size_t r = 0; r < st->sh.size(); ++r) {
+                Shard &s = st->sh[r];
                 void *dU = nullptr;
-                if (need_dev && (rc = arena_push(s, cu.data(), cu.size(), &dU))) return rc;
-                if ((rc = exec_apply(st, s, d, cu.data(), dU))) return rc;
+                if (!p.payload.empty() && (rc = arena_push(s, p.payload.data(), p.payload.size(), &dU)))
+                    return rc;
+                if ((rc = exec_apply(st, s, p, dU))) return rc;
             }
         } else if (op.kind == OP_REMAP) {
             rc = exec_remap(st, op);
@@ -657,8 +708,7 @@ static hq_status circuit_compile(hq_state *st, hq_circuit *c, const std::vector<
     c->pi_start = st->pi;
     c->pi_end = st->pi;
     schedule(st->n, st->m, refs, c->pi_end, c->ops);
-    c->desc.assign(c->ops.size(), ApplyDesc{});
-    c->host_U.assign(c->ops.size(), {});
+    c->prep.assign(c->ops.size(), Prep{});
     c->op_uoff.assign(c->ops.size(), -1);
     size_t total = 0;
     c->passes = c->remaps = c->permutes = 0;
@@ -666,9 +716,11 @@ static hq_status circuit_compile(hq_state *st, hq_circuit *c, const std::vector<
         const Op &op = c->ops[i];
         if (op.kind == OP_APPLY) {
             const GateRef &g = refs[op.gate];
-            canonical_U(st->dtype, g.U, g.k, op.bits, c->desc[i], c->host_U[i], st->nl);
-            c->op_uoff[i] = (int)total;
-            total += (c->host_U[i].size() + 255) & ~(size_t)255;
+            prepare(st->dtype, g.U, g.k, op.bits, st->nl, c->prep[i]);
+            if (!c->prep[i].payload.empty()) {
+                c->op_uoff[i] = (long long)total;
+                total += (c->prep[i].payload.size() + 255) & ~(size_t)255;
+            }
             c->passes++;
         } else if (op.kind == OP_REMAP) {
             c->remaps++;
@@ -681,7 +733,8 @@ static hq_status circuit_compile(hq_state *st, hq_circuit *c, const std::vector<
     if (total == 0) return HQ_OK;
     std::vector<char> blob(total, 0);
     for (size_t i = 0; i < c->ops.size(); ++i)
-        if (c->op_uoff[i] >= 0) memcpy(blob.data() + c->op_uoff[i], c->host_U[i].data(), c->host_U[i].size());
+        if (c->op_uoff[i] >= 0)
+            memcpy(blob.data() + c->op_uoff[i], c->prep[i].payload.data(), c->prep[i].payload.size());
     for (size_t r = 0; r < st->sh.size(); ++r) {
         Shard &s = st->sh[r];
         if (r > 0 && st->mode == MODE_VIRTUAL) { c->dev_U[r] = nullptr; continue; }
@@ -722,8 +775,8 @@ extern "C" hq_status hq_circuit_run(hq_state *st, hq_circuit *c) {
         if (op.kind == OP_APPLY) {
             for (size_t r = 0; r < st->sh.size(); ++r) {
                 const char *base = c->dev_U[st->mode == MODE_VIRTUAL ? 0 : r];
-                const void *dU = base ? base + c->op_uoff[i] : nullptr;
-                if ((rc = exec_apply(st, st->sh[r], c->desc[i], c->host_U[i].data(), dU))) return rc;
+                const void *dU = (base && c->op_uoff[i] >= 0) ? base + c->op_uoff[i] : nullptr;
+                if ((rc = exec_apply(st, st->sh[r], c->prep[i], dU))) return rc;
             }
         } else if (op.kind == OP_REMAP) {
             rc = exec_remap(st, op);
@@ -776,8 +829,8 @@ extern "C" hq_status hq_state_init_basis(hq_state *st, uint64_t x) {
     clear_error();
     if (!st) return set_error(HQ_ERR_ARG, "state is NULL");
     if (st->n < 64 && x >= (1ull << st->n)) return set_error(HQ_ERR_RANGE, "basis index out of range");
-    // the whole state is overwritten: restore the canonical layout q -> n-1-q
-    for (int q = 0; q < st->n; ++q) st->pi[q] = st->n - 1 - q;
+    // the whole state is overwritten: restore the chosen initial layout
+    st->pi = st->pi_init;
     const uint64_t p = phys_of(st, x);
     for (auto &s : st->sh) {
         CUDA_TRY(cudaSetDevice(s.device));

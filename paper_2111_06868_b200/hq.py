@@ -85,6 +85,10 @@ def lib():
             "hq_schedule": [ctypes.c_int, ctypes.c_int, P, ctypes.c_size_t,
                             ctypes.POINTER(ctypes.POINTER(hq_op)), ctypes.POINTER(ctypes.c_size_t), P],
             "hq_free_ops": [P],
+            "hq_plan_layout": [ctypes.c_int, ctypes.c_int, ctypes.c_int, P, ctypes.c_size_t, P,
+                               ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)],
+            "hq_state_set_layout": [P, P],
+            "hq_state_get_layout": [P, P],
             "hq_sync": [P],
             "hq_stats_get": [P, ctypes.POINTER(hq_stats)],
             "hq_stats_reset": [P],
@@ -333,6 +337,27 @@ def hq_schedule(n, m, gates):
     finally:
         lib().hq_free_ops(ops)
     return res, [int(x) for x in pi[:n]]
+
+
+def hq_plan_layout(n, m, gates, dtype="c64"):
+    """Returns (pi list, model cost before, model cost after)."""
+    arr, ng, keep = _gate_array(gates)
+    pi = np.zeros(max(n, 1), dtype=np.int32)
+    cb, ca = ctypes.c_double(), ctypes.c_double()
+    _check(lib().hq_plan_layout(int(n), int(m), _dt(dtype), arr, ng, pi.ctypes.data,
+                                ctypes.byref(cb), ctypes.byref(ca)))
+    return [int(x) for x in pi[:n]], cb.value, ca.value
+
+
+def hq_state_set_layout(state, pi):
+    v = np.ascontiguousarray(pi, dtype=np.int32)
+    _check(lib().hq_state_set_layout(state.ptr, v.ctypes.data))
+
+
+def hq_state_get_layout(state):
+    v = np.zeros(state.n, dtype=np.int32)
+    _check(lib().hq_state_get_layout(state.ptr, v.ctypes.data))
+    return [int(x) for x in v]
 
 
 # ------------------------------------------------------------------ diagnostics

@@ -158,3 +158,21 @@ def test_schedule_errors():
     with pytest.raises(hq.HQError) as e:
         hq.hq_schedule(8, 0, [Gate("U", (8,), np.eye(2))])
     assert e.value.status == "HQ_ERR_QUBIT"
+
+
+@pytest.mark.parametrize("kmax", [4, 6])
+def test_plan_layout_is_permutation_and_improves(kmax):
+    fused = hq.hq_fuse(sycamore_circuit(34, 20, 3000), kmax)
+    pi, before, after = hq.hq_plan_layout(34, 0, fused)
+    assert sorted(pi) == list(range(34))
+    assert after <= before
+    if kmax == 6:
+        # no tensor-core pass gathers from more than 4 bits >= 20 (16 8-MB regions)
+        for q, _ in fused:
+            if len(q) >= 5:
+                assert sum(pi[x] >= 20 for x in q) <= 4
+
+
+def test_plan_layout_errors():
+    with pytest.raises(hq.HQError):
+        hq.hq_plan_layout(8, 0, [Gate("U", (9,), np.eye(2))])

@@ -299,3 +299,38 @@ def test_reversible_full_size_bit_exact():
     hq.hq_apply_circuit(s, gates)
     assert hq.hq_get_amplitudes(s, y, 1)[0] == 1.0
     assert hq.hq_norm(s) == 1.0
+
+
+# ---------------------------------------------------------------- qubit layouts
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_layout_invariance(dtype):
+    """Any logical->physical layout gives the same logical state (C14)."""
+    n = 20
+    gates = hq.hq_fuse(sycamore_circuit(n, 10, 8), 6)
+    want = O.simulate(n, [Gate("F", q, U) for q, U in gates])
+    rng = np.random.default_rng(5)
+    for trial in range(3):
+        pi = [int(x) for x in rng.permutation(n)] if trial else hq.hq_plan_layout(n, 0, gates, dtype)[0]
+        s = hq.hq_state_create(n, dtype, 1)
+        hq.hq_state_set_layout(s, pi)
+        assert hq.hq_state_get_layout(s) == pi
+        hq.hq_state_init_basis(s, 0)
+        c = hq.hq_circuit_create(s, gates)
+        hq.hq_circuit_run(s, c)
+        assert _err(hq.hq_get_amplitudes(s), want) <= TOL[dtype]
+        assert np.allclose(hq.hq_get_amplitudes(s, 1000, 64), want[1000:1064], atol=1e-5)
+
+
+def test_layout_bit_exact_permutations():
+    n = 18
+    gates = reversible_circuit(n, 80, 21, kmax=4)
+    psi0 = integer_state(n, 9)
+    want = O.simulate(n, gates, psi0)
+    pi = [int(x) for x in np.random.default_rng(1).permutation(n)]
+    s = hq.hq_state_create(n, "c64", 1)
+    hq.hq_state_set_layout(s, pi)
+    hq.hq_set_amplitudes(s, psi0)
+    hq.hq_apply_circuit(s, gates)
+    assert np.array_equal(hq.hq_get_amplitudes(s).astype(np.complex128), want)
+    with pytest.raises(hq.HQError):
+        hq.hq_state_set_layout(s, [0] * n)
