@@ -32,10 +32,10 @@ sys.path.insert(0, ROOT)
 
 CONFIGS = {
     # name: (n, cycles, seed, default kmax, BASELINE configs index)
-    "12q": (12, 10, 0, 4, 0),
+    "12q": (12, 10, 0, 6, 0),
     "30q": (30, 20, 1000, 2, 1),
-    "34q": (34, 20, 3000, 4, 3),
-    "36q": (36, 24, 4000, 4, 4),
+    "34q": (34, 20, 3000, 6, 3),
+    "36q": (36, 24, 4000, 6, 4),
 }
 
 

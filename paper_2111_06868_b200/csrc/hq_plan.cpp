@@ -226,23 +226,19 @@ void schedule(int n, int m, const std::vector<GateRef> &g, std::vector<int> &pi,
 
 // Estimated relative cost of one pass with physical targets `bits` (k of them)
 // for the kernel the executor will pick.  The
-// weights are the measured slowdowns of bench_sweep.py on a B200:
-//   SIMT (k <= 4): each target inside the warp-lane bit range [1, 6) costs a
+// weights follow the measured pass times of bench_sweep.py on a B200:
+//   SIMT (k <= 4): each target inside the warp-lane bit range costs a
 //     shuffle transpose (~10% per target at k = 4);
-//   tensor cores (complex64 k = 5, 6): gathers that span more than 16 distinct
-//     8 MB regions (targets at amplitude bit >= 20) fall off a cliff (0.66 ->
-//     0.53 -> 0.19 of HBM for 4, 5, 6 such targets); targets in [0, 6) make
-//     the tile loads less coalesced.
+//   tensor cores (complex64 k = 5, 6): warp lanes are gather sets, whose
+//     addresses are consecutive only when no target sits in the lowest bits;
+//     targets at bits 0..3 make the tile loads/stores poorly coalesced
+//     (k = 6 at bits 0..5: 0.30 of HBM vs ~0.9 elsewhere).
 double layout_pass_cost(int dtype, int k, const int *bits) {
     double c = 1.0;
     if (dtype == HQ_C64 && k >= 5) {
-        int hi = 0, lo = 0;
-        for (int j = 0; j < k; ++j) {
-            hi += bits[j] >= 20;
-            lo += bits[j] < 6;
-        }
-        if (hi > 4) c += hi == 5 ? 0.3 : 2.5;
-        c += 0.05 * lo;
+        int lo = 0;
+        for (int j = 0; j < k; ++j) lo += bits[j] < 4;
+        c += 0.25 * lo;
     } else {
         const int lane_lo = dtype == HQ_C64 ? 1 : 0, lane_hi = lane_lo + 5;
         for (int j = 0; j < k; ++j)

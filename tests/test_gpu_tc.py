@@ -83,3 +83,42 @@ def test_tc_sycamore_fused(kmax):
     hq.hq_apply_circuit(s, fused)
     err = np.linalg.norm(hq.hq_get_amplitudes(s).astype(np.complex128) - want)
     assert err <= 1e-4, err
+
+
+@pytest.mark.parametrize("k", [3, 4])
+def test_simt_many_passes_error_reference(k):
+    """Reference point for the TC error budget: the FP32 SIMT path on the same
+    kind of workload (60 Haar passes, n = 16)."""
+    n = 16
+    rng = np.random.default_rng(70 + k)
+    gates = []
+    for _ in range(60):
+        qs = tuple(int(q) for q in rng.choice(n, size=k, replace=False))
+        gates.append(Gate("U", qs, haar_unitary(k, rng)))
+    psi0 = random_state(n, 8)
+    want = O.simulate(n, gates, psi0)
+    s = _state(n, psi0)
+    hq.hq_apply_circuit(s, gates)
+    err = np.linalg.norm(hq.hq_get_amplitudes(s).astype(np.complex128) - want)
+    print("SIMT k=%d 60 passes: err %.3e" % (k, err))
+    assert err < 2e-5
+
+
+@pytest.mark.parametrize("kmax", [5, 6])
+def test_tc_long_circuit_vs_oracle(kmax):
+    """More tensor-core passes than any benchmark circuit (34q d20: 68, 36q
+    d24: ~85) on a 22-qubit Sycamore-style circuit of depth 56, with the
+    planned layout; the whole-state error must stay within the 1e-4 bound.
+    The per-pass error does not depend on n (relative per amplitude)."""
+    n = 22
+    gates = sycamore_circuit(n, 56, 5)
+    want = O.simulate(n, gates)
+    fused = hq.hq_fuse(gates, kmax)
+    assert sum(len(q) >= 5 for q, _ in fused) >= (90 if kmax == 6 else 8)
+    s = hq.hq_state_create(n, "c64", 1)
+    hq.hq_state_set_layout(s, hq.hq_plan_layout(n, 0, fused)[0])
+    hq.hq_state_init_basis(s, 0)
+    hq.hq_apply_circuit(s, fused)
+    err = np.linalg.norm(hq.hq_get_amplitudes(s).astype(np.complex128) - want)
+    print("22q d56 kmax=%d passes=%d err=%.3e" % (kmax, len(fused), err))
+    assert err <= 1e-4
