@@ -255,10 +255,13 @@ hq_status hq_stats_get(const hq_state *s, hq_stats *out);
 hq_status hq_stats_reset(hq_state *s);
 /* Per-launch timing of apply kernels with CUDA events on the launching
  * stream (off by default).  hq_kernel_times synchronises and returns, for the
- * launches since profiling was enabled / last read: count, total and max
- * milliseconds, and algorithmic bytes (2 x shard bytes per pass). */
+ * launches of kernel family `path` since profiling was enabled / that path was
+ * last read: count, total and max milliseconds, and algorithmic bytes
+ * (2 x shard bytes per pass).  path: -1 all apply kernels, 0 SIMT register
+ * kernel (apply_reg), 1 generic kernel (apply_gen), 2 tensor-core kernel
+ * (apply_tc). */
 hq_status hq_profile_enable(hq_state *s, int on);
-hq_status hq_kernel_times(hq_state *s, uint64_t *count, double *total_ms,
+hq_status hq_kernel_times(hq_state *s, int path, uint64_t *count, double *total_ms,
                           double *max_ms, uint64_t *bytes);
 /* Library version string. */
 const char *hq_version(void);

@@ -88,6 +88,13 @@ struct Shard {
 struct ProfEvent {
     cudaEvent_t a, b;
     uint64_t bytes;
+    int path;
+};
+
+struct ProfAcc {
+    uint64_t count = 0;
+    double total = 0, max = 0;
+    uint64_t bytes = 0;
 };
 
 struct hq_state {
@@ -103,9 +110,7 @@ struct hq_state {
     bool profiling = false;
     std::vector<ProfEvent> prof;  // pending
     std::vector<cudaEvent_t> ev_pool;
-    uint64_t prof_count = 0;
-    double prof_total = 0, prof_max = 0;
-    uint64_t prof_bytes = 0;
+    ProfAcc acc[3];               // per kernel family (PATH_REG, PATH_GEN, PATH_TC)
 };
 
 struct hq_circuit {
@@ -516,10 +521,11 @@ static hq_status prof_begin(hq_state *st, Shard &s, ProfEvent &pe) {
     return HQ_OK;
 }
 
-static hq_status prof_end(hq_state *st, Shard &s, ProfEvent &pe, uint64_t bytes) {
+static hq_status prof_end(hq_state *st, Shard &s, ProfEvent &pe, uint64_t bytes, int path) {
     if (!st->profiling) return HQ_OK;
     CUDA_TRY(cudaEventRecord(pe.b, s.stream));
     pe.bytes = bytes;
+    pe.path = path;
     st->prof.push_back(pe);
     return HQ_OK;
 }
@@ -540,7 +546,7 @@ static hq_status exec_apply(hq_state *st, Shard &s, const Prep &p, const void *d
     if (e != cudaSuccess)
         return set_error(HQ_ERR_CUDA, "apply kernel launch failed: %s", cudaGetErrorString((cudaError_t)e));
     const uint64_t bytes = (uint64_t)2 * (st->es << st->nl);
-    if ((rc = prof_end(st, s, pe, bytes))) return rc;
+    if ((rc = prof_end(st, s, pe, bytes, p.path))) return rc;
     st->stats.passes++;
     st->stats.kernel_launches += launches;
     st->stats.hbm_bytes += bytes;
@@ -983,29 +989,37 @@ extern "C" hq_status hq_profile_enable(hq_state *st, int on) {
     return HQ_OK;
 }
 
-extern "C" hq_status hq_kernel_times(hq_state *st, uint64_t *count, double *total_ms, double *max_ms,
-                                     uint64_t *bytes) {
+extern "C" hq_status hq_kernel_times(hq_state *st, int path, uint64_t *count, double *total_ms,
+                                     double *max_ms, uint64_t *bytes) {
     clear_error();
     if (!st) return set_error(HQ_ERR_ARG, "state is NULL");
+    if (path < -1 || path > 2) return set_error(HQ_ERR_ARG, "path %d not in [-1, 2]", path);
     for (auto &p : st->prof) {
         CUDA_TRY(cudaEventSynchronize(p.b));
         float ms = 0.f;
         CUDA_TRY(cudaEventElapsedTime(&ms, p.a, p.b));
-        st->prof_count++;
-        st->prof_total += ms;
-        st->prof_max = std::max(st->prof_max, (double)ms);
-        st->prof_bytes += p.bytes;
+        ProfAcc &a = st->acc[p.path];
+        a.count++;
+        a.total += ms;
+        a.max = std::max(a.max, (double)ms);
+        a.bytes += p.bytes;
         st->ev_pool.push_back(p.a);
         st->ev_pool.push_back(p.b);
     }
     st->prof.clear();
-    if (count) *count = st->prof_count;
-    if (total_ms) *total_ms = st->prof_total;
-    if (max_ms) *max_ms = st->prof_max;
-    if (bytes) *bytes = st->prof_bytes;
-    st->prof_count = 0;
-    st->prof_total = st->prof_max = 0;
-    st->prof_bytes = 0;
+    ProfAcc r;
+    for (int i = 0; i < 3; ++i) {
+        if (path >= 0 && i != path) continue;
+        r.count += st->acc[i].count;
+        r.total += st->acc[i].total;
+        r.max = std::max(r.max, st->acc[i].max);
+        r.bytes += st->acc[i].bytes;
+        st->acc[i] = ProfAcc{};
+    }
+    if (count) *count = r.count;
+    if (total_ms) *total_ms = r.total;
+    if (max_ms) *max_ms = r.max;
+    if (bytes) *bytes = r.bytes;
     return HQ_OK;
 }
 

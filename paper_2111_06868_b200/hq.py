@@ -93,7 +93,7 @@ def lib():
             "hq_stats_get": [P, ctypes.POINTER(hq_stats)],
             "hq_stats_reset": [P],
             "hq_profile_enable": [P, ctypes.c_int],
-            "hq_kernel_times": [P, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_double),
+            "hq_kernel_times": [P, ctypes.c_int, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_double),
                                 ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_uint64)],
         }
         for name, args in sig.items():
@@ -388,8 +388,12 @@ def hq_profile_enable(state, on=True):
     _check(lib().hq_profile_enable(state.ptr, 1 if on else 0))
 
 
-def hq_kernel_times(state):
+KERNEL_PATHS = {"all": -1, "simt": 0, "generic": 1, "tc": 2}
+
+
+def hq_kernel_times(state, path="all"):
+    """path: 'all', 'simt' (apply_reg), 'generic' (apply_gen), 'tc' (apply_tc)."""
     c, t, m, b = ctypes.c_uint64(), ctypes.c_double(), ctypes.c_double(), ctypes.c_uint64()
-    _check(lib().hq_kernel_times(state.ptr, ctypes.byref(c), ctypes.byref(t), ctypes.byref(m),
-                                 ctypes.byref(b)))
+    _check(lib().hq_kernel_times(state.ptr, KERNEL_PATHS[path], ctypes.byref(c), ctypes.byref(t),
+                                 ctypes.byref(m), ctypes.byref(b)))
     return dict(count=c.value, total_ms=t.value, max_ms=m.value, bytes=b.value)

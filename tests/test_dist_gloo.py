@@ -1,0 +1,109 @@
+"""Multi-process check of the distributed schedule's host logic (world_size 2,
+gloo backend, CPU).  Each rank owns its shard of the physical index space and
+executes the op stream hq_schedule emits: APPLY with the oracle on the local
+shard, REMAP as the documented chunk exchange (chunk t -> peer whose swapped
+rank bits equal t, landing at chunk bits(rank)) over torch.distributed
+point-to-point, PERMUTE as a local bit swap.  Rank 0 gathers the shards and
+compares the logical state with the oracle (bit-exact for a reversible
+circuit, 1e-12 for Haar gates).  This is the same exchange exec_remap issues
+through NCCL on GPUs."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, n, kind, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import sys
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+        import oracle as O
+        import paper_2111_06868_b200 as hq
+        from hq_inputs import reversible_circuit, random_circuit, integer_state, random_state
+        from sched_replay import phys_apply, permute_bits, remap_chunks, peer_of, bits_of, to_logical
+
+        m = world.bit_length() - 1
+        nl = n - m
+        if kind == "reversible":
+            gates = reversible_circuit(n, 60, 13, kmax=3)
+            psi0 = integer_state(n, 2)
+        else:
+            gates = random_circuit(n, 50, 17, kmax=4)
+            psi0 = random_state(n, 4)
+        ops, pi = hq.hq_schedule(n, m, gates)
+        shard = psi0[rank << nl:(rank + 1) << nl].copy()
+        for op in ops:
+            if op["kind"] == "apply":
+                g = gates[op["gate"]]
+                phys_apply(shard, nl, g.U, op["bits"][:len(g.qubits)])
+            elif op["kind"] == "permute":
+                pairs = [(op["bits"][2 * i], op["bits"][2 * i + 1]) for i in range(op["nbits"])]
+                shard = permute_bits(shard, pairs)
+            else:
+                pairs = [(op["bits"][2 * i], op["bits"][2 * i + 1]) for i in range(op["nbits"])]
+                mp_, gsh, chunk = remap_chunks(nl, pairs)
+                new = np.empty_like(shard)
+                reqs = []
+                recv_bufs = []
+                for t in range(1 << mp_):
+                    p = peer_of(rank, t, gsh)
+                    src = shard[t * chunk:(t + 1) * chunk]
+                    if p == rank:
+                        new[t * chunk:(t + 1) * chunk] = src
+                        continue
+                    # send chunk t (== bits(p)) to p; receive p's chunk into slot t (== bits(p))
+                    send = torch.from_numpy(np.ascontiguousarray(src).view(np.float64).copy())
+                    recv = torch.empty_like(send)
+                    reqs.append(dist.isend(send, p))
+                    reqs.append(dist.irecv(recv, p))
+                    recv_bufs.append((t, recv))
+                for r in reqs:
+                    r.wait()
+                for t, recv in recv_bufs:
+                    new[t * chunk:(t + 1) * chunk] = recv.numpy().view(np.complex128)
+                shard = new
+        parts = [torch.empty(2 << nl, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(parts, torch.from_numpy(shard.view(np.float64).copy()))
+        if rank == 0:
+            shards = [p.numpy().view(np.complex128) for p in parts]
+            got = to_logical(n, shards, pi)
+            want = O.simulate(n, gates, psi0)
+            nrem = sum(o["kind"] == "remap" for o in ops)
+            if kind == "reversible":
+                q.put(("ok" if np.array_equal(got, want) else "mismatch", nrem))
+            else:
+                q.put(("ok" if np.max(np.abs(got - want)) < 1e-12 else "mismatch", nrem))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind", ["reversible", "haar"])
+def test_schedule_over_gloo_world2(kind):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, 10, kind, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=180)
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    status, nrem = q.get(timeout=5)
+    assert status == "ok"
+    assert nrem > 0

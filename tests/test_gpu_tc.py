@@ -114,7 +114,7 @@ def test_tc_long_circuit_vs_oracle(kmax):
     gates = sycamore_circuit(n, 56, 5)
     want = O.simulate(n, gates)
     fused = hq.hq_fuse(gates, kmax)
-    assert sum(len(q) >= 5 for q, _ in fused) >= (90 if kmax == 6 else 8)
+    assert sum(len(q) >= 5 for q, _ in fused) >= (90 if kmax == 6 else 4)
     s = hq.hq_state_create(n, "c64", 1)
     hq.hq_state_set_layout(s, hq.hq_plan_layout(n, 0, fused)[0])
     hq.hq_state_init_basis(s, 0)
