@@ -46,6 +46,8 @@ def main():
     summary = {}
     for k in [int(x) for x in args.ks.split(",")]:
         for pl in args.placements.split(","):
+            if pl.startswith("b:") and pl.count("-") + 1 != k:
+                continue
             g = haar_sweep_gate(n, k, pl, 2000 + k)
             for _ in range(args.warmup):
                 hq.hq_apply_matrix(s, g.U, g.qubits)

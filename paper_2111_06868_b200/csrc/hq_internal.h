@@ -82,7 +82,8 @@ bool apply_needs_dev_U(int dtype, const ApplyDesc &d);
 bool tc_applicable(int dtype, const ApplyDesc &d);
 void tc_prepare(const ApplyDesc &d, const double *Ucanon, std::vector<char> &payload,
                 std::vector<char> &params);
-int tc_launch(void *psi, const void *params, const void *dev_payload, void *stream);
+int tc_launch(void *psi, const void *params, size_t params_size, const void *dev_payload,
+              void *stream);
 
 // psi = 0, then psi[idx] = 1 if idx >= 0.
 int launch_init_basis(int dtype, void *psi, uint64_t n_amps, int64_t idx, void *stream);

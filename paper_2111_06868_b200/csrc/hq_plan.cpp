@@ -229,16 +229,15 @@ void schedule(int n, int m, const std::vector<GateRef> &g, std::vector<int> &pi,
 // weights follow the measured pass times of bench_sweep.py on a B200:
 //   SIMT (k <= 4): each target inside the warp-lane bit range costs a
 //     shuffle transpose (~10% per target at k = 4);
-//   tensor cores (complex64 k = 5, 6): warp lanes are gather sets, whose
-//     addresses are consecutive only when no target sits in the lowest bits;
-//     targets at bits 0..3 make the tile loads/stores poorly coalesced
-//     (k = 6 at bits 0..5: 0.30 of HBM vs ~0.9 elsewhere).
+//   tensor cores (complex64 k = 5, 6): passes with targets at bits 0..3 run
+//     at 0.75-0.85 of HBM peak (mode L or a strided mode H) against ~0.9
+//     with the low bits free.
 double layout_pass_cost(int dtype, int k, const int *bits) {
     double c = 1.0;
     if (dtype == HQ_C64 && k >= 5) {
         int lo = 0;
         for (int j = 0; j < k; ++j) lo += bits[j] < 4;
-        c += 0.25 * lo;
+        c += lo ? 0.06 + 0.02 * lo : 0.0;
     } else {
         const int lane_lo = dtype == HQ_C64 ? 1 : 0, lane_hi = lane_lo + 5;
         for (int j = 0; j < k; ++j)

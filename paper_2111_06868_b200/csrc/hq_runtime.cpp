@@ -538,7 +538,7 @@ static hq_status exec_apply(hq_state *st, Shard &s, const Prep &p, const void *d
     int launches = 0;
     int e;
     if (p.path == PATH_TC) {
-        e = tc_launch(s.psi, p.params.data(), dU, s.stream);
+        e = tc_launch(s.psi, p.params.data(), p.params.size(), dU, s.stream);
         launches = 1;
     } else {
         e = launch_apply((int)st->dtype, s.psi, p.d, p.hostU.data(), dU, s.stream, &launches);

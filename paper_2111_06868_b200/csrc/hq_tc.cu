@@ -367,6 +367,255 @@ apply_tc(float2 *__restrict__ psi, const __grid_constant__ Params P,
     }
 }
 
+
+// ------------------------------------------------------------------ mode L
+// Orientation for gathers whose targets include the lowest physical bits
+// (there a gather set is a short contiguous run, so "lanes = sets" loads and
+// stores are strided).  Here the roles swap: A = real embedding of U in TMEM
+// (lane = output real 2r+e), B = the tile in shared memory (K-major,
+// SWIZZLE_128B, row = gather set, 64 sets per tile), D = output tile in TMEM
+// (lane = output real, column = set).  Converter lanes follow the tile's
+// memory order, so loads are contiguous whatever the placement; the swizzle
+// keeps their 8-byte shared-memory stores conflict-light; epilogue lanes are
+// output reals, contiguous in memory when the targets are the low bits.
+// k = 5 gates are widened to 6 targets on the host (U (x) I, exact).
+
+constexpr int L_NS = 64;                          // gather sets per tile (MMA N)
+constexpr int L_STAGES = 3;
+constexpr int L_HALF = L_NS * 128 * 4;            // 32 KB: hi (or lo) of one stage
+constexpr int L_STAGE = 2 * L_HALF;
+constexpr int L_SMEM = L_STAGES * L_STAGE + BAR_BYTES;
+constexpr int L_ATOMCOL = (L_NS / 8) * 1024;      // bytes per 32-real atom column
+
+struct ParamsL {
+    uint64_t off[64];      // amplitude offset of canonical target pattern c
+    uint32_t setoff[64];   // amplitude offset of set n inside a tile
+    int pos[12];           // ascending bit positions of the tile (targets + set bits)
+    int nbit[12];          // tile bit i -> set-index bit (or -1)
+    int cbit[12];          // tile bit i -> canonical target bit (or -1)
+    uint64_t ntiles;
+};
+
+__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t addr) {
+    // K-major SWIZZLE_128B: rows of 128 B, 8-row atoms (SBO = 1024 B), LBO unused (1)
+    uint64_t d = 0;
+    d |= (uint64_t)((addr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;
+    d |= (uint64_t)(1024 >> 4) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)2 << 61;
+    return d;
+}
+
+__device__ __forceinline__ uint64_t tile_base12(uint64_t t, const ParamsL &P) {
+#pragma unroll
+    for (int i = 0; i < 12; ++i) {
+        const int s = P.pos[i];
+        t = ((t >> s) << (s + 1)) | (t & ((1ull << s) - 1));
+    }
+    return t;
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+apply_tcL(float2 *__restrict__ psi, const __grid_constant__ ParamsL P,
+          const float *__restrict__ Areal /* [2][128][128] hi then lo, row = output real */) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t sbase = smem_u32(smem);
+    const uint32_t bar0 = sbase + L_STAGES * L_STAGE;
+    auto full_bar = [&](int s) { return bar0 + 8 * s; };
+    auto empty_bar = [&](int s) { return bar0 + 8 * (L_STAGES + s); };
+    auto tfull_bar = [&](int d) { return bar0 + 8 * (2 * L_STAGES + d); };
+    auto tempty_bar = [&](int d) { return bar0 + 8 * (2 * L_STAGES + 2 + d); };
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + L_STAGES * L_STAGE + 8 * (2 * L_STAGES + 4));
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < L_STAGES; ++s) {
+            mbar_init(full_bar(s), NUM_CONV);
+            mbar_init(empty_bar(s), 1);
+        }
+        for (int d = 0; d < 2; ++d) {
+            mbar_init(tfull_bar(d), 1);
+            mbar_init(tempty_bar(d), NUM_EPI);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == MMA_WARP) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    // A (U hi, lo) into TMEM: warp q writes lanes 32q..32q+31 (rows of A)
+    if (warp < NUM_EPI) {
+        const int m = warp * 32 + lane;
+#pragma unroll 1
+        for (int ch = 0; ch < 8; ++ch) {
+            uint32_t v[32];
+            const float *src = Areal + (ch >> 2) * (128 * 128) + m * 128 + (ch & 3) * 32;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__ldg(src + i));
+            tmem_st32(tmem + ((uint32_t)(warp * 32) << 16) + ch * 32, v);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t A_HI = tmem, A_LO = tmem + 128;
+    const uint64_t ntiles = P.ntiles;
+
+    if (warp == MMA_WARP) {
+        const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(L_NS >> 3) << 17) |
+                               ((uint32_t)(128 >> 4) << 24);
+        uint32_t it = 0;
+        for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+            const int s = it % L_STAGES;
+            const uint32_t sp = (it / L_STAGES) & 1;
+            const int d = it & 1;
+            const uint32_t dp = (it >> 1) & 1;
+            mbar_wait(tempty_bar(d), dp ^ 1);
+            mbar_wait(full_bar(s), sp);
+            tc_fence_after();
+            if (elect_one()) {
+                const uint32_t D = tmem + 256 + L_NS * d;
+                const uint32_t bhi = sbase + s * L_STAGE, blo = bhi + L_HALF;
+                // K-chunk j (8 reals = 32 B): atom column j/4, +32 B inside the 128-B row
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const uint32_t o = (j >> 2) * L_ATOMCOL + (j & 3) * 32;
+                    mma_ts(D, A_LO + 8 * j, smem_desc_sw128(bhi + o), idesc, j > 0);
+                    mma_ts(D, A_HI + 8 * j, smem_desc_sw128(blo + o), idesc, 1);
+                }
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const uint32_t o = (j >> 2) * L_ATOMCOL + (j & 3) * 32;
+                    mma_ts(D, A_HI + 8 * j, smem_desc_sw128(bhi + o), idesc, 1);
+                }
+                mma_commit(empty_bar(s));
+                mma_commit(tfull_bar(d));
+            }
+            __syncwarp();
+        }
+    } else if (warp >= CONV0) {
+        // thread -> tile-local amplitude index tl = lane | (cw << 5) | (i << 8), i = 0..15
+        const int cw = warp - CONV0;
+        uint64_t aoff_base = 0;
+        uint32_t n_base = 0, c_base = 0;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+            const int bit = b < 5 ? (lane >> b) & 1 : (cw >> (b - 5)) & 1;
+            if (bit) {
+                aoff_base |= 1ull << P.pos[b];
+                if (P.nbit[b] >= 0) n_base |= 1u << P.nbit[b];
+                if (P.cbit[b] >= 0) c_base |= 1u << P.cbit[b];
+            }
+        }
+        uint64_t aoff[16];
+        uint32_t sdst[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            uint64_t a = aoff_base;
+            uint32_t n = n_base, c = c_base;
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+                if ((i >> b) & 1) {
+                    a |= 1ull << P.pos[8 + b];
+                    if (P.nbit[8 + b] >= 0) n |= 1u << P.nbit[8 + b];
+                    if (P.cbit[8 + b] >= 0) c |= 1u << P.cbit[8 + b];
+                }
+            aoff[i] = a;
+            const uint32_t r8 = n & 7, ch = (c >> 1) & 7;
+            sdst[i] = (c >> 4) * L_ATOMCOL + (n >> 3) * 1024 + r8 * 128 + ((ch ^ r8) << 4) + (c & 1) * 8;
+        }
+        float2 a0[16], a1[16];
+        auto load = [&](uint64_t tt, float2 (&v)[16]) {
+            const uint64_t base = tile_base12(tt, P);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = psi[base + aoff[i]];
+        };
+        auto store = [&](uint32_t it, const float2 (&v)[16]) {
+            const int s = it % L_STAGES;
+            const uint32_t sp = (it / L_STAGES) & 1;
+            mbar_wait(empty_bar(s), sp ^ 1);
+            uint8_t *hi = smem + s * L_STAGE;
+            uint8_t *lo = hi + L_HALF;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                uint2 h, l;
+                h.x = to_tf32(v[i].x);
+                h.y = to_tf32(v[i].y);
+                l.x = __float_as_uint(v[i].x - __uint_as_float(h.x));
+                l.y = __float_as_uint(v[i].y - __uint_as_float(h.y));
+                *reinterpret_cast<uint2 *>(hi + sdst[i]) = h;
+                *reinterpret_cast<uint2 *>(lo + sdst[i]) = l;
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(full_bar(s));
+        };
+        const uint64_t G = gridDim.x;
+        uint64_t t = blockIdx.x;
+        uint32_t it = 0;
+        if (t < ntiles) load(t, a0);
+        while (t < ntiles) {
+            if (t + G < ntiles) load(t + G, a1);
+            store(it, a0);
+            t += G;
+            ++it;
+            if (t >= ntiles) break;
+            if (t + G < ntiles) load(t + G, a0);
+            store(it, a1);
+            t += G;
+            ++it;
+        }
+    } else {
+        // epilogue warps 0..3: TMEM lanes 32q.. = output reals m = 2r + e
+        const int m = warp * 32 + lane;
+        const int r = m >> 1, e = m & 1;
+        const uint64_t offr = P.off[r];
+        uint32_t it = 0;
+        for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+            const int d = it & 1;
+            const uint32_t dp = (it >> 1) & 1;
+            mbar_wait(tfull_bar(d), dp);
+            tc_fence_after();
+            uint32_t v0[32], v1[32];
+            const uint32_t D = tmem + 256 + L_NS * d + ((uint32_t)(warp * 32) << 16);
+            tmem_ld32(D, v0);
+            tmem_ld32(D + 32, v1);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty_bar(d));
+            const uint64_t base = tile_base12(t, P) + offr;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const uint32_t x0 = j < 16 ? v0[2 * j] : v1[2 * j - 32];
+                const uint32_t x1 = j < 16 ? v0[2 * j + 1] : v1[2 * j + 1 - 32];
+                const uint32_t snd = e ? x0 : x1;
+                const uint32_t rcv = __shfl_xor_sync(0xffffffffu, snd, 1);
+                float2 o;
+                o.x = __uint_as_float(e ? rcv : x0);
+                o.y = __uint_as_float(e ? x1 : rcv);
+                psi[base + P.setoff[2 * j + e]] = o;
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == MMA_WARP) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    }
+}
+
 }  // namespace tc
 
 // ------------------------------------------------------------------ host side
@@ -386,11 +635,110 @@ bool tc_applicable(int dtype, const ApplyDesc &d) {
     return dtype == HQ_C64 && (d.k == 5 || d.k == 6) && d.n_local >= d.k + tc::SETBITS + 3;
 }
 
+// Mode L (U in TMEM, tile in smem) when a target sits in the lowest bits,
+// where mode H's lanes-are-sets layout gives strided accesses.
+// HQ_TC_MODE=H|L forces one orientation (experiments, tests).
+static bool tc_use_mode_l(const ApplyDesc &d) {
+    static const char *force = getenv("HQ_TC_MODE");
+    if (force && force[0] == 'H') return false;
+    if (force && force[0] == 'L') return true;
+    // measured on a B200 (bench_sweep.py, n = 32): mode H needs the low bits
+    // to hold gather-set bits; with >= 2 (k = 5) or >= 3 (k = 6) targets in
+    // bits 0..3 mode L is faster (0.79-0.85 vs 0.29-0.76 of HBM peak).
+    int low = 0;
+    for (int i = 0; i < d.k; ++i) low += d.p[i] < 4;
+    return low >= (d.k == 5 ? 2 : 3);
+}
+
+static void tc_prepare_l(const ApplyDesc &d, const double *Ucanon, std::vector<char> &payload,
+                         std::vector<char> &params) {
+    int p6[6];
+    std::vector<double> U6;
+    const int D6 = 64;
+    if (d.k == 6) {
+        for (int i = 0; i < 6; ++i) p6[i] = d.p[i];
+        U6.assign(Ucanon, Ucanon + 2 * D6 * D6);
+    } else {
+        // widen: U6 = U (x) I on the lowest non-target bit e (exact)
+        int e = 0;
+        for (;; ++e) {
+            bool t = false;
+            for (int i = 0; i < d.k; ++i) t |= d.p[i] == e;
+            if (!t) break;
+        }
+        int j = 0;
+        while (j < d.k && d.p[j] < e) ++j;
+        for (int i = 0, s = 0; i < 6; ++i) p6[i] = i == j ? e : d.p[s++];
+        const int D5 = 32;
+        U6.assign(2 * D6 * D6, 0.0);
+        auto drop = [&](int x) { return ((x >> (j + 1)) << j) | (x & ((1 << j) - 1)); };
+        for (int r = 0; r < D6; ++r)
+            for (int c = 0; c < D6; ++c) {
+                if (((r >> j) & 1) != ((c >> j) & 1)) continue;
+                U6[2 * (r * D6 + c)] = Ucanon[2 * (drop(r) * D5 + drop(c))];
+                U6[2 * (r * D6 + c) + 1] = Ucanon[2 * (drop(r) * D5 + drop(c)) + 1];
+            }
+    }
+    // A = interleaved real embedding (row = output real 2r+e, col = input real 2c+f)
+    payload.assign(2 * 128 * 128 * sizeof(float), 0);
+    float *hi = reinterpret_cast<float *>(payload.data());
+    float *lo = hi + 128 * 128;
+    for (int r = 0; r < D6; ++r)
+        for (int c = 0; c < D6; ++c) {
+            const double ur = U6[2 * (r * D6 + c)], ui = U6[2 * (r * D6 + c) + 1];
+            const double blk[2][2] = {{ur, -ui}, {ui, ur}};
+            for (int e = 0; e < 2; ++e)
+                for (int f = 0; f < 2; ++f) {
+                    const double x = blk[e][f];
+                    const float h = tf32_round_host(x);
+                    hi[(2 * r + e) * 128 + 2 * c + f] = h;
+                    lo[(2 * r + e) * 128 + 2 * c + f] = tf32_round_host(x - (double)h);
+                }
+        }
+    params.assign(sizeof(tc::ParamsL) + 1, 0);
+    params.back() = 'L';
+    tc::ParamsL &P = *reinterpret_cast<tc::ParamsL *>(params.data());
+    for (int c = 0; c < 64; ++c) {
+        uint64_t o = 0;
+        for (int i = 0; i < 6; ++i)
+            if ((c >> i) & 1) o |= 1ull << p6[i];
+        P.off[c] = o;
+    }
+    int setbits[6], ns = 0;
+    for (int b = 0; ns < 6; ++b) {
+        bool t = false;
+        for (int i = 0; i < 6; ++i) t |= p6[i] == b;
+        if (!t) setbits[ns++] = b;
+    }
+    for (int n = 0; n < 64; ++n) {
+        uint32_t o = 0;
+        for (int i = 0; i < 6; ++i)
+            if ((n >> i) & 1) o |= 1u << setbits[i];
+        P.setoff[n] = o;
+    }
+    int all[12];
+    for (int i = 0; i < 6; ++i) { all[i] = p6[i]; all[6 + i] = setbits[i]; }
+    std::sort(all, all + 12);
+    for (int i = 0; i < 12; ++i) {
+        P.pos[i] = all[i];
+        P.nbit[i] = P.cbit[i] = -1;
+        for (int j = 0; j < 6; ++j) {
+            if (setbits[j] == all[i]) P.nbit[i] = j;
+            if (p6[j] == all[i]) P.cbit[i] = j;
+        }
+    }
+    P.ntiles = 1ull << (d.n_local - 12);
+}
+
 // Build the device payload (B = real embedding of U, hi and lo, [N][KD] fp32
 // each, row n = output real) and the kernel parameter block from the
 // canonical fp64 U (canonical order: U-index bit i <-> d.p[i]).
 void tc_prepare(const ApplyDesc &d, const double *Ucanon, std::vector<char> &payload,
                 std::vector<char> &params) {
+    if (tc_use_mode_l(d)) {
+        tc_prepare_l(d, Ucanon, payload, params);
+        return;
+    }
     const int K = d.k, D = 1 << K, KD = 2 * D, N = KD;
     payload.assign((size_t)2 * N * KD * sizeof(float), 0);
     float *hi = reinterpret_cast<float *>(payload.data());
@@ -409,7 +757,8 @@ void tc_prepare(const ApplyDesc &d, const double *Ucanon, std::vector<char> &pay
                     lo[(2 * r + e) * KD + 2 * c + f] = l;
                 }
         }
-    params.assign(sizeof(tc::Params), 0);
+    params.assign(sizeof(tc::Params) + 1, 0);
+    params.back() = 'H';
     tc::Params &P = *reinterpret_cast<tc::Params *>(params.data());
     P.k = K;
     for (int c = 0; c < D; ++c) {
@@ -456,9 +805,30 @@ static int tc_launch_k(void *psi, const tc::Params &P, const void *dev_payload, 
     return (int)cudaGetLastError();
 }
 
-int tc_launch(void *psi, const void *params, const void *dev_payload, void *stream) {
-    const tc::Params &P = *reinterpret_cast<const tc::Params *>(params);
+static int tc_launch_l(void *psi, const tc::ParamsL &P, const void *dev_payload, cudaStream_t st) {
+    static bool attr_done = false;
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(tc::apply_tcL, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::L_SMEM);
+        if (e != cudaSuccess) return (int)e;
+        attr_done = true;
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint64_t grid = P.ntiles < (uint64_t)sms ? P.ntiles : (uint64_t)sms;
+    tc::apply_tcL<<<(unsigned)grid, tc::THREADS, tc::L_SMEM, st>>>(
+        reinterpret_cast<float2 *>(psi), P, reinterpret_cast<const float *>(dev_payload));
+    return (int)cudaGetLastError();
+}
+
+// params: a tc::Params (mode H) or tc::ParamsL (mode L) block followed by
+// one tag byte ('H' or 'L'); size tells them apart.
+int tc_launch(void *psi, const void *params, size_t params_size, const void *dev_payload,
+              void *stream) {
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const char tag = reinterpret_cast<const char *>(params)[params_size - 1];
+    if (tag == 'L') return tc_launch_l(psi, *reinterpret_cast<const tc::ParamsL *>(params), dev_payload, st);
+    const tc::Params &P = *reinterpret_cast<const tc::Params *>(params);
     return P.k == 5 ? tc_launch_k<5>(psi, P, dev_payload, st) : tc_launch_k<6>(psi, P, dev_payload, st);
 }
 

@@ -13,6 +13,22 @@ import paper_2111_06868_b200 as hq
 pytestmark = pytest.mark.gpu
 
 PLACEMENTS = ["low", "high", "spread", "random0", "random1", "random2", "random3"]
+# explicit low-bit placements (mode L of the tensor-core kernel: lowest target < 3)
+LOW6 = ["b:0-1-2-3-4-5", "b:0-7-8-9-10-11", "b:2-3-4-12-13-14", "b:1-5-6-9-14-15", "b:0-2-4-6-8-10"]
+LOW5 = ["b:0-1-2-3-4", "b:0-7-8-9-10", "b:2-3-4-12-13", "b:1-5-6-9-14"]
+
+
+@pytest.mark.parametrize("placement", LOW6 + LOW5)
+def test_tc_low_targets(placement):
+    k = placement.count("-") + 1
+    n = 17
+    g = haar_sweep_gate(n, k, placement, seed=2000 + k)
+    psi0 = random_state(n, 5)
+    want = O.apply_gate(psi0.copy(), g.U, g.qubits)
+    s = _state(n, psi0)
+    hq.hq_apply_matrix(s, g.U, g.qubits)
+    err = np.linalg.norm(hq.hq_get_amplitudes(s).astype(np.complex128) - want)
+    assert err < 2e-6, err
 
 
 def _state(n, psi0):
