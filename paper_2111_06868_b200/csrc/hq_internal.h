@@ -84,6 +84,9 @@ void tc_prepare(const ApplyDesc &d, const double *Ucanon, std::vector<char> &pay
                 std::vector<char> &params);
 int tc_launch(void *psi, const void *params, size_t params_size, const void *dev_payload,
               void *stream);
+// Set the FP16 input scale of a mode-H parameter block from a rigorous upper
+// bound on max |amplitude| of the state the pass will read.
+void tc_set_amp_bound(std::vector<char> &params, double bound);
 
 // psi = 0, then psi[idx] = 1 if idx >= 0.
 int launch_init_basis(int dtype, void *psi, uint64_t n_amps, int64_t idx, void *stream);

@@ -106,6 +106,10 @@ struct hq_state {
     std::vector<Shard> sh;
     std::vector<int> pi;          // logical qubit -> physical bit
     std::vector<int> pi_init;     // layout restored by hq_state_init_basis
+    // Rigorous upper bound on ||psi||_2 (hence on every |amplitude|), kept
+    // through every pass from per-gate spectral-norm bounds; the FP16 tensor-
+    // core path scales the state into range with it.  < 0: unknown.
+    double amp_bound = -1.0;
     hq_stats stats{};
     bool profiling = false;
     std::vector<ProfEvent> prof;  // pending
@@ -478,15 +482,40 @@ enum { PATH_REG = 0, PATH_GEN = 1, PATH_TC = 2 };
 
 struct Prep {
     ApplyDesc d;
+    double gnorm = 1.0;          // upper bound on the spectral norm of U
     int path = PATH_GEN;
     std::vector<char> hostU;     // canonical U in the state dtype (RN from fp64)
     std::vector<char> payload;   // bytes the kernel reads from device memory
     std::vector<char> params;    // TC parameter block
 };
 
+// Upper bound on ||U||_2: sqrt of the Gershgorin bound on lambda_max(U^H U)
+// (max_i sum_j |(U^H U)_ij|), times a small slack for the FP32 rounding of the
+// pass.  Tight (1 + ~1e-15) for unitary U; rigorous for any U.
+static double spectral_bound(const double *U, int k) {
+    const int D = 1 << k;
+    double worst = 0.0;
+    for (int i = 0; i < D; ++i) {
+        double row = 0.0;
+        for (int j = 0; j < D; ++j) {
+            double re = 0.0, im = 0.0;     // (U^H U)_ij = sum_r conj(U_ri) U_rj
+            for (int r = 0; r < D; ++r) {
+                const double ar = U[2 * (r * D + i)], ai = -U[2 * (r * D + i) + 1];
+                const double br = U[2 * (r * D + j)], bi = U[2 * (r * D + j) + 1];
+                re += ar * br - ai * bi;
+                im += ar * bi + ai * br;
+            }
+            row += std::sqrt(re * re + im * im);
+        }
+        worst = std::max(worst, row);
+    }
+    return std::sqrt(worst) * (1.0 + 1e-5);
+}
+
 static void prepare(hq_dtype dt, const double *U, int k, const int *phys, int nl, Prep &p) {
     std::vector<double> Uc;
     canonical_U64(U, k, phys, p.d, Uc, nl);
+    p.gnorm = spectral_bound(Uc.data(), k);
     const int D = 1 << k;
     const size_t es = dt == HQ_C64 ? 8 : 16;
     p.hostU.resize(es * D * D);
@@ -530,15 +559,23 @@ static hq_status prof_end(hq_state *st, Shard &s, ProfEvent &pe, uint64_t bytes,
     return HQ_OK;
 }
 
+static hq_status ensure_bound(hq_state *st);
+
 static hq_status exec_apply(hq_state *st, Shard &s, const Prep &p, const void *dU) {
     CUDA_TRY(cudaSetDevice(s.device));
     ProfEvent pe{};
-    hq_status rc = prof_begin(st, s, pe);
-    if (rc) return rc;
+    hq_status rc = HQ_OK;
+    std::vector<char> params;
+    if (p.path == PATH_TC) {
+        if ((rc = ensure_bound(st))) return rc;
+        params = p.params;
+        tc_set_amp_bound(params, st->amp_bound);
+    }
+    if ((rc = prof_begin(st, s, pe))) return rc;
     int launches = 0;
     int e;
     if (p.path == PATH_TC) {
-        e = tc_launch(s.psi, p.params.data(), p.params.size(), dU, s.stream);
+        e = tc_launch(s.psi, params.data(), params.size(), dU, s.stream);
         launches = 1;
     } else {
         e = launch_apply((int)st->dtype, s.psi, p.d, p.hostU.data(), dU, s.stream, &launches);
@@ -672,6 +709,7 @@ static hq_status run_ops(hq_state *st, const std::vector<GateRef> &refs, const s
                     return rc;
                 if ((rc = exec_apply(st, s, p, dU))) return rc;
             }
+            if (st->amp_bound >= 0) st->amp_bound *= p.gnorm;
         } else if (op.kind == OP_REMAP) {
             rc = exec_remap(st, op);
         } else {
@@ -784,6 +822,7 @@ extern "C" hq_status hq_circuit_run(hq_state *st, hq_circuit *c) {
                 const void *dU = (base && c->op_uoff[i] >= 0) ? base + c->op_uoff[i] : nullptr;
                 if ((rc = exec_apply(st, st->sh[r], c->prep[i], dU))) return rc;
             }
+            if (st->amp_bound >= 0) st->amp_bound *= c->prep[i].gnorm;
         } else if (op.kind == OP_REMAP) {
             rc = exec_remap(st, op);
         } else {
@@ -837,6 +876,7 @@ extern "C" hq_status hq_state_init_basis(hq_state *st, uint64_t x) {
     if (st->n < 64 && x >= (1ull << st->n)) return set_error(HQ_ERR_RANGE, "basis index out of range");
     // the whole state is overwritten: restore the chosen initial layout
     st->pi = st->pi_init;
+    st->amp_bound = 1.0;
     const uint64_t p = phys_of(st, x);
     for (auto &s : st->sh) {
         CUDA_TRY(cudaSetDevice(s.device));
@@ -921,6 +961,7 @@ extern "C" hq_status hq_get_amplitudes(hq_state *st, uint64_t first, uint64_t co
 extern "C" hq_status hq_set_amplitudes(hq_state *st, uint64_t first, uint64_t count, const void *host_in) {
     clear_error();
     if (!st || (!host_in && count)) return set_error(HQ_ERR_ARG, "NULL argument");
+    st->amp_bound = -1.0;    // recomputed (hq_norm) before the next pass that needs it
     return io_amplitudes(st, first, count, const_cast<void *>(host_in), false);
 }
 
@@ -951,7 +992,14 @@ extern "C" hq_status hq_norm(hq_state *st, double *out) {
         total = s.h_part[0];
     }
     *out = sqrt(total);
+    st->amp_bound = *out * (1.0 + 1e-6) + 1e-300;
     return HQ_OK;
+}
+
+static hq_status ensure_bound(hq_state *st) {
+    if (st->amp_bound >= 0) return HQ_OK;
+    double nrm = 0.0;
+    return hq_norm(st, &nrm);
 }
 
 // ------------------------------------------------------------------ diagnostics

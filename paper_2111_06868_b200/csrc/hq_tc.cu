@@ -16,10 +16,17 @@
 //   D = output tile in TMEM, lane m = set, column 2r+e = (re, im) of w_r, so
 //       each epilogue thread owns a whole output gather set and its global
 //       stores (lanes = consecutive sets) are fully coalesced.
-// Precision: 3xTF32: B = Bhi + Blo (split on the host from
-// fp64), A = Ahi + Alo (cvt.rna.tf32 in the converters), D = Alo.Bhi +
-// Ahi.Blo + Ahi.Bhi with FP32 accumulation in TMEM.  Plain 1xTF32 fails the
-// 1e-4 bound.
+// Precision: a 3-term split product with FP32 accumulation
+// in TMEM, D = Alo.Bhi + Ahi.Blo + Ahi.Bhi, each operand carried as hi + lo
+// with 11-bit significands (~22 bits together, FP32-class; a single-term
+// TF32/FP16 product fails the 1e-4 bound).  Mode H uses FP16 operands
+// (kind::f16, K = 16 per MMA: half the MMAs of TF32, which matters under the
+// 1 kW power cap).  The FP16 range is handled by exact power-of-two scaling:
+// B = U 2^ue (host, per gate) and A = psi 2^ea with ea chosen by the runtime
+// from its rigorous bound on max |amplitude| (the tracked state norm), so that
+// every scaled amplitude is <= 2^14 < 65504; amplitudes 2^-28 below the bound
+// and smaller lose relative precision gracefully (absolute error <= 2^-38 of
+// the bound).  Mode L (below) uses TF32 (kind::tf32), which needs no scaling.
 //
 // Warp roles (persistent, one CTA per SM, static round-robin tiles):
 //   warps 0-3   epilogue: TMEM -> registers (tcgen05.ld) -> global stores.
@@ -32,9 +39,11 @@
 //               accumulator d: [2*KD + d*KD, 2*KD + (d+1)*KD).
 // Synchronisation: mbarriers full[h]/empty[h] (converters <-> MMA per K-half)
 // and tfull[d]/tempty[d] (MMA <-> epilogue, double-buffered accumulator).
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <vector>
 
@@ -52,16 +61,26 @@ constexpr int MMA_WARP = NUM_EPI;
 constexpr int CONV0 = NUM_EPI + 1;
 constexpr int THREADS = (NUM_EPI + 1 + NUM_CONV) * 32;
 constexpr int BAR_BYTES = 128;
+// mode H: 8 converter warps (2 per TMEM lane quarter, each owning one K-half
+// of its gather set) prefetching the next tile with cp.async into a 2-tile
+// shared-memory ring, so loads stay in flight while a tile is converted
+constexpr int H_NUM_CONV = 8;
+constexpr int H_THREADS = (NUM_EPI + 1 + H_NUM_CONV) * 32;
 
 template <int K> struct Cfg {
     static constexpr int D = 1 << K;             // amplitudes per gather set
     static constexpr int KD = 2 * D;             // reals per set = MMA N = reduction length
     static constexpr int N = KD;
     static constexpr int HALF_AMPS = D / 2;      // amplitudes per K-half
-    static constexpr int B_BYTES = N * KD * 4;   // one of Bhi / Blo
-    static constexpr int SMEM = 2 * B_BYTES + BAR_BYTES;
-    static constexpr int TMEM_COLS = 4 * KD;     // 2 A halves (hi+lo) + 2 accumulators
-    static constexpr int LBO = N * 16;           // K-chunk stride in the B layout
+    static constexpr int B_BYTES = N * KD * 2;   // one of Bhi / Blo (fp16)
+    static constexpr int RAW_BYTES = H_NUM_CONV * 32 * HALF_AMPS * 8;   // one prefetched tile
+    static constexpr int SMEM = 2 * B_BYTES + BAR_BYTES + 2 * RAW_BYTES;
+    // TMEM columns (32-bit; A holds packed f16x2 = one complex amplitude):
+    //   A half h: hi [h*KD/2, h*KD/2 + KD/4), lo [h*KD/2 + KD/4, (h+1)*KD/2)
+    //   accumulator d: [KD + d*N, KD + (d+1)*N)
+    static constexpr int A_COLS = KD;
+    static constexpr int TMEM_COLS = K == 6 ? 512 : 256;
+    static constexpr int LBO = N * 16;           // K-chunk (8 fp16) stride in the B layout
 };
 
 struct Params {
@@ -69,6 +88,8 @@ struct Params {
     uint32_t setoff[128];  // amplitude offset of set n inside a tile
     int pos[13];           // ascending bit positions of targets + set bits
     int k;
+    int ue;                // B = U * 2^ue (host scaling into the fp16 range)
+    int ea;                // A = psi * 2^ea (runtime: from the amplitude bound)
     uint64_t ntiles;
 };
 
@@ -166,6 +187,43 @@ __device__ __forceinline__ void tmem_ld32(uint32_t addr, uint32_t (&v)[32]) {
                  : "r"(addr));
 }
 
+__device__ __forceinline__ void tmem_st1(uint32_t addr, uint32_t v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(addr), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t tmem_ld1(uint32_t addr) {
+    uint32_t v;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
+// 2^e as two float factors (each a normal power of two for |e| <= 252), so
+// that x * f.x * f.y == x * 2^e exactly whenever the result is normal.  Kept
+// branch-free and tiny: the converter applies it to every real of a tile.
+__device__ __forceinline__ float2 pow2_factors(int e) {
+    e = max(-252, min(252, e));
+    const int a = e >> 1, b = e - (e >> 1);
+    return make_float2(__int_as_float((127 + a) << 23), __int_as_float((127 + b) << 23));
+}
+
+// floor(log2(x)) + 1 for x > 0 (frexp exponent), including subnormals
+__device__ __forceinline__ int frexp_exp(float x) {
+    const uint32_t b = __float_as_uint(x);
+    const int f = (int)((b >> 23) & 0xff);
+    if (f != 0) return f - 126;
+    return (int)((__float_as_uint(x * 18446744073709551616.0f) >> 23) & 0xff) - 126 - 64;
+}
+
+__device__ __forceinline__ uint32_t pack_h2(__half a, __half b) {
+    return (uint32_t)__half_as_ushort(a) | ((uint32_t)__half_as_ushort(b) << 16);
+}
+
+__device__ __forceinline__ void tmem_st8(uint32_t addr, const uint32_t (&v)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(addr),
+                 "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
+}
+
 __device__ __forceinline__ void tmem_st16(uint32_t addr, const uint32_t (&v)[16]) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
                  "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16};" ::"r"(addr),
@@ -194,9 +252,9 @@ __device__ __forceinline__ uint64_t tile_base(uint64_t t, const Params &P) {
 }
 
 template <int K>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(H_THREADS, 1)
 apply_tc(float2 *__restrict__ psi, const __grid_constant__ Params P,
-         const float *__restrict__ Breal /* [2][N][KD]: hi then lo, row n = output real */) {
+         const __half *__restrict__ Breal /* [2][N][KD]: hi then lo, row n = output real */) {
     using C = Cfg<K>;
     constexpr int KD = C::KD, N = C::N, HA = C::HALF_AMPS;
     constexpr int NPOS = K + SETBITS;
@@ -226,14 +284,14 @@ apply_tc(float2 *__restrict__ psi, const __grid_constant__ Params P,
                      "r"(C::TMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    // B (U hi, lo) into shared memory in the K-major SWIZZLE_NONE layout:
-    // byte offset(n, kk) = (kk/4) * LBO + n * 16 + (kk%4) * 4.
-    for (int i = threadIdx.x; i < 2 * N * KD / 4; i += THREADS) {
-        const int part = i / (N * KD / 4);
-        const int r = i % (N * KD / 4);
-        const int n = r / (KD / 4), kq = r % (KD / 4);
-        const float4 v = *reinterpret_cast<const float4 *>(Breal + part * N * KD + n * KD + 4 * kq);
-        *reinterpret_cast<float4 *>(smem + part * C::B_BYTES + kq * C::LBO + n * 16) = v;
+    // B (U hi, lo; fp16) into shared memory in the K-major SWIZZLE_NONE layout:
+    // byte offset(n, kk) = (kk/8) * LBO + n * 16 + (kk%8) * 2.
+    for (int i = threadIdx.x; i < 2 * N * KD / 8; i += H_THREADS) {
+        const int part = i / (N * KD / 8);
+        const int r = i % (N * KD / 8);
+        const int n = r / (KD / 8), kq = r % (KD / 8);
+        const uint4 v = *reinterpret_cast<const uint4 *>(Breal + part * N * KD + n * KD + 8 * kq);
+        *reinterpret_cast<uint4 *>(smem + part * C::B_BYTES + kq * C::LBO + n * 16) = v;
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     tc_fence_before();
@@ -243,31 +301,32 @@ apply_tc(float2 *__restrict__ psi, const __grid_constant__ Params P,
     const uint64_t ntiles = P.ntiles;
 
     if (warp == MMA_WARP) {
-        const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) |
+        // idesc: F32 accumulate, A/B F16, K-major, N = KD, M = 128
+        const uint32_t idesc = (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(N >> 3) << 17) |
                                ((uint32_t)(M >> 4) << 24);
         const uint64_t dbhi = smem_desc(sbase, C::LBO, 128);
         const uint64_t dblo = smem_desc(sbase + C::B_BYTES, C::LBO, 128);
-        constexpr int JH = KD / 16;                 // K-chunks (of 8 reals) per half
+        constexpr int JH = KD / 32;                 // K-chunks (of 16 reals) per half
         constexpr uint32_t DSTEP = (2 * C::LBO) >> 4;   // descriptor address step per K-chunk
         uint32_t it = 0;
         for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
             const int d = it & 1;
             const uint32_t ph = it & 1;               // each half barrier completes once per tile
             const uint32_t dp = (it >> 1) & 1;
-            const uint32_t Dt = tmem + 2 * KD + d * KD;
+            const uint32_t Dt = tmem + C::A_COLS + d * N;
             mbar_wait(tempty_bar(d), dp ^ 1);
             // Accumulation order matters for accuracy: the tensor core rounds
             // the FP32 accumulator coarsely at every MMA, so the error grows
             // with the number of MMAs that add into an accumulator of full
             // magnitude.  Issue all correction terms (Alo.Bhi, Ahi.Blo; ~2^-11
-            // of the result) first, then the KD/8 main terms Ahi.Bhi.
+            // of the result) first, then the main terms Ahi.Bhi.
             mbar_wait(full_bar(0), ph);
             tc_fence_after();
             if (elect_one()) {
-#pragma unroll
+#pragma unroll 1
                 for (int jj = 0; jj < JH; ++jj) {
                     const uint32_t jk = jj * DSTEP;
-                    mma_ts(Dt, tmem + KD / 2 + 8 * jj, dbhi + jk, idesc, jj != 0);
+                    mma_ts(Dt, tmem + KD / 4 + 8 * jj, dbhi + jk, idesc, jj != 0);
                     mma_ts(Dt, tmem + 8 * jj, dblo + jk, idesc, 1);
                 }
             }
@@ -275,52 +334,80 @@ apply_tc(float2 *__restrict__ psi, const __grid_constant__ Params P,
             mbar_wait(full_bar(1), ph);
             tc_fence_after();
             if (elect_one()) {
-#pragma unroll
+                const uint32_t a1 = tmem + KD / 2;
+#pragma unroll 1
                 for (int jj = 0; jj < JH; ++jj) {
                     const uint32_t jk = (JH + jj) * DSTEP;
-                    mma_ts(Dt, tmem + KD + KD / 2 + 8 * jj, dbhi + jk, idesc, 1);
-                    mma_ts(Dt, tmem + KD + 8 * jj, dblo + jk, idesc, 1);
+                    mma_ts(Dt, a1 + KD / 4 + 8 * jj, dbhi + jk, idesc, 1);
+                    mma_ts(Dt, a1 + 8 * jj, dblo + jk, idesc, 1);
                 }
-#pragma unroll
+#pragma unroll 1
                 for (int jj = 0; jj < JH; ++jj)
                     mma_ts(Dt, tmem + 8 * jj, dbhi + jj * DSTEP, idesc, 1);
                 mma_commit(empty_bar(0));
-#pragma unroll
+#pragma unroll 1
                 for (int jj = 0; jj < JH; ++jj)
-                    mma_ts(Dt, tmem + KD + 8 * jj, dbhi + (JH + jj) * DSTEP, idesc, 1);
+                    mma_ts(Dt, a1 + 8 * jj, dbhi + (JH + jj) * DSTEP, idesc, 1);
                 mma_commit(empty_bar(1));
                 mma_commit(tfull_bar(d));
             }
             __syncwarp();
         }
     } else if (warp >= CONV0) {
-        const int h = (warp - CONV0) >> 2;          // K-half owned by this warp group
+        // converter group h (4 warps, one per TMEM lane quarter) owns K-half h
+        // (amplitudes [h*HA, (h+1)*HA)) of every gather set
+        const int ct = (warp - CONV0) * 32 + lane;  // 0..255
+        const int h = (warp - CONV0) >> 2;
         const int q = warp & 3;                     // TMEM lane quarter of this warp
         const int n = q * 32 + lane;                // gather set (TMEM lane)
-        const uint64_t soff = P.setoff[n];
         const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
-        const uint32_t chi = tmem + h * KD, clo = chi + KD / 2;
-        uint32_t it = 0;
-        for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-            const uint64_t base = tile_base<NPOS>(t, P) + soff;
-            float2 v[HA];
+        const uint32_t chi = tmem + h * (KD / 2), clo = chi + KD / 4;
+        const float sA = __int_as_float((127 + max(-126, min(127, P.ea))) << 23);
+        const uint64_t soff = P.setoff[n];
+        const uint64_t *offh = P.off + h * HA;
+        // raw ring: [buf][c][ct] float2, conflict-free (consecutive threads, 8 B)
+        const uint32_t raw0 = sbase + 2 * C::B_BYTES + BAR_BYTES;
+        auto prefetch = [&](uint64_t tt, int buf) {
+            const float2 *b = psi + tile_base<NPOS>(tt, P) + soff;
+            const uint32_t dst = raw0 + buf * C::RAW_BYTES + ct * 8;
 #pragma unroll
-            for (int c = 0; c < HA; ++c) v[c] = psi[base + P.off[h * HA + c]];
+            for (int c = 0; c < HA; ++c)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst + c * 256 * 8),
+                             "l"(b + offh[c])
+                             : "memory");
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        };
+        const uint64_t G = gridDim.x;
+        uint32_t it = 0;
+        uint64_t t = blockIdx.x;
+        if (t < ntiles) prefetch(t, 0);
+        for (; t < ntiles; t += G, ++it) {
+            const int buf = it & 1;
+            if (t + G < ntiles) {
+                prefetch(t + G, buf ^ 1);
+                asm volatile("cp.async.wait_group 1;" ::: "memory");
+            } else {
+                asm volatile("cp.async.wait_group 0;" ::: "memory");
+            }
+            const float2 *raw = reinterpret_cast<const float2 *>(smem + 2 * C::B_BYTES + BAR_BYTES +
+                                                                 buf * C::RAW_BYTES) + ct;
             mbar_wait(empty_bar(h), (it & 1) ^ 1);
             tc_fence_after();
 #pragma unroll
-            for (int ch = 0; ch < HA / 8; ++ch) {
+            for (int c0 = 0; c0 < HA; c0 += 16) {
                 uint32_t hi[16], lo[16];
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const float2 x = v[ch * 8 + i];
-                    hi[2 * i] = to_tf32(x.x);
-                    hi[2 * i + 1] = to_tf32(x.y);
-                    lo[2 * i] = __float_as_uint(x.x - __uint_as_float(hi[2 * i]));
-                    lo[2 * i + 1] = __float_as_uint(x.y - __uint_as_float(hi[2 * i + 1]));
+                for (int i = 0; i < 16; ++i) {
+                    const float2 v = raw[(c0 + i) * 256];
+                    const float2 x = make_float2(v.x * sA, v.y * sA);
+                    const __half2 h2 = __floats2half2_rn(x.x, x.y);
+                    const float2 hf = __half22float2(h2);
+                    const __half2 l2 = __floats2half2_rn(x.x - hf.x, x.y - hf.y);
+                    hi[i] = *reinterpret_cast<const uint32_t *>(&h2);
+                    lo[i] = *reinterpret_cast<const uint32_t *>(&l2);
                 }
-                tmem_st16(chi + lane_addr + 16 * ch, hi);
-                tmem_st16(clo + lane_addr + 16 * ch, lo);
+                tmem_st16(chi + lane_addr + c0, hi);
+                tmem_st16(clo + lane_addr + c0, lo);
             }
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             tc_fence_before();
@@ -339,8 +426,9 @@ apply_tc(float2 *__restrict__ psi, const __grid_constant__ Params P,
             mbar_wait(tfull_bar(d), dp);
             tc_fence_after();
             const uint64_t base = tile_base<NPOS>(t, P) + soff;
-            const uint32_t Dt = tmem + 2 * KD + d * KD + lane_addr;
-#pragma unroll
+            const float2 sf = pow2_factors(-(max(-126, min(127, P.ea)) + P.ue));
+            const uint32_t Dt = tmem + C::A_COLS + d * N + lane_addr;
+#pragma unroll 1
             for (int ch = 0; ch < N / 32; ++ch) {
                 uint32_t v[32];
                 tmem_ld32(Dt + 32 * ch, v);
@@ -348,8 +436,8 @@ apply_tc(float2 *__restrict__ psi, const __grid_constant__ Params P,
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
                     float2 o;
-                    o.x = __uint_as_float(v[2 * i]);
-                    o.y = __uint_as_float(v[2 * i + 1]);
+                    o.x = __uint_as_float(v[2 * i]) * sf.x * sf.y;
+                    o.y = __uint_as_float(v[2 * i + 1]) * sf.x * sf.y;
                     psi[base + P.off[16 * ch + i]] = o;
                 }
             }
@@ -740,9 +828,15 @@ void tc_prepare(const ApplyDesc &d, const double *Ucanon, std::vector<char> &pay
         return;
     }
     const int K = d.k, D = 1 << K, KD = 2 * D, N = KD;
-    payload.assign((size_t)2 * N * KD * sizeof(float), 0);
-    float *hi = reinterpret_cast<float *>(payload.data());
-    float *lo = hi + N * KD;
+    // B = U * 2^ue in fp16 hi + lo, with max |U| * 2^ue in [2^14, 2^15)
+    double umax = 0.0;
+    for (int i = 0; i < 2 * D * D; ++i) umax = std::max(umax, std::fabs(Ucanon[i]));
+    int ex = 0;
+    if (umax > 0) std::frexp(umax, &ex);
+    const int ue = umax > 0 ? 15 - ex : 0;
+    payload.assign((size_t)2 * N * KD * sizeof(__half), 0);
+    __half *hi = reinterpret_cast<__half *>(payload.data());
+    __half *lo = hi + N * KD;
     for (int r = 0; r < D; ++r)
         for (int c = 0; c < D; ++c) {
             const double ur = Ucanon[2 * (r * D + c)], ui = Ucanon[2 * (r * D + c) + 1];
@@ -750,17 +844,18 @@ void tc_prepare(const ApplyDesc &d, const double *Ucanon, std::vector<char> &pay
             const double blk[2][2] = {{ur, -ui}, {ui, ur}};
             for (int e = 0; e < 2; ++e)
                 for (int f = 0; f < 2; ++f) {
-                    const double x = blk[e][f];
-                    const float h = tf32_round_host(x);
-                    const float l = tf32_round_host(x - (double)h);
+                    const double x = std::ldexp(blk[e][f], ue);
+                    const __half h = __double2half(x);
                     hi[(2 * r + e) * KD + 2 * c + f] = h;
-                    lo[(2 * r + e) * KD + 2 * c + f] = l;
+                    lo[(2 * r + e) * KD + 2 * c + f] = __double2half(x - (double)__half2float(h));
                 }
         }
     params.assign(sizeof(tc::Params) + 1, 0);
     params.back() = 'H';
     tc::Params &P = *reinterpret_cast<tc::Params *>(params.data());
     P.k = K;
+    P.ue = ue;
+    P.ea = 14;             // set per launch by the runtime (tc_set_amp_bound)
     for (int c = 0; c < D; ++c) {
         uint64_t o = 0;
         for (int i = 0; i < K; ++i)
@@ -800,8 +895,8 @@ static int tc_launch_k(void *psi, const tc::Params &P, const void *dev_payload, 
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const uint64_t grid = P.ntiles < (uint64_t)sms ? P.ntiles : (uint64_t)sms;
-    tc::apply_tc<K><<<(unsigned)grid, tc::THREADS, C::SMEM, st>>>(
-        reinterpret_cast<float2 *>(psi), P, reinterpret_cast<const float *>(dev_payload));
+    tc::apply_tc<K><<<(unsigned)grid, tc::H_THREADS, C::SMEM, st>>>(
+        reinterpret_cast<float2 *>(psi), P, reinterpret_cast<const __half *>(dev_payload));
     return (int)cudaGetLastError();
 }
 
@@ -819,6 +914,16 @@ static int tc_launch_l(void *psi, const tc::ParamsL &P, const void *dev_payload,
     tc::apply_tcL<<<(unsigned)grid, tc::THREADS, tc::L_SMEM, st>>>(
         reinterpret_cast<float2 *>(psi), P, reinterpret_cast<const float *>(dev_payload));
     return (int)cudaGetLastError();
+}
+
+// Mode H scales the state into the FP16 range by 2^ea with max |psi| * 2^ea
+// <= 2^14, from the runtime's rigorous bound on max |amplitude|.
+void tc_set_amp_bound(std::vector<char> &params, double bound) {
+    if (params.empty() || params.back() != 'H') return;
+    tc::Params &P = *reinterpret_cast<tc::Params *>(params.data());
+    int ex = 0;
+    if (bound > 0 && std::isfinite(bound)) std::frexp(bound, &ex);   // bound < 2^ex
+    P.ea = std::max(-126, std::min(127, 14 - ex));
 }
 
 // params: a tc::Params (mode H) or tc::ParamsL (mode L) block followed by
