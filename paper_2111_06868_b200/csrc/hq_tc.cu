@@ -469,10 +469,11 @@ apply_tc(float2 *__restrict__ psi, const __grid_constant__ Params P,
 // k = 5 gates are widened to 6 targets on the host (U (x) I, exact).
 
 constexpr int L_NS = 64;                          // gather sets per tile (MMA N)
-constexpr int L_STAGES = 3;
+constexpr int L_STAGES = 2;
 constexpr int L_HALF = L_NS * 128 * 4;            // 32 KB: hi (or lo) of one stage
 constexpr int L_STAGE = 2 * L_HALF;
-constexpr int L_SMEM = L_STAGES * L_STAGE + BAR_BYTES;
+constexpr int L_RAW = NUM_CONV * 32 * 16 * 8;     // one prefetched tile (cp.async ring slot)
+constexpr int L_SMEM = L_STAGES * L_STAGE + BAR_BYTES + 2 * L_RAW;
 constexpr int L_ATOMCOL = (L_NS / 8) * 1024;      // bytes per 32-real atom column
 
 struct ParamsL {
@@ -621,13 +622,33 @@ apply_tcL(float2 *__restrict__ psi, const __grid_constant__ ParamsL P,
             const uint32_t r8 = n & 7, ch = (c >> 1) & 7;
             sdst[i] = (c >> 4) * L_ATOMCOL + (n >> 3) * 1024 + r8 * 128 + ((ch ^ r8) << 4) + (c & 1) * 8;
         }
-        float2 a0[16], a1[16];
-        auto load = [&](uint64_t tt, float2 (&v)[16]) {
-            const uint64_t base = tile_base12(tt, P);
+        // cp.async prefetch of the next tile into a 2-slot raw ring [slot][i][thread]
+        const int ct = cw * 32 + lane;
+        const uint32_t raw0 = sbase + L_STAGES * L_STAGE + BAR_BYTES;
+        auto prefetch = [&](uint64_t tt, int slot) {
+            const float2 *b = psi + tile_base12(tt, P);
+            const uint32_t dst = raw0 + slot * L_RAW + ct * 8;
 #pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] = psi[base + aoff[i]];
+            for (int i = 0; i < 16; ++i)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst + i * 256 * 8),
+                             "l"(b + aoff[i])
+                             : "memory");
+            asm volatile("cp.async.commit_group;" ::: "memory");
         };
-        auto store = [&](uint32_t it, const float2 (&v)[16]) {
+        const uint64_t G = gridDim.x;
+        uint64_t t = blockIdx.x;
+        uint32_t it = 0;
+        if (t < ntiles) prefetch(t, 0);
+        for (; t < ntiles; t += G, ++it) {
+            const int slot = it & 1;
+            if (t + G < ntiles) {
+                prefetch(t + G, slot ^ 1);
+                asm volatile("cp.async.wait_group 1;" ::: "memory");
+            } else {
+                asm volatile("cp.async.wait_group 0;" ::: "memory");
+            }
+            const float2 *raw = reinterpret_cast<const float2 *>(smem + L_STAGES * L_STAGE + BAR_BYTES +
+                                                                 slot * L_RAW) + ct;
             const int s = it % L_STAGES;
             const uint32_t sp = (it / L_STAGES) & 1;
             mbar_wait(empty_bar(s), sp ^ 1);
@@ -635,32 +656,18 @@ apply_tcL(float2 *__restrict__ psi, const __grid_constant__ ParamsL P,
             uint8_t *lo = hi + L_HALF;
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
-                uint2 h, l;
-                h.x = to_tf32(v[i].x);
-                h.y = to_tf32(v[i].y);
-                l.x = __float_as_uint(v[i].x - __uint_as_float(h.x));
-                l.y = __float_as_uint(v[i].y - __uint_as_float(h.y));
-                *reinterpret_cast<uint2 *>(hi + sdst[i]) = h;
-                *reinterpret_cast<uint2 *>(lo + sdst[i]) = l;
+                const float2 v = raw[i * 256];
+                uint2 hh, ll;
+                hh.x = to_tf32(v.x);
+                hh.y = to_tf32(v.y);
+                ll.x = __float_as_uint(v.x - __uint_as_float(hh.x));
+                ll.y = __float_as_uint(v.y - __uint_as_float(hh.y));
+                *reinterpret_cast<uint2 *>(hi + sdst[i]) = hh;
+                *reinterpret_cast<uint2 *>(lo + sdst[i]) = ll;
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(full_bar(s));
-        };
-        const uint64_t G = gridDim.x;
-        uint64_t t = blockIdx.x;
-        uint32_t it = 0;
-        if (t < ntiles) load(t, a0);
-        while (t < ntiles) {
-            if (t + G < ntiles) load(t + G, a1);
-            store(it, a0);
-            t += G;
-            ++it;
-            if (t >= ntiles) break;
-            if (t + G < ntiles) load(t + G, a0);
-            store(it, a1);
-            t += G;
-            ++it;
         }
     } else {
         // epilogue warps 0..3: TMEM lanes 32q.. = output reals m = 2r + e
@@ -731,11 +738,17 @@ static bool tc_use_mode_l(const ApplyDesc &d) {
     if (force && force[0] == 'H') return false;
     if (force && force[0] == 'L') return true;
     // measured on a B200 (bench_sweep.py, n = 32): mode H needs the low bits
-    // to hold gather-set bits; with >= 2 (k = 5) or >= 3 (k = 6) targets in
-    // bits 0..3 mode L is faster (0.79-0.85 vs 0.29-0.76 of HBM peak).
+    // to hold gather-set bits; when both bits 0 and 1, or three of bits 0..3,
+    // are targets, mode L is faster (0.91-0.93 vs 0.28-0.81 of HBM peak);
+    // otherwise mode H is (0.85-0.99 vs 0.83-0.91).
     int low = 0;
-    for (int i = 0; i < d.k; ++i) low += d.p[i] < 4;
-    return low >= (d.k == 5 ? 2 : 3);
+    bool b0 = false, b1 = false;
+    for (int i = 0; i < d.k; ++i) {
+        low += d.p[i] < 4;
+        b0 |= d.p[i] == 0;
+        b1 |= d.p[i] == 1;
+    }
+    return (b0 && b1) || low >= 3;
 }
 
 static void tc_prepare_l(const ApplyDesc &d, const double *Ucanon, std::vector<char> &payload,
