@@ -154,6 +154,12 @@ void schedule(int n, int m, const std::vector<GateRef> &g, std::vector<int> &pi,
         while (c < u.size() && u[c] <= after) ++c;
         return c < u.size() ? u[c] : std::numeric_limits<size_t>::max();
     };
+    // Evictees (local qubits that become global) are taken from the top
+    // RUNWIN local bits: there a remap's per-peer data is at most
+    // 2^(RUNWIN - m') contiguous runs, which the executor sends as grouped
+    // point-to-point transfers with no packing pass.  Only when that window
+    // cannot supply enough candidates do we fall back to a PERMUTE pass.
+    const int RUNWIN = std::min(nl, 7);
     for (size_t i = 0; i < g.size(); ++i) {
         const GateRef &gt = g[i];
         if (m > 0) {
@@ -162,10 +168,9 @@ void schedule(int n, int m, const std::vector<GateRef> &g, std::vector<int> &pi,
             for (int j = 0; j < gt.k; ++j)
                 if (pi[gt.q[j]] >= nl) need[nneed++] = gt.q[j];
             if (nneed > 0) {
-                // choose evictees: local logical qubits not in Q, furthest next use;
-                // ties broken toward higher physical bit (fewer permutes).
-                std::vector<std::pair<size_t, int>> cand;   // (next use, -physbit)
-                for (int p = 0; p < nl; ++p) {
+                // candidates in the run window, furthest next use first (Belady)
+                std::vector<std::pair<size_t, int>> cand;   // (next use, phys bit)
+                for (int p = nl - RUNWIN; p < nl; ++p) {
                     const int q = inv[p];
                     if ((Q >> q) & 1) continue;
                     cand.push_back({next_use(q, i), p});
@@ -174,44 +179,79 @@ void schedule(int n, int m, const std::vector<GateRef> &g, std::vector<int> &pi,
                     if (a.first != b.first) return a.first > b.first;
                     return a.second > b.second;
                 });
-                int ev[6];
-                for (int t = 0; t < nneed; ++t) ev[t] = inv[cand[t].second];
-                // bring evictees to the top nneed local bits [nl-nneed, nl)
-                Op perm{OP_PERMUTE, -1, 0, {0}};
-                // evictees already in the top slots stay; others swap into free top slots
-                bool in_top[6] = {false, false, false, false, false, false};
-                int slot_used[6] = {0, 0, 0, 0, 0, 0};
-                for (int t = 0; t < nneed; ++t) {
-                    const int p = pi[ev[t]];
-                    if (p >= nl - nneed) { in_top[t] = true; slot_used[p - (nl - nneed)] = 1; }
+                if ((int)cand.size() < nneed) {
+                    // fallback: permute the best evictees from anywhere into the window
+                    std::vector<std::pair<size_t, int>> all;
+                    for (int p = 0; p < nl; ++p) {
+                        const int q = inv[p];
+                        if ((Q >> q) & 1) continue;
+                        all.push_back({next_use(q, i), p});
+                    }
+                    std::sort(all.begin(), all.end(), [](const auto &a, const auto &b) {
+                        if (a.first != b.first) return a.first > b.first;
+                        return a.second > b.second;
+                    });
+                    Op perm{OP_PERMUTE, -1, 0, {0}};
+                    int used = 0;
+                    for (auto &c : all) {
+                        if ((int)cand.size() >= nneed) break;
+                        if (c.second >= nl - RUNWIN) continue;     // already in the window
+                        // swap into a window slot holding a target-free... any non-Q slot
+                        // is already a candidate, so the free slots hold Q qubits: swap
+                        // with the lowest window slot not yet used as a candidate
+                        int slot = -1;
+                        for (int p = nl - RUNWIN; p < nl && slot < 0; ++p) {
+                            bool taken = false;
+                            for (auto &cc : cand) taken |= cc.second == p;
+                            if (!taken) slot = p;
+                        }
+                        if (slot < 0 || used >= 6) break;
+                        perm.bits[2 * perm.nbits] = c.second;
+                        perm.bits[2 * perm.nbits + 1] = slot;
+                        perm.nbits++;
+                        ++used;
+                        const int qa = inv[c.second], qb = inv[slot];
+                        std::swap(pi[qa], pi[qb]);
+                        inv[c.second] = qb;
+                        inv[slot] = qa;
+                        cand.push_back({c.first, slot});
+                    }
+                    if (perm.nbits > 0) ops.push_back(perm);
                 }
-                for (int t = 0; t < nneed; ++t) {
-                    if (in_top[t]) continue;
-                    int s = 0;
-                    while (slot_used[s]) ++s;
-                    slot_used[s] = 1;
-                    const int a = pi[ev[t]], b = nl - nneed + s;
-                    perm.bits[2 * perm.nbits] = a;
-                    perm.bits[2 * perm.nbits + 1] = b;
-                    perm.nbits++;
-                    const int qa = inv[a], qb = inv[b];
-                    std::swap(pi[qa], pi[qb]);
-                    inv[a] = qb; inv[b] = qa;
+                // also bring in other global qubits needed sooner than the local
+                // qubits the window would keep (one exchange instead of several)
+                std::vector<std::pair<size_t, int>> gl;       // (next use, logical q)
+                for (int p = nl; p < n; ++p) {
+                    const int q = inv[p];
+                    bool in_need = false;
+                    for (int t = 0; t < nneed; ++t) in_need |= need[t] == q;
+                    if (!in_need) gl.push_back({next_use(q, i), q});
                 }
-                if (perm.nbits > 0) ops.push_back(perm);
-                // swap global bits of `need` with the top local bits; pair the
-                // lowest global bit with the lowest top-local bit, etc.
-                int gb[6];
-                for (int t = 0; t < nneed; ++t) gb[t] = pi[need[t]];
-                std::sort(gb, gb + nneed);
-                Op rem{OP_REMAP, -1, nneed, {0}};
-                for (int t = 0; t < nneed; ++t) {
-                    const int a = gb[t], b = nl - nneed + t;
+                std::sort(gl.begin(), gl.end());
+                int nb = nneed;
+                int bring[6];
+                for (int t = 0; t < nneed; ++t) bring[t] = need[t];
+                for (auto &x : gl) {
+                    if (nb >= (int)cand.size() || nb >= 6) break;
+                    if (x.first >= cand[nb].first) break;   // evicting cand[nb] would cost more
+                    bring[nb++] = x.second;
+                }
+                int gb[6], lb[6];
+                for (int t = 0; t < nb; ++t) {
+                    gb[t] = pi[bring[t]];
+                    lb[t] = cand[t].second;
+                }
+                std::sort(gb, gb + nb);
+                std::sort(lb, lb + nb);
+                Op rem{OP_REMAP, -1, nb, {0}};
+                for (int t = 0; t < nb; ++t) {
+                    const int a = gb[t], b = lb[t];
                     rem.bits[2 * t] = a;
                     rem.bits[2 * t + 1] = b;
                     const int qa = inv[a], qb = inv[b];
                     std::swap(pi[qa], pi[qb]);
-                    inv[a] = qb; inv[b] = qa;
+                    inv[a] = qb;
+                    inv[b] = qa;
                 }
                 ops.push_back(rem);
             }

@@ -607,21 +607,45 @@ static hq_status exec_permute(hq_state *st, const Op &op) {
     return HQ_OK;
 }
 
-// REMAP: swap global bits g_i with local bits l_i = nl - m' + i (top local
-// bits).  Rank r's chunk t (top m' local bits = t) goes to the peer p whose
-// swapped rank bits equal t, landing in p's chunk whose index is r's swapped
-// rank bits.  Symmetric: for each peer p in the exchange group, send chunk
-// bits(p) and receive into chunk bits(p).
+// REMAP: swap global (rank) bits g_i with local bits l_i (any local bits; the
+// scheduler keeps them in the top local bits so the data per peer is a few
+// long runs).  Element x of rank r goes to the peer p whose g-bits equal x's
+// l-bits, landing at x with its l-bits replaced by r's g-bits.  This is
+// symmetric: for each peer p (index t = p's g-bits), rank r sends the runs of
+// x whose l-bits equal t and receives p's runs into the same offsets.
+// The runs: x = pdep(rho << lmin, ~Lmask) | pdep(t, Lmask), length 2^lmin.
 static hq_status exec_remap(hq_state *st, const Op &op) {
     const int mp = op.nbits;
-    int gsh[6];
+    int gsh[6], lb[6];
+    uint64_t lmask = 0;
+    int lmin = 64;
     for (int i = 0; i < mp; ++i) {
         gsh[i] = op.bits[2 * i] - st->nl;               // rank bit
-        if (op.bits[2 * i + 1] != st->nl - mp + i)
-            return set_error(HQ_ERR_STATE, "internal: remap local bit is not a top bit");
+        lb[i] = op.bits[2 * i + 1];
+        if (lb[i] < 0 || lb[i] >= st->nl || gsh[i] < 0 || gsh[i] >= st->m)
+            return set_error(HQ_ERR_STATE, "internal: bad remap bits");
+        lmask |= 1ull << lb[i];
+        lmin = std::min(lmin, lb[i]);
     }
-    const uint64_t chunk = 1ull << (st->nl - mp);       // amplitudes per chunk
-    const size_t cbytes = chunk * st->es;
+    const uint64_t runlen = 1ull << lmin;                     // amplitudes per run
+    const uint64_t nruns = 1ull << (st->nl - mp - lmin);      // runs per peer
+    const size_t rbytes = runlen * st->es;
+    // start (in amplitudes) of run rho of peer index t
+    auto run_start = [&](uint64_t rho, int t) {
+        uint64_t x = 0, src = rho << lmin;
+        int b = 0;
+        for (int pos = 0; pos < st->nl; ++pos) {
+            if ((lmask >> pos) & 1) {
+                int i = 0;
+                while (lb[i] != pos) ++i;
+                x |= (uint64_t)((t >> i) & 1) << pos;
+            } else {
+                x |= ((src >> b) & 1) << pos;
+                ++b;
+            }
+        }
+        return x;
+    };
     auto bits_of = [&](int r) {
         int t = 0;
         for (int i = 0; i < mp; ++i) t |= ((r >> gsh[i]) & 1) << i;
@@ -634,13 +658,15 @@ static hq_status exec_remap(hq_state *st, const Op &op) {
     };
     if (st->mode == MODE_VIRTUAL) {
         for (auto &s : st->sh) {
+            const int u = bits_of(s.rank);
             for (int t = 0; t < (1 << mp); ++t) {
-                const int p = peer_of(s.rank, t);
-                Shard &d = st->sh[p];
-                char *src = (char *)s.psi + (size_t)t * cbytes;
-                char *dst = (char *)d.buf + (size_t)bits_of(s.rank) * cbytes;
-                CUDA_TRY(cudaMemcpyAsync(dst, src, cbytes, cudaMemcpyDeviceToDevice, s.stream));
-                if (p != s.rank) st->stats.link_bytes += cbytes;
+                Shard &d = st->sh[peer_of(s.rank, t)];
+                for (uint64_t rho = 0; rho < nruns; ++rho) {
+                    const char *src = (const char *)s.psi + run_start(rho, t) * st->es;
+                    char *dst = (char *)d.buf + run_start(rho, u) * st->es;
+                    CUDA_TRY(cudaMemcpyAsync(dst, src, rbytes, cudaMemcpyDeviceToDevice, s.stream));
+                }
+                if (d.rank != s.rank) st->stats.link_bytes += nruns * rbytes;
             }
         }
     } else {
@@ -649,15 +675,18 @@ static hq_status exec_remap(hq_state *st, const Op &op) {
             cudaSetDevice(s.device);
             for (int t = 0; t < (1 << mp); ++t) {
                 const int p = peer_of(s.rank, t);
-                char *src = (char *)s.psi + (size_t)t * cbytes;
-                char *dst = (char *)s.buf + (size_t)t * cbytes;   // from p: chunk bits(p) == t
-                if (p == s.rank) {
-                    CUDA_TRY(cudaMemcpyAsync(dst, src, cbytes, cudaMemcpyDeviceToDevice, s.stream));
-                } else {
-                    NCCL_TRY(ncclSend(src, cbytes, ncclChar, p, s.comm, s.stream));
-                    NCCL_TRY(ncclRecv(dst, cbytes, ncclChar, p, s.comm, s.stream));
-                    st->stats.link_bytes += cbytes;
+                for (uint64_t rho = 0; rho < nruns; ++rho) {
+                    const uint64_t off = run_start(rho, t) * st->es;
+                    const char *src = (const char *)s.psi + off;
+                    char *dst = (char *)s.buf + off;     // from p: its runs for our g-bits land here
+                    if (p == s.rank) {
+                        CUDA_TRY(cudaMemcpyAsync(dst, src, rbytes, cudaMemcpyDeviceToDevice, s.stream));
+                    } else {
+                        NCCL_TRY(ncclSend(src, rbytes, ncclChar, p, s.comm, s.stream));
+                        NCCL_TRY(ncclRecv(dst, rbytes, ncclChar, p, s.comm, s.stream));
+                    }
                 }
+                if (p != s.rank) st->stats.link_bytes += nruns * rbytes;
             }
         }
         NCCL_TRY(ncclGroupEnd());

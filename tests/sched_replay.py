@@ -30,13 +30,25 @@ def permute_bits(shard, pairs):
     return out
 
 
-def remap_chunks(nl, pairs):
-    """Returns (mp, gsh, chunk) for a REMAP op."""
+def remap_runs(nl, pairs):
+    """Run decomposition of a REMAP (see exec_remap): returns (mp, gsh, lmask,
+    lmin, runlen, nruns, run_start(rho, t))."""
     mp = len(pairs)
     gsh = [a - nl for a, _ in pairs]
-    for i, (_, b) in enumerate(pairs):
-        assert b == nl - mp + i, "remap local bit must be a top bit"
-    return mp, gsh, 1 << (nl - mp)
+    lb = [b for _, b in pairs]
+    lmask = sum(1 << b for b in lb)
+    lmin = min(lb)
+
+    def run_start(rho, t):
+        x, src, b = 0, rho << lmin, 0
+        for pos in range(nl):
+            if (lmask >> pos) & 1:
+                x |= ((t >> lb.index(pos)) & 1) << pos
+            else:
+                x |= ((src >> b) & 1) << pos
+                b += 1
+        return x
+    return mp, gsh, lmask, lmin, 1 << lmin, 1 << (nl - mp - lmin), run_start
 
 
 def peer_of(r, t, gsh):
@@ -66,13 +78,15 @@ def replay_all_shards(n, m, gates, ops, psi_logical):
             shards = [permute_bits(s, pairs) for s in shards]
         else:
             pairs = [(op["bits"][2 * i], op["bits"][2 * i + 1]) for i in range(op["nbits"])]
-            mp, gsh, chunk = remap_chunks(nl, pairs)
+            mp, gsh, lmask, lmin, runlen, nruns, run_start = remap_runs(nl, pairs)
             new = [np.empty_like(s) for s in shards]
             for r in range(G):
+                u = bits_of(r, gsh)
                 for t in range(1 << mp):
                     p = peer_of(r, t, gsh)
-                    c = bits_of(r, gsh)
-                    new[p][c * chunk:(c + 1) * chunk] = shards[r][t * chunk:(t + 1) * chunk]
+                    for rho in range(nruns):
+                        a, b = run_start(rho, t), run_start(rho, u)
+                        new[p][b:b + runlen] = shards[r][a:a + runlen]
             shards = new
     return shards
 

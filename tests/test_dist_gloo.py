@@ -2,11 +2,11 @@
 gloo backend, CPU).  Each rank owns its shard of the physical index space and
 executes the op stream hq_schedule emits: APPLY with the oracle on the local
 shard, REMAP as the documented chunk exchange (chunk t -> peer whose swapped
-rank bits equal t, landing at chunk bits(rank)) over torch.distributed
+rank bits equal t, landing at the run offsets of bits(rank)) over torch.distributed
 point-to-point, PERMUTE as a local bit swap.  Rank 0 gathers the shards and
 compares the logical state with the oracle (bit-exact for a reversible
 circuit, 1e-12 for Haar gates).  This is the same exchange exec_remap issues
-through NCCL on GPUs."""
+through NCCL on GPUs (one send/recv pair per contiguous run)."""
 import os
 import socket
 
@@ -36,7 +36,7 @@ def _worker(rank, world, port, n, kind, q):
         import oracle as O
         import paper_2111_06868_b200 as hq
         from hq_inputs import reversible_circuit, random_circuit, integer_state, random_state
-        from sched_replay import phys_apply, permute_bits, remap_chunks, peer_of, bits_of, to_logical
+        from sched_replay import phys_apply, permute_bits, remap_runs, peer_of, bits_of, to_logical
 
         m = world.bit_length() - 1
         nl = n - m
@@ -57,26 +57,28 @@ def _worker(rank, world, port, n, kind, q):
                 shard = permute_bits(shard, pairs)
             else:
                 pairs = [(op["bits"][2 * i], op["bits"][2 * i + 1]) for i in range(op["nbits"])]
-                mp_, gsh, chunk = remap_chunks(nl, pairs)
+                mp_, gsh, lmask, lmin, runlen, nruns, run_start = remap_runs(nl, pairs)
                 new = np.empty_like(shard)
                 reqs = []
                 recv_bufs = []
                 for t in range(1 << mp_):
                     p = peer_of(rank, t, gsh)
-                    src = shard[t * chunk:(t + 1) * chunk]
-                    if p == rank:
-                        new[t * chunk:(t + 1) * chunk] = src
-                        continue
-                    # send chunk t (== bits(p)) to p; receive p's chunk into slot t (== bits(p))
-                    send = torch.from_numpy(np.ascontiguousarray(src).view(np.float64).copy())
-                    recv = torch.empty_like(send)
-                    reqs.append(dist.isend(send, p))
-                    reqs.append(dist.irecv(recv, p))
-                    recv_bufs.append((t, recv))
+                    for rho in range(nruns):
+                        a = run_start(rho, t)
+                        src = shard[a:a + runlen]
+                        if p == rank:
+                            new[a:a + runlen] = src
+                            continue
+                        # send my runs with l-bits t to p; receive p's runs into the same offsets
+                        send = torch.from_numpy(np.ascontiguousarray(src).view(np.float64).copy())
+                        recv = torch.empty_like(send)
+                        reqs.append(dist.isend(send, p))
+                        reqs.append(dist.irecv(recv, p))
+                        recv_bufs.append((a, recv))
                 for r in reqs:
                     r.wait()
-                for t, recv in recv_bufs:
-                    new[t * chunk:(t + 1) * chunk] = recv.numpy().view(np.complex128)
+                for a, recv in recv_bufs:
+                    new[a:a + runlen] = recv.numpy().view(np.complex128)
                 shard = new
         parts = [torch.empty(2 << nl, dtype=torch.float64) for _ in range(world)]
         dist.all_gather(parts, torch.from_numpy(shard.view(np.float64).copy()))
