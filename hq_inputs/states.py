@@ -30,3 +30,35 @@ def basis_index(bits):
     for b in bits:
         x = (x << 1) | int(b)
     return x
+
+
+# ---------------------------------------------------------------- hash states
+# A deterministic, index-addressable integer-valued state: re/im are integers
+# in [-2^10, 2^10) (exact in FP32/TF32/FP64), computed from the amplitude index
+# alone so that any single amplitude can be regenerated on the host while the
+# full state (up to 2^34 amplitudes) is generated on the device by torch.
+_HM1, _HM2 = 0x9E3779B97F4A7C15 & ((1 << 63) - 1), 0xBF58476D1CE4E5B9 & ((1 << 63) - 1)
+
+
+def hash_amplitudes_np(idx):
+    """numpy: complex128 values of the hash state at int64 indices idx."""
+    i = np.asarray(idx, dtype=np.int64)
+    a = (i * np.int64(_HM1)) ^ (i >> np.int64(7))
+    b = (i * np.int64(_HM2)) ^ (i >> np.int64(11))
+    re = ((a >> np.int64(20)) & np.int64(2047)) - 1024
+    im = ((b >> np.int64(24)) & np.int64(2047)) - 1024
+    return re.astype(np.float64) + 1j * im.astype(np.float64)
+
+
+def hash_state_torch(n, device, chunk=1 << 26):
+    """torch: the same hash state as complex64 on `device` (2^n amplitudes)."""
+    import torch
+    out = torch.empty(1 << n, dtype=torch.complex64, device=device)
+    view = torch.view_as_real(out)
+    for s in range(0, 1 << n, chunk):
+        i = torch.arange(s, min(s + chunk, 1 << n), dtype=torch.int64, device=device)
+        a = (i * _HM1) ^ (i >> 7)
+        b = (i * _HM2) ^ (i >> 11)
+        view[s:s + i.numel(), 0] = (((a >> 20) & 2047) - 1024).to(torch.float32)
+        view[s:s + i.numel(), 1] = (((b >> 24) & 2047) - 1024).to(torch.float32)
+    return out

@@ -274,8 +274,8 @@ def test_mirror_circuit_full_size(n):
     hq.hq_apply_circuit(s, fused)
     a0 = hq.hq_get_amplitudes(s, 0, 1)[0]
     nrm = hq.hq_norm(s)
-    # ||psi - |0>||^2 = ||psi||^2 - 2 Re psi_0 + 1
-    dist = np.sqrt(max(nrm ** 2 - 2 * a0.real + 1, 0.0))
+    # ||psi - |0>||^2 = (||psi||^2 - |psi_0|^2) + |psi_0 - 1|^2
+    dist = np.sqrt(max(nrm ** 2 - abs(a0) ** 2, 0.0) + abs(a0 - 1) ** 2)
     assert dist <= 1e-4
 
 
