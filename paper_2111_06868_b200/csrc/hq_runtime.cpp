@@ -125,6 +125,13 @@ struct hq_circuit {
     std::vector<struct Prep> prep;         // per op (APPLY)
     std::vector<char *> dev_U;             // per shard: all payloads
     uint64_t passes = 0, remaps = 0, permutes = 0;
+    // CUDA graph of the whole op stream (single-shard states, profiling off):
+    // captured on the first run, replayed while the capture key matches.
+    cudaGraphExec_t graph = nullptr;
+    std::vector<int> graph_ea;             // TC input-scale exponents baked into the graph
+    cudaStream_t graph_stream = nullptr;
+    void *graph_psi = nullptr;
+    uint64_t graph_launches = 0;
 };
 
 // ------------------------------------------------------------------ helpers
@@ -836,12 +843,7 @@ extern "C" hq_status hq_circuit_create(hq_state *st, const hq_gate *gates, size_
     return HQ_OK;
 }
 
-extern "C" hq_status hq_circuit_run(hq_state *st, hq_circuit *c) {
-    clear_error();
-    if (!st || !c) return set_error(HQ_ERR_ARG, "NULL argument");
-    if (c->owner != st) return set_error(HQ_ERR_STATE, "circuit was compiled for another state");
-    if (st->pi != c->pi_start)
-        return set_error(HQ_ERR_STATE, "state qubit layout differs from the one the circuit was compiled for");
+static hq_status circuit_run_ops(hq_state *st, hq_circuit *c) {
     for (size_t i = 0; i < c->ops.size(); ++i) {
         const Op &op = c->ops[i];
         hq_status rc = HQ_OK;
@@ -859,6 +861,77 @@ extern "C" hq_status hq_circuit_run(hq_state *st, hq_circuit *c) {
         }
         if (rc) return rc;
     }
+    return HQ_OK;
+}
+
+extern "C" hq_status hq_circuit_run(hq_state *st, hq_circuit *c) {
+    clear_error();
+    if (!st || !c) return set_error(HQ_ERR_ARG, "NULL argument");
+    if (c->owner != st) return set_error(HQ_ERR_STATE, "circuit was compiled for another state");
+    if (st->pi != c->pi_start)
+        return set_error(HQ_ERR_STATE, "state qubit layout differs from the one the circuit was compiled for");
+    hq_status rc;
+    const bool graphable = st->sh.size() == 1 && !st->profiling && c->remaps == 0 && c->permutes == 0 &&
+                           !c->ops.empty();
+    if (!graphable) {
+        if ((rc = circuit_run_ops(st, c))) return rc;
+        st->pi = c->pi_end;
+        return HQ_OK;
+    }
+    Shard &s0 = st->sh[0];
+    CUDA_TRY(cudaSetDevice(s0.device));
+    bool has_tc = false;
+    for (auto &p : c->prep) has_tc |= p.path == PATH_TC;
+    if (has_tc && (rc = ensure_bound(st))) return rc;     // sync happens outside the capture
+    const double bound0 = st->amp_bound;
+    // the FP16 input scales the TC passes would use from this bound
+    std::vector<int> ea;
+    if (has_tc) {
+        double b = bound0;
+        for (size_t i = 0; i < c->ops.size(); ++i) {
+            if (c->ops[i].kind != OP_APPLY) continue;
+            if (c->prep[i].path == PATH_TC) {
+                int ex = 0;
+                std::frexp(b, &ex);
+                ea.push_back(ex);
+            }
+            b *= c->prep[i].gnorm;
+        }
+    }
+    if (c->graph && (c->graph_stream != s0.stream || c->graph_psi != s0.psi || c->graph_ea != ea)) {
+        cudaGraphExecDestroy(c->graph);
+        c->graph = nullptr;
+    }
+    if (!c->graph) {
+        // capture: the op stream's launches on the state's stream become one graph
+        if (!s0.stream) {           // the legacy default stream cannot be captured
+            if ((rc = circuit_run_ops(st, c))) return rc;
+            st->pi = c->pi_end;
+            return HQ_OK;
+        }
+        const hq_stats before = st->stats;
+        CUDA_TRY(cudaStreamBeginCapture(s0.stream, cudaStreamCaptureModeThreadLocal));
+        rc = circuit_run_ops(st, c);
+        cudaGraph_t g = nullptr;
+        cudaError_t e = cudaStreamEndCapture(s0.stream, &g);
+        if (rc) { if (g) cudaGraphDestroy(g); return rc; }
+        if (e != cudaSuccess) return set_error(HQ_ERR_CUDA, "graph capture: %s", cudaGetErrorString(e));
+        e = cudaGraphInstantiate(&c->graph, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) { c->graph = nullptr; return set_error(HQ_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(e)); }
+        c->graph_stream = s0.stream;
+        c->graph_psi = s0.psi;
+        c->graph_ea = ea;
+        c->graph_launches = st->stats.kernel_launches - before.kernel_launches;
+        st->amp_bound = bound0;     // the capture advanced it; the replay below does so again
+        st->stats = before;
+    }
+    CUDA_TRY(cudaGraphLaunch(c->graph, s0.stream));
+    for (size_t i = 0; i < c->ops.size(); ++i)
+        if (c->ops[i].kind == OP_APPLY && st->amp_bound >= 0) st->amp_bound *= c->prep[i].gnorm;
+    st->stats.passes += c->passes;
+    st->stats.kernel_launches += c->graph_launches;
+    st->stats.hbm_bytes += c->passes * (uint64_t)2 * (st->es << st->nl);
     st->pi = c->pi_end;
     return HQ_OK;
 }
@@ -875,6 +948,7 @@ extern "C" hq_status hq_circuit_info(const hq_circuit *c, uint64_t *passes, uint
 
 extern "C" hq_status hq_circuit_destroy(hq_circuit *c) {
     if (!c) return HQ_OK;
+    if (c->graph) cudaGraphExecDestroy(c->graph);
     for (size_t r = 0; r < c->dev_U.size(); ++r)
         if (c->dev_U[r]) {
             if (c->owner && r < c->owner->sh.size()) cudaSetDevice(c->owner->sh[r].device);

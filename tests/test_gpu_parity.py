@@ -334,3 +334,35 @@ def test_layout_bit_exact_permutations():
     assert np.array_equal(hq.hq_get_amplitudes(s).astype(np.complex128), want)
     with pytest.raises(hq.HQError):
         hq.hq_state_set_layout(s, [0] * n)
+
+
+# ---------------------------------------------------------------- CUDA graph replay
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_circuit_graph_replay(dtype):
+    """hq_circuit_run captures the op stream into a CUDA graph (single shard,
+    profiling off) and replays it; every replay must equal the oracle."""
+    n = 17
+    gates = hq.hq_fuse(sycamore_circuit(n, 12, 21), 6)
+    want = O.simulate(n, [Gate("F", q, U) for q, U in gates])
+    s = hq.hq_state_create(n, dtype, 1)
+    c = hq.hq_circuit_create(s, gates)
+    hq.hq_stats_reset(s)
+    for rep in range(3):
+        hq.hq_state_init_basis(s, 0)
+        hq.hq_circuit_run(s, c)
+        assert _err(hq.hq_get_amplitudes(s), want) <= TOL[dtype]
+    st = hq.hq_stats_get(s)
+    assert st["passes"] == 3 * len(gates)
+    # a run from a different starting state (no re-init) replays the same graph
+    psi1 = hq.hq_get_amplitudes(s).astype(np.complex128)
+    hq.hq_circuit_run(s, c)
+    want2 = O.simulate(n, [Gate("F", q, U) for q, U in gates], psi1)
+    assert _err(hq.hq_get_amplitudes(s), want2) <= 2 * TOL[dtype]
+    # profiling disables the graph path; results stay identical
+    hq.hq_state_init_basis(s, 0)
+    hq.hq_profile_enable(s, True)
+    hq.hq_circuit_run(s, c)
+    hq.hq_profile_enable(s, False)
+    t = hq.hq_kernel_times(s)
+    assert t["count"] == len(gates)
+    assert _err(hq.hq_get_amplitudes(s), want) <= TOL[dtype]
