@@ -230,6 +230,41 @@ apply_gen(typename C2<R>::T *__restrict__ psi, const __grid_constant__ GenParams
     }
 }
 
+// Small-state variant of the generic kernel: one warp per gather set (the
+// set is staged in shared memory, lanes own output rows), so that a pass over
+// a few thousand amplitudes is not a handful of serial threads.
+template <typename R, int K>
+__global__ void __launch_bounds__(128)
+apply_gen_warp(typename C2<R>::T *__restrict__ psi, const __grid_constant__ GenParams P,
+               const typename C2<R>::T *__restrict__ Ud) {
+    using V = typename C2<R>::T;
+    constexpr int D = 1 << K;
+    __shared__ V sv[4][D];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t o = (uint64_t)blockIdx.x * 4 + w;
+    if (o >= P.nsets) return;
+    uint64_t base = o;
+#pragma unroll
+    for (int j = 0; j < K; ++j) base = insert_zero(base, P.s[j]);
+    for (int c = lane; c < D; c += 32) sv[w][c] = psi[base + P.off[c]];
+    __syncwarp();
+    for (int r = lane; r < D; r += 32) {
+        R ar = 0, ai = 0;
+        for (int c = 0; c < D; ++c) {
+            const V u = __ldg(&Ud[r * D + c]);
+            const V v = sv[w][c];
+            ar = fma(u.x, v.x, ar);
+            ar = fma(-u.y, v.y, ar);
+            ai = fma(u.x, v.y, ai);
+            ai = fma(u.y, v.x, ai);
+        }
+        V out;
+        out.x = ar;
+        out.y = ai;
+        psi[base + P.off[r]] = out;
+    }
+}
+
 // ------------------------------------------------------------------ dispatch
 
 namespace {
@@ -273,6 +308,21 @@ cudaError_t launch_reg_f(int VEC, int T0, int KL, void *psi, const RegParams &P,
 template <typename R>
 cudaError_t launch_gen(int K, void *psi, const GenParams &P, const void *dU, cudaStream_t st) {
     using V = typename C2<R>::T;
+    if (P.nsets <= (1ull << 15)) {
+        const unsigned blocks = (unsigned)((P.nsets + 3) / 4);
+        V *p = reinterpret_cast<V *>(psi);
+        const V *u = reinterpret_cast<const V *>(dU);
+        switch (K) {
+            case 1: apply_gen_warp<R, 1><<<blocks, 128, 0, st>>>(p, P, u); break;
+            case 2: apply_gen_warp<R, 2><<<blocks, 128, 0, st>>>(p, P, u); break;
+            case 3: apply_gen_warp<R, 3><<<blocks, 128, 0, st>>>(p, P, u); break;
+            case 4: apply_gen_warp<R, 4><<<blocks, 128, 0, st>>>(p, P, u); break;
+            case 5: apply_gen_warp<R, 5><<<blocks, 128, 0, st>>>(p, P, u); break;
+            case 6: apply_gen_warp<R, 6><<<blocks, 128, 0, st>>>(p, P, u); break;
+            default: return cudaErrorInvalidValue;
+        }
+        return cudaGetLastError();
+    }
     uint64_t blocks = (P.nsets + kThreads - 1) / kThreads;
     if (blocks > 148ull * 64) blocks = 148ull * 64;
     if (blocks == 0) blocks = 1;
