@@ -79,7 +79,7 @@ template <int K> struct Cfg {
     //   A half h: hi [h*KD/2, h*KD/2 + KD/4), lo [h*KD/2 + KD/4, (h+1)*KD/2)
     //   accumulator d: [KD + d*N, KD + (d+1)*N)
     static constexpr int A_COLS = KD;
-    static constexpr int TMEM_COLS = K == 6 ? 512 : 256;
+    static constexpr int TMEM_COLS = K == 6 ? 512 : (K == 5 ? 256 : 128);
     static constexpr int LBO = N * 16;           // K-chunk (8 fp16) stride in the B layout
 };
 
@@ -394,10 +394,11 @@ apply_tc(float2 *__restrict__ psi, const __grid_constant__ Params P,
             mbar_wait(empty_bar(h), (it & 1) ^ 1);
             tc_fence_after();
 #pragma unroll
-            for (int c0 = 0; c0 < HA; c0 += 16) {
-                uint32_t hi[16], lo[16];
+            constexpr int CH = HA < 16 ? HA : 16;     // amplitudes per tcgen05.st
+            for (int c0 = 0; c0 < HA; c0 += CH) {
+                uint32_t hi[CH], lo[CH];
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
+                for (int i = 0; i < CH; ++i) {
                     const float2 v = raw[(c0 + i) * 256];
                     const float2 x = make_float2(v.x * sA, v.y * sA);
                     const __half2 h2 = __floats2half2_rn(x.x, x.y);
@@ -406,8 +407,13 @@ apply_tc(float2 *__restrict__ psi, const __grid_constant__ Params P,
                     hi[i] = *reinterpret_cast<const uint32_t *>(&h2);
                     lo[i] = *reinterpret_cast<const uint32_t *>(&l2);
                 }
-                tmem_st16(chi + lane_addr + c0, hi);
-                tmem_st16(clo + lane_addr + c0, lo);
+                if constexpr (CH == 16) {
+                    tmem_st16(chi + lane_addr + c0, hi);
+                    tmem_st16(clo + lane_addr + c0, lo);
+                } else {
+                    tmem_st8(chi + lane_addr + c0, hi);
+                    tmem_st8(clo + lane_addr + c0, lo);
+                }
             }
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             tc_fence_before();
@@ -727,7 +733,14 @@ static inline float tf32_round_host(double x) {
 }
 
 bool tc_applicable(int dtype, const ApplyDesc &d) {
-    return dtype == HQ_C64 && (d.k == 5 || d.k == 6) && d.n_local >= d.k + tc::SETBITS + 3;
+    static const char *k4 = getenv("HQ_TC_K4");   // experiment: k = 4 on tensor cores
+    bool k_ok = d.k == 5 || d.k == 6;
+    if (d.k == 4 && k4 && k4[0] == '1') {          // mode H only (no low-bit targets)
+        int low = 0;
+        for (int i = 0; i < 4; ++i) low += d.p[i] < 4;
+        k_ok = low == 0;
+    }
+    return dtype == HQ_C64 && k_ok && d.n_local >= d.k + tc::SETBITS + 3;
 }
 
 // Mode L (U in TMEM, tile in smem) when a target sits in the lowest bits,
@@ -947,6 +960,7 @@ int tc_launch(void *psi, const void *params, size_t params_size, const void *dev
     const char tag = reinterpret_cast<const char *>(params)[params_size - 1];
     if (tag == 'L') return tc_launch_l(psi, *reinterpret_cast<const tc::ParamsL *>(params), dev_payload, st);
     const tc::Params &P = *reinterpret_cast<const tc::Params *>(params);
+    if (P.k == 4) return tc_launch_k<4>(psi, P, dev_payload, st);
     return P.k == 5 ? tc_launch_k<5>(psi, P, dev_payload, st) : tc_launch_k<6>(psi, P, dev_payload, st);
 }
 
