@@ -172,6 +172,36 @@ hq_status hq_set_amplitudes(hq_state *s, uint64_t first, uint64_t count, const v
  * reduced over all ranks.  Synchronises.  (SPEC S:221.) */
 hq_status hq_norm(hq_state *s, double *out);
 
+/* Product initial state from tokens: a
+ * NUL-terminated string of n characters over {0, 1, +, -} (character j is
+ * qubit j), or a single character broadcast to every qubit (as the paper's
+ * initial_state='+' benchmark).  '+' = (|0>+|1>)/sqrt2,
+ * '-' = (|0>-|1>)/sqrt2.  '.' and letters are tensor-network-only tokens
+ * and any other character is rejected with HQ_ERR_ARG.  Like
+ * init_basis it restores the state's initial layout. */
+hq_status hq_state_init_tokens(hq_state *s, const char *tokens);
+
+/* Projection: zero every
+ * amplitude whose qubit qubits[j] is not bits[j] (0/1), j < nq; if
+ * renormalize, rescale to unit norm.  norm_out (may be NULL) receives the norm
+ * of the projected state before renormalisation.  With renormalize and a
+ * projected norm < 1e-14 the call returns HQ_ERR_RANGE (SPEC ZeroNormProjection)
+ * leaving the projected, unnormalised state. */
+hq_status hq_project(hq_state *s, const int32_t *qubits, const int32_t *bits, int nq,
+                     int renormalize, double *norm_out);
+
+/* Born probabilities of the 2^nq outcomes of measuring
+ * qubits[0..nq) (1 <= nq <= 10): probs_out[x] = sum of |psi_i|^2 over the
+ * indices whose measured qubits read x, qubits[0] the MSB of x (C1).  FP64,
+ * reduced over all ranks; not normalised (the sum is ||psi||^2).  Synchronises. */
+hq_status hq_probabilities(hq_state *s, const int32_t *qubits, int nq, double *probs_out);
+
+/* Measurement: draw the outcome x from the
+ * Born distribution with the caller's uniform random number u in [0, 1) (the
+ * random numbers the method draws are inputs), then collapse: project onto x
+ * and renormalise.  *outcome_out = x (qubits[0] = MSB). */
+hq_status hq_measure(hq_state *s, const int32_t *qubits, int nq, double u, uint64_t *outcome_out);
+
 /* ------------------------------------------------------------------ apply */
 
 /* psi <- (U embedded on qubits) psi.

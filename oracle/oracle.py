@@ -25,6 +25,11 @@ Contents, each following the passage cited:
   U_group = U_last ... U_first embedded on the ascending support (P:493-494,
   readings C8, C9).
 
+* ``init_tokens`` / ``project`` / ``probabilities`` -- token product states
+   as a Kronecker product of single-qubit
+  vectors, projection and Born
+  probabilities written out from their definitions.
+
 Parity pins for every function live in ``tests/test_oracle_pins.py``.
 """
 import ctypes
@@ -213,3 +218,53 @@ def fused_gates(gates, kmax):
             M = embed_dense(m, gates[i].U, [pos[q] for q in gates[i].qubits]) @ M
         out.append((tuple(support), M))
     return out
+
+
+# ---------------------------------------------------------------- f4: tokens, projection
+
+_TOKENS = {"0": np.array([1.0, 0.0]), "1": np.array([0.0, 1.0]),
+           "+": np.array([1.0, 1.0]) / np.sqrt(2.0), "-": np.array([1.0, -1.0]) / np.sqrt(2.0)}
+
+
+def init_tokens(n, tokens):
+    """Tensor product of single-qubit states, qubit 0 the leftmost (most
+    significant) factor (C1); a single character is broadcast."""
+    if len(tokens) == 1:
+        tokens = tokens * n
+    if len(tokens) != n or any(t not in _TOKENS for t in tokens):
+        raise OracleError("BadToken")
+    psi = np.array([1.0 + 0j])
+    for t in tokens:
+        psi = np.kron(psi, _TOKENS[t])
+    return psi.astype(np.complex128)
+
+
+def _qubit_bits(n, qubits):
+    idx = np.arange(2 ** n, dtype=np.int64)
+    return [((idx >> (n - 1 - q)) & 1) for q in qubits]
+
+
+def project(psi, qubits, bits, renormalize=False):
+    """Zero the amplitudes inconsistent with bits on qubits; optionally
+    renormalise.  Returns (new psi, projected norm)."""
+    n = _nqubits(psi)
+    keep = np.ones(2 ** n, dtype=bool)
+    for b, col in zip(bits, _qubit_bits(n, qubits)):
+        keep &= col == b
+    out = np.where(keep, psi, 0).astype(np.complex128)
+    nrm = norm(out)
+    if renormalize:
+        if nrm < 1e-14:
+            raise OracleError("ZeroNormProjection")
+        out = out / nrm
+    return out, nrm
+
+
+def probabilities(psi, qubits):
+    """P[x] = sum of |psi_i|^2 over indices whose qubits read x (qubits[0] MSB)."""
+    n = _nqubits(psi)
+    x = np.zeros(2 ** n, dtype=np.int64)
+    k = len(qubits)
+    for j, col in enumerate(_qubit_bits(n, qubits)):
+        x |= col << (k - 1 - j)
+    return np.bincount(x, weights=np.abs(psi) ** 2, minlength=2 ** k)

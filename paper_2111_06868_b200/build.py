@@ -18,7 +18,7 @@ LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libhq.so")
 INCLUDE = os.path.join(ROOT, "include")
 
-SOURCES = ["hq_apply.cu", "hq_tc.cu", "hq_runtime.cpp", "hq_plan.cpp"]
+SOURCES = ["hq_apply.cu", "hq_tc.cu", "hq_state_ops.cu", "hq_runtime.cpp", "hq_plan.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -106,4 +106,17 @@ int launch_gather(int dtype, const void *psi, void *dst, uint64_t first, uint64_
 int launch_scatter(int dtype, void *psi, const void *src, uint64_t first, uint64_t count,
                    int n, int n_local, const int *bitmap, int my_rank, void *stream);
 
+// ------------------------------------------------------------------ state ops (hq_state_ops.cu)
+struct ProbParams {
+    int nq;
+    int pos[16];            // physical bit of outcome bit nq-1-j (pos[0] = MSB of x)
+};
+int launch_init_tokens(int dtype, void *psi, uint64_t n_amps, uint64_t fix_mask, uint64_t fix_val,
+                       uint64_t minus_mask, double mag, void *stream);
+int launch_project(int dtype, void *psi, uint64_t n_amps, uint64_t mask, uint64_t val, int keep_all,
+                   double *dev_partial, int max_blocks, void *stream, int *nblocks_out);
+int launch_scale(int dtype, void *psi, uint64_t n_amps, double s, void *stream);
+int launch_probabilities(int dtype, const void *psi, uint64_t n_amps, const ProbParams &P,
+                         double *dev_hist, int max_blocks, void *stream, int *nblocks_out);
+
 }  // namespace hq

@@ -1105,6 +1105,205 @@ static hq_status ensure_bound(hq_state *st) {
     return hq_norm(st, &nrm);
 }
 
+// ------------------------------------------------------------------ f4: tokens, projection, measurement
+
+static hq_status validate_targets(const hq_state *st, const int32_t *qubits, int nq, int maxq) {
+    if (!qubits || nq < 1 || nq > maxq) return set_error(HQ_ERR_ARG, "nq=%d not in [1,%d]", nq, maxq);
+    for (int j = 0; j < nq; ++j) {
+        if (qubits[j] < 0 || qubits[j] >= st->n) return set_error(HQ_ERR_QUBIT, "qubit %d not in [0,%d)", qubits[j], st->n);
+        for (int l = 0; l < j; ++l)
+            if (qubits[l] == qubits[j]) return set_error(HQ_ERR_DUP_QUBIT, "repeated qubit %d", qubits[j]);
+    }
+    return HQ_OK;
+}
+
+extern "C" hq_status hq_state_init_tokens(hq_state *st, const char *tokens) {
+    clear_error();
+    if (!st || !tokens) return set_error(HQ_ERR_ARG, "NULL argument");
+    const size_t len = strlen(tokens);
+    if (len != 1 && len != (size_t)st->n)
+        return set_error(HQ_ERR_ARG, "token string has %zu characters; need 1 or n=%d", len, st->n);
+    for (size_t i = 0; i < len; ++i)
+        if (tokens[i] != '0' && tokens[i] != '1' && tokens[i] != '+' && tokens[i] != '-')
+            return set_error(HQ_ERR_ARG, "token '%c' not in {0,1,+,-} (tensor-network-only or invalid)", tokens[i]);
+    st->pi = st->pi_init;
+    for (auto &s : st->sh) {
+        uint64_t fix_mask = 0, fix_val = 0, minus = 0;
+        int npm = 0;
+        bool zero = false;
+        double sign = 1.0;
+        for (int q = 0; q < st->n; ++q) {
+            const char t = tokens[len == 1 ? 0 : q];
+            const int p = st->pi[q];
+            if (p < st->nl) {
+                if (t == '0' || t == '1') {
+                    fix_mask |= 1ull << p;
+                    if (t == '1') fix_val |= 1ull << p;
+                } else {
+                    ++npm;
+                    if (t == '-') minus |= 1ull << p;
+                }
+            } else {
+                const int rb = (s.rank >> (p - st->nl)) & 1;
+                if (t == '0' || t == '1') zero |= rb != (t == '1');
+                else {
+                    ++npm;
+                    if (t == '-' && rb) sign = -sign;
+                }
+            }
+        }
+        double mag = sign * std::pow(2.0, -0.5 * npm);
+        if (zero) { fix_mask = 1; fix_val = 2; }      // never matches: all-zero shard
+        CUDA_TRY(cudaSetDevice(s.device));
+        int e = launch_init_tokens((int)st->dtype, s.psi, 1ull << st->nl, fix_mask, fix_val, minus, mag, s.stream);
+        if (e) return set_error(HQ_ERR_CUDA, "init_tokens launch: %s", cudaGetErrorString((cudaError_t)e));
+        st->stats.kernel_launches++;
+    }
+    st->amp_bound = 1.0 + 1e-12;
+    return HQ_OK;
+}
+
+static hq_status allreduce_host(hq_state *st, double *v, int count) {
+    if (st->mode != MODE_RANK) return HQ_OK;
+    Shard &s = st->sh[0];
+    double *d = nullptr;
+    CUDA_TRY(cudaSetDevice(s.device));
+    CUDA_TRY(cudaMalloc((void **)&d, sizeof(double) * count));
+    cudaError_t ce = cudaMemcpyAsync(d, v, sizeof(double) * count, cudaMemcpyHostToDevice, s.stream);
+    ncclResult_t nr = ce ? ncclSuccess : ncclAllReduce(d, d, count, ncclDouble, ncclSum, s.comm, s.stream);
+    if (!ce && nr == ncclSuccess) ce = cudaMemcpyAsync(v, d, sizeof(double) * count, cudaMemcpyDeviceToHost, s.stream);
+    if (!ce) ce = cudaStreamSynchronize(s.stream);
+    cudaFree(d);
+    if (nr != ncclSuccess) return set_error(HQ_ERR_NCCL, "ncclAllReduce: %s", ncclGetErrorString(nr));
+    if (ce) return set_error(HQ_ERR_CUDA, "allreduce copy: %s", cudaGetErrorString(ce));
+    return HQ_OK;
+}
+
+extern "C" hq_status hq_project(hq_state *st, const int32_t *qubits, const int32_t *bits, int nq,
+                                int renormalize, double *norm_out) {
+    clear_error();
+    if (!st || !bits) return set_error(HQ_ERR_ARG, "NULL argument");
+    hq_status rc = validate_targets(st, qubits, nq, st->n);
+    if (rc) return rc;
+    for (int j = 0; j < nq; ++j)
+        if (bits[j] != 0 && bits[j] != 1) return set_error(HQ_ERR_ARG, "bits[%d]=%d not 0/1", j, bits[j]);
+    double total = 0.0;
+    for (auto &s : st->sh) {
+        uint64_t mask = 0, val = 0;
+        bool zero = false;
+        for (int j = 0; j < nq; ++j) {
+            const int p = st->pi[qubits[j]];
+            if (p < st->nl) {
+                mask |= 1ull << p;
+                if (bits[j]) val |= 1ull << p;
+            } else {
+                zero |= ((s.rank >> (p - st->nl)) & 1) != bits[j];
+            }
+        }
+        if (zero) { mask = 0; val = 1; }           // (i & 0) != 1: zero the shard
+        CUDA_TRY(cudaSetDevice(s.device));
+        int nb = 0;
+        int e = launch_project((int)st->dtype, s.psi, 1ull << st->nl, mask, val, 0, s.d_part, 148 * 16, s.stream, &nb);
+        if (e) return set_error(HQ_ERR_CUDA, "project launch: %s", cudaGetErrorString((cudaError_t)e));
+        st->stats.kernel_launches++;
+        st->stats.hbm_bytes += (uint64_t)2 * (st->es << st->nl);
+        CUDA_TRY(cudaMemcpyAsync(s.h_part, s.d_part, sizeof(double) * nb, cudaMemcpyDeviceToHost, s.stream));
+        CUDA_TRY(cudaStreamSynchronize(s.stream));
+        double acc = 0.0;
+        for (int b = 0; b < nb; ++b) acc += s.h_part[b];
+        total += acc;
+    }
+    if ((rc = allreduce_host(st, &total, 1))) return rc;
+    const double nrm = std::sqrt(total);
+    if (norm_out) *norm_out = nrm;
+    if (!renormalize) return HQ_OK;            // amp_bound unchanged: projection never grows the norm
+    if (nrm < 1e-14) return set_error(HQ_ERR_RANGE, "projected norm %.3e < 1e-14 (ZeroNormProjection)", nrm);
+    for (auto &s : st->sh) {
+        CUDA_TRY(cudaSetDevice(s.device));
+        int e = launch_scale((int)st->dtype, s.psi, 1ull << st->nl, 1.0 / nrm, s.stream);
+        if (e) return set_error(HQ_ERR_CUDA, "scale launch: %s", cudaGetErrorString((cudaError_t)e));
+        st->stats.kernel_launches++;
+        st->stats.hbm_bytes += (uint64_t)2 * (st->es << st->nl);
+    }
+    st->amp_bound = 1.0 + 1e-6;
+    return HQ_OK;
+}
+
+extern "C" hq_status hq_probabilities(hq_state *st, const int32_t *qubits, int nq, double *probs_out) {
+    clear_error();
+    if (!st || !probs_out) return set_error(HQ_ERR_ARG, "NULL argument");
+    hq_status rc = validate_targets(st, qubits, nq, 10);
+    if (rc) return rc;
+    const int nout = 1 << nq;
+    std::vector<double> probs(nout, 0.0);
+    for (auto &s : st->sh) {
+        ProbParams P;
+        int loc[16], nloc = 0;      // local measured qubits, in qubits[] order
+        for (int j = 0; j < nq; ++j)
+            if (st->pi[qubits[j]] < st->nl) loc[nloc++] = j;
+        P.nq = nloc;
+        for (int t = 0; t < nloc; ++t) P.pos[t] = st->pi[qubits[loc[t]]];
+        const int nb_max = 148 * 2;
+        double *dh = nullptr;
+        CUDA_TRY(cudaSetDevice(s.device));
+        CUDA_TRY(cudaMalloc((void **)&dh, sizeof(double) * (size_t)nb_max << nloc));
+        int nb = 0;
+        int e = launch_probabilities((int)st->dtype, s.psi, 1ull << st->nl, P, dh, nb_max, s.stream, &nb);
+        if (e) { cudaFree(dh); return set_error(HQ_ERR_CUDA, "probabilities launch: %s", cudaGetErrorString((cudaError_t)e)); }
+        std::vector<double> h((size_t)nb << nloc);
+        cudaError_t ce = cudaMemcpyAsync(h.data(), dh, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, s.stream);
+        if (!ce) ce = cudaStreamSynchronize(s.stream);
+        cudaFree(dh);
+        if (ce) return set_error(HQ_ERR_CUDA, "probabilities copy: %s", cudaGetErrorString(ce));
+        st->stats.kernel_launches++;
+        st->stats.hbm_bytes += st->es << st->nl;
+        // local outcome y (bits of the local measured qubits) -> full outcome x
+        int gx = 0;       // bits of global measured qubits for this shard
+        for (int j = 0; j < nq; ++j) {
+            const int p = st->pi[qubits[j]];
+            if (p >= st->nl) gx |= ((s.rank >> (p - st->nl)) & 1) << (nq - 1 - j);
+        }
+        for (int y = 0; y < (1 << nloc); ++y) {
+            double acc = 0.0;
+            for (int b = 0; b < nb; ++b) acc += h[((size_t)b << nloc) + y];
+            int x = gx;
+            for (int t = 0; t < nloc; ++t)
+                if ((y >> (nloc - 1 - t)) & 1) x |= 1 << (nq - 1 - loc[t]);
+            probs[x] += acc;
+        }
+    }
+    if ((rc = allreduce_host(st, probs.data(), nout))) return rc;
+    for (int x = 0; x < nout; ++x) probs_out[x] = probs[x];
+    return HQ_OK;
+}
+
+extern "C" hq_status hq_measure(hq_state *st, const int32_t *qubits, int nq, double u, uint64_t *outcome_out) {
+    clear_error();
+    if (!st || !outcome_out) return set_error(HQ_ERR_ARG, "NULL argument");
+    if (!(u >= 0.0 && u < 1.0)) return set_error(HQ_ERR_ARG, "u=%g not in [0,1)", u);
+    hq_status rc = validate_targets(st, qubits, nq, 10);
+    if (rc) return rc;
+    std::vector<double> p(1u << nq);
+    if ((rc = hq_probabilities(st, qubits, nq, p.data()))) return rc;
+    double total = 0.0;
+    for (double v : p) total += v;
+    if (!(total > 0.0)) return set_error(HQ_ERR_RANGE, "zero state cannot be measured");
+    const double target = u * total;
+    double cum = 0.0;
+    int x = (int)p.size() - 1;
+    for (int i = 0; i < (int)p.size(); ++i) {
+        cum += p[i];
+        if (target < cum && p[i] > 0.0) { x = i; break; }
+    }
+    while (x > 0 && p[x] == 0.0) --x;               // u at the very top: last non-zero outcome
+    std::vector<int32_t> bits(nq);
+    for (int j = 0; j < nq; ++j) bits[j] = (x >> (nq - 1 - j)) & 1;
+    double nrm = 0.0;
+    if ((rc = hq_project(st, qubits, bits.data(), nq, 1, &nrm))) return rc;
+    *outcome_out = (uint64_t)x;
+    return HQ_OK;
+}
+
 // ------------------------------------------------------------------ diagnostics
 
 extern "C" const char *hq_last_error(void) { return g_err.c_str(); }

@@ -1,0 +1,152 @@
+// State preparation and measurement kernels:
+// token product states, projection
+// and Born probabilities for measurement.
+//
+// All masks are PHYSICAL bit masks of the local index; the runtime maps
+// logical qubits through pi and handles the rank (global) bits on the host.
+// Each kernel is one streaming pass over the shard: init writes 8/16 B per
+// amplitude, project reads+writes, probabilities reads.
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "hq_internal.h"
+
+namespace hq {
+
+namespace {
+
+template <typename V>
+__global__ void __launch_bounds__(256) init_tokens_kernel(V *__restrict__ psi, uint64_t n_amps,
+                                                          uint64_t fix_mask, uint64_t fix_val,
+                                                          uint64_t minus_mask, double mag) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_amps;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        V v;
+        v.y = 0;
+        if ((i & fix_mask) != fix_val) {
+            v.x = 0;
+        } else {
+            const int neg = __popcll(i & minus_mask) & 1;
+            v.x = (decltype(v.x))(neg ? -mag : mag);
+        }
+        psi[i] = v;
+    }
+}
+
+template <typename V>
+__global__ void __launch_bounds__(256) project_kernel(V *__restrict__ psi, uint64_t n_amps,
+                                                      uint64_t mask, uint64_t val, int keep_all,
+                                                      double *__restrict__ part) {
+    double acc = 0.0;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_amps;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        if (keep_all || (i & mask) == val) {
+            const V v = psi[i];
+            acc += (double)v.x * (double)v.x + (double)v.y * (double)v.y;
+        } else {
+            V z;
+            z.x = 0;
+            z.y = 0;
+            psi[i] = z;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    __shared__ double red[8];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+        part[blockIdx.x] = t;
+    }
+}
+
+template <typename V>
+__global__ void __launch_bounds__(256) scale_kernel(V *__restrict__ psi, uint64_t n_amps, double s) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_amps;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        V v = psi[i];
+        v.x = (decltype(v.x))(v.x * s);
+        v.y = (decltype(v.y))(v.y * s);
+        psi[i] = v;
+    }
+}
+
+// hist[block][x] = sum over this block's amplitudes with outcome x of |psi|^2,
+// outcome x = bits of i at positions pos[0..nq) (pos[0] = MSB of x).
+template <typename V>
+__global__ void __launch_bounds__(256) prob_kernel(const V *__restrict__ psi, uint64_t n_amps,
+                                                   const __grid_constant__ ProbParams P,
+                                                   double *__restrict__ hist) {
+    extern __shared__ double sh[];
+    const int nb = 1 << P.nq;
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) sh[b] = 0.0;
+    __syncthreads();
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_amps;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const V v = psi[i];
+        const double p = (double)v.x * (double)v.x + (double)v.y * (double)v.y;
+        if (p == 0.0) continue;
+        int x = 0;
+        for (int j = 0; j < P.nq; ++j) x |= (int)((i >> P.pos[j]) & 1) << (P.nq - 1 - j);
+        atomicAdd(&sh[x], p);
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) hist[(size_t)blockIdx.x * nb + b] = sh[b];
+}
+
+unsigned grid_for(uint64_t n) {
+    uint64_t b = (n + 255) / 256;
+    if (b > 148ull * 8) b = 148ull * 8;
+    return (unsigned)(b ? b : 1);
+}
+
+}  // namespace
+
+int launch_init_tokens(int dtype, void *psi, uint64_t n_amps, uint64_t fix_mask, uint64_t fix_val,
+                       uint64_t minus_mask, double mag, void *stream) {
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (dtype == HQ_C64)
+        init_tokens_kernel<float2><<<grid_for(n_amps), 256, 0, st>>>((float2 *)psi, n_amps, fix_mask,
+                                                                     fix_val, minus_mask, mag);
+    else
+        init_tokens_kernel<double2><<<grid_for(n_amps), 256, 0, st>>>((double2 *)psi, n_amps, fix_mask,
+                                                                      fix_val, minus_mask, mag);
+    return (int)cudaGetLastError();
+}
+
+int launch_project(int dtype, void *psi, uint64_t n_amps, uint64_t mask, uint64_t val, int keep_all,
+                   double *dev_partial, int max_blocks, void *stream, int *nblocks_out) {
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    unsigned g = grid_for(n_amps);
+    if (g > (unsigned)max_blocks) g = max_blocks;
+    if (dtype == HQ_C64)
+        project_kernel<float2><<<g, 256, 0, st>>>((float2 *)psi, n_amps, mask, val, keep_all, dev_partial);
+    else
+        project_kernel<double2><<<g, 256, 0, st>>>((double2 *)psi, n_amps, mask, val, keep_all, dev_partial);
+    *nblocks_out = (int)g;
+    return (int)cudaGetLastError();
+}
+
+int launch_scale(int dtype, void *psi, uint64_t n_amps, double s, void *stream) {
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (dtype == HQ_C64) scale_kernel<float2><<<grid_for(n_amps), 256, 0, st>>>((float2 *)psi, n_amps, s);
+    else scale_kernel<double2><<<grid_for(n_amps), 256, 0, st>>>((double2 *)psi, n_amps, s);
+    return (int)cudaGetLastError();
+}
+
+int launch_probabilities(int dtype, const void *psi, uint64_t n_amps, const ProbParams &P,
+                         double *dev_hist, int max_blocks, void *stream, int *nblocks_out) {
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    unsigned g = grid_for(n_amps);
+    if (g > (unsigned)max_blocks) g = max_blocks;
+    const size_t shm = sizeof(double) << P.nq;
+    if (dtype == HQ_C64)
+        prob_kernel<float2><<<g, 256, shm, st>>>((const float2 *)psi, n_amps, P, dev_hist);
+    else
+        prob_kernel<double2><<<g, 256, shm, st>>>((const double2 *)psi, n_amps, P, dev_hist);
+    *nblocks_out = (int)g;
+    return (int)cudaGetLastError();
+}
+
+}  // namespace hq

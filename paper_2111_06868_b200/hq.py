@@ -88,6 +88,10 @@ def lib():
             "hq_plan_layout": [ctypes.c_int, ctypes.c_int, ctypes.c_int, P, ctypes.c_size_t, P,
                                ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)],
             "hq_state_set_layout": [P, P],
+            "hq_state_init_tokens": [P, ctypes.c_char_p],
+            "hq_project": [P, P, P, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double)],
+            "hq_probabilities": [P, P, ctypes.c_int, P],
+            "hq_measure": [P, P, ctypes.c_int, ctypes.c_double, ctypes.POINTER(ctypes.c_uint64)],
             "hq_state_get_layout": [P, P],
             "hq_sync": [P],
             "hq_stats_get": [P, ctypes.POINTER(hq_stats)],
@@ -216,6 +220,34 @@ def hq_state_info(state):
 
 def hq_state_init_basis(state, x=0):
     _check(lib().hq_state_init_basis(state.ptr, int(x)))
+
+
+def hq_state_init_tokens(state, tokens):
+    _check(lib().hq_state_init_tokens(state.ptr, tokens.encode()))
+
+
+def hq_project(state, qubits, bits, renormalize=False):
+    """Returns the norm of the projected state (before renormalisation)."""
+    q = np.ascontiguousarray(qubits, dtype=np.int32)
+    b = np.ascontiguousarray(bits, dtype=np.int32)
+    out = ctypes.c_double()
+    _check(lib().hq_project(state.ptr, q.ctypes.data, b.ctypes.data, int(q.size), int(bool(renormalize)),
+                            ctypes.byref(out)))
+    return out.value
+
+
+def hq_probabilities(state, qubits):
+    q = np.ascontiguousarray(qubits, dtype=np.int32)
+    out = np.zeros(2 ** q.size, dtype=np.float64)
+    _check(lib().hq_probabilities(state.ptr, q.ctypes.data, int(q.size), out.ctypes.data))
+    return out
+
+
+def hq_measure(state, qubits, u):
+    q = np.ascontiguousarray(qubits, dtype=np.int32)
+    out = ctypes.c_uint64()
+    _check(lib().hq_measure(state.ptr, q.ctypes.data, int(q.size), float(u), ctypes.byref(out)))
+    return out.value
 
 
 def hq_get_amplitudes(state, first=0, count=None, out=None):

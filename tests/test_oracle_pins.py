@@ -308,3 +308,63 @@ def test_C18_haar_unitary():
     for k in range(1, 7):
         U = haar_unitary(k, rng)
         assert np.max(np.abs(U @ U.conj().T - np.eye(2 ** k))) < 1e-14
+
+
+# ---------------------------------------------------------------- f4: tokens, projection, probabilities
+def test_tokens_spec_examples():
+    """SPEC S:229-236 examples."""
+    a = O.init_tokens(2, "00")
+    assert a[0] == 1 and np.count_nonzero(a) == 1
+    assert np.allclose(O.init_tokens(6, "++++++"), 2 ** -3, atol=1e-16)
+    assert np.allclose(O.init_tokens(2, "+-"), [0.5, -0.5, 0.5, -0.5], atol=1e-16)
+    assert np.array_equal(O.init_tokens(5, "+"), O.init_tokens(5, "+++++"))     # broadcast (P:750)
+    # qubit 0 is the MSB (C1): |1> on qubit 0 of 3 qubits is index 100
+    assert np.flatnonzero(O.init_tokens(3, "100")).tolist() == [4]
+    with pytest.raises(O.OracleError):
+        O.init_tokens(3, "0.1")
+
+
+def test_tokens_vs_gates():
+    """'+'/'-' tokens equal H (and X then H) applied to |0> (closed form)."""
+    n = 5
+    tok = "+-01+"
+    gates = []
+    for q, t in enumerate(tok):
+        if t in "1-":
+            gates.append(Gate("X", (q,), X))
+        if t in "+-":
+            gates.append(Gate("H", (q,), H))
+    assert np.max(np.abs(O.init_tokens(n, tok) - O.simulate(n, gates))) < 1e-15
+
+
+def test_projection_spec_examples_and_grover():
+    """SPEC S:252-255; the paper's own Grover oracle psi -= 2 * Projection(psi)
+    on qubits [1, 2] reproduces the printed listing."""
+    plus = O.init_tokens(1, "+")
+    out, nrm = O.project(plus, [0], [0])
+    assert np.allclose(out, [1 / np.sqrt(2), 0], atol=1e-16) and abs(nrm - 1 / np.sqrt(2)) < 1e-15
+    psi = O.init_tokens(3, "+")
+    psi0, _ = O.project(psi, [1, 2], [0, 0], renormalize=False)
+    new = psi - 2 * psi0
+    for bits, val in _golden("grover_P403-422.txt"):
+        assert abs(new[int(bits, 2)].real - float(val)) < 1e-6
+    basis = O.init_basis(4, 9)
+    again, _ = O.project(basis, [0, 3], [1, 1], renormalize=True)
+    assert np.array_equal(again, basis)
+    with pytest.raises(O.OracleError):
+        O.project(O.init_basis(2, 0), [0], [1], renormalize=True)
+
+
+def test_probabilities_closed_forms():
+    assert np.allclose(O.probabilities(O.init_basis(1, 1), [0]), [0, 1])
+    assert np.allclose(O.probabilities(O.init_tokens(1, "+"), [0]), [0.5, 0.5])
+    psi = random_state(6, 3)
+    joint = O.probabilities(psi, [4, 1])
+    # chain rule: marginal of qubit 4 = sum over qubit 1 of the joint
+    assert np.allclose(joint.reshape(2, 2).sum(axis=1), O.probabilities(psi, [4]), atol=1e-15)
+    assert abs(joint.sum() - 1) < 1e-14
+    # brute force on tiny input
+    brute = np.zeros(4)
+    for i in range(64):
+        brute[(((i >> 1) & 1) << 1) | ((i >> 4) & 1)] += abs(psi[i]) ** 2
+    assert np.allclose(joint, brute, atol=1e-15)
