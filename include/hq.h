@@ -202,6 +202,34 @@ hq_status hq_probabilities(hq_state *s, const int32_t *qubits, int nq, double *p
  * and renormalise.  *outcome_out = x (qubits[0] = MSB). */
 hq_status hq_measure(hq_state *s, const int32_t *qubits, int nq, double u, uint64_t *outcome_out);
 
+/* ------------------------------------------------------------------ density matrices
+ * Density-matrix evolution by doubling (PAPER P:286-289 MatrixSuperGate "using
+ * a matrix-vector multiplication", "a super circuit [becomes] a
+ * regular circuit" on 2N qubits): an N-qubit density matrix rho
+ * is the 2N-qubit state vec(rho) with vec(rho)[i 2^N + j] = rho[i][j], i.e.
+ * logical qubits 0..N-1 index the rows and N..2N-1 the columns.  The state
+ * must have an even number of qubits n = 2N.  Channels run through the same
+ * apply kernels as any gate. */
+
+/* Superoperator of the Kraus map rho -> sum_m K_m rho K_m^dagger on k qubits
+ * (1 <= k <= 3): S = sum_m K_m (x) conj(K_m), a 2k-qubit matrix whose targets
+ * are (qubits, qubits + N) in that order.  K[m] = 2*4^k doubles (interleaved,
+ * row-major); S_out = 2*16^k doubles.  Host-only. */
+hq_status hq_dm_superop(const double *const *K, int nkraus, int k, double *S_out);
+
+/* rho -> U rho U^dagger on qubits[0..k) (1 <= k <= 3: one fused 2k-qubit pass;
+ * 4 <= k <= 6: two passes, U on the row qubits and conj(U) on the columns). */
+hq_status hq_dm_apply_unitary(hq_state *s, const double *U, const int32_t *qubits, int k);
+
+/* rho -> sum_m K_m rho K_m^dagger on qubits[0..k), 1 <= k <= 3 (one 2k-qubit
+ * superoperator pass; the channel need not be trace preserving). */
+hq_status hq_dm_apply_kraus(hq_state *s, const double *const *K, int nkraus, const int32_t *qubits,
+                            int k);
+
+/* tr(rho) (complex, FP64 accumulation over the 2^N diagonal entries, all
+ * ranks).  Synchronises. */
+hq_status hq_dm_trace(hq_state *s, double *re, double *im);
+
 /* ------------------------------------------------------------------ apply */
 
 /* psi <- (U embedded on qubits) psi.

@@ -30,6 +30,11 @@ Contents, each following the passage cited:
   vectors, projection and Born
   probabilities written out from their definitions.
 
+* ``dm_apply_kraus`` -- a Kraus map rho -> sum_m K_m rho K_m^dagger on the
+  density matrix itself, with embedded K_m, and
+  ``dm_vec`` -- the row-major vectorisation vec(rho)[i 2^N + j] = rho[i][j]
+  that the doubling reading (row f2) applies gates to.
+
 Parity pins for every function live in ``tests/test_oracle_pins.py``.
 """
 import ctypes
@@ -268,3 +273,20 @@ def probabilities(psi, qubits):
     for j, col in enumerate(_qubit_bits(n, qubits)):
         x |= col << (k - 1 - j)
     return np.bincount(x, weights=np.abs(psi) ** 2, minlength=2 ** k)
+
+
+# ---------------------------------------------------------------- f2: density matrices
+
+def dm_apply_kraus(rho, K, qubits):
+    """rho -> sum_m E_m rho E_m^dagger, E_m = K_m embedded on qubits of N."""
+    N = int(np.log2(rho.shape[0]))
+    out = np.zeros_like(rho, dtype=np.complex128)
+    for k in K:
+        E = embed_dense(N, k, qubits)
+        out += E @ rho @ E.conj().T
+    return out
+
+
+def dm_vec(rho):
+    """vec(rho)[i 2^N + j] = rho[i][j] (logical qubits 0..N-1 = rows)."""
+    return np.ascontiguousarray(rho, dtype=np.complex128).reshape(-1)

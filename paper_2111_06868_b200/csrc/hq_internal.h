@@ -7,6 +7,8 @@
 #include <string>
 #include <vector>
 
+#include <cuda_runtime.h>
+
 #include "hq.h"
 
 namespace hq {
@@ -118,5 +120,10 @@ int launch_project(int dtype, void *psi, uint64_t n_amps, uint64_t mask, uint64_
 int launch_scale(int dtype, void *psi, uint64_t n_amps, double s, void *stream);
 int launch_probabilities(int dtype, const void *psi, uint64_t n_amps, const ProbParams &P,
                          double *dev_hist, int max_blocks, void *stream, int *nblocks_out);
+struct DmParams {
+    int bitmap[64];          // logical index bit -> physical bit
+};
+int launch_dm_trace(int dtype, const void *psi, int N, int n_local, int rank, const DmParams &P,
+                    double2 *dev_part, int max_blocks, void *stream, int *nblocks_out);
 
 }  // namespace hq

@@ -1304,6 +1304,108 @@ extern "C" hq_status hq_measure(hq_state *st, const int32_t *qubits, int nq, dou
     return HQ_OK;
 }
 
+// ------------------------------------------------------------------ f2: density matrices
+
+extern "C" hq_status hq_dm_superop(const double *const *K, int nkraus, int k, double *S_out) {
+    clear_error();
+    if (!K || !S_out || nkraus < 1) return set_error(HQ_ERR_ARG, "NULL argument or no Kraus operators");
+    if (k < 1 || k > 3) return set_error(HQ_ERR_K, "k=%d not in [1,3] (superoperator has 2k <= 6 targets)", k);
+    const int d = 1 << k, D = d * d;
+    for (int i = 0; i < 2 * D * D; ++i) S_out[i] = 0.0;
+    for (int m = 0; m < nkraus; ++m) {
+        if (!K[m]) return set_error(HQ_ERR_ARG, "K[%d] is NULL", m);
+        const double *A = K[m];
+        // S[(r, c), (r', c')] += A[r][r'] * conj(A[c][c'])
+        for (int r = 0; r < d; ++r)
+            for (int c = 0; c < d; ++c)
+                for (int rp = 0; rp < d; ++rp)
+                    for (int cp = 0; cp < d; ++cp) {
+                        const double ar = A[2 * (r * d + rp)], ai = A[2 * (r * d + rp) + 1];
+                        const double br = A[2 * (c * d + cp)], bi = -A[2 * (c * d + cp) + 1];
+                        const int row = r * d + c, col = rp * d + cp;
+                        S_out[2 * (row * D + col)] += ar * br - ai * bi;
+                        S_out[2 * (row * D + col) + 1] += ar * bi + ai * br;
+                    }
+    }
+    return HQ_OK;
+}
+
+static hq_status dm_check(const hq_state *st, const int32_t *qubits, int k) {
+    if (st->n % 2) return set_error(HQ_ERR_STATE, "density-matrix calls need an even number of qubits (n=%d)", st->n);
+    const int N = st->n / 2;
+    if (!qubits) return set_error(HQ_ERR_ARG, "qubits is NULL");
+    for (int j = 0; j < k; ++j) {
+        if (qubits[j] < 0 || qubits[j] >= N) return set_error(HQ_ERR_QUBIT, "qubit %d not in [0,%d)", qubits[j], N);
+        for (int l = 0; l < j; ++l)
+            if (qubits[l] == qubits[j]) return set_error(HQ_ERR_DUP_QUBIT, "repeated qubit %d", qubits[j]);
+    }
+    return HQ_OK;
+}
+
+extern "C" hq_status hq_dm_apply_kraus(hq_state *st, const double *const *K, int nkraus,
+                                       const int32_t *qubits, int k) {
+    clear_error();
+    if (!st) return set_error(HQ_ERR_ARG, "state is NULL");
+    hq_status rc = dm_check(st, qubits, k);
+    if (rc) return rc;
+    if (k < 1 || k > 3) return set_error(HQ_ERR_K, "k=%d not in [1,3]", k);
+    std::vector<double> S((size_t)2 << (4 * k));
+    if ((rc = hq_dm_superop(K, nkraus, k, S.data()))) return rc;
+    const int N = st->n / 2;
+    int32_t q2[6];
+    for (int j = 0; j < k; ++j) { q2[j] = qubits[j]; q2[k + j] = qubits[j] + N; }
+    return hq_apply_matrix(st, S.data(), q2, 2 * k);
+}
+
+extern "C" hq_status hq_dm_apply_unitary(hq_state *st, const double *U, const int32_t *qubits, int k) {
+    clear_error();
+    if (!st || !U) return set_error(HQ_ERR_ARG, "NULL argument");
+    hq_status rc = dm_check(st, qubits, k);
+    if (rc) return rc;
+    if (k < 1 || k > 6) return set_error(HQ_ERR_K, "k=%d not in [1,6]", k);
+    const int N = st->n / 2, d = 1 << k;
+    if (k <= 3) {
+        const double *K[1] = {U};
+        return hq_dm_apply_kraus(st, K, 1, qubits, k);
+    }
+    std::vector<double> Uc((size_t)2 * d * d);
+    for (int i = 0; i < d * d; ++i) { Uc[2 * i] = U[2 * i]; Uc[2 * i + 1] = -U[2 * i + 1]; }
+    int32_t qc[6];
+    for (int j = 0; j < k; ++j) qc[j] = qubits[j] + N;
+    hq_gate g[2];
+    g[0].k = k; g[1].k = k;
+    for (int j = 0; j < 6; ++j) { g[0].qubits[j] = j < k ? qubits[j] : -1; g[1].qubits[j] = j < k ? qc[j] : -1; }
+    g[0].U = U;
+    g[1].U = Uc.data();
+    return hq_apply_circuit(st, g, 2);
+}
+
+extern "C" hq_status hq_dm_trace(hq_state *st, double *re, double *im) {
+    clear_error();
+    if (!st || !re || !im) return set_error(HQ_ERR_ARG, "NULL argument");
+    if (st->n % 2) return set_error(HQ_ERR_STATE, "density-matrix calls need an even number of qubits");
+    const int N = st->n / 2;
+    DmParams P;
+    for (int q = 0; q < st->n; ++q) P.bitmap[st->n - 1 - q] = st->pi[q];
+    double t[2] = {0.0, 0.0};
+    for (auto &s : st->sh) {
+        CUDA_TRY(cudaSetDevice(s.device));
+        int nb = 0;
+        int e = launch_dm_trace((int)st->dtype, s.psi, N, st->nl, s.rank, P,
+                                reinterpret_cast<double2 *>(s.d_part), 148 * 8, s.stream, &nb);
+        if (e) return set_error(HQ_ERR_CUDA, "dm_trace launch: %s", cudaGetErrorString((cudaError_t)e));
+        st->stats.kernel_launches++;
+        CUDA_TRY(cudaMemcpyAsync(s.h_part, s.d_part, sizeof(double) * 2 * nb, cudaMemcpyDeviceToHost, s.stream));
+        CUDA_TRY(cudaStreamSynchronize(s.stream));
+        for (int b = 0; b < nb; ++b) { t[0] += s.h_part[2 * b]; t[1] += s.h_part[2 * b + 1]; }
+    }
+    hq_status rc = allreduce_host(st, t, 2);
+    if (rc) return rc;
+    *re = t[0];
+    *im = t[1];
+    return HQ_OK;
+}
+
 // ------------------------------------------------------------------ diagnostics
 
 extern "C" const char *hq_last_error(void) { return g_err.c_str(); }

@@ -101,7 +101,53 @@ unsigned grid_for(uint64_t n) {
     return (unsigned)(b ? b : 1);
 }
 
+// Sum of the diagonal of an N-qubit density matrix stored as the 2N-qubit
+// vec(rho): logical index (i, i) = i * 2^N + i, mapped to physical bits by
+// bitmap (logical bit -> physical bit); only amplitudes of this rank count.
+template <typename V>
+__global__ void __launch_bounds__(256) dm_trace_kernel(const V *__restrict__ psi, int N, int n_local,
+                                                       int rank, const __grid_constant__ DmParams P,
+                                                       double2 *__restrict__ part) {
+    double re = 0.0, im = 0.0;
+    const uint64_t cnt = 1ull << N;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t li = (i << N) | i;
+        uint64_t phys = 0;
+        for (int b = 0; b < 2 * N; ++b) phys |= ((li >> b) & 1) << P.bitmap[b];
+        if ((int)(phys >> n_local) != rank) continue;
+        const V v = psi[phys & ((1ull << n_local) - 1)];
+        re += (double)v.x;
+        im += (double)v.y;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        re += __shfl_xor_sync(0xffffffffu, re, o);
+        im += __shfl_xor_sync(0xffffffffu, im, o);
+    }
+    __shared__ double2 red[8];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = make_double2(re, im);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double2 t = make_double2(0.0, 0.0);
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { t.x += red[w].x; t.y += red[w].y; }
+        part[blockIdx.x] = t;
+    }
+}
+
 }  // namespace
+
+int launch_dm_trace(int dtype, const void *psi, int N, int n_local, int rank, const DmParams &P,
+                    double2 *dev_part, int max_blocks, void *stream, int *nblocks_out) {
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    unsigned g = grid_for(1ull << N);
+    if (g > (unsigned)max_blocks) g = max_blocks;
+    if (dtype == HQ_C64)
+        dm_trace_kernel<float2><<<g, 256, 0, st>>>((const float2 *)psi, N, n_local, rank, P, dev_part);
+    else
+        dm_trace_kernel<double2><<<g, 256, 0, st>>>((const double2 *)psi, N, n_local, rank, P, dev_part);
+    *nblocks_out = (int)g;
+    return (int)cudaGetLastError();
+}
 
 int launch_init_tokens(int dtype, void *psi, uint64_t n_amps, uint64_t fix_mask, uint64_t fix_val,
                        uint64_t minus_mask, double mag, void *stream) {

@@ -89,6 +89,10 @@ def lib():
                                ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)],
             "hq_state_set_layout": [P, P],
             "hq_state_init_tokens": [P, ctypes.c_char_p],
+            "hq_dm_superop": [P, ctypes.c_int, ctypes.c_int, P],
+            "hq_dm_apply_unitary": [P, P, P, ctypes.c_int],
+            "hq_dm_apply_kraus": [P, P, ctypes.c_int, P, ctypes.c_int],
+            "hq_dm_trace": [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)],
             "hq_project": [P, P, P, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double)],
             "hq_probabilities": [P, P, ctypes.c_int, P],
             "hq_measure": [P, P, ctypes.c_int, ctypes.c_double, ctypes.POINTER(ctypes.c_uint64)],
@@ -248,6 +252,39 @@ def hq_measure(state, qubits, u):
     out = ctypes.c_uint64()
     _check(lib().hq_measure(state.ptr, q.ctypes.data, int(q.size), float(u), ctypes.byref(out)))
     return out.value
+
+
+def _kraus_array(K):
+    mats = [np.ascontiguousarray(k, dtype=np.complex128) for k in K]
+    ptrs = (ctypes.c_void_p * len(mats))(*[m.ctypes.data for m in mats])
+    return ptrs, mats
+
+
+def hq_dm_superop(K):
+    """Superoperator sum_m K_m (x) conj(K_m) as a complex128 (4^k x 4^k) array."""
+    ptrs, mats = _kraus_array(K)
+    k = int(np.log2(mats[0].shape[0]))
+    S = np.zeros((4 ** k, 4 ** k), dtype=np.complex128)
+    _check(lib().hq_dm_superop(ptrs, len(mats), k, S.ctypes.data))
+    return S
+
+
+def hq_dm_apply_unitary(state, U, qubits):
+    U, Uf = _u_buffer(U)
+    q = np.ascontiguousarray(qubits, dtype=np.int32)
+    _check(lib().hq_dm_apply_unitary(state.ptr, Uf.ctypes.data, q.ctypes.data, int(q.size)))
+
+
+def hq_dm_apply_kraus(state, K, qubits):
+    ptrs, mats = _kraus_array(K)
+    q = np.ascontiguousarray(qubits, dtype=np.int32)
+    _check(lib().hq_dm_apply_kraus(state.ptr, ptrs, len(mats), q.ctypes.data, int(q.size)))
+
+
+def hq_dm_trace(state):
+    re, im = ctypes.c_double(), ctypes.c_double()
+    _check(lib().hq_dm_trace(state.ptr, ctypes.byref(re), ctypes.byref(im)))
+    return complex(re.value, im.value)
 
 
 def hq_get_amplitudes(state, first=0, count=None, out=None):

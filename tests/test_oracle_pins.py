@@ -368,3 +368,46 @@ def test_probabilities_closed_forms():
     for i in range(64):
         brute[(((i >> 1) & 1) << 1) | ((i >> 4) & 1)] += abs(psi[i]) ** 2
     assert np.allclose(joint, brute, atol=1e-15)
+
+
+# ---------------------------------------------------------------- f2: density matrices
+def _depolarizing(p):
+    s = np.sqrt(p / 4)
+    return [np.sqrt(1 - 3 * p / 4) * np.eye(2), s * X, s * Y, s * np.diag([1, -1]).astype(complex)]
+
+
+def _amp_damping(g):
+    return [np.array([[1, 0], [0, np.sqrt(1 - g)]], dtype=complex),
+            np.array([[0, np.sqrt(g)], [0, 0]], dtype=complex)]
+
+
+def test_dm_closed_forms():
+    """Depolarizing: rho -> (1-p) rho + p I/2 on one qubit; amplitude damping
+    on |1><1|: gamma |0><0| + (1-gamma) |1><1| (textbook closed forms)."""
+    psi = random_state(1, 4)
+    rho = np.outer(psi, psi.conj())
+    p = 0.3
+    assert np.max(np.abs(O.dm_apply_kraus(rho, _depolarizing(p), [0]) - ((1 - p) * rho + p * np.eye(2) / 2))) < 1e-15
+    one = np.diag([0, 1]).astype(complex)
+    g = 0.25
+    assert np.max(np.abs(O.dm_apply_kraus(one, _amp_damping(g), [0]) - np.diag([g, 1 - g]))) < 1e-15
+
+
+def test_dm_pure_state_consistency_and_trace():
+    """The paper's cross-check: evolving psi psi^dagger equals the
+    density matrix of the evolved pure state; CPTP maps preserve the trace."""
+    N = 4
+    gates = random_circuit(N, 12, 3, kmax=2)
+    psi = random_state(N, 2)
+    rho = np.outer(psi, psi.conj())
+    for gt in gates:
+        rho = O.dm_apply_kraus(rho, [gt.U], list(gt.qubits))
+    out = O.simulate(N, gates, psi)
+    assert np.max(np.abs(rho - np.outer(out, out.conj()))) < 1e-14
+    rho2 = O.dm_apply_kraus(rho, _amp_damping(0.4), [2])
+    assert abs(np.trace(rho2) - 1) < 1e-14
+    # vec(U rho U^dagger) = (U on rows) (conj U on columns) vec(rho): the doubling reading
+    U = haar_unitary(2, np.random.default_rng(5))
+    v = O.dm_vec(rho)
+    v2 = O.apply_gate(O.apply_gate(v.copy(), U, [1, 3]), U.conj(), [1 + N, 3 + N])
+    assert np.max(np.abs(v2 - O.dm_vec(O.dm_apply_kraus(rho, [U], [1, 3])))) < 1e-14
