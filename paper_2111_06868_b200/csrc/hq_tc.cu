@@ -461,6 +461,305 @@ apply_tc(float2 *__restrict__ psi, const __grid_constant__ Params P,
     }
 }
 
+// ------------------------------------------------------------------ mode H, bulk-copy producer
+// Same contraction and precision as apply_tc<K>; what changes is how the tile
+// reaches shared memory.  A tile spans 13 (K = 6) "tile bits": the targets and
+// the 7 lowest non-target bits, so physical bits 0..6 are always tile bits and
+// the tile is a union of 2^(K + 7 - 7) contiguous 1 KB blocks (128
+// amplitudes, bits 0..6), whatever the placement.  One producer warp moves
+// them with cp.async.bulk (the TMA engine's 1-D bulk copy, completion counted
+// in bytes on an mbarrier) into an NS-deep ring of K-half slots; the K-half
+// bit is the highest target, required to be >= 7 so a block never straddles
+// halves.  Shared memory holds a slot in tile-index order (tile bits
+// ascending, the half bit removed); converter thread (set n, pattern c) reads
+// slot index nidx[n] | cidx[c].  No per-thread address arithmetic or LDGSTS,
+// up to NS - 1 slots in flight while one is converted, and the A operand is
+// double-buffered in TMEM so conversion of tile i+1 overlaps the MMAs of tile i.
+//   warps 0-3 epilogue, 4 MMA, 5-12 converters, 13 producer.
+// TMEM columns: A buffer a, half h: hi [a*KD + h*KD/2, + KD/4), lo the next
+// KD/4; accumulator d: [2*KD + d*N, 2*KD + (d+1)*N).
+constexpr int BK_PROD = NUM_EPI + 1 + H_NUM_CONV;
+constexpr int bk_threads(int np) { return (BK_PROD + np) * 32; }   // np producer warps
+
+template <int K, int NS> struct CfgB {
+    static constexpr int D = 1 << K;
+    static constexpr int KD = 2 * D;
+    static constexpr int N = KD;
+    static constexpr int HA = D / 2;
+    static constexpr int B_BYTES = N * KD * 2;
+    static constexpr int SLOT_BYTES = M * HA * 8;              // one K-half of a tile
+    static constexpr int NBLK = SLOT_BYTES / 1024;             // 1 KB blocks per slot
+    static constexpr int NSLOT = NS;
+    static constexpr int RING = 2 * B_BYTES;
+    static constexpr int BARS = RING + NSLOT * SLOT_BYTES;
+    static constexpr int SMEM = BARS + 256;
+    static constexpr int TMEM_COLS = 4 * KD;                   // 2 A buffers + 2 accumulators
+    static constexpr int LBO = N * 16;
+};
+
+struct ParamsB {
+    Params h;
+    uint64_t off8[64];     // byte offset of canonical target pattern c (= 8 * off[c])
+    uint64_t boff[2][32];  // amplitude offset (from the tile base) of block j of K-half h
+    uint32_t cidx8[32];    // byte offset in a slot of pattern c (low K-1 bits of c)
+    uint16_t nidx[128];    // slot index of gather set n (pattern 0)
+    int ns;                // ring depth (template parameter NS)
+    int np;                // producer warps (template parameter NP)
+};
+
+__device__ __forceinline__ void mbar_arrive_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+
+__device__ __forceinline__ uint64_t f2_as_u64(float2 v) {
+    return (uint64_t)__float_as_uint(v.x) | ((uint64_t)__float_as_uint(v.y) << 32);
+}
+__device__ __forceinline__ float2 u64_as_f2(uint64_t u) {
+    return make_float2(__uint_as_float((uint32_t)u), __uint_as_float((uint32_t)(u >> 32)));
+}
+__device__ __forceinline__ uint64_t mul_f32x2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ uint64_t sub_f32x2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+
+template <int K, int NS, int NP>
+__global__ void __launch_bounds__(bk_threads(NP), 1)
+apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
+          const __half *__restrict__ Breal /* [2][N][KD]: hi then lo, row n = output real */) {
+    static_assert(NS % 2 == 0, "slot parity = K-half needs an even ring");
+    using C = CfgB<K, NS>;
+    constexpr int KD = C::KD, N = C::N, HA = C::HA, NSLOT = C::NSLOT;
+    constexpr int NPOS = K + SETBITS;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t sbase = smem_u32(smem);
+    const uint32_t bar0 = sbase + C::BARS;
+    auto afull = [&](int a, int h) { return bar0 + 8 * (2 * a + h); };
+    auto aempty = [&](int a, int h) { return bar0 + 8 * (4 + 2 * a + h); };
+    auto tfull = [&](int d) { return bar0 + 8 * (8 + d); };
+    auto tempty = [&](int d) { return bar0 + 8 * (10 + d); };
+    auto rfull = [&](int s) { return bar0 + 8 * (12 + s); };
+    auto rempty = [&](int s) { return bar0 + 8 * (12 + NSLOT + s); };
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + C::BARS + 8 * (12 + 2 * NSLOT));
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 4; ++i) {
+            mbar_init(bar0 + 8 * i, 4);              // afull: 4 converter warps
+            mbar_init(bar0 + 8 * (4 + i), 1);        // aempty: MMA commit
+        }
+        for (int d = 0; d < 2; ++d) {
+            mbar_init(tfull(d), 1);
+            mbar_init(tempty(d), NUM_EPI);
+        }
+        for (int s = 0; s < NSLOT; ++s) {
+            mbar_init(rfull(s), 1);                  // producer arrive.expect_tx + bytes
+            mbar_init(rempty(s), 4);                 // 4 converter warps
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == MMA_WARP) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(C::TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    for (int i = threadIdx.x; i < 2 * N * KD / 8; i += bk_threads(NP)) {
+        const int part = i / (N * KD / 8);
+        const int r = i % (N * KD / 8);
+        const int n = r / (KD / 8), kq = r % (KD / 8);
+        const uint4 v = *reinterpret_cast<const uint4 *>(Breal + part * N * KD + n * KD + 8 * kq);
+        *reinterpret_cast<uint4 *>(smem + part * C::B_BYTES + kq * C::LBO + n * 16) = v;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint64_t ntiles = P.h.ntiles;
+    const uint64_t G = gridDim.x;
+
+    if (warp >= BK_PROD) {
+        // NP = 1: one warp fills slots in order.  NP >= 2: producer warp p
+        // fills K-half h = p % 2 (slot parity = h, NS even), blocks
+        // [sub * NB, (sub + 1) * NB) of each slot, sub = p / 2; the sub = 0
+        // warp posts the byte count (a copy may complete before it: the
+        // mbarrier's tx-count may go transiently negative, and the phase
+        // cannot complete while that arrival is pending).
+        const int p = warp - BK_PROD;
+        constexpr int NPH = NP == 1 ? 1 : NP / 2;
+        constexpr int NB = C::NBLK / NPH;
+        const int sub = NP == 1 ? 0 : p / 2;
+        uint32_t it = 0;
+        for (uint64_t t = blockIdx.x; t < ntiles; t += G, ++it) {
+            const float2 *tb = psi + tile_base<NPOS>(t, P.h);
+#pragma unroll 1
+            for (int h = NP == 1 ? 0 : p % 2; h < (NP == 1 ? 2 : p % 2 + 1); ++h) {
+                const uint32_t sidx = 2 * it + h;
+                const int s = sidx % NSLOT;
+                mbar_wait(rempty(s), ((sidx / NSLOT) & 1) ^ 1);
+                if (sub == 0 && lane == 0) mbar_arrive_tx(rfull(s), C::SLOT_BYTES);
+                __syncwarp();
+                if (lane < NB) {
+                    const int j = sub * NB + lane;
+                    bulk_g2s(sbase + C::RING + s * C::SLOT_BYTES + j * 1024, tb + P.boff[h][j], 1024, rfull(s));
+                }
+            }
+        }
+    } else if (warp == MMA_WARP) {
+        const uint32_t idesc = (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(N >> 3) << 17) |
+                               ((uint32_t)(M >> 4) << 24);
+        const uint64_t dbhi = smem_desc(sbase, C::LBO, 128);
+        const uint64_t dblo = smem_desc(sbase + C::B_BYTES, C::LBO, 128);
+        constexpr int JH = KD / 32;
+        constexpr uint32_t DSTEP = (2 * C::LBO) >> 4;
+        uint32_t it = 0;
+        for (uint64_t t = blockIdx.x; t < ntiles; t += G, ++it) {
+            const int d = it & 1;                      // accumulator and A buffer
+            const uint32_t ph = (it >> 1) & 1;
+            const uint32_t Dt = tmem + 2 * KD + d * N;
+            const uint32_t a0 = tmem + d * KD, a1 = a0 + KD / 2;
+            mbar_wait(tempty(d), ph ^ 1);
+            mbar_wait(afull(d, 0), ph);
+            tc_fence_after();
+            // correction terms first, main terms last (see apply_tc)
+            if (elect_one()) {
+#pragma unroll 1
+                for (int jj = 0; jj < JH; ++jj) {
+                    const uint32_t jk = jj * DSTEP;
+                    mma_ts(Dt, a0 + KD / 4 + 8 * jj, dbhi + jk, idesc, jj != 0);
+                    mma_ts(Dt, a0 + 8 * jj, dblo + jk, idesc, 1);
+                }
+            }
+            __syncwarp();
+            mbar_wait(afull(d, 1), ph);
+            tc_fence_after();
+            if (elect_one()) {
+#pragma unroll 1
+                for (int jj = 0; jj < JH; ++jj) {
+                    const uint32_t jk = (JH + jj) * DSTEP;
+                    mma_ts(Dt, a1 + KD / 4 + 8 * jj, dbhi + jk, idesc, 1);
+                    mma_ts(Dt, a1 + 8 * jj, dblo + jk, idesc, 1);
+                }
+#pragma unroll 1
+                for (int jj = 0; jj < JH; ++jj)
+                    mma_ts(Dt, a0 + 8 * jj, dbhi + jj * DSTEP, idesc, 1);
+                mma_commit(aempty(d, 0));
+#pragma unroll 1
+                for (int jj = 0; jj < JH; ++jj)
+                    mma_ts(Dt, a1 + 8 * jj, dbhi + (JH + jj) * DSTEP, idesc, 1);
+                mma_commit(aempty(d, 1));
+                mma_commit(tfull(d));
+            }
+            __syncwarp();
+        }
+    } else if (warp >= CONV0) {
+        const int h = (warp - CONV0) >> 2;
+        const int q = warp & 3;
+        const int n = q * 32 + lane;
+        const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+        const float sA = __int_as_float((127 + max(-126, min(127, P.h.ea))) << 23);
+        const uint64_t sA2 = f2_as_u64(make_float2(sA, sA));
+        const uint32_t nb8 = (uint32_t)P.nidx[n] * 8;
+        uint32_t it = 0;
+        for (uint64_t t = blockIdx.x; t < ntiles; t += G, ++it) {
+            const int a = it & 1;
+            const uint32_t sidx = 2 * it + h;
+            const int s = sidx % NSLOT;
+            // read the whole K-half of this set into registers and hand the
+            // slot back before converting, so the producer can refill it
+            // while this warp waits for the A buffer and converts
+            mbar_wait(rfull(s), (sidx / NSLOT) & 1);
+            const char *raw = reinterpret_cast<const char *>(smem + C::RING + s * C::SLOT_BYTES) + nb8;
+            uint64_t v[HA];
+#pragma unroll
+            for (int c = 0; c < HA; ++c) v[c] = *reinterpret_cast<const uint64_t *>(raw + P.cidx8[c]);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(rempty(s));
+            mbar_wait(aempty(a, h), ((it >> 1) & 1) ^ 1);
+            tc_fence_after();
+            const uint32_t chi = tmem + a * KD + h * (KD / 2) + lane_addr, clo = chi + KD / 4;
+            constexpr int CH = HA < 16 ? HA : 16;
+#pragma unroll
+            for (int c0 = 0; c0 < HA; c0 += CH) {
+                uint32_t hi[CH], lo[CH];
+#pragma unroll
+                for (int i = 0; i < CH; ++i) {
+                    const uint64_t x = mul_f32x2(v[c0 + i], sA2);
+                    const float2 xf = u64_as_f2(x);
+                    const __half2 h2 = __floats2half2_rn(xf.x, xf.y);
+                    const uint64_t r = sub_f32x2(x, f2_as_u64(__half22float2(h2)));
+                    const float2 rf = u64_as_f2(r);
+                    const __half2 l2 = __floats2half2_rn(rf.x, rf.y);
+                    hi[i] = *reinterpret_cast<const uint32_t *>(&h2);
+                    lo[i] = *reinterpret_cast<const uint32_t *>(&l2);
+                }
+                if constexpr (CH == 16) {
+                    tmem_st16(chi + c0, hi);
+                    tmem_st16(clo + c0, lo);
+                } else {
+                    tmem_st8(chi + c0, hi);
+                    tmem_st8(clo + c0, lo);
+                }
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(afull(a, h));
+        }
+    } else {
+        // epilogue: warp q reads TMEM lanes 32q.. = gather sets n
+        const int n = warp * 32 + lane;
+        const uint64_t soff8 = (uint64_t)P.h.setoff[n] * 8;
+        const uint32_t lane_addr = (uint32_t)(warp * 32) << 16;
+        const float2 sf = pow2_factors(-(max(-126, min(127, P.h.ea)) + P.h.ue));
+        const uint64_t f1 = f2_as_u64(make_float2(sf.x, sf.x)), f2 = f2_as_u64(make_float2(sf.y, sf.y));
+        uint32_t it = 0;
+        for (uint64_t t = blockIdx.x; t < ntiles; t += G, ++it) {
+            const int d = it & 1;
+            mbar_wait(tfull(d), (it >> 1) & 1);
+            tc_fence_after();
+            char *pb = reinterpret_cast<char *>(psi + tile_base<NPOS>(t, P.h)) + soff8;
+            const uint32_t Dt = tmem + 2 * KD + d * N + lane_addr;
+#pragma unroll 2
+            for (int ch = 0; ch < N / 32; ++ch) {
+                uint32_t v[32];
+                tmem_ld32(Dt + 32 * ch, v);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (ch == N / 32 - 1) {
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(tempty(d));   // accumulator drained
+                }
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const uint64_t x = (uint64_t)v[2 * i] | ((uint64_t)v[2 * i + 1] << 32);
+                    *reinterpret_cast<float2 *>(pb + P.off8[16 * ch + i]) = u64_as_f2(mul_f32x2(mul_f32x2(x, f1), f2));
+                }
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == MMA_WARP) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TMEM_COLS));
+    }
+}
+
 
 // ------------------------------------------------------------------ mode L
 // Orientation for gathers whose targets include the lowest physical bits
@@ -906,6 +1205,54 @@ void tc_prepare(const ApplyDesc &d, const double *Ucanon, std::vector<char> &pay
     std::sort(all, all + na);
     for (int i = 0; i < na; ++i) P.pos[i] = all[i];
     P.ntiles = 1ull << (d.n_local - K - tc::SETBITS);
+    // bulk-copy producer (apply_tcb) when the highest target is at bit >= 7
+    // (the K-half bit must lie above the 1 KB blocks of bits 0..6)
+    static const char *bulk = getenv("HQ_TC_BULK");   // "0" keeps the cp.async kernel (experiments)
+    static const char *nsenv = getenv("HQ_TC_NSLOT");  // ring depth override (experiments)
+    if (d.p[K - 1] >= 7 && !(bulk && bulk[0] == '0')) {
+        std::vector<char> pb(sizeof(tc::ParamsB) + 1, 0);
+        tc::ParamsB &B = *reinterpret_cast<tc::ParamsB *>(pb.data());
+        B.h = P;
+        for (int c = 0; c < D; ++c) B.off8[c] = P.off[c] * 8;
+        auto tpos = [&](int phys) { return (int)(std::find(all, all + na, phys) - all); };
+        const int hp = tpos(d.p[K - 1]);
+        auto slot_of = [&](uint64_t ti) { return (ti & ((1ull << hp) - 1)) | ((ti >> (hp + 1)) << hp); };
+        for (int n = 0; n < tc::M; ++n) {
+            uint64_t ti = 0;
+            for (int i = 0; i < tc::SETBITS; ++i)
+                if ((n >> i) & 1) ti |= 1ull << tpos(setbits[i]);
+            B.nidx[n] = (uint16_t)slot_of(ti);
+        }
+        for (int c = 0; c < D / 2; ++c) {
+            uint64_t ti = 0;
+            for (int i = 0; i < K - 1; ++i)
+                if ((c >> i) & 1) ti |= 1ull << tpos(d.p[i]);
+            B.cidx8[c] = (uint32_t)slot_of(ti) * 8;
+        }
+        for (int h = 0; h < 2; ++h)
+            for (int j = 0; j < D / 2; ++j) {
+                const uint64_t x = (uint64_t)j << 7;
+                const uint64_t ti = (x & ((1ull << hp) - 1)) | ((uint64_t)h << hp) | ((x >> hp) << (hp + 1));
+                uint64_t o = 0;
+                for (int i = 0; i < na; ++i)
+                    if ((ti >> i) & 1) o |= 1ull << all[i];
+                B.boff[h][j] = o;
+            }
+        // ring depth and producer warps; HQ_TC_NSLOT="<ns><np>" overrides (experiments)
+        // measured on the 34q bench circuit in the sustained (power-capped)
+        // regime (tools/pass_times.py): (4, 2) beats (4, 1) and (8, *) and
+        // the cp.async kernel (3.91 s vs 4.28 s and 4.08 s); in 32q bursts
+        // (4, 1) is ahead for K = 6 (bench_sweep.py, profiles/r01/SUMMARY.md)
+        int ns = 4, np = 2;
+        if (nsenv && nsenv[0] >= '2' && nsenv[0] <= '8') {
+            ns = nsenv[0] - '0';
+            np = nsenv[1] == '2' ? 2 : (nsenv[1] == '4' ? 4 : 1);
+        }
+        B.ns = ns;
+        B.np = np;
+        pb.back() = 'B';
+        params.swap(pb);
+    }
 }
 
 template <int K>
@@ -924,6 +1271,42 @@ static int tc_launch_k(void *psi, const tc::Params &P, const void *dev_payload, 
     tc::apply_tc<K><<<(unsigned)grid, tc::H_THREADS, C::SMEM, st>>>(
         reinterpret_cast<float2 *>(psi), P, reinterpret_cast<const __half *>(dev_payload));
     return (int)cudaGetLastError();
+}
+
+template <int K, int NS, int NP>
+static int tc_launch_b(void *psi, const tc::ParamsB &P, const void *dev_payload, cudaStream_t st) {
+    using C = tc::CfgB<K, NS>;
+    static bool attr_done = false;
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(tc::apply_tcb<K, NS, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        if (e != cudaSuccess) return (int)e;
+        attr_done = true;
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint64_t grid = P.h.ntiles < (uint64_t)sms ? P.h.ntiles : (uint64_t)sms;
+    tc::apply_tcb<K, NS, NP><<<(unsigned)grid, tc::bk_threads(NP), C::SMEM, st>>>(
+        reinterpret_cast<float2 *>(psi), P, reinterpret_cast<const __half *>(dev_payload));
+    return (int)cudaGetLastError();
+}
+
+// ring depth NS and producer warps NP: (NS, NP) from the host's choice
+template <int K>
+static int tc_launch_bk(void *psi, const tc::ParamsB &P, const void *dev_payload, cudaStream_t st) {
+    const int v = P.ns * 10 + P.np;
+    if constexpr (K == 6) {
+        if (v == 21) return tc_launch_b<6, 2, 1>(psi, P, dev_payload, st);
+        if (v == 42) return tc_launch_b<6, 4, 2>(psi, P, dev_payload, st);
+        if (v == 44) return tc_launch_b<6, 4, 4>(psi, P, dev_payload, st);
+        return tc_launch_b<6, 4, 1>(psi, P, dev_payload, st);
+    } else {
+        if (v == 41) return tc_launch_b<K, 4, 1>(psi, P, dev_payload, st);
+        if (v == 42) return tc_launch_b<K, 4, 2>(psi, P, dev_payload, st);
+        if (v == 61) return tc_launch_b<K, 6, 1>(psi, P, dev_payload, st);
+        if (v == 82) return tc_launch_b<K, 8, 2>(psi, P, dev_payload, st);
+        return tc_launch_b<K, 8, 1>(psi, P, dev_payload, st);
+    }
 }
 
 static int tc_launch_l(void *psi, const tc::ParamsL &P, const void *dev_payload, cudaStream_t st) {
@@ -945,7 +1328,7 @@ static int tc_launch_l(void *psi, const tc::ParamsL &P, const void *dev_payload,
 // Mode H scales the state into the FP16 range by 2^ea with max |psi| * 2^ea
 // <= 2^14, from the runtime's rigorous bound on max |amplitude|.
 void tc_set_amp_bound(std::vector<char> &params, double bound) {
-    if (params.empty() || params.back() != 'H') return;
+    if (params.empty() || (params.back() != 'H' && params.back() != 'B')) return;
     tc::Params &P = *reinterpret_cast<tc::Params *>(params.data());
     int ex = 0;
     if (bound > 0 && std::isfinite(bound)) std::frexp(bound, &ex);   // bound < 2^ex
@@ -959,6 +1342,11 @@ int tc_launch(void *psi, const void *params, size_t params_size, const void *dev
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const char tag = reinterpret_cast<const char *>(params)[params_size - 1];
     if (tag == 'L') return tc_launch_l(psi, *reinterpret_cast<const tc::ParamsL *>(params), dev_payload, st);
+    if (tag == 'B') {
+        const tc::ParamsB &B = *reinterpret_cast<const tc::ParamsB *>(params);
+        if (B.h.k == 4) return tc_launch_bk<4>(psi, B, dev_payload, st);
+        return B.h.k == 5 ? tc_launch_bk<5>(psi, B, dev_payload, st) : tc_launch_bk<6>(psi, B, dev_payload, st);
+    }
     const tc::Params &P = *reinterpret_cast<const tc::Params *>(params);
     if (P.k == 4) return tc_launch_k<4>(psi, P, dev_payload, st);
     return P.k == 5 ? tc_launch_k<5>(psi, P, dev_payload, st) : tc_launch_k<6>(psi, P, dev_payload, st);
