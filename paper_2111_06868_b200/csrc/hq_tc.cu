@@ -538,6 +538,8 @@ template <int K, int NS, int NP>
 __global__ void __launch_bounds__(bk_threads(NP), 1)
 apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
           const __half *__restrict__ Breal /* [2][N][KD]: hi then lo, row n = output real */) {
+    // even NS only: odd rings (a slot shared by both K-halves) failed with a
+    // launch error at n >= 32 in the ring experiments; not pursued
     static_assert(NS % 2 == 0, "slot parity = K-half needs an even ring");
     using C = CfgB<K, NS>;
     constexpr int KD = C::KD, N = C::N, HA = C::HA, NSLOT = C::NSLOT;
@@ -592,8 +594,8 @@ apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
     const uint64_t G = gridDim.x;
 
     if (warp >= BK_PROD) {
-        // NP = 1: one warp fills slots in order.  NP >= 2: producer warp p
-        // fills K-half h = p % 2 (slot parity = h, NS even), blocks
+        // NP = 1: one warp fills slots in sidx order.  NP >= 2: producer warp
+        // p fills the K-half h = p % 2 slots (sidx = 2 * it + h), blocks
         // [sub * NB, (sub + 1) * NB) of each slot, sub = p / 2; the sub = 0
         // warp posts the byte count (a copy may complete before it: the
         // mbarrier's tx-count may go transiently negative, and the phase

@@ -20,7 +20,7 @@ python bench.py --steps 2 --warmup 1 --no-cpu-baseline --e2e-steps 1 > $OUT/plai
 echo "launches rc=$?" >> $OUT/ncu_launches.log
 # full capture of the tensor-core and SIMT kernels at 32q (same kernels as the bench)
 python prof_one.py --n 32 --k 6 --placement b:8-9-10-20-21-22 --reps 2 > $OUT/p_tc.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k 'regex:apply_tc(<|$)' -s 1 -c 1 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:apply_tcb -s 1 -c 1 \
     -o $OUT/prof_tc6 python prof_one.py --n 32 --k 6 --placement b:8-9-10-20-21-22 --reps 2 > $OUT/ncu_tc.log 2>&1
 echo "ncu tc rc=$?" >> $OUT/ncu_tc.log
 python prof_one.py --n 32 --k 6 --placement b:0-1-2-3-4-5 --reps 2 > $OUT/p_tcl.log 2>&1 && \
