@@ -202,6 +202,33 @@ hq_status hq_probabilities(hq_state *s, const int32_t *qubits, int nq, double *p
  * and renormalise.  *outcome_out = x (qubits[0] = MSB). */
 hq_status hq_measure(hq_state *s, const int32_t *qubits, int nq, double u, uint64_t *outcome_out);
 
+/* ------------------------------------------------------------------ trajectories
+ * Noise by pure-state sampling of the Kraus operators (PAPER P:1032-1041
+ * "pure state sampling of the Kraus operators"; SURVEY row
+ * f3).  Each shot owns a state; batches of shots shard across GPUs with no
+ * data-path collective (paper_2111_06868_b200/trajectories.py). */
+
+/* Reduced density matrix of qubits[0..k) (1 <= k <= 3):
+ * rho[a][b] = sum_r psi[a, r] conj(psi[b, r]), a, b in [0, 2^k) with
+ * qubits[0] the MSB (C1), r over the other qubits; trace = ||psi||^2.
+ * rho_out: 2*4^k doubles (interleaved complex, row-major), FP64 accumulation
+ * over all ranks (one read pass).  If a target is a global qubit the library
+ * first remaps as hq_apply_matrix would (the layout changes, the state does
+ * not).  Errors: HQ_ERR_ARG, HQ_ERR_K, HQ_ERR_QUBIT, HQ_ERR_DUP_QUBIT.
+ * Synchronises. */
+hq_status hq_reduced_dm(hq_state *s, const int32_t *qubits, int k, double *rho_out);
+
+/* One trajectory step of the Kraus channel {K_i} (i < nkraus) on qubits[0..k)
+ * (1 <= k <= 3), K[i] = 2*4^k doubles as U in hq_apply_matrix:
+ * p_i = ||K_i psi||^2 = Tr(K_i rho_T K_i^dagger) (rho_T from hq_reduced_dm),
+ * i = the first index with u * sum(p) < p_0 + ... + p_i (u in [0, 1) is the
+ * caller's uniform random number), then psi <- K_i psi / sqrt(p_i) (one apply
+ * pass).  *chosen_out = i; probs_out (nkraus doubles, may be NULL) = p.
+ * Errors: HQ_ERR_RANGE if every p_i < 1e-14 (ZeroNormBranch; state
+ * unchanged), else as hq_reduced_dm.  Synchronises. */
+hq_status hq_kraus_sample(hq_state *s, const double *const *K, int nkraus, const int32_t *qubits, int k,
+                          double u, int *chosen_out, double *probs_out);
+
 /* ------------------------------------------------------------------ density matrices
  * Density-matrix evolution by doubling (PAPER P:286-289 MatrixSuperGate "using
  * a matrix-vector multiplication", "a super circuit [becomes] a

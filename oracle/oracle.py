@@ -35,6 +35,10 @@ Contents, each following the passage cited:
   ``dm_vec`` -- the row-major vectorisation vec(rho)[i 2^N + j] = rho[i][j]
   that the doubling reading (row f2) applies gates to.
 
+* ``reduced_dm`` / ``kraus_sample_step`` -- the partial trace written out as
+  M M^H of the reshaped state, and one trajectory step by explicit branches
+  (row f3).
+
 Parity pins for every function live in ``tests/test_oracle_pins.py``.
 """
 import ctypes
@@ -290,3 +294,45 @@ def dm_apply_kraus(rho, K, qubits):
 def dm_vec(rho):
     """vec(rho)[i 2^N + j] = rho[i][j] (logical qubits 0..N-1 = rows)."""
     return np.ascontiguousarray(rho, dtype=np.complex128).reshape(-1)
+
+
+# ---------------------------------------------------------------- f3: trajectories
+
+def reduced_dm(psi, qubits):
+    """rho_T[a][b] = sum_r psi[a, r] conj(psi[b, r]) -- the partial trace of
+    |psi><psi| over every qubit not in ``qubits`` (a, b read qubits[0] as the
+    MSB, reading C1): psi reshaped to (2,)*n, target axes moved to the front
+    in ``qubits`` order, flattened to a 2^k x 2^(n-k) matrix M, rho = M M^H."""
+    n = _nqubits(psi)
+    k = len(qubits)
+    t = np.asarray(psi, dtype=np.complex128).reshape((2,) * n)
+    t = np.moveaxis(t, list(qubits), list(range(k)))
+    M = t.reshape(2 ** k, -1)
+    return M @ M.conj().T
+
+
+def kraus_sample_step(psi, K, qubits, u):
+    """One trajectory step ("pure state sampling of the
+    Kraus operators"): every branch K_i psi by the plain
+    apply, p_i = ||K_i psi||^2, i = the first index with
+    u * sum(p) < p_0 + ... + p_i (and p_i > 0), psi <- K_i psi / sqrt(p_i).
+    Returns (new psi, i, p)."""
+    branches = []
+    for Ki in K:
+        b = np.array(psi, dtype=np.complex128, copy=True)
+        apply_gate(b, Ki, list(qubits))
+        branches.append(b)
+    p = np.array([float(np.vdot(b, b).real) for b in branches])
+    if not np.any(p >= 1e-14):
+        raise OracleError("ZeroNormBranch")
+    target = u * p.sum()
+    cum = 0.0
+    i = len(p) - 1
+    for j, pj in enumerate(p):
+        cum += pj
+        if target < cum and pj > 0:
+            i = j
+            break
+    while i > 0 and p[i] == 0:
+        i -= 1
+    return branches[i] / np.sqrt(p[i]), i, p

@@ -125,5 +125,16 @@ struct DmParams {
 };
 int launch_dm_trace(int dtype, const void *psi, int N, int n_local, int rank, const DmParams &P,
                     double2 *dev_part, int max_blocks, void *stream, int *nblocks_out);
+// Reduced density matrix of k <= 3 local targets (row-major upper triangle,
+// entry e of (a, b >= a) in row order; a's MSB = qubits[0]).
+struct RdmParams {
+    uint64_t off[8];         // amplitude offset of target pattern a
+    int pos[3];              // ascending physical bits of the targets
+    int k;
+};
+constexpr int RDM_MAX_BLOCKS = 148 * 4;
+constexpr int RDM_MAX_ENTRIES = 2 * 36;  // doubles per block partial (k = 3)
+int launch_reduced_dm(int dtype, const void *psi, uint64_t n_amps, const RdmParams &P, double *dev_part,
+                      void *stream, int *nblocks_out);
 
 }  // namespace hq

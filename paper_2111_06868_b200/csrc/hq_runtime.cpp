@@ -82,6 +82,8 @@ struct Shard {
     ncclComm_t comm = nullptr;
     double *d_part = nullptr;     // norm partials
     double *h_part = nullptr;     // pinned
+    double *d_red = nullptr;      // reduced-density-matrix partials (lazy)
+    double *h_red = nullptr;      // pinned
     Arena arena;
 };
 
@@ -205,6 +207,8 @@ static void shard_free(Shard &s) {
     if (s.own_buf && s.buf) cudaFree(s.buf);
     if (s.d_part) cudaFree(s.d_part);
     if (s.h_part) cudaFreeHost(s.h_part);
+    if (s.d_red) cudaFree(s.d_red);
+    if (s.h_red) cudaFreeHost(s.h_red);
     if (s.arena.dev) cudaFree(s.arena.dev);
     if (s.arena.host) cudaFreeHost(s.arena.host);
     if (s.comm) ncclCommDestroy(s.comm);
@@ -1301,6 +1305,135 @@ extern "C" hq_status hq_measure(hq_state *st, const int32_t *qubits, int nq, dou
     double nrm = 0.0;
     if ((rc = hq_project(st, qubits, bits.data(), nq, 1, &nrm))) return rc;
     *outcome_out = (uint64_t)x;
+    return HQ_OK;
+}
+
+// ------------------------------------------------------------------ f3: reduced density matrices, trajectories
+
+// Bring every qubit of `qubits` to a local physical bit with the scheduler's
+// remaps (as a gate on them would), without applying anything.
+static hq_status ensure_local(hq_state *st, const int32_t *qubits, int k) {
+    bool local = true;
+    for (int j = 0; j < k; ++j) local &= st->pi[qubits[j]] < st->nl;
+    if (local) return HQ_OK;
+    std::vector<GateRef> refs(1);
+    refs[0].k = k;
+    refs[0].U = nullptr;
+    for (int j = 0; j < k; ++j) refs[0].q[j] = qubits[j];
+    std::vector<Op> ops;
+    std::vector<int> pi = st->pi;
+    schedule(st->n, st->m, refs, pi, ops);
+    for (const Op &op : ops) {
+        hq_status rc = HQ_OK;
+        if (op.kind == OP_REMAP) rc = exec_remap(st, op);
+        else if (op.kind == OP_PERMUTE) rc = exec_permute(st, op);
+        if (rc) return rc;
+    }
+    st->pi = pi;
+    return HQ_OK;
+}
+
+extern "C" hq_status hq_reduced_dm(hq_state *st, const int32_t *qubits, int k, double *rho_out) {
+    clear_error();
+    if (!st || !rho_out) return set_error(HQ_ERR_ARG, "NULL argument");
+    if (k < 1 || k > 3) return set_error(HQ_ERR_K, "k=%d not in [1,3]", k);
+    hq_status rc = validate_targets(st, qubits, k, 3);
+    if (rc) return rc;
+    if (k > st->nl) return set_error(HQ_ERR_K, "k=%d > %d local qubits", k, st->nl);
+    if ((rc = ensure_local(st, qubits, k))) return rc;
+    const int D = 1 << k, E = D * (D + 1) / 2;
+    RdmParams P;
+    P.k = k;
+    int pos[3];
+    for (int j = 0; j < k; ++j) pos[j] = st->pi[qubits[j]];
+    for (int a = 0; a < D; ++a) {
+        uint64_t o = 0;
+        for (int j = 0; j < k; ++j)
+            if ((a >> (k - 1 - j)) & 1) o |= 1ull << pos[j];
+        P.off[a] = o;
+    }
+    std::sort(pos, pos + k);
+    for (int j = 0; j < 3; ++j) P.pos[j] = j < k ? pos[j] : 0;
+    std::vector<double> acc(2 * E, 0.0);
+    for (auto &s : st->sh) {
+        CUDA_TRY(cudaSetDevice(s.device));
+        if (!s.d_red) {
+            CUDA_TRY(cudaMalloc((void **)&s.d_red, sizeof(double) * RDM_MAX_BLOCKS * RDM_MAX_ENTRIES));
+            CUDA_TRY(cudaMallocHost((void **)&s.h_red, sizeof(double) * RDM_MAX_BLOCKS * RDM_MAX_ENTRIES));
+        }
+        int nb = 0;
+        int e = launch_reduced_dm((int)st->dtype, s.psi, 1ull << st->nl, P, s.d_red, s.stream, &nb);
+        if (e) return set_error(HQ_ERR_CUDA, "reduced_dm launch: %s", cudaGetErrorString((cudaError_t)e));
+        st->stats.kernel_launches++;
+        st->stats.hbm_bytes += st->es << st->nl;
+        CUDA_TRY(cudaMemcpyAsync(s.h_red, s.d_red, sizeof(double) * 2 * E * nb, cudaMemcpyDeviceToHost, s.stream));
+        CUDA_TRY(cudaStreamSynchronize(s.stream));
+        for (int b = 0; b < nb; ++b)
+            for (int x = 0; x < 2 * E; ++x) acc[x] += s.h_red[(size_t)b * 2 * E + x];
+    }
+    if ((rc = allreduce_host(st, acc.data(), 2 * E))) return rc;
+    for (int a = 0, e = 0; a < D; ++a)
+        for (int b = a; b < D; ++b, ++e) {
+            rho_out[2 * (a * D + b)] = acc[2 * e];
+            rho_out[2 * (a * D + b) + 1] = acc[2 * e + 1];
+            rho_out[2 * (b * D + a)] = acc[2 * e];
+            rho_out[2 * (b * D + a) + 1] = -acc[2 * e + 1];
+        }
+    return HQ_OK;
+}
+
+extern "C" hq_status hq_kraus_sample(hq_state *st, const double *const *K, int nkraus, const int32_t *qubits,
+                                     int k, double u, int *chosen_out, double *probs_out) {
+    clear_error();
+    if (!st || !K || !chosen_out || nkraus < 1) return set_error(HQ_ERR_ARG, "NULL argument or no Kraus operators");
+    if (!(u >= 0.0 && u < 1.0)) return set_error(HQ_ERR_ARG, "u=%g not in [0,1)", u);
+    if (k < 1 || k > 3) return set_error(HQ_ERR_K, "k=%d not in [1,3]", k);
+    for (int i = 0; i < nkraus; ++i)
+        if (!K[i]) return set_error(HQ_ERR_ARG, "K[%d] is NULL", i);
+    const int D = 1 << k;
+    std::vector<double> rho((size_t)2 * D * D);
+    hq_status rc = hq_reduced_dm(st, qubits, k, rho.data());
+    if (rc) return rc;
+    // p_i = ||K_i psi||^2 = Tr(K_i rho K_i^H) = sum_{a,b,c} K[a][b] rho[b][c] conj(K[a][c])
+    std::vector<double> p(nkraus, 0.0);
+    double total = 0.0;
+    for (int i = 0; i < nkraus; ++i) {
+        const double *A = K[i];
+        double acc = 0.0;
+        for (int a = 0; a < D; ++a)
+            for (int b = 0; b < D; ++b) {
+                const double kr = A[2 * (a * D + b)], ki = A[2 * (a * D + b) + 1];
+                if (kr == 0.0 && ki == 0.0) continue;
+                for (int c = 0; c < D; ++c) {
+                    const double rr = rho[2 * (b * D + c)], ri = rho[2 * (b * D + c) + 1];
+                    const double cr = A[2 * (a * D + c)], ci = -A[2 * (a * D + c) + 1];
+                    // real part of K[a][b] * rho[b][c] * conj(K[a][c])
+                    const double tr = kr * rr - ki * ri, ti = kr * ri + ki * rr;
+                    acc += tr * cr - ti * ci;
+                }
+            }
+        p[i] = std::max(acc, 0.0);
+        total += p[i];
+    }
+    if (probs_out)
+        for (int i = 0; i < nkraus; ++i) probs_out[i] = p[i];
+    double pmax = 0.0;
+    for (double v : p) pmax = std::max(pmax, v);
+    if (!(pmax >= 1e-14)) return set_error(HQ_ERR_RANGE, "all branch probabilities < 1e-14 (ZeroNormBranch)");
+    const double target = u * total;
+    double cum = 0.0;
+    int x = nkraus - 1;
+    for (int i = 0; i < nkraus; ++i) {
+        cum += p[i];
+        if (target < cum && p[i] > 0.0) { x = i; break; }
+    }
+    while (x > 0 && p[x] == 0.0) --x;
+    std::vector<double> Ks((size_t)2 * D * D);
+    const double sc = 1.0 / std::sqrt(p[x]);
+    for (int i = 0; i < 2 * D * D; ++i) Ks[i] = K[x][i] * sc;
+    if ((rc = hq_apply_matrix(st, Ks.data(), qubits, k))) return rc;
+    st->amp_bound = 1.0 + 1e-3;       // ||K_x psi|| / sqrt(p_x) = 1 up to the rounding of p_x
+    *chosen_out = x;
     return HQ_OK;
 }
 

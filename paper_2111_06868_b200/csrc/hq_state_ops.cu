@@ -134,7 +134,78 @@ __global__ void __launch_bounds__(256) dm_trace_kernel(const V *__restrict__ psi
     }
 }
 
+// rho[a][b] = sum over gather sets of psi_a conj(psi_b) (upper triangle,
+// fp64 accumulation); one gather set per thread per step, consecutive
+// threads on consecutive sets (coalesced unless bit 0 is a target).
+template <typename V, int K>
+__global__ void __launch_bounds__(256) reduced_dm_kernel(const V *__restrict__ psi, uint64_t nsets,
+                                                         const __grid_constant__ RdmParams P,
+                                                         double *__restrict__ part) {
+    constexpr int D = 1 << K, E = D * (D + 1) / 2;
+    double acc[2 * E];
+#pragma unroll
+    for (int e = 0; e < 2 * E; ++e) acc[e] = 0.0;
+    for (uint64_t o = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; o < nsets;
+         o += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t base = o;
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            const int s = P.pos[i];
+            base = ((base >> s) << (s + 1)) | (base & ((1ull << s) - 1));
+        }
+        double re[D], im[D];
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            const V v = psi[base + P.off[a]];
+            re[a] = (double)v.x;
+            im[a] = (double)v.y;
+        }
+        int e = 0;
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+#pragma unroll
+            for (int b = a; b < D; ++b, ++e) {
+                acc[2 * e] += re[a] * re[b] + im[a] * im[b];
+                acc[2 * e + 1] += im[a] * re[b] - re[a] * im[b];
+            }
+    }
+    __shared__ double red[8][2 * E];
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+#pragma unroll
+    for (int e = 0; e < 2 * E; ++e) {
+        double x = acc[e];
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if (l == 0) red[w][e] = x;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < 2 * E; e += blockDim.x) {
+        double t = 0.0;
+        for (int j = 0; j < (int)(blockDim.x >> 5); ++j) t += red[j][e];
+        part[(size_t)blockIdx.x * 2 * E + e] = t;
+    }
+}
+
+template <typename V>
+int reduced_dm_dispatch(const V *psi, uint64_t nsets, const RdmParams &P, double *part, unsigned g,
+                        cudaStream_t st) {
+    if (P.k == 1) reduced_dm_kernel<V, 1><<<g, 256, 0, st>>>(psi, nsets, P, part);
+    else if (P.k == 2) reduced_dm_kernel<V, 2><<<g, 256, 0, st>>>(psi, nsets, P, part);
+    else reduced_dm_kernel<V, 3><<<g, 256, 0, st>>>(psi, nsets, P, part);
+    return (int)cudaGetLastError();
+}
+
 }  // namespace
+
+int launch_reduced_dm(int dtype, const void *psi, uint64_t n_amps, const RdmParams &P, double *dev_part,
+                      void *stream, int *nblocks_out) {
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const uint64_t nsets = n_amps >> P.k;
+    unsigned g = grid_for(nsets);
+    if (g > (unsigned)RDM_MAX_BLOCKS) g = RDM_MAX_BLOCKS;
+    *nblocks_out = (int)g;
+    if (dtype == HQ_C64) return reduced_dm_dispatch((const float2 *)psi, nsets, P, dev_part, g, st);
+    return reduced_dm_dispatch((const double2 *)psi, nsets, P, dev_part, g, st);
+}
 
 int launch_dm_trace(int dtype, const void *psi, int N, int n_local, int rank, const DmParams &P,
                     double2 *dev_part, int max_blocks, void *stream, int *nblocks_out) {

@@ -96,6 +96,8 @@ def lib():
             "hq_project": [P, P, P, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double)],
             "hq_probabilities": [P, P, ctypes.c_int, P],
             "hq_measure": [P, P, ctypes.c_int, ctypes.c_double, ctypes.POINTER(ctypes.c_uint64)],
+            "hq_reduced_dm": [P, P, ctypes.c_int, P],
+            "hq_kraus_sample": [P, P, ctypes.c_int, P, ctypes.c_int, ctypes.c_double, ctypes.POINTER(ctypes.c_int), P],
             "hq_state_get_layout": [P, P],
             "hq_sync": [P],
             "hq_stats_get": [P, ctypes.POINTER(hq_stats)],
@@ -258,6 +260,27 @@ def _kraus_array(K):
     mats = [np.ascontiguousarray(k, dtype=np.complex128) for k in K]
     ptrs = (ctypes.c_void_p * len(mats))(*[m.ctypes.data for m in mats])
     return ptrs, mats
+
+
+def hq_reduced_dm(state, qubits):
+    """Reduced density matrix of k <= 3 qubits (complex128 2^k x 2^k;
+    qubits[0] = MSB of the row index)."""
+    q = np.ascontiguousarray(qubits, dtype=np.int32)
+    rho = np.zeros((2 ** q.size, 2 ** q.size), dtype=np.complex128)
+    _check(lib().hq_reduced_dm(state.ptr, q.ctypes.data, int(q.size), rho.ctypes.data))
+    return rho
+
+
+def hq_kraus_sample(state, K, qubits, u):
+    """One trajectory step of the Kraus channel K on qubits with uniform u in
+    [0, 1): returns (chosen index, branch probabilities p_i = ||K_i psi||^2)."""
+    ptrs, mats = _kraus_array(K)
+    q = np.ascontiguousarray(qubits, dtype=np.int32)
+    probs = np.zeros(len(mats), dtype=np.float64)
+    chosen = ctypes.c_int()
+    _check(lib().hq_kraus_sample(state.ptr, ptrs, len(mats), q.ctypes.data, int(q.size), float(u),
+                                 ctypes.byref(chosen), probs.ctypes.data))
+    return chosen.value, probs
 
 
 def hq_dm_superop(K):

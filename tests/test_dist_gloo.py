@@ -109,3 +109,58 @@ def test_schedule_over_gloo_world2(kind):
     status, nrem = q.get(timeout=5)
     assert status == "ok"
     assert nrem > 0
+
+
+def _traj_worker(rank, world, port, q):
+    """Row f3 host logic over gloo: shots shard round robin (shard_shots),
+    each with its private stream (shot_rng), per-rank sums added by the one
+    all-reduce (reduce_sum).  The per-shot numerics here are the oracle's
+    trajectory step (the GPU path does them with hq_kraus_sample)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import sys
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        import oracle as O
+        from paper_2111_06868_b200.trajectories import shard_shots, shot_rng, reduce_sum
+        n, shots, seed = 3, 37, 11
+        p = 0.2
+        K = [np.sqrt(1 - p) * np.eye(2), np.sqrt(p) * np.diag([1.0, -1.0])]
+        H = np.array([[1, 1], [1, -1]]) / np.sqrt(2)
+
+        def run(shot):
+            rng = shot_rng(seed, shot)
+            psi = O.init_tokens(n, "0")
+            for q_ in range(n):
+                O.apply_gate(psi, H, [q_])
+            for step in range(3):
+                psi, _, _ = O.kraus_sample_step(psi, K, [step % n], rng.random())
+            return O.reduced_dm(psi, [0, 2])
+
+        acc = np.zeros((4, 4), dtype=complex)
+        mine = shard_shots(shots, rank, world)
+        for s in mine:
+            acc += run(s)
+        tot = reduce_sum(np.concatenate([acc.real.ravel(), acc.imag.ravel(), [len(mine)]]), dist.group.WORLD)
+        if rank == 0:
+            ref = sum(run(s) for s in range(shots)) / shots
+            mean = (tot[:16] + 1j * tot[16:32]).reshape(4, 4) / tot[-1]
+            ok = tot[-1] == shots and np.max(np.abs(mean - ref)) < 1e-14
+            cover = sorted(shard_shots(shots, 0, world) + shard_shots(shots, 1, world)) == list(range(shots))
+            q.put("ok" if ok and cover else "mismatch")
+    finally:
+        dist.destroy_process_group()
+
+
+def test_trajectory_shots_over_gloo_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_traj_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=180)
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    assert q.get(timeout=5) == "ok"

@@ -411,3 +411,105 @@ def test_dm_pure_state_consistency_and_trace():
     v = O.dm_vec(rho)
     v2 = O.apply_gate(O.apply_gate(v.copy(), U, [1, 3]), U.conj(), [1 + N, 3 + N])
     assert np.max(np.abs(v2 - O.dm_vec(O.dm_apply_kraus(rho, [U], [1, 3])))) < 1e-14
+
+
+# ---------------------------------------------------------------- f3: reduced density matrix, trajectories
+
+def _rdm_brute(psi, qubits):
+    """rho[a][b] = sum over index pairs (i, j) that agree off the targets and
+    read a, b on them (qubits[0] = MSB) of psi_i conj(psi_j): explicit loops."""
+    n = int(np.log2(psi.size))
+    k = len(qubits)
+    rho = np.zeros((2 ** k, 2 ** k), dtype=complex)
+    tmask = sum(1 << (n - 1 - q) for q in qubits)
+    for i in range(2 ** n):
+        a = sum(((i >> (n - 1 - q)) & 1) << (k - 1 - j) for j, q in enumerate(qubits))
+        for j in range(2 ** n):
+            if (i & ~tmask) != (j & ~tmask):
+                continue
+            b = sum(((j >> (n - 1 - q)) & 1) << (k - 1 - t) for t, q in enumerate(qubits))
+            rho[a, b] += psi[i] * np.conj(psi[j])
+    return rho
+
+
+def test_reduced_dm_closed_forms():
+    """Product state: the reduced state of a qubit is its own |v><v| (in the
+    order asked for); GHZ: every 2-qubit marginal is diag(1/2, 0, 0, 1/2) and
+    every 1-qubit marginal I/2 (textbook partial traces)."""
+    psi = O.init_tokens(4, "0+1-")
+    plus = np.array([1, 1]) / np.sqrt(2)
+    minus = np.array([1, -1]) / np.sqrt(2)
+    assert np.max(np.abs(O.reduced_dm(psi, [1]) - np.outer(plus, plus))) < 1e-15
+    v = np.kron(minus, [1, 0])                      # qubits [3, 0]: qubit 3 is the MSB
+    assert np.max(np.abs(O.reduced_dm(psi, [3, 0]) - np.outer(v, v))) < 1e-15
+    ghz = np.zeros(8, dtype=complex)
+    ghz[0] = ghz[7] = 1 / np.sqrt(2)
+    for qs in ([0, 1], [2, 0], [1, 2]):
+        assert np.max(np.abs(O.reduced_dm(ghz, qs) - np.diag([0.5, 0, 0, 0.5]))) < 1e-15
+    assert np.max(np.abs(O.reduced_dm(ghz, [1]) - np.eye(2) / 2)) < 1e-15
+
+
+@pytest.mark.parametrize("qubits", [[2], [4, 1], [0, 3, 2]])
+def test_reduced_dm_brute_force_and_observables(qubits):
+    """Against the explicit double loop, and Tr(O rho_T) = <psi| O (x) I |psi>
+    with O embedded by embed_dense (an independent route, order-sensitive)."""
+    n = 5
+    psi = random_state(n, 31)
+    rho = O.reduced_dm(psi, qubits)
+    assert np.max(np.abs(rho - _rdm_brute(psi, qubits))) < 1e-14
+    rng = np.random.default_rng(9)
+    d = 2 ** len(qubits)
+    A = rng.standard_normal((d, d)) + 1j * rng.standard_normal((d, d))
+    Oh = A + A.conj().T
+    want = np.vdot(psi, O.embed_dense(n, Oh, qubits) @ psi)
+    assert abs(np.trace(Oh @ rho) - want) < 1e-12
+    assert abs(np.trace(rho) - 1) < 1e-14 and np.max(np.abs(rho - rho.conj().T)) < 1e-15
+    assert np.min(np.linalg.eigvalsh(rho)) > -1e-14
+
+
+def _dephasing(p):
+    return [np.sqrt(1 - p) * np.eye(2, dtype=complex), np.sqrt(p) * np.diag([1, -1]).astype(complex)]
+
+
+def test_kraus_step_closed_forms():
+    """Dephasing on |+>: p = (1 - p, p), branch 1 leaves |->; amplitude
+    damping on |1>: p = (1 - g, g), branch 1 decays to |0>; a one-element
+    channel {U} is the plain gate with p = (1,)."""
+    plus = O.init_tokens(1, "+")
+    out, i, p = O.kraus_sample_step(plus, _dephasing(0.3), [0], 0.2)
+    assert i == 0 and np.allclose(p, [0.7, 0.3], atol=1e-15) and np.allclose(out, plus, atol=1e-15)
+    out, i, p = O.kraus_sample_step(plus, _dephasing(0.3), [0], 0.8)
+    assert i == 1 and np.allclose(out, O.init_tokens(1, "-"), atol=1e-15)
+    one = O.init_tokens(1, "1")
+    out, i, p = O.kraus_sample_step(one, _amp_damping(0.25), [0], 0.9)
+    assert i == 1 and np.allclose(p, [0.75, 0.25], atol=1e-15) and np.allclose(out, [1, 0], atol=1e-15)
+    psi = random_state(3, 4)
+    U = haar_unitary(2, np.random.default_rng(3))
+    out, i, p = O.kraus_sample_step(psi, [U], [2, 0], 0.5)
+    assert i == 0 and abs(p[0] - 1) < 1e-14
+    assert np.max(np.abs(out - O.simulate(3, [Gate("U", (2, 0), U)], psi))) < 1e-14
+    with pytest.raises(O.OracleError):
+        O.kraus_sample_step(O.init_tokens(1, "0"), [np.diag([0, 1]).astype(complex)], [0], 0.5)
+
+
+def test_kraus_step_unravels_the_channel():
+    """Averaging the post-step pure states over u (exactly: each branch with
+    weight p_i / sum p) gives sum_i K_i rho K_i^dagger / sum p -- the
+    trajectory unraveling of the density-matrix map."""
+    n = 3
+    psi = random_state(n, 8)
+    rng = np.random.default_rng(4)
+    Z = rng.standard_normal((12, 4)) + 1j * rng.standard_normal((12, 4))
+    V, _ = np.linalg.qr(Z)
+    K = [V[4 * i:4 * (i + 1)] for i in range(3)]            # CPTP 2-qubit channel
+    _, _, p = O.kraus_sample_step(psi, K, [2, 0], 0.0)
+    mean = np.zeros((2 ** n, 2 ** n), dtype=complex)
+    cum = np.concatenate([[0], np.cumsum(p)])
+    for i in range(3):
+        u = (cum[i] + p[i] / 2) / p.sum()
+        out, j, _ = O.kraus_sample_step(psi, K, [2, 0], u)
+        assert j == i
+        mean += p[i] / p.sum() * np.outer(out, out.conj())
+    want = O.dm_apply_kraus(np.outer(psi, psi.conj()), K, [2, 0])
+    assert abs(p.sum() - 1) < 1e-14
+    assert np.max(np.abs(mean - want)) < 1e-14
