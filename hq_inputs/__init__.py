@@ -11,7 +11,7 @@ from .gates import (SQRT_X, SQRT_Y, SQRT_W, H, X, Y, Z, CX, CZ, SWAP, CCX,
 from .circuits import (Gate, sycamore_circuit, haar_unitary, haar_sweep_gate,
                        random_circuit, grid_shape, circuit_bytes, circuit_sha256,
                        circuit_to_json, circuit_from_json, reversible_circuit,
-                       CONFIG_SEEDS)
+                       qft_circuit, qaoa_circuit, CONFIG_SEEDS)
 from .states import random_state, integer_state, basis_index
 
 __all__ = [
@@ -19,6 +19,7 @@ __all__ = [
     "fsim", "cphase", "cr_m", "rz", "permutation_matrix",
     "Gate", "sycamore_circuit", "haar_unitary", "haar_sweep_gate",
     "random_circuit", "grid_shape", "circuit_bytes", "circuit_sha256",
-    "circuit_to_json", "circuit_from_json", "reversible_circuit", "CONFIG_SEEDS",
+    "circuit_to_json", "circuit_from_json", "reversible_circuit", "qft_circuit",
+    "qaoa_circuit", "CONFIG_SEEDS",
     "random_state", "integer_state", "basis_index",
 ]

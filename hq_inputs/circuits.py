@@ -165,6 +165,41 @@ def reversible_circuit(n, n_gates, seed, kmax=3):
     return out
 
 
+def qft_circuit(n, with_swaps=False):
+    """Quantum Fourier transform: for q = 0..n-1, H on q then controlled-R_m
+    (m = 2, 3, ...) from each later qubit (textbook; pin P5's gates).  Most of
+    its gates are diagonal controlled phases (row f1 workload)."""
+    out = []
+    for q in range(n):
+        out.append(Gate("H", (q,), G.H))
+        for j in range(q + 1, n):
+            out.append(Gate("CR%d" % (j - q + 1), (j, q), G.cr_m(j - q + 1)))
+    if with_swaps:
+        for q in range(n // 2):
+            out.append(Gate("SWAP", (q, n - 1 - q), G.SWAP))
+    return out
+
+
+def qaoa_circuit(n, layers, seed):
+    """QAOA-style circuit on a ring plus random chords: per layer ZZ(gamma)
+    phases (diagonal) on every edge, then RX(beta) on every qubit; starts
+    from H on every qubit.  Diagonal-heavy (row f1 workload)."""
+    rng = np.random.default_rng(seed)
+    edges = [(q, (q + 1) % n) for q in range(n)]
+    edges += [tuple(int(x) for x in rng.choice(n, size=2, replace=False)) for _ in range(n // 2)]
+    out = [Gate("H", (q,), G.H) for q in range(n)]
+    for _ in range(layers):
+        gamma, beta = rng.uniform(0, np.pi, size=2)
+        zz = np.diag(np.exp(-0.5j * gamma * np.array([1, -1, -1, 1]))).astype(np.complex128)
+        for a, b in edges:
+            out.append(Gate("ZZ", (a, b), zz))
+        c, s = np.cos(beta / 2), np.sin(beta / 2)
+        rx = np.array([[c, -1j * s], [-1j * s, c]], dtype=np.complex128)
+        for q in range(n):
+            out.append(Gate("RX", (q,), rx))
+    return out
+
+
 def circuit_to_json(n, gates, meta=None):
     return json.dumps({
         "n": n, "meta": meta or {},

@@ -64,7 +64,7 @@ typedef enum hq_status {
 } hq_status;
 
 typedef enum hq_dtype {
-    HQ_C64 = 0,   /* complex64: FP32 storage; FP32 FMA (k<=4), 3xTF32 tcgen05 (k=5,6) */
+    HQ_C64 = 0,   /* complex64: FP32 storage; FP32 FMA (k<=4), 3-term FP16/TF32 tcgen05 (k=5,6) */
     HQ_C128 = 1   /* complex128: FP64 storage and FP64 FMA                            */
 } hq_dtype;
 
@@ -263,7 +263,11 @@ hq_status hq_dm_trace(hq_state *s, double *re, double *im);
  * U: 2*4^k doubles (interleaved, row-major, qubits[0] = MSB of U's index).
  * Errors (state unchanged): HQ_ERR_ARG (NULL), HQ_ERR_K (k<1, k>6, k > n - m),
  * HQ_ERR_QUBIT, HQ_ERR_DUP_QUBIT.  If a target is a global (rank) qubit the
- * library first remaps (all-to-all) so that every target is local. */
+ * library first remaps (all-to-all) so that every target is local -- unless
+ * U is block-diagonal in its global targets (exact zeros off the blocks:
+ * controlled phases, CZ, ZZ, RZ and their products): then
+ * every rank applies, with no communication, the block its rank bits select
+ * to the local targets (a complex phase when every target is global). */
 hq_status hq_apply_matrix(hq_state *s, const double *U, const int32_t *qubits, int k);
 
 /* Apply an (already fused) gate list in order, leftmost first.
@@ -304,7 +308,9 @@ hq_status hq_fuse_plan(const hq_gate *in, size_t ngates, int kmax, int32_t *grou
  * state on G = 2^m ranks, the op stream hq_apply_circuit would execute.
  * ops[i] = {kind, gate, nbits, bits[12]}:
  *   kind 0 APPLY  : gate index `gate`, bits[0..k-1] = physical target bits of
- *                   qubits[0..k-1];
+ *                   qubits[0..k-1]; a bit >= n - m is a global target of a
+ *                   gate block-diagonal in its global targets (row f1): rank
+ *                   r applies the block its rank bits select;
  *   kind 1 REMAP  : swap global bit bits[2i] with local bit bits[2i+1],
  *                   i < nbits (all-to-all among 2^nbits ranks);
  *   kind 2 PERMUTE: local bit swap bits[2i] <-> bits[2i+1], i < nbits.

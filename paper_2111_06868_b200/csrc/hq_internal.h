@@ -44,8 +44,12 @@ struct Op {
     int nbits;
     int bits[12];
 };
+// APPLY ops may carry global target bits (>= n - m): the scheduler emits them
+// only for gates block-diagonal in those targets (block_diag_in), and rank r
+// applies the block selected by its rank bits to the local targets (row f1).
 void schedule(int n, int m, const std::vector<GateRef> &g, std::vector<int> &pi,
               std::vector<Op> &ops);
+bool block_diag_in(const double *U, int k, int umask);
 
 // Layout planner: logical->physical map of the local qubits minimising the
 // estimated pass cost of `g` (hq_plan_layout).
@@ -118,6 +122,7 @@ int launch_init_tokens(int dtype, void *psi, uint64_t n_amps, uint64_t fix_mask,
 int launch_project(int dtype, void *psi, uint64_t n_amps, uint64_t mask, uint64_t val, int keep_all,
                    double *dev_partial, int max_blocks, void *stream, int *nblocks_out);
 int launch_scale(int dtype, void *psi, uint64_t n_amps, double s, void *stream);
+int launch_scale_complex(int dtype, void *psi, uint64_t n_amps, double re, double im, void *stream);
 int launch_probabilities(int dtype, const void *psi, uint64_t n_amps, const ProbParams &P,
                          double *dev_hist, int max_blocks, void *stream, int *nblocks_out);
 struct DmParams {

@@ -133,6 +133,19 @@ void fuse_build(const std::vector<GateRef> &g, int kmax, std::vector<FusedGate> 
 
 // ------------------------------------------------------------------ schedule
 
+// True when U (2^k x 2^k, interleaved complex, qubits[0] = MSB of the index)
+// is block-diagonal in the U-index bits of `umask`: U[r][c] == 0 whenever r
+// and c differ in one of those bits.  Exact zeros only: products of
+// structurally block-diagonal gates (diagonal, controlled) keep exact zeros.
+bool block_diag_in(const double *U, int k, int umask) {
+    if (!U || umask == 0) return false;
+    const int D = 1 << k;
+    for (int r = 0; r < D; ++r)
+        for (int c = 0; c < D; ++c)
+            if (((r ^ c) & umask) && (U[2 * (r * D + c)] != 0.0 || U[2 * (r * D + c) + 1] != 0.0)) return false;
+    return true;
+}
+
 void schedule(int n, int m, const std::vector<GateRef> &g, std::vector<int> &pi,
               std::vector<Op> &ops) {
     const int nl = n - m;
@@ -164,9 +177,16 @@ void schedule(int n, int m, const std::vector<GateRef> &g, std::vector<int> &pi,
         const GateRef &gt = g[i];
         if (m > 0) {
             uint64_t Q = qmask(gt);
-            int need[6], nneed = 0;
+            int need[6], nneed = 0, umask = 0;
             for (int j = 0; j < gt.k; ++j)
-                if (pi[gt.q[j]] >= nl) need[nneed++] = gt.q[j];
+                if (pi[gt.q[j]] >= nl) {
+                    need[nneed++] = gt.q[j];
+                    umask |= 1 << (gt.k - 1 - j);
+                }
+            // Row f1: a gate block-diagonal in its global targets needs no
+            // remap; every rank applies the block its rank bits select
+            // (an APPLY whose bits include global positions >= nl).
+            if (nneed > 0 && block_diag_in(gt.U, gt.k, umask)) nneed = 0;
             if (nneed > 0) {
                 // candidates in the run window, furthest next use first (Belady)
                 std::vector<std::pair<size_t, int>> cand;   // (next use, phys bit)

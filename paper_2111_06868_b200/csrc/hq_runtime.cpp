@@ -125,6 +125,11 @@ struct hq_circuit {
     std::vector<Op> ops;
     std::vector<long long> op_uoff;        // per APPLY op: byte offset of its payload (-1: none)
     std::vector<struct Prep> prep;         // per op (APPLY)
+    // row f1: APPLY ops with global targets, one Prep (and payload offset)
+    // per shard; empty for the others
+    std::vector<std::vector<struct Prep>> cprep;
+    std::vector<std::vector<long long>> cuoff;
+    std::vector<double> cgnorm;            // spectral bound of the whole U
     std::vector<char *> dev_U;             // per shard: all payloads
     uint64_t passes = 0, remaps = 0, permutes = 0;
     // CUDA graph of the whole op stream (single-shard states, profiling off):
@@ -498,6 +503,8 @@ struct Prep {
     std::vector<char> hostU;     // canonical U in the state dtype (RN from fp64)
     std::vector<char> payload;   // bytes the kernel reads from device memory
     std::vector<char> params;    // TC parameter block
+    bool scalar = false;         // row f1: every target global -> a phase sre + i sim
+    double sre = 1.0, sim = 0.0;
 };
 
 // Upper bound on ||U||_2: sqrt of the Gershgorin bound on lambda_max(U^H U)
@@ -524,6 +531,7 @@ static double spectral_bound(const double *U, int k) {
 }
 
 static void prepare(hq_dtype dt, const double *U, int k, const int *phys, int nl, Prep &p) {
+    p.scalar = false;
     std::vector<double> Uc;
     canonical_U64(U, k, phys, p.d, Uc, nl);
     p.gnorm = spectral_bound(Uc.data(), k);
@@ -598,6 +606,66 @@ static hq_status exec_apply(hq_state *st, Shard &s, const Prep &p, const void *d
     st->stats.passes++;
     st->stats.kernel_launches += launches;
     st->stats.hbm_bytes += bytes;
+    return HQ_OK;
+}
+
+// ------------------------------------------------------------------ row f1: global-diagonal gates
+// The scheduler leaves a gate on its global targets when U is block-diagonal
+// in them (block_diag_in): rank r then applies the block V_x, x = r's values
+// of those bits, to the local targets; with no local target V_x is a phase.
+static bool op_conditioned(const hq_state *st, const Op &op) {
+    for (int j = 0; j < op.nbits; ++j)
+        if (op.bits[j] >= st->nl) return true;
+    return false;
+}
+
+static void prepare_cond(const hq_state *st, const GateRef &g, const Op &op, int rank, Prep &p) {
+    const int k = g.k, D = 1 << k;
+    int lb[6], lu[6], kl = 0, fixval = 0;
+    for (int j = 0; j < k; ++j) {
+        const int ub = k - 1 - j, b = op.bits[j];
+        if (b >= st->nl) {
+            if ((rank >> (b - st->nl)) & 1) fixval |= 1 << ub;
+        } else {
+            lb[kl] = b;
+            lu[kl] = ub;
+            ++kl;
+        }
+    }
+    p.scalar = kl == 0;
+    if (p.scalar) {
+        p.sre = g.U[2 * (fixval * D + fixval)];
+        p.sim = g.U[2 * (fixval * D + fixval) + 1];
+        p.gnorm = std::hypot(p.sre, p.sim) * (1.0 + 1e-5);
+        p.payload.clear();
+        return;
+    }
+    const int d = 1 << kl;
+    auto expand = [&](int a) {
+        int x = fixval;
+        for (int t = 0; t < kl; ++t)
+            if ((a >> (kl - 1 - t)) & 1) x |= 1 << lu[t];
+        return x;
+    };
+    std::vector<double> V((size_t)2 * d * d);
+    for (int r = 0; r < d; ++r)
+        for (int c = 0; c < d; ++c) {
+            const size_t src = 2 * ((size_t)expand(r) * D + expand(c));
+            V[2 * (r * d + c)] = g.U[src];
+            V[2 * (r * d + c) + 1] = g.U[src + 1];
+        }
+    prepare(st->dtype, V.data(), kl, lb, st->nl, p);
+}
+
+static hq_status exec_prep(hq_state *st, Shard &s, const Prep &p, const void *dU) {
+    if (!p.scalar) return exec_apply(st, s, p, dU);
+    if (p.sre == 1.0 && p.sim == 0.0) return HQ_OK;
+    CUDA_TRY(cudaSetDevice(s.device));
+    int e = launch_scale_complex((int)st->dtype, s.psi, 1ull << st->nl, p.sre, p.sim, s.stream);
+    if (e) return set_error(HQ_ERR_CUDA, "phase launch: %s", cudaGetErrorString((cudaError_t)e));
+    st->stats.passes++;
+    st->stats.kernel_launches++;
+    st->stats.hbm_bytes += (uint64_t)2 * (st->es << st->nl);
     return HQ_OK;
 }
 
@@ -741,15 +809,17 @@ static hq_status run_ops(hq_state *st, const std::vector<GateRef> &refs, const s
         hq_status rc = HQ_OK;
         if (op.kind == OP_APPLY) {
             const GateRef &g = refs[op.gate];
-            prepare(st->dtype, g.U, g.k, op.bits, st->nl, p);
+            const bool cond = op_conditioned(st, op);
+            if (!cond) prepare(st->dtype, g.U, g.k, op.bits, st->nl, p);
             for (size_t r = 0; r < st->sh.size(); ++r) {
                 Shard &s = st->sh[r];
+                if (cond) prepare_cond(st, g, op, s.rank, p);
                 void *dU = nullptr;
                 if (!p.payload.empty() && (rc = arena_push(s, p.payload.data(), p.payload.size(), &dU)))
                     return rc;
-                if ((rc = exec_apply(st, s, p, dU))) return rc;
+                if ((rc = exec_prep(st, s, p, dU))) return rc;
             }
-            if (st->amp_bound >= 0) st->amp_bound *= p.gnorm;
+            if (st->amp_bound >= 0) st->amp_bound *= cond ? spectral_bound(g.U, g.k) : p.gnorm;
         } else if (op.kind == OP_REMAP) {
             rc = exec_remap(st, op);
         } else {
@@ -794,12 +864,30 @@ static hq_status circuit_compile(hq_state *st, hq_circuit *c, const std::vector<
     schedule(st->n, st->m, refs, c->pi_end, c->ops);
     c->prep.assign(c->ops.size(), Prep{});
     c->op_uoff.assign(c->ops.size(), -1);
+    c->cprep.assign(c->ops.size(), {});
+    c->cuoff.assign(c->ops.size(), {});
+    c->cgnorm.assign(c->ops.size(), 1.0);
     size_t total = 0;
     c->passes = c->remaps = c->permutes = 0;
     for (size_t i = 0; i < c->ops.size(); ++i) {
         const Op &op = c->ops[i];
         if (op.kind == OP_APPLY) {
             const GateRef &g = refs[op.gate];
+            if (op_conditioned(st, op)) {
+                const size_t G = st->sh.size();
+                c->cprep[i].assign(G, Prep{});
+                c->cuoff[i].assign(G, -1);
+                c->cgnorm[i] = spectral_bound(g.U, g.k);
+                for (size_t r = 0; r < G; ++r) {
+                    prepare_cond(st, g, op, st->sh[r].rank, c->cprep[i][r]);
+                    if (!c->cprep[i][r].payload.empty()) {
+                        c->cuoff[i][r] = (long long)total;
+                        total += (c->cprep[i][r].payload.size() + 255) & ~(size_t)255;
+                    }
+                }
+                c->passes++;
+                continue;
+            }
             prepare(st->dtype, g.U, g.k, op.bits, st->nl, c->prep[i]);
             if (!c->prep[i].payload.empty()) {
                 c->op_uoff[i] = (long long)total;
@@ -816,9 +904,13 @@ static hq_status circuit_compile(hq_state *st, hq_circuit *c, const std::vector<
     c->dev_U.assign(st->sh.size(), nullptr);
     if (total == 0) return HQ_OK;
     std::vector<char> blob(total, 0);
-    for (size_t i = 0; i < c->ops.size(); ++i)
+    for (size_t i = 0; i < c->ops.size(); ++i) {
         if (c->op_uoff[i] >= 0)
             memcpy(blob.data() + c->op_uoff[i], c->prep[i].payload.data(), c->prep[i].payload.size());
+        for (size_t r = 0; r < c->cuoff[i].size(); ++r)
+            if (c->cuoff[i][r] >= 0)
+                memcpy(blob.data() + c->cuoff[i][r], c->cprep[i][r].payload.data(), c->cprep[i][r].payload.size());
+    }
     for (size_t r = 0; r < st->sh.size(); ++r) {
         Shard &s = st->sh[r];
         if (r > 0 && st->mode == MODE_VIRTUAL) { c->dev_U[r] = nullptr; continue; }
@@ -852,12 +944,14 @@ static hq_status circuit_run_ops(hq_state *st, hq_circuit *c) {
         const Op &op = c->ops[i];
         hq_status rc = HQ_OK;
         if (op.kind == OP_APPLY) {
+            const bool cond = !c->cprep[i].empty();
             for (size_t r = 0; r < st->sh.size(); ++r) {
                 const char *base = c->dev_U[st->mode == MODE_VIRTUAL ? 0 : r];
-                const void *dU = (base && c->op_uoff[i] >= 0) ? base + c->op_uoff[i] : nullptr;
-                if ((rc = exec_apply(st, st->sh[r], c->prep[i], dU))) return rc;
+                const long long off = cond ? c->cuoff[i][r] : c->op_uoff[i];
+                const void *dU = (base && off >= 0) ? base + off : nullptr;
+                if ((rc = exec_prep(st, st->sh[r], cond ? c->cprep[i][r] : c->prep[i], dU))) return rc;
             }
-            if (st->amp_bound >= 0) st->amp_bound *= c->prep[i].gnorm;
+            if (st->amp_bound >= 0) st->amp_bound *= cond ? c->cgnorm[i] : c->prep[i].gnorm;
         } else if (op.kind == OP_REMAP) {
             rc = exec_remap(st, op);
         } else {

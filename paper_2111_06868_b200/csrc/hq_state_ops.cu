@@ -72,6 +72,21 @@ __global__ void __launch_bounds__(256) scale_kernel(V *__restrict__ psi, uint64_
     }
 }
 
+template <typename V>
+__global__ void __launch_bounds__(256) scale_complex_kernel(V *__restrict__ psi, uint64_t n_amps, double re,
+                                                            double im) {
+    using T = decltype(V::x);
+    const T sr = (T)re, si = (T)im;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_amps;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const V v = psi[i];
+        V o;
+        o.x = sr * v.x - si * v.y;
+        o.y = sr * v.y + si * v.x;
+        psi[i] = o;
+    }
+}
+
 // hist[block][x] = sum over this block's amplitudes with outcome x of |psi|^2,
 // outcome x = bits of i at positions pos[0..nq) (pos[0] = MSB of x).
 template <typename V>
@@ -249,6 +264,15 @@ int launch_scale(int dtype, void *psi, uint64_t n_amps, double s, void *stream) 
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     if (dtype == HQ_C64) scale_kernel<float2><<<grid_for(n_amps), 256, 0, st>>>((float2 *)psi, n_amps, s);
     else scale_kernel<double2><<<grid_for(n_amps), 256, 0, st>>>((double2 *)psi, n_amps, s);
+    return (int)cudaGetLastError();
+}
+
+int launch_scale_complex(int dtype, void *psi, uint64_t n_amps, double re, double im, void *stream) {
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (dtype == HQ_C64)
+        scale_complex_kernel<float2><<<grid_for(n_amps), 256, 0, st>>>((float2 *)psi, n_amps, re, im);
+    else
+        scale_complex_kernel<double2><<<grid_for(n_amps), 256, 0, st>>>((double2 *)psi, n_amps, re, im);
     return (int)cudaGetLastError();
 }
 

@@ -17,6 +17,38 @@ def phys_apply(shard, nl, U, phys_bits):
     O.apply_gate(shard, U, [nl - 1 - p for p in phys_bits])
 
 
+def cond_block(U, phys_bits, nl, rank):
+    """Row f1: for an APPLY whose bits include global positions (>= nl), the
+    block of U rank `rank` applies: rows/columns whose global-target bits equal
+    the rank's bits, on the local targets.  Returns (V, local bits)."""
+    k = len(phys_bits)
+    fix, loc = 0, []
+    for j, b in enumerate(phys_bits):
+        if b >= nl:
+            fix |= ((rank >> (b - nl)) & 1) << (k - 1 - j)
+        else:
+            loc.append(j)
+    idx = []
+    for a in range(2 ** len(loc)):
+        x = fix
+        for t, j in enumerate(loc):
+            x |= ((a >> (len(loc) - 1 - t)) & 1) << (k - 1 - j)
+        idx.append(x)
+    return U[np.ix_(idx, idx)], [phys_bits[j] for j in loc]
+
+
+def apply_on_shard(shard, nl, U, phys_bits, rank):
+    """Apply a scheduled gate on one shard (conditioned when a bit is global)."""
+    if all(b < nl for b in phys_bits):
+        phys_apply(shard, nl, U, phys_bits)
+        return
+    V, lb = cond_block(np.asarray(U), phys_bits, nl, rank)
+    if lb:
+        phys_apply(shard, nl, V, lb)
+    else:
+        shard *= V[0, 0]
+
+
 def permute_bits(shard, pairs):
     idx = np.arange(shard.size, dtype=np.int64)
     dst = idx.copy()
@@ -71,8 +103,8 @@ def replay_all_shards(n, m, gates, ops, psi_logical):
         if op["kind"] == "apply":
             g = gates[op["gate"]]
             k = len(g.qubits)
-            for s in shards:
-                phys_apply(s, nl, g.U, op["bits"][:k])
+            for r, s in enumerate(shards):
+                apply_on_shard(s, nl, g.U, op["bits"][:k], r)
         elif op["kind"] == "permute":
             pairs = [(op["bits"][2 * i], op["bits"][2 * i + 1]) for i in range(op["nbits"])]
             shards = [permute_bits(s, pairs) for s in shards]

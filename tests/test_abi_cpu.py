@@ -115,16 +115,73 @@ def test_schedule_replay_matches_oracle(m, kind):
     assert sum(o["kind"] == "apply" for o in ops) == len(gates)
     if m == 0:
         assert all(o["kind"] == "apply" for o in ops)
-    # every APPLY target is local
+    # every APPLY target is local, or the gate is block-diagonal in its
+    # global targets (row f1), checked here independently on U
     for o in ops:
         if o["kind"] == "apply":
-            k = len(gates[o["gate"]].qubits)
-            assert all(b < n - m for b in o["bits"][:k])
+            g = gates[o["gate"]]
+            _assert_local_or_block_diag(g.U, o["bits"][:len(g.qubits)], n - m)
     psi0 = random_state(n, 3)
     shards = replay_all_shards(n, m, gates, ops, psi0)
     got = to_logical(n, shards, pi)
     want = O.simulate(n, gates, psi0)
     assert np.max(np.abs(got - want)) < 1e-12
+
+
+def _assert_local_or_block_diag(U, bits, nl):
+    k = len(bits)
+    gmask = sum(1 << (k - 1 - j) for j, b in enumerate(bits) if b >= nl)
+    if gmask == 0:
+        return
+    D = 2 ** k
+    for r in range(D):
+        for c in range(D):
+            if (r ^ c) & gmask:
+                assert U[r, c] == 0, "APPLY on a global target with a non-block-diagonal U"
+
+
+@pytest.mark.parametrize("m", [1, 2, 3])
+@pytest.mark.parametrize("kind", ["qft", "qaoa"])
+def test_schedule_global_diagonal_gates_skip_remaps(m, kind):
+    """Row f1: controlled-phase / ZZ gates on global qubits run in place with
+    rank-selected blocks; the replay (cond_block per rank) matches the oracle
+    and the op stream needs fewer remaps than the same circuit with every
+    diagonal gate replaced by a dense one on the same qubits."""
+    from hq_inputs import qft_circuit, qaoa_circuit
+    n = 12
+    gates = qft_circuit(n) if kind == "qft" else qaoa_circuit(n, 3, 7)
+    ops, pi = hq.hq_schedule(n, m, gates)
+    cond = [o for o in ops if o["kind"] == "apply"
+            and any(b >= n - m for b in o["bits"][:len(gates[o["gate"]].qubits)])]
+    assert cond, "expected in-place applies on global qubits"
+    for o in cond:
+        g = gates[o["gate"]]
+        _assert_local_or_block_diag(g.U, o["bits"][:len(g.qubits)], n - m)
+    psi0 = random_state(n, 5)
+    got = to_logical(n, replay_all_shards(n, m, gates, ops, psi0), pi)
+    assert np.max(np.abs(got - O.simulate(n, gates, psi0))) < 1e-12
+    rng = np.random.default_rng(1)
+    dense = [Gate(g.name, g.qubits, haar_unitary(len(g.qubits), rng))
+             if np.count_nonzero(g.U - np.diag(np.diag(g.U))) == 0 else g for g in gates]
+    ops_d, _ = hq.hq_schedule(n, m, dense)
+    r_diag = sum(o["kind"] == "remap" for o in ops)
+    r_dense = sum(o["kind"] == "remap" for o in ops_d)
+    assert r_diag < r_dense, (r_diag, r_dense)
+
+
+def test_schedule_phase_only_on_global_qubits():
+    """A diagonal gate whose targets are all global is a per-rank phase."""
+    n, m = 8, 2
+    from hq_inputs import CZ, H
+    gates = [Gate("H", (q,), H) for q in range(2, n)] + [Gate("CZ", (0, 1), CZ),
+                                                         Gate("CP", (1, 0), np.diag([1, 1j, -1j, -1]).astype(complex))]
+    ops, pi = hq.hq_schedule(n, m, gates)
+    assert all(o["kind"] == "apply" for o in ops)              # no remap at all
+    tail = [o for o in ops if o["gate"] >= n - 2]
+    assert len(tail) == 2 and all(all(b >= n - m for b in o["bits"][:2]) for o in tail)
+    psi0 = random_state(n, 2)
+    got = to_logical(n, replay_all_shards(n, m, gates, ops, psi0), pi)
+    assert np.max(np.abs(got - O.simulate(n, gates, psi0))) < 1e-13
 
 
 def test_schedule_reversible_bit_exact():

@@ -36,7 +36,7 @@ def _worker(rank, world, port, n, kind, q):
         import oracle as O
         import paper_2111_06868_b200 as hq
         from hq_inputs import reversible_circuit, random_circuit, integer_state, random_state
-        from sched_replay import phys_apply, permute_bits, remap_runs, peer_of, bits_of, to_logical
+        from sched_replay import apply_on_shard, permute_bits, remap_runs, peer_of, bits_of, to_logical
 
         m = world.bit_length() - 1
         nl = n - m
@@ -51,7 +51,7 @@ def _worker(rank, world, port, n, kind, q):
         for op in ops:
             if op["kind"] == "apply":
                 g = gates[op["gate"]]
-                phys_apply(shard, nl, g.U, op["bits"][:len(g.qubits)])
+                apply_on_shard(shard, nl, g.U, op["bits"][:len(g.qubits)], rank)
             elif op["kind"] == "permute":
                 pairs = [(op["bits"][2 * i], op["bits"][2 * i + 1]) for i in range(op["nbits"])]
                 shard = permute_bits(shard, pairs)
