@@ -399,6 +399,122 @@ bool plan_reg(int dtype, const ApplyDesc &d, RegParams &P, int &VEC, int &T0, in
 
 }  // namespace
 
+// ------------------------------------------------------------------ complex128, k = 5, 6: FP64 tiles
+// At k = 5, 6 a complex128 pass costs 2^(k-2) = 8, 16 flop/B: above the FP64
+// ridge (~6 flop/B), so the bound is the FP64 pipe (<= ~0.7 / ~0.36 of the
+// HBM roofline), and tcgen05 has no f64 kind.  The pass is then a small ZGEMM
+// per tile: out (64 sets x D) = in (64 sets x D) . U^T.
+//   * U^T staged once per persistent CTA in shared memory, Us[c][r] = U[r][c];
+//   * the tile's inputs In[c][set] (set-contiguous: the 16 lanes of a
+//     half-warp read 16 consecutive sets, conflict-free) double-buffered with
+//     cp.async, the next tile loading while this one is computed;
+//   * 256 threads, each 4 sets x D/16 rows of complex accumulators (k = 6:
+//     64 DFMA per 8 shared loads); stores for a fixed row are 16 consecutive
+//     sets.
+// In place: a tile's outputs are exactly its inputs' amplitudes.
+constexpr int ZT_SETS = 64;
+
+template <int K>
+__global__ void __launch_bounds__(256, K == 6 ? 1 : 2)
+apply_ztile(double2 *__restrict__ psi, const __grid_constant__ GenParams P, const double2 *__restrict__ U,
+            uint64_t ntiles) {
+    constexpr int D = 1 << K, RJ = D / 16;       // rows per thread
+    extern __shared__ __align__(16) double2 zsm[];
+    double2 *Us = zsm;                           // [D][D]: Us[c][r] = U[r][c]
+    double2 *In = zsm + D * D;                   // [2][D][ZT_SETS]
+    const int tid = threadIdx.x;
+    for (int i = tid; i < D * D; i += 256) {
+        const int r = i / D, c = i % D;
+        Us[c * D + r] = U[i];
+    }
+    auto base_of = [&](uint64_t o) {
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            const int b = P.s[i];
+            o = ((o >> b) << (b + 1)) | (o & ((1ull << b) - 1));
+        }
+        return o;
+    };
+    const int lset = tid & (ZT_SETS - 1), lc0 = tid >> 6;          // loader: one set, c = lc0 + 4m
+    auto prefetch = [&](uint64_t t, int buf) {
+        const double2 *src = psi + base_of(t * ZT_SETS + lset);
+        const uint32_t dst0 = (uint32_t)__cvta_generic_to_shared(In + buf * D * ZT_SETS + lset);
+#pragma unroll
+        for (int m = 0; m < D / 4; ++m) {
+            const int c = lc0 + 4 * m;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst0 + (uint32_t)(c * ZT_SETS) * 16),
+                         "l"(src + P.off[c])
+                         : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    const int tx = tid & 15, ty = tid >> 4;
+    const uint64_t G = gridDim.x;
+    uint64_t t = blockIdx.x;
+    if (t < ntiles) prefetch(t, 0);
+    for (int it = 0; t < ntiles; t += G, ++it) {
+        const int buf = it & 1;
+        if (t + G < ntiles) {
+            prefetch(t + G, buf ^ 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncthreads();
+        const double2 *in = In + buf * D * ZT_SETS;
+        double2 acc[4][RJ];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < RJ; ++j) acc[i][j] = make_double2(0.0, 0.0);
+#pragma unroll 4
+        for (int c = 0; c < D; ++c) {
+            double2 a[4], b[RJ];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = in[c * ZT_SETS + tx + 16 * i];
+#pragma unroll
+            for (int j = 0; j < RJ; ++j) b[j] = Us[c * D + ty + 16 * j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < RJ; ++j) {
+                    acc[i][j].x = fma(a[i].x, b[j].x, acc[i][j].x);
+                    acc[i][j].x = fma(-a[i].y, b[j].y, acc[i][j].x);
+                    acc[i][j].y = fma(a[i].x, b[j].y, acc[i][j].y);
+                    acc[i][j].y = fma(a[i].y, b[j].x, acc[i][j].y);
+                }
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            double2 *dst = psi + base_of(t * ZT_SETS + tx + 16 * i);
+#pragma unroll
+            for (int j = 0; j < RJ; ++j) dst[P.off[ty + 16 * j]] = acc[i][j];
+        }
+        __syncthreads();        // every thread is done with In[buf] before it is refilled
+    }
+}
+
+template <int K>
+static cudaError_t launch_ztile(void *psi, const GenParams &P, const void *dU, cudaStream_t st) {
+    constexpr int D = 1 << K;
+    constexpr size_t smem = sizeof(double2) * (D * D + 2 * D * ZT_SETS);
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(apply_ztile<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    const uint64_t ntiles = P.nsets / ZT_SETS;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint64_t per = K == 6 ? 1 : 2;
+    const uint64_t grid = ntiles < per * sms ? ntiles : per * sms;
+    apply_ztile<K><<<(unsigned)grid, 256, smem, st>>>(reinterpret_cast<double2 *>(psi), P,
+                                                      reinterpret_cast<const double2 *>(dU), ntiles);
+    return cudaGetLastError();
+}
+
 int launch_apply(int dtype, void *psi, const ApplyDesc &d, const void *host_U, const void *dev_U,
                  void *stream, int *launches) {
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -432,8 +548,12 @@ int launch_apply(int dtype, void *psi, const ApplyDesc &d, const void *host_U, c
         for (int i = 0; i < d.k; ++i) gp.s[i] = d.p[i];
         gp.nsets = 1ull << (d.n_local - d.k);
         if (!dev_U) return (int)cudaErrorInvalidValue;
-        e = dtype == HQ_C64 ? launch_gen<float>(d.k, psi, gp, dev_U, st)
-                            : launch_gen<double>(d.k, psi, gp, dev_U, st);
+        static const char *zt = getenv("HQ_ZTILE");     // "0": generic kernel (experiments)
+        if (dtype == HQ_C128 && d.k >= 5 && gp.nsets >= (1ull << 12) && !(zt && zt[0] == '0'))
+            e = d.k == 5 ? launch_ztile<5>(psi, gp, dev_U, st) : launch_ztile<6>(psi, gp, dev_U, st);
+        else
+            e = dtype == HQ_C64 ? launch_gen<float>(d.k, psi, gp, dev_U, st)
+                                : launch_gen<double>(d.k, psi, gp, dev_U, st);
     }
     if (launches) ++*launches;
     return (int)e;
