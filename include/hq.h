@@ -229,6 +229,29 @@ hq_status hq_reduced_dm(hq_state *s, const int32_t *qubits, int k, double *rho_o
 hq_status hq_kraus_sample(hq_state *s, const double *const *K, int nkraus, const int32_t *qubits, int k,
                           double u, int *chosen_out, double *probs_out);
 
+/* Batched trajectories: 2^nb shots in ONE single-shard state.  Logical
+ * qubits 0..nb-1 index the shot (they must sit on the top physical bits,
+ * pi[q] = n-1-q, as in the default layout) and qubits nb..n-1 hold each shot's
+ * system, so one apply pass of a gate on system qubits advances every shot.
+ * 0 <= nb <= 16; targets must be system qubits.  Errors: HQ_ERR_STATE
+ * (sharded state or batch qubits moved), HQ_ERR_ARG, HQ_ERR_K, HQ_ERR_QUBIT.
+ *
+ * hq_reduced_dm_batched: rho_out[shot] (2^nb blocks of 2*4^k doubles) = the
+ * reduced density matrix of qubits[0..k) within that shot's block, unnormalised
+ * (trace = the block's squared norm).  One read pass.  Synchronises.
+ *
+ * hq_kraus_sample_batched: one trajectory step per shot with its own uniform
+ * u[shot] (same rule as hq_kraus_sample); shot s becomes
+ * K_i psi_s * sqrt(2^-nb / p_i), so every block keeps squared norm 2^-nb and
+ * the state norm stays 1.  chosen_out[shot] = i; probs_out (2^nb x nkraus,
+ * may be NULL) = the unnormalised p_i.  One read pass + one apply pass (a
+ * per-shot matrix).  HQ_ERR_RANGE if some shot has every p_i ~ 0 (state
+ * unchanged).  Synchronises. */
+hq_status hq_reduced_dm_batched(hq_state *s, int nb, const int32_t *qubits, int k, double *rho_out);
+hq_status hq_kraus_sample_batched(hq_state *s, int nb, const double *const *K, int nkraus,
+                                  const int32_t *qubits, int k, const double *u, int32_t *chosen_out,
+                                  double *probs_out);
+
 /* ------------------------------------------------------------------ density matrices
  * Density-matrix evolution by doubling (PAPER P:286-289 MatrixSuperGate "using
  * a matrix-vector multiplication", "a super circuit [becomes] a

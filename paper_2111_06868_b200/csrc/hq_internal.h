@@ -141,5 +141,12 @@ constexpr int RDM_MAX_BLOCKS = 148 * 4;
 constexpr int RDM_MAX_ENTRIES = 2 * 36;  // doubles per block partial (k = 3)
 int launch_reduced_dm(int dtype, const void *psi, uint64_t n_amps, const RdmParams &P, double *dev_part,
                       void *stream, int *nblocks_out);
+// Batched trajectories (shots along the top physical bits): per-shot reduced
+// density matrices (partials [shot][block][2E], blocks <= max_parts / nshots,
+// <= 64) and a per-shot matrix apply (mats[shot], D x D in the state dtype).
+int launch_reduced_dm_batched(int dtype, const void *psi, uint64_t shot_amps, int nshots, const RdmParams &P,
+                              double *dev_part, int max_parts, void *stream, int *nblocks_out);
+int launch_apply_batched(int dtype, void *psi, uint64_t n_amps, const RdmParams &P, const void *dev_mats,
+                         int sys_bits, void *stream);
 
 }  // namespace hq

@@ -84,6 +84,7 @@ struct Shard {
     double *h_part = nullptr;     // pinned
     double *d_red = nullptr;      // reduced-density-matrix partials (lazy)
     double *h_red = nullptr;      // pinned
+    size_t red_cap = 0;           // doubles in d_red / h_red
     Arena arena;
 };
 
@@ -1454,6 +1455,7 @@ extern "C" hq_status hq_reduced_dm(hq_state *st, const int32_t *qubits, int k, d
         if (!s.d_red) {
             CUDA_TRY(cudaMalloc((void **)&s.d_red, sizeof(double) * RDM_MAX_BLOCKS * RDM_MAX_ENTRIES));
             CUDA_TRY(cudaMallocHost((void **)&s.h_red, sizeof(double) * RDM_MAX_BLOCKS * RDM_MAX_ENTRIES));
+            s.red_cap = (size_t)RDM_MAX_BLOCKS * RDM_MAX_ENTRIES;
         }
         int nb = 0;
         int e = launch_reduced_dm((int)st->dtype, s.psi, 1ull << st->nl, P, s.d_red, s.stream, &nb);
@@ -1528,6 +1530,164 @@ extern "C" hq_status hq_kraus_sample(hq_state *st, const double *const *K, int n
     if ((rc = hq_apply_matrix(st, Ks.data(), qubits, k))) return rc;
     st->amp_bound = 1.0 + 1e-3;       // ||K_x psi|| / sqrt(p_x) = 1 up to the rounding of p_x
     *chosen_out = x;
+    return HQ_OK;
+}
+
+// Batched trajectories: 2^nb shots in one state, shot = logical qubits
+// 0..nb-1 (they must sit on the top physical bits of a single shard), the
+// system on qubits nb..n-1.
+static hq_status batch_check(hq_state *st, int nb, const int32_t *qubits, int k) {
+    if (st->sh.size() != 1) return set_error(HQ_ERR_STATE, "batched trajectories need a single-shard state");
+    if (nb < 0 || nb > 16 || nb >= st->n) return set_error(HQ_ERR_ARG, "nb=%d not in [0, min(16, n))", nb);
+    for (int q = 0; q < nb; ++q)
+        if (st->pi[q] != st->n - 1 - q)
+            return set_error(HQ_ERR_STATE, "batch qubit %d is not on physical bit %d (set a layout that keeps "
+                                           "qubits 0..nb-1 on the top bits)", q, st->n - 1 - q);
+    if (k < 1 || k > 3) return set_error(HQ_ERR_K, "k=%d not in [1,3]", k);
+    hq_status rc = validate_targets(st, qubits, k, 3);
+    if (rc) return rc;
+    for (int j = 0; j < k; ++j)
+        if (qubits[j] < nb) return set_error(HQ_ERR_QUBIT, "target %d is a batch qubit (< nb=%d)", qubits[j], nb);
+    return HQ_OK;
+}
+
+static RdmParams rdm_params(const hq_state *st, const int32_t *qubits, int k) {
+    RdmParams P;
+    P.k = k;
+    int pos[3];
+    for (int j = 0; j < k; ++j) pos[j] = st->pi[qubits[j]];
+    for (int a = 0; a < (1 << k); ++a) {
+        uint64_t o = 0;
+        for (int j = 0; j < k; ++j)
+            if ((a >> (k - 1 - j)) & 1) o |= 1ull << pos[j];
+        P.off[a] = o;
+    }
+    std::sort(pos, pos + k);
+    for (int j = 0; j < 3; ++j) P.pos[j] = j < k ? pos[j] : 0;
+    return P;
+}
+
+extern "C" hq_status hq_reduced_dm_batched(hq_state *st, int nb, const int32_t *qubits, int k, double *rho_out) {
+    clear_error();
+    if (!st || !rho_out) return set_error(HQ_ERR_ARG, "NULL argument");
+    hq_status rc = batch_check(st, nb, qubits, k);
+    if (rc) return rc;
+    const int D = 1 << k, E = D * (D + 1) / 2, S = 1 << nb;
+    const RdmParams P = rdm_params(st, qubits, k);
+    Shard &s = st->sh[0];
+    CUDA_TRY(cudaSetDevice(s.device));
+    const size_t cap = (size_t)std::max(RDM_MAX_BLOCKS, S * 4) * RDM_MAX_ENTRIES;
+    if (s.red_cap < cap) {
+        if (s.d_red) cudaFree(s.d_red);
+        if (s.h_red) cudaFreeHost(s.h_red);
+        s.d_red = nullptr;
+        s.h_red = nullptr;
+        s.red_cap = 0;
+        CUDA_TRY(cudaMalloc((void **)&s.d_red, sizeof(double) * cap));
+        CUDA_TRY(cudaMallocHost((void **)&s.h_red, sizeof(double) * cap));
+        s.red_cap = cap;
+    }
+    int nblk = 0;
+    int e = launch_reduced_dm_batched((int)st->dtype, s.psi, 1ull << (st->n - nb), S, P, s.d_red,
+                                      (int)(cap / (2 * E)), s.stream, &nblk);
+    if (e) return set_error(HQ_ERR_CUDA, "reduced_dm_batched launch: %s", cudaGetErrorString((cudaError_t)e));
+    st->stats.kernel_launches++;
+    st->stats.hbm_bytes += st->es << st->nl;
+    CUDA_TRY(cudaMemcpyAsync(s.h_red, s.d_red, sizeof(double) * 2 * E * nblk * S, cudaMemcpyDeviceToHost, s.stream));
+    CUDA_TRY(cudaStreamSynchronize(s.stream));
+    for (int sh = 0; sh < S; ++sh) {
+        double acc[2 * 36] = {0};
+        for (int b = 0; b < nblk; ++b)
+            for (int x = 0; x < 2 * E; ++x) acc[x] += s.h_red[((size_t)sh * nblk + b) * 2 * E + x];
+        double *rho = rho_out + (size_t)sh * 2 * D * D;
+        for (int a = 0, q = 0; a < D; ++a)
+            for (int b = a; b < D; ++b, ++q) {
+                rho[2 * (a * D + b)] = acc[2 * q];
+                rho[2 * (a * D + b) + 1] = acc[2 * q + 1];
+                rho[2 * (b * D + a)] = acc[2 * q];
+                rho[2 * (b * D + a) + 1] = -acc[2 * q + 1];
+            }
+    }
+    return HQ_OK;
+}
+
+// p_i = Re Tr(K_i rho K_i^H) for one shot
+static double branch_weight(const double *A, const double *rho, int D) {
+    double acc = 0.0;
+    for (int a = 0; a < D; ++a)
+        for (int b = 0; b < D; ++b) {
+            const double kr = A[2 * (a * D + b)], ki = A[2 * (a * D + b) + 1];
+            if (kr == 0.0 && ki == 0.0) continue;
+            for (int c = 0; c < D; ++c) {
+                const double rr = rho[2 * (b * D + c)], ri = rho[2 * (b * D + c) + 1];
+                const double cr = A[2 * (a * D + c)], ci = -A[2 * (a * D + c) + 1];
+                const double tr = kr * rr - ki * ri, ti = kr * ri + ki * rr;
+                acc += tr * cr - ti * ci;
+            }
+        }
+    return std::max(acc, 0.0);
+}
+
+extern "C" hq_status hq_kraus_sample_batched(hq_state *st, int nb, const double *const *K, int nkraus,
+                                             const int32_t *qubits, int k, const double *u, int32_t *chosen_out,
+                                             double *probs_out) {
+    clear_error();
+    if (!st || !K || !u || !chosen_out || nkraus < 1) return set_error(HQ_ERR_ARG, "NULL argument or no Kraus operators");
+    hq_status rc = batch_check(st, nb, qubits, k);
+    if (rc) return rc;
+    for (int i = 0; i < nkraus; ++i)
+        if (!K[i]) return set_error(HQ_ERR_ARG, "K[%d] is NULL", i);
+    const int S = 1 << nb, D = 1 << k;
+    for (int sh = 0; sh < S; ++sh)
+        if (!(u[sh] >= 0.0 && u[sh] < 1.0)) return set_error(HQ_ERR_ARG, "u[%d]=%g not in [0,1)", sh, u[sh]);
+    std::vector<double> rho((size_t)S * 2 * D * D);
+    if ((rc = hq_reduced_dm_batched(st, nb, qubits, k, rho.data()))) return rc;
+    // choose every shot's branch first (all-or-nothing: no state change on error)
+    std::vector<int> pick(S);
+    std::vector<double> scale(S), p(nkraus);
+    const double w = 1.0 / S;        // each shot keeps norm^2 1/S: the state norm stays 1
+    for (int sh = 0; sh < S; ++sh) {
+        double total = 0.0, pmax = 0.0;
+        for (int i = 0; i < nkraus; ++i) {
+            p[i] = branch_weight(K[i], rho.data() + (size_t)sh * 2 * D * D, D);
+            total += p[i];
+            pmax = std::max(pmax, p[i]);
+        }
+        if (probs_out)
+            for (int i = 0; i < nkraus; ++i) probs_out[(size_t)sh * nkraus + i] = p[i];
+        if (!(pmax >= 1e-14 * w)) return set_error(HQ_ERR_RANGE, "shot %d: all branch probabilities ~0 (ZeroNormBranch)", sh);
+        const double target = u[sh] * total;
+        double cum = 0.0;
+        int x = nkraus - 1;
+        for (int i = 0; i < nkraus; ++i) {
+            cum += p[i];
+            if (target < cum && p[i] > 0.0) { x = i; break; }
+        }
+        while (x > 0 && p[x] == 0.0) --x;
+        pick[sh] = x;
+        scale[sh] = std::sqrt(w / p[x]);
+    }
+    // per-shot matrices K_x * scale in the state dtype, in qubits[] index order
+    Shard &s = st->sh[0];
+    std::vector<char> mats((size_t)S * D * D * st->es);
+    for (int sh = 0; sh < S; ++sh) {
+        const double *A = K[pick[sh]];
+        for (int i = 0; i < 2 * D * D; ++i) {
+            const double v = A[i] * scale[sh];
+            if (st->dtype == HQ_C64) reinterpret_cast<float *>(mats.data())[(size_t)sh * 2 * D * D + i] = (float)v;
+            else reinterpret_cast<double *>(mats.data())[(size_t)sh * 2 * D * D + i] = v;
+        }
+        chosen_out[sh] = pick[sh];
+    }
+    void *dm = nullptr;
+    if ((rc = arena_push(s, mats.data(), mats.size(), &dm))) return rc;
+    const RdmParams P = rdm_params(st, qubits, k);
+    int e = launch_apply_batched((int)st->dtype, s.psi, 1ull << st->nl, P, dm, st->n - nb, s.stream);
+    if (e) return set_error(HQ_ERR_CUDA, "apply_batched launch: %s", cudaGetErrorString((cudaError_t)e));
+    st->stats.passes++;
+    st->stats.kernel_launches++;
+    st->stats.hbm_bytes += (uint64_t)2 * (st->es << st->nl);
+    st->amp_bound = 1.0 + 1e-3;
     return HQ_OK;
 }
 

@@ -8,6 +8,7 @@
 // amplitude, project reads+writes, probabilities reads.
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <algorithm>
 
 #include "hq_internal.h"
 
@@ -152,11 +153,16 @@ __global__ void __launch_bounds__(256) dm_trace_kernel(const V *__restrict__ psi
 // rho[a][b] = sum over gather sets of psi_a conj(psi_b) (upper triangle,
 // fp64 accumulation); one gather set per thread per step, consecutive
 // threads on consecutive sets (coalesced unless bit 0 is a target).
+// Batched form (row f3, shots along the top physical bits): blockIdx.y is
+// the shot, whose amplitudes are [shot * shot_amps, (shot + 1) * shot_amps);
+// partials go to part[shot][block][2E].  shot_amps = 0: one unbatched state.
 template <typename V, int K>
 __global__ void __launch_bounds__(256) reduced_dm_kernel(const V *__restrict__ psi, uint64_t nsets,
                                                          const __grid_constant__ RdmParams P,
-                                                         double *__restrict__ part) {
+                                                         double *__restrict__ part, uint64_t shot_amps) {
     constexpr int D = 1 << K, E = D * (D + 1) / 2;
+    psi += (uint64_t)blockIdx.y * shot_amps;
+    part += (size_t)blockIdx.y * gridDim.x * 2 * E;
     double acc[2 * E];
 #pragma unroll
     for (int e = 0; e < 2 * E; ++e) acc[e] = 0.0;
@@ -201,12 +207,51 @@ __global__ void __launch_bounds__(256) reduced_dm_kernel(const V *__restrict__ p
 }
 
 template <typename V>
-int reduced_dm_dispatch(const V *psi, uint64_t nsets, const RdmParams &P, double *part, unsigned g,
-                        cudaStream_t st) {
-    if (P.k == 1) reduced_dm_kernel<V, 1><<<g, 256, 0, st>>>(psi, nsets, P, part);
-    else if (P.k == 2) reduced_dm_kernel<V, 2><<<g, 256, 0, st>>>(psi, nsets, P, part);
-    else reduced_dm_kernel<V, 3><<<g, 256, 0, st>>>(psi, nsets, P, part);
+int reduced_dm_dispatch(const V *psi, uint64_t nsets, const RdmParams &P, double *part, dim3 g,
+                        cudaStream_t st, uint64_t shot_amps) {
+    if (P.k == 1) reduced_dm_kernel<V, 1><<<g, 256, 0, st>>>(psi, nsets, P, part, shot_amps);
+    else if (P.k == 2) reduced_dm_kernel<V, 2><<<g, 256, 0, st>>>(psi, nsets, P, part, shot_amps);
+    else reduced_dm_kernel<V, 3><<<g, 256, 0, st>>>(psi, nsets, P, part, shot_amps);
     return (int)cudaGetLastError();
+}
+
+// psi <- M_shot psi on the k <= 3 targets, M_shot = mats[shot] (row-major
+// D x D in the state dtype, canonical target order), shot = physical index
+// >> sys_bits.  One thread per gather set; a block's sets share a shot (the
+// matrices stay in L1).
+template <typename V, int K>
+__global__ void __launch_bounds__(256) apply_batched_kernel(V *__restrict__ psi, uint64_t nsets,
+                                                            const __grid_constant__ RdmParams P,
+                                                            const V *__restrict__ mats, int sys_bits) {
+    constexpr int D = 1 << K;
+    using T = decltype(V::x);
+    for (uint64_t o = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; o < nsets;
+         o += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t base = o;
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            const int s = P.pos[i];
+            base = ((base >> s) << (s + 1)) | (base & ((1ull << s) - 1));
+        }
+        const V *M = mats + (size_t)(base >> sys_bits) * D * D;
+        V x[D];
+#pragma unroll
+        for (int c = 0; c < D; ++c) x[c] = psi[base + P.off[c]];
+#pragma unroll
+        for (int r = 0; r < D; ++r) {
+            T re = 0, im = 0;
+#pragma unroll
+            for (int c = 0; c < D; ++c) {
+                const V m = M[r * D + c];
+                re += m.x * x[c].x - m.y * x[c].y;
+                im += m.x * x[c].y + m.y * x[c].x;
+            }
+            V y;
+            y.x = re;
+            y.y = im;
+            psi[base + P.off[r]] = y;
+        }
+    }
 }
 
 }  // namespace
@@ -218,8 +263,43 @@ int launch_reduced_dm(int dtype, const void *psi, uint64_t n_amps, const RdmPara
     unsigned g = grid_for(nsets);
     if (g > (unsigned)RDM_MAX_BLOCKS) g = RDM_MAX_BLOCKS;
     *nblocks_out = (int)g;
-    if (dtype == HQ_C64) return reduced_dm_dispatch((const float2 *)psi, nsets, P, dev_part, g, st);
-    return reduced_dm_dispatch((const double2 *)psi, nsets, P, dev_part, g, st);
+    if (dtype == HQ_C64) return reduced_dm_dispatch((const float2 *)psi, nsets, P, dev_part, dim3(g), st, 0);
+    return reduced_dm_dispatch((const double2 *)psi, nsets, P, dev_part, dim3(g), st, 0);
+}
+
+int launch_reduced_dm_batched(int dtype, const void *psi, uint64_t shot_amps, int nshots, const RdmParams &P,
+                              double *dev_part, int max_parts, void *stream, int *nblocks_out) {
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const uint64_t nsets = shot_amps >> P.k;
+    unsigned g = grid_for(nsets);
+    const unsigned cap = (unsigned)std::max(1, max_parts / nshots);
+    if (g > cap) g = cap;
+    if (g > 64) g = 64;
+    *nblocks_out = (int)g;
+    const dim3 grid(g, (unsigned)nshots);
+    if (dtype == HQ_C64) return reduced_dm_dispatch((const float2 *)psi, nsets, P, dev_part, grid, st, shot_amps);
+    return reduced_dm_dispatch((const double2 *)psi, nsets, P, dev_part, grid, st, shot_amps);
+}
+
+int launch_apply_batched(int dtype, void *psi, uint64_t n_amps, const RdmParams &P, const void *dev_mats,
+                         int sys_bits, void *stream) {
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const uint64_t nsets = n_amps >> P.k;
+    const unsigned g = grid_for(nsets);
+    if (dtype == HQ_C64) {
+        float2 *p = (float2 *)psi;
+        const float2 *m = (const float2 *)dev_mats;
+        if (P.k == 1) apply_batched_kernel<float2, 1><<<g, 256, 0, st>>>(p, nsets, P, m, sys_bits);
+        else if (P.k == 2) apply_batched_kernel<float2, 2><<<g, 256, 0, st>>>(p, nsets, P, m, sys_bits);
+        else apply_batched_kernel<float2, 3><<<g, 256, 0, st>>>(p, nsets, P, m, sys_bits);
+    } else {
+        double2 *p = (double2 *)psi;
+        const double2 *m = (const double2 *)dev_mats;
+        if (P.k == 1) apply_batched_kernel<double2, 1><<<g, 256, 0, st>>>(p, nsets, P, m, sys_bits);
+        else if (P.k == 2) apply_batched_kernel<double2, 2><<<g, 256, 0, st>>>(p, nsets, P, m, sys_bits);
+        else apply_batched_kernel<double2, 3><<<g, 256, 0, st>>>(p, nsets, P, m, sys_bits);
+    }
+    return (int)cudaGetLastError();
 }
 
 int launch_dm_trace(int dtype, const void *psi, int N, int n_local, int rank, const DmParams &P,

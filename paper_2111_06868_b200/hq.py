@@ -97,6 +97,8 @@ def lib():
             "hq_probabilities": [P, P, ctypes.c_int, P],
             "hq_measure": [P, P, ctypes.c_int, ctypes.c_double, ctypes.POINTER(ctypes.c_uint64)],
             "hq_reduced_dm": [P, P, ctypes.c_int, P],
+            "hq_reduced_dm_batched": [P, ctypes.c_int, P, ctypes.c_int, P],
+            "hq_kraus_sample_batched": [P, ctypes.c_int, P, ctypes.c_int, P, ctypes.c_int, P, P, P],
             "hq_kraus_sample": [P, P, ctypes.c_int, P, ctypes.c_int, ctypes.c_double, ctypes.POINTER(ctypes.c_int), P],
             "hq_state_get_layout": [P, P],
             "hq_sync": [P],
@@ -281,6 +283,29 @@ def hq_kraus_sample(state, K, qubits, u):
     _check(lib().hq_kraus_sample(state.ptr, ptrs, len(mats), q.ctypes.data, int(q.size), float(u),
                                  ctypes.byref(chosen), probs.ctypes.data))
     return chosen.value, probs
+
+
+def hq_reduced_dm_batched(state, nb, qubits):
+    """Per-shot reduced density matrices (2^nb, 2^k, 2^k), unnormalised."""
+    q = np.ascontiguousarray(qubits, dtype=np.int32)
+    d = 2 ** q.size
+    rho = np.zeros((2 ** nb, d, d), dtype=np.complex128)
+    _check(lib().hq_reduced_dm_batched(state.ptr, int(nb), q.ctypes.data, int(q.size), rho.ctypes.data))
+    return rho
+
+
+def hq_kraus_sample_batched(state, nb, K, qubits, u):
+    """One trajectory step for each of the 2^nb shots with uniforms u (2^nb):
+    returns (chosen indices int32 array, probabilities (2^nb, nkraus))."""
+    ptrs, mats = _kraus_array(K)
+    q = np.ascontiguousarray(qubits, dtype=np.int32)
+    uu = np.ascontiguousarray(u, dtype=np.float64)
+    assert uu.size == 2 ** nb
+    chosen = np.zeros(2 ** nb, dtype=np.int32)
+    probs = np.zeros((2 ** nb, len(mats)), dtype=np.float64)
+    _check(lib().hq_kraus_sample_batched(state.ptr, int(nb), ptrs, len(mats), q.ctypes.data, int(q.size),
+                                         uu.ctypes.data, chosen.ctypes.data, probs.ctypes.data))
+    return chosen, probs
 
 
 def hq_dm_superop(K):

@@ -15,6 +15,12 @@ apply pass), and the observable is hq_reduced_dm.  This module only orders the
 calls, draws the uniforms and sums.  Shots shard round-robin over ranks with
 no data-path collective; the per-rank sums are added with one all-reduce of a
 few doubles at the end.
+
+For small systems one shot per state is launch-bound, so `batch=B` advances B
+shots in one state of n + log2(B) qubits (shot index on the top qubits): every
+unitary pass serves all B shots, and a channel is one batched
+reduced-density-matrix pass plus one apply pass with a per-shot matrix
+(hq_reduced_dm_batched / hq_kraus_sample_batched).
 """
 import numpy as np
 
@@ -74,14 +80,20 @@ def reduce_sum(arr, group=None):
 
 
 def sample_trajectories(n, ops, n_shots, observe, seed=0, init="0", dtype="c64", kmax=6,
-                        rank=0, world=1, group=None, per_step=None):
+                        rank=0, world=1, group=None, per_step=None, batch=1):
     """Run this rank's share of `n_shots` trajectories of the noisy circuit
     `ops` (gates as (qubits, U) or objects with .qubits/.U, and Channel
     objects) from the token state `init`, and return the mean over ALL shots
     of the reduced density matrix of `observe` (k <= 3 qubits) at the end.
 
     per_step: optional list of op indices after which the reduced density
-    matrix is also recorded (means returned as a list in that order)."""
+    matrix is also recorded (means returned as a list in that order).
+    batch: shots advanced together in one state of n + log2(batch) qubits
+    (a power of two; hq_kraus_sample_batched).  Each shot keeps its own
+    uniform stream, so the branch choices are those of batch=1."""
+    if batch > 1:
+        return _sample_batched(n, ops, n_shots, observe, seed, init, dtype, kmax, rank, world, group,
+                               per_step, batch)
     segs = split_segments(ops)
     marks = sorted(set(per_step or []))
     # op index -> segment boundary: record after segment j when its last op index is marked
@@ -115,6 +127,70 @@ def sample_trajectories(n, ops, n_shots, observe, seed=0, init="0", dtype="c64",
                 r += 1
         acc[-1] += hq.hq_reduced_dm(s, observe)
         chosen.append(picks)
+    flat = np.concatenate([acc.real.ravel(), acc.imag.ravel(), [len(mine)]])
+    tot = reduce_sum(flat, group)
+    m = nrec * d * d
+    mean = (tot[:m] + 1j * tot[m:2 * m]).reshape(nrec, d, d) / max(tot[-1], 1)
+    return {"rho": mean[-1], "rho_steps": list(mean[:-1]), "shots": int(tot[-1]), "chosen": chosen}
+
+
+def _sample_batched(n, ops, n_shots, observe, seed, init, dtype, kmax, rank, world, group, per_step, batch):
+    nb = int(batch).bit_length() - 1
+    if 1 << nb != batch:
+        raise ValueError("batch must be a power of two")
+    segs = split_segments(ops)
+    marks = sorted(set(per_step or []))
+    bounds, idx = [], -1
+    for kind, body in segs:
+        idx += len(body) if kind == "U" else 1
+        bounds.append(idx)
+    if any(m not in bounds for m in marks):
+        raise ValueError("per_step indices must end a unitary stretch or be a channel")
+
+    def shift(g):
+        qs = g.qubits if hasattr(g, "qubits") else g[0]
+        U = g.U if hasattr(g, "U") else g[1]
+        return (tuple(int(q) + nb for q in qs), U)
+
+    s = hq.hq_state_create(n + nb, dtype, 1)
+    compiled = []
+    for kind, body in segs:
+        if kind == "U":
+            compiled.append(hq.hq_circuit_create(s, hq.hq_fuse([shift(g) for g in body], kmax)))
+        else:
+            compiled.append(Channel([q + nb for q in body.qubits], body.kraus, body.name))
+    tokens = "+" * nb + (init * n if len(init) == 1 else init)
+    obs = [q + nb for q in observe]
+    d = 2 ** len(observe)
+    nrec = len(marks) + 1
+    acc = np.zeros((nrec, d, d), dtype=np.complex128)
+    chosen = []
+    mine = shard_shots(n_shots, rank, world)
+    for b0 in range(0, len(mine), batch):
+        shots = mine[b0:b0 + batch]
+        live = len(shots)
+        rngs = [shot_rng(seed, sh) for sh in shots] + [np.random.default_rng(0)] * (batch - live)
+        hq.hq_state_init_tokens(s, tokens)
+        picks, r = [[] for _ in range(live)], 0
+
+        def record(slot):
+            rho = hq.hq_reduced_dm_batched(s, nb, obs)[:live]
+            tr = np.einsum("sii->s", rho).real
+            acc[slot] += np.sum(rho / tr[:, None, None], axis=0)
+
+        for j, ((kind, _), item) in enumerate(zip(segs, compiled)):
+            if kind == "U":
+                hq.hq_circuit_run(s, item)
+            else:
+                u = np.array([g.random() for g in rngs[:live]] + [0.5] * (batch - live))
+                ci, _ = hq.hq_kraus_sample_batched(s, nb, item.kraus, item.qubits, u)
+                for t in range(live):
+                    picks[t].append(int(ci[t]))
+            if r < len(marks) and bounds[j] == marks[r]:
+                record(r)
+                r += 1
+        record(-1)
+        chosen.extend(picks)
     flat = np.concatenate([acc.real.ravel(), acc.imag.ravel(), [len(mine)]])
     tot = reduce_sum(flat, group)
     m = nrec * d * d

@@ -151,3 +151,108 @@ def test_trajectories_mean_matches_density_matrix():
     r = rho.reshape(4, 4, 4, 4)
     want = np.einsum("aibi->ab", r)
     assert np.max(np.abs(res["rho"] - want)) < 5 / np.sqrt(shots)
+
+
+# ---------------------------------------------------------------- batched trajectories
+
+def _batched_state(nb, n, dtype, seed):
+    """2^nb shots, shot s holding random_state(n, seed + s) / sqrt(2^nb)."""
+    S = 2 ** nb
+    blocks = [random_state(n, seed + s) for s in range(S)]
+    psi = np.concatenate(blocks) / np.sqrt(S)
+    st = hq.hq_state_create(n + nb, dtype, 1)
+    hq.hq_set_amplitudes(st, psi.astype(st.np_dtype))
+    return st, blocks
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("qubits", [[0], [9, 2], [7, 0, 4]])
+def test_reduced_dm_batched_matches_oracle(dtype, qubits):
+    nb, n = 5, 10
+    st, blocks = _batched_state(nb, n, dtype, 40)
+    rho = hq.hq_reduced_dm_batched(st, nb, [q + nb for q in qubits])
+    for s_, b in enumerate(blocks):
+        want = O.reduced_dm(b, qubits) / 2 ** nb
+        assert np.max(np.abs(rho[s_] - want)) < TOL[dtype] / 2 ** nb * 4, s_
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("k,m", [(1, 4), (2, 3), (3, 2)])
+def test_kraus_sample_batched_matches_oracle(dtype, k, m):
+    nb, n = 4, 9
+    S = 2 ** nb
+    st, blocks = _batched_state(nb, n, dtype, 70)
+    K = _channel(k, m, 7 * k + m)
+    qubits = [8, 3, 0][:k]
+    rng = np.random.default_rng(k)
+    us, wants, idx = [], [], []
+    for b in blocks:
+        _, _, p = O.kraus_sample_step(b, K, qubits, 0.0)
+        i = int(rng.integers(m))
+        cum = np.concatenate([[0], np.cumsum(p)]) / p.sum()
+        u = (cum[i] + cum[i + 1]) / 2
+        w, wi, _ = O.kraus_sample_step(b, K, qubits, u)
+        assert wi == i
+        us.append(u)
+        wants.append(w)
+        idx.append(i)
+    chosen, probs = hq.hq_kraus_sample_batched(st, nb, K, [q + nb for q in qubits], np.array(us))
+    assert list(chosen) == idx
+    got = hq.hq_get_amplitudes(st).astype(np.complex128).reshape(S, -1) * np.sqrt(S)
+    for s_ in range(S):
+        assert np.linalg.norm(got[s_] - wants[s_]) < (1e-5 if dtype == "c64" else 1e-12), s_
+    assert abs(hq.hq_norm(st) - 1) < 1e-5
+
+
+def test_batched_errors():
+    st = hq.hq_state_create(8, "c64", 1)
+    hq.hq_state_init_tokens(st, "+")
+    with pytest.raises(hq.HQError) as e:
+        hq.hq_reduced_dm_batched(st, 3, [1])          # target on a batch qubit
+    assert e.value.status == "HQ_ERR_QUBIT"
+    v = hq.hq_state_create_virtual(10, "c64", 2)
+    hq.hq_state_init_tokens(v, "+")
+    with pytest.raises(hq.HQError) as e:
+        hq.hq_reduced_dm_batched(v, 2, [5])
+    assert e.value.status == "HQ_ERR_STATE"
+    lay = hq.hq_state_create(8, "c64", 1)
+    hq.hq_state_set_layout(lay, list(range(8)))        # qubit 0 on physical bit 0
+    hq.hq_state_init_tokens(lay, "+")
+    with pytest.raises(hq.HQError) as e:
+        hq.hq_reduced_dm_batched(lay, 2, [5])
+    assert e.value.status == "HQ_ERR_STATE"
+
+
+def test_batched_runner_equals_unbatched():
+    """Same seeds -> same branch choices and the same mean as one shot per
+    state (batch = 8 with a ragged last batch: 21 shots)."""
+    n = 6
+    rng = np.random.default_rng(12)
+    ops = []
+    for layer in range(3):
+        for q in range(0, n - 1, 2):
+            ops.append(Gate("U", (q, q + 1), haar_unitary(2, rng)))
+        ops.append(Channel([layer % n, (layer + 2) % n], _channel(2, 3, 90 + layer)))
+        ops.append(Channel([5], _channel(1, 2, 80 + layer)))
+    a = sample_trajectories(n, ops, 21, observe=[1, 4], seed=3)
+    b = sample_trajectories(n, ops, 21, observe=[1, 4], seed=3, batch=8)
+    assert a["chosen"] == b["chosen"]
+    assert np.max(np.abs(a["rho"] - b["rho"])) < 2e-6
+
+
+def test_trajectories_fig1_batched():
+    theta, p, steps, shots = 0.3, 0.08, 6, 4096
+    RZ = np.diag([np.exp(-0.5j * theta), np.exp(0.5j * theta)])
+    s4 = np.sqrt(p / 4)
+    X = np.array([[0, 1], [1, 0]], dtype=complex)
+    Y = np.array([[0, -1j], [1j, 0]])
+    Z = np.diag([1, -1]).astype(complex)
+    depol = [np.sqrt(1 - 3 * p / 4) * np.eye(2), s4 * X, s4 * Y, s4 * Z]
+    ops = []
+    for t in range(steps):
+        ops += [Gate("RZ", (0,), RZ), Channel([0], depol)]
+    marks = [2 * t + 1 for t in range(steps - 1)]
+    res = sample_trajectories(1, ops, shots, observe=[0], seed=9, init="+", per_step=marks, batch=1024)
+    for t, rho in enumerate(res["rho_steps"] + [res["rho"]], start=1):
+        ex = 2 * rho[0, 1].real
+        assert abs(ex - (1 - p) ** t * np.cos(t * theta)) < 4 / np.sqrt(shots), t
