@@ -1039,6 +1039,229 @@ apply_tcL(float2 *__restrict__ psi, const __grid_constant__ ParamsL P,
     }
 }
 
+// ------------------------------------------------------------------ mode L, bulk-copy producer
+// Mode L's tile (6 targets + the 6 lowest non-target bits) always contains
+// physical bits 0..6, because at least one target is below bit 7 in mode L;
+// the tile is therefore 32 contiguous 1 KB blocks.  A producer warp moves them
+// with cp.async.bulk into an L_NR-slot raw ring laid out in tile-index order
+// (exactly the [i][thread] order the converters read), replacing the
+// converters' per-thread cp.async.
+constexpr int L_NR = 3;
+constexpr int LB_PROD = NUM_EPI + 1 + NUM_CONV;             // warp 13
+constexpr int LB_THREADS = (LB_PROD + 1) * 32;
+constexpr int LB_SMEM = L_STAGES * L_STAGE + BAR_BYTES + L_NR * L_RAW;
+
+struct ParamsLB {
+    ParamsL l;
+    uint64_t boff[32];     // amplitude offset of 1 KB block j of a tile (tile bits >= 7 of j << 7)
+    int spin;
+};
+
+__global__ void __launch_bounds__(LB_THREADS, 1)
+apply_tcLb(float2 *__restrict__ psi, const __grid_constant__ ParamsLB PB,
+           const float *__restrict__ Areal /* [2][128][128] hi then lo, row = output real */) {
+    const ParamsL &P = PB.l;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t sbase = smem_u32(smem);
+    const uint32_t bar0 = sbase + L_STAGES * L_STAGE;
+    auto full_bar = [&](int s) { return bar0 + 8 * s; };
+    auto empty_bar = [&](int s) { return bar0 + 8 * (L_STAGES + s); };
+    auto tfull_bar = [&](int d) { return bar0 + 8 * (2 * L_STAGES + d); };
+    auto tempty_bar = [&](int d) { return bar0 + 8 * (2 * L_STAGES + 2 + d); };
+    auto rfull = [&](int r) { return bar0 + 8 * (2 * L_STAGES + 4 + r); };
+    auto rempty = [&](int r) { return bar0 + 8 * (2 * L_STAGES + 4 + L_NR + r); };
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + L_STAGES * L_STAGE + 8 * (2 * L_STAGES + 4 + 2 * L_NR));
+    const uint32_t raw0 = sbase + L_STAGES * L_STAGE + BAR_BYTES;
+    const bool spin = PB.spin != 0;
+    auto wait = [&](uint32_t bar, uint32_t parity) {
+        if (spin) mbar_wait(bar, parity);
+        else mbar_wait_sleep(bar, parity);
+    };
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < L_STAGES; ++s) {
+            mbar_init(full_bar(s), NUM_CONV);
+            mbar_init(empty_bar(s), 1);
+        }
+        for (int d = 0; d < 2; ++d) {
+            mbar_init(tfull_bar(d), 1);
+            mbar_init(tempty_bar(d), NUM_EPI);
+        }
+        for (int r = 0; r < L_NR; ++r) {
+            mbar_init(rfull(r), 1);
+            mbar_init(rempty(r), NUM_CONV);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == MMA_WARP) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    if (warp < NUM_EPI) {
+        const int m = warp * 32 + lane;
+#pragma unroll 1
+        for (int ch = 0; ch < 8; ++ch) {
+            uint32_t v[32];
+            const float *src = Areal + (ch >> 2) * (128 * 128) + m * 128 + (ch & 3) * 32;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__ldg(src + i));
+            tmem_st32(tmem + ((uint32_t)(warp * 32) << 16) + ch * 32, v);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t A_HI = tmem, A_LO = tmem + 128;
+    const uint64_t ntiles = P.ntiles;
+    const uint64_t G = gridDim.x;
+
+    if (warp == LB_PROD) {
+        uint32_t it = 0;
+        for (uint64_t t = blockIdx.x; t < ntiles; t += G, ++it) {
+            const int r = it % L_NR;
+            wait(rempty(r), ((it / L_NR) & 1) ^ 1);
+            if (lane == 0) mbar_arrive_tx(rfull(r), L_RAW);
+            __syncwarp();
+            const float2 *tb = psi + tile_base12(t, P);
+            bulk_g2s(raw0 + r * L_RAW + lane * 1024, tb + PB.boff[lane], 1024, rfull(r));
+        }
+    } else if (warp == MMA_WARP) {
+        const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(L_NS >> 3) << 17) |
+                               ((uint32_t)(128 >> 4) << 24);
+        uint32_t it = 0;
+        for (uint64_t t = blockIdx.x; t < ntiles; t += G, ++it) {
+            const int s = it % L_STAGES;
+            const uint32_t sp = (it / L_STAGES) & 1;
+            const int d = it & 1;
+            const uint32_t dp = (it >> 1) & 1;
+            mbar_wait(tempty_bar(d), dp ^ 1);
+            mbar_wait(full_bar(s), sp);
+            tc_fence_after();
+            if (elect_one()) {
+                const uint32_t D = tmem + 256 + L_NS * d;
+                const uint32_t bhi = sbase + s * L_STAGE, blo = bhi + L_HALF;
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const uint32_t o = (j >> 2) * L_ATOMCOL + (j & 3) * 32;
+                    mma_ts(D, A_LO + 8 * j, smem_desc_sw128(bhi + o), idesc, j > 0);
+                    mma_ts(D, A_HI + 8 * j, smem_desc_sw128(blo + o), idesc, 1);
+                }
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const uint32_t o = (j >> 2) * L_ATOMCOL + (j & 3) * 32;
+                    mma_ts(D, A_HI + 8 * j, smem_desc_sw128(bhi + o), idesc, 1);
+                }
+                mma_commit(empty_bar(s));
+                mma_commit(tfull_bar(d));
+            }
+            __syncwarp();
+        }
+    } else if (warp >= CONV0) {
+        // thread -> tile-local amplitude index tl = lane | (cw << 5) | (i << 8), i = 0..15
+        const int cw = warp - CONV0;
+        uint32_t n_base = 0, c_base = 0;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+            const int bit = b < 5 ? (lane >> b) & 1 : (cw >> (b - 5)) & 1;
+            if (bit) {
+                if (P.nbit[b] >= 0) n_base |= 1u << P.nbit[b];
+                if (P.cbit[b] >= 0) c_base |= 1u << P.cbit[b];
+            }
+        }
+        uint32_t sdst[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            uint32_t n = n_base, c = c_base;
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+                if ((i >> b) & 1) {
+                    if (P.nbit[8 + b] >= 0) n |= 1u << P.nbit[8 + b];
+                    if (P.cbit[8 + b] >= 0) c |= 1u << P.cbit[8 + b];
+                }
+            const uint32_t r8 = n & 7, ch = (c >> 1) & 7;
+            sdst[i] = (c >> 4) * L_ATOMCOL + (n >> 3) * 1024 + r8 * 128 + ((ch ^ r8) << 4) + (c & 1) * 8;
+        }
+        const int ct = cw * 32 + lane;
+        uint32_t it = 0;
+        for (uint64_t t = blockIdx.x; t < ntiles; t += G, ++it) {
+            const int r = it % L_NR;
+            wait(rfull(r), (it / L_NR) & 1);
+            const float2 *raw = reinterpret_cast<const float2 *>(smem + L_STAGES * L_STAGE + BAR_BYTES + r * L_RAW) + ct;
+            float2 v[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = raw[i * 256];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(rempty(r));
+            const int s = it % L_STAGES;
+            const uint32_t sp = (it / L_STAGES) & 1;
+            wait(empty_bar(s), sp ^ 1);
+            uint8_t *hi = smem + s * L_STAGE;
+            uint8_t *lo = hi + L_HALF;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                uint2 hh, ll;
+                hh.x = to_tf32(v[i].x);
+                hh.y = to_tf32(v[i].y);
+                ll.x = __float_as_uint(v[i].x - __uint_as_float(hh.x));
+                ll.y = __float_as_uint(v[i].y - __uint_as_float(hh.y));
+                *reinterpret_cast<uint2 *>(hi + sdst[i]) = hh;
+                *reinterpret_cast<uint2 *>(lo + sdst[i]) = ll;
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(full_bar(s));
+        }
+    } else {
+        // epilogue warps 0..3: TMEM lanes 32q.. = output reals m = 2r + e
+        const int m = warp * 32 + lane;
+        const int r = m >> 1, e = m & 1;
+        const uint64_t offr = P.off[r];
+        uint32_t it = 0;
+        for (uint64_t t = blockIdx.x; t < ntiles; t += G, ++it) {
+            const int d = it & 1;
+            const uint32_t dp = (it >> 1) & 1;
+            wait(tfull_bar(d), dp);
+            tc_fence_after();
+            uint32_t v0[32], v1[32];
+            const uint32_t D = tmem + 256 + L_NS * d + ((uint32_t)(warp * 32) << 16);
+            tmem_ld32(D, v0);
+            tmem_ld32(D + 32, v1);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty_bar(d));
+            const uint64_t base = tile_base12(t, P) + offr;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const uint32_t x0 = j < 16 ? v0[2 * j] : v1[2 * j - 32];
+                const uint32_t x1 = j < 16 ? v0[2 * j + 1] : v1[2 * j + 1 - 32];
+                const uint32_t snd = e ? x0 : x1;
+                const uint32_t rcv = __shfl_xor_sync(0xffffffffu, snd, 1);
+                float2 o;
+                o.x = __uint_as_float(e ? rcv : x0);
+                o.y = __uint_as_float(e ? x1 : rcv);
+                psi[base + P.setoff[2 * j + e]] = o;
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == MMA_WARP) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    }
+}
+
 }  // namespace tc
 
 // ------------------------------------------------------------------ host side
@@ -1164,6 +1387,27 @@ static void tc_prepare_l(const ApplyDesc &d, const double *Ucanon, std::vector<c
         }
     }
     P.ntiles = 1ull << (d.n_local - 12);
+    // bulk-copy producer: physical bits 0..6 are tile bits 0..6 (some target
+    // is below bit 7 in mode L), so a tile is 32 contiguous 1 KB blocks
+    static const char *bulk = getenv("HQ_TC_BULK");
+    static const char *lbulk = getenv("HQ_TC_LBULK");   // "0": cp.async mode L only (experiments)
+    // (measured: 0.95 vs 0.83-0.91 of peak for split placements; for a fully
+    // contiguous tile, bits 0..11, the cp.async kernel is 1% ahead)
+    if (P.pos[6] == 6 && P.pos[11] != 11 && !(bulk && bulk[0] == '0') && !(lbulk && lbulk[0] == '0')) {
+        std::vector<char> pb(sizeof(tc::ParamsLB) + 1, 0);
+        tc::ParamsLB &B = *reinterpret_cast<tc::ParamsLB *>(pb.data());
+        B.l = P;
+        for (int j = 0; j < 32; ++j) {
+            uint64_t o = 0;
+            for (int b = 7; b < 12; ++b)
+                if (((uint64_t)j << 7 >> b) & 1) o |= 1ull << P.pos[b];
+            B.boff[j] = o;
+        }
+        static const char *spin = getenv("HQ_TC_SPIN");
+        B.spin = spin && spin[0] == '1';
+        pb.back() = 'M';
+        params.swap(pb);
+    }
 }
 
 // Build the device payload (B = real embedding of U, hi and lo, [N][KD] fp32
@@ -1334,6 +1578,22 @@ static int tc_launch_bk(void *psi, const tc::ParamsB &P, const void *dev_payload
     }
 }
 
+static int tc_launch_lb(void *psi, const tc::ParamsLB &P, const void *dev_payload, cudaStream_t st) {
+    static bool attr_done = false;
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(tc::apply_tcLb, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::LB_SMEM);
+        if (e != cudaSuccess) return (int)e;
+        attr_done = true;
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint64_t grid = P.l.ntiles < (uint64_t)sms ? P.l.ntiles : (uint64_t)sms;
+    tc::apply_tcLb<<<(unsigned)grid, tc::LB_THREADS, tc::LB_SMEM, st>>>(
+        reinterpret_cast<float2 *>(psi), P, reinterpret_cast<const float *>(dev_payload));
+    return (int)cudaGetLastError();
+}
+
 static int tc_launch_l(void *psi, const tc::ParamsL &P, const void *dev_payload, cudaStream_t st) {
     static bool attr_done = false;
     if (!attr_done) {
@@ -1367,6 +1627,7 @@ int tc_launch(void *psi, const void *params, size_t params_size, const void *dev
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const char tag = reinterpret_cast<const char *>(params)[params_size - 1];
     if (tag == 'L') return tc_launch_l(psi, *reinterpret_cast<const tc::ParamsL *>(params), dev_payload, st);
+    if (tag == 'M') return tc_launch_lb(psi, *reinterpret_cast<const tc::ParamsLB *>(params), dev_payload, st);
     if (tag == 'B') {
         const tc::ParamsB &B = *reinterpret_cast<const tc::ParamsB *>(params);
         if (B.h.k == 4) return tc_launch_bk<4>(psi, B, dev_payload, st);
