@@ -16,6 +16,7 @@
 // to evict by furthest next use (Belady).  The paper's own idea is the same
 // swap applied to the least-significant qubits for AVX.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 #include <limits>
@@ -295,9 +296,21 @@ void schedule(int n, int m, const std::vector<GateRef> &g, std::vector<int> &pi,
 double layout_pass_cost(int dtype, int k, const int *bits) {
     double c = 1.0;
     if (dtype == HQ_C64 && k >= 5) {
+        // tensor-core pass, measured per pass on the sustained 34q circuit
+        // (tools/pass_times.py): mode H with <= 1 target in bits 0..3 is the
+        // baseline; 2 such targets cost 1.19x; mode L (bits 0 and 1, or >= 3
+        // targets in bits 0..3) 1.29x
         int lo = 0;
-        for (int j = 0; j < k; ++j) lo += bits[j] < 4;
-        c += lo ? 0.06 + 0.02 * lo : 0.0;
+        bool b0 = false, b1 = false;
+        for (int j = 0; j < k; ++j) {
+            lo += bits[j] < 4;
+            b0 |= bits[j] == 0;
+            b1 |= bits[j] == 1;
+        }
+        static const char *old_model = getenv("HQ_LAYOUT_V4");   // "1": the round-1 v4 model (experiments)
+        if (old_model && old_model[0] == '1') c += lo ? 0.06 + 0.02 * lo : 0.0;
+        else if ((b0 && b1) || lo >= 3) c += 0.29;
+        else if (lo == 2) c += 0.19;
     } else {
         const int lane_lo = dtype == HQ_C64 ? 1 : 0, lane_hi = lane_lo + 5;
         for (int j = 0; j < k; ++j)
