@@ -224,6 +224,8 @@ hq_status hq_reduced_dm(hq_state *s, const int32_t *qubits, int k, double *rho_o
  * i = the first index with u * sum(p) < p_0 + ... + p_i (u in [0, 1) is the
  * caller's uniform random number), then psi <- K_i psi / sqrt(p_i) (one apply
  * pass).  *chosen_out = i; probs_out (nkraus doubles, may be NULL) = p.
+ * On a multi-rank state the call is collective and every rank must pass the
+ * same u (p is all-reduced, so every rank then picks the same branch).
  * Errors: HQ_ERR_RANGE if every p_i < 1e-14 (ZeroNormBranch; state
  * unchanged), else as hq_reduced_dm.  Synchronises. */
 hq_status hq_kraus_sample(hq_state *s, const double *const *K, int nkraus, const int32_t *qubits, int k,
