@@ -307,7 +307,7 @@ def run_hq(args):
     bytes_per_launch = kt["bytes"] / max(kt["count"], 1)
     achieved = bytes_per_launch / (avg_ms * 1e-3) / 1e9
     traffic, traffic_src = traffic_from_profiles(args.config, kmax, dom, bytes_per_launch)
-    names = {"tc": "apply_tc<K> / apply_tcL (tcgen05, 3-term split products)", "simt": "apply_reg (SIMT FFMA2)",
+    names = {"tc": "apply_tcb / apply_tcL(b) (tcgen05, TMA bulk-copy producers, 3-term split products)", "simt": "apply_reg (SIMT FFMA2)",
              "generic": "apply_gen (generic SIMT)"}
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
