@@ -232,14 +232,20 @@ def run_hq(args):
     plan_ms = (time.perf_counter() - t0) * 1e3
     es = 8 if args.dtype == "c64" else 16
 
+    # PyTorch owns the device memory and the stream (plumbing); the library
+    # only borrows them: this rank's shard and, for world > 1, its receive buffer
+    nid = [None]
     if world > 1:
         nid = [hq.hq_nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(nid, src=0)
-        state = hq.hq_state_create_rank(n, args.dtype, world, rank, local, nid[0])
-    else:
-        state = hq.hq_state_create(n, args.dtype, 1)
+    m_bits = world.bit_length() - 1
+    cdt = torch.complex64 if args.dtype == "c64" else torch.complex128
+    psi_t = torch.empty(2 ** (n - m_bits), dtype=cdt, device="cuda:%d" % local)
+    buf_t = torch.empty_like(psi_t) if world > 1 else None
     stream = torch.cuda.Stream(device=local)
-    hq.hq_state_set_stream(state, stream.cuda_stream)
+    state = hq.hq_state_create_rank_from_buffers(n, args.dtype, world, rank, psi_t.data_ptr(),
+                                                 buf_t.data_ptr() if buf_t is not None else None,
+                                                 stream.cuda_stream, nid[0])
     layout = None
     if world == 1 and not args.no_layout:
         t0 = time.perf_counter()

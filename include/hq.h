@@ -128,6 +128,18 @@ hq_status hq_state_create_virtual(int n, hq_dtype dtype, int nshards, hq_state *
 hq_status hq_state_create_from_buffers(int n, hq_dtype dtype, void *psi_device,
                                        void *stream, hq_state **out);
 
+/* Borrowed-memory variant of hq_state_create_rank (PyTorch allocates the
+ * memory, the library never frees it): psi = this rank's shard of
+ * 2^(n - log2 world_size) amplitudes and, for world_size > 1, buf = a receive
+ * buffer of the same size (both device memory, 256-byte aligned, e.g.
+ * torch.empty on the rank's device); stream = a cudaStream_t or NULL.  Remaps
+ * swap the roles of psi and buf, so both must outlive the state.  Collective
+ * for world_size > 1 (ncclCommInitRank).  Errors: HQ_ERR_ARG, HQ_ERR_NGPUS,
+ * HQ_ERR_NCCL, HQ_ERR_CUDA. */
+hq_status hq_state_create_rank_from_buffers(int n, hq_dtype dtype, int world_size, int rank,
+                                            const void *nccl_id, void *psi_device, void *buf_device,
+                                            void *stream, hq_state **out);
+
 /* Qubit layout (the logical->physical bit map pi, pi[q] = physical index bit
  * of logical qubit q).  The default is pi[q] = n-1-q, i.e. physical index ==
  * logical index.  A layout is a permutation of [0, n); it changes only where

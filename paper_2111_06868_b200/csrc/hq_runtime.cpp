@@ -132,6 +132,7 @@ struct hq_circuit {
     std::vector<std::vector<long long>> cuoff;
     std::vector<double> cgnorm;            // spectral bound of the whole U
     std::vector<char *> dev_U;             // per shard: all payloads
+    std::vector<int> dev_of;               // per shard: its device (destroy must not read the state)
     uint64_t passes = 0, remaps = 0, permutes = 0;
     // CUDA graph of the whole op stream (single-shard states, profiling off):
     // captured on the first run, replayed while the capture key matches.
@@ -208,7 +209,9 @@ static hq_status shard_alloc(hq_state *st, Shard &s, bool need_buf, bool make_st
 
 static void shard_free(Shard &s) {
     cudaSetDevice(s.device);
-    if (s.stream) cudaStreamSynchronize(s.stream);
+    // a borrowed stream may already be destroyed by its owner: only our own
+    // stream is synchronised here (cudaFree below synchronises the device)
+    if (s.own_stream && s.stream) cudaStreamSynchronize(s.stream);
     if (s.own_psi && s.psi) cudaFree(s.psi);
     if (s.own_buf && s.buf) cudaFree(s.buf);
     if (s.d_part) cudaFree(s.d_part);
@@ -220,6 +223,7 @@ static void shard_free(Shard &s) {
     if (s.comm) ncclCommDestroy(s.comm);
     if (s.own_stream && s.stream) cudaStreamDestroy(s.stream);
     s = Shard{};
+    cudaGetLastError();        // teardown errors must not surface in a later launch check
 }
 
 static hq_status check_device() {
@@ -338,6 +342,62 @@ extern "C" hq_status hq_state_create_rank(int n, hq_dtype dtype, int world_size,
         ncclResult_t nr = ncclCommInitRank(&st->sh[0].comm, world_size, id, rank);
         if (nr != ncclSuccess) {
             shard_free(st->sh[0]);
+            delete st;
+            return set_error(HQ_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(nr));
+        }
+    }
+    *out = st;
+    return HQ_OK;
+}
+
+extern "C" hq_status hq_state_create_rank_from_buffers(int n, hq_dtype dtype, int world_size, int rank,
+                                                       const void *nccl_id, void *psi_device, void *buf_device,
+                                                       void *stream, hq_state **out) {
+    clear_error();
+    if (!out || !psi_device) return set_error(HQ_ERR_ARG, "NULL argument");
+    *out = nullptr;
+    hq_status rc = validate_common(n, dtype, world_size);
+    if (rc) return rc;
+    if (rank < 0 || rank >= world_size) return set_error(HQ_ERR_ARG, "rank %d not in [0,%d)", rank, world_size);
+    if (world_size > 1 && (!nccl_id || !buf_device))
+        return set_error(HQ_ERR_ARG, "world_size > 1 needs nccl_id and a receive buffer");
+    if ((rc = check_device())) return rc;
+    for (void *p : {psi_device, buf_device}) {
+        if (!p) continue;
+        if (((uintptr_t)p) & 255) return set_error(HQ_ERR_ARG, "buffer not 256-byte aligned");
+        cudaPointerAttributes at;
+        CUDA_TRY(cudaPointerGetAttributes(&at, p));
+        if (at.type != cudaMemoryTypeDevice) return set_error(HQ_ERR_ARG, "buffer is not device memory");
+    }
+    cudaPointerAttributes at;
+    CUDA_TRY(cudaPointerGetAttributes(&at, psi_device));
+    hq_state *st = new_state(n, dtype, world_size);
+    if (!st) return set_error(HQ_ERR_OOM, "host allocation failed");
+    st->mode = world_size == 1 ? MODE_SINGLE : MODE_RANK;
+    st->sh.resize(1);
+    Shard &sh = st->sh[0];
+    sh.device = at.device;
+    sh.rank = rank;
+    sh.psi = psi_device;
+    sh.own_psi = false;
+    if (world_size > 1) {
+        sh.buf = buf_device;
+        sh.own_buf = false;
+    }
+    sh.stream = reinterpret_cast<cudaStream_t>(stream);
+    sh.own_stream = false;
+    if ((rc = shard_alloc(st, sh, false, false))) {
+        shard_free(sh);
+        delete st;
+        return rc;
+    }
+    if (world_size > 1) {
+        ncclUniqueId id;
+        memcpy(&id, nccl_id, sizeof id);
+        cudaSetDevice(sh.device);
+        ncclResult_t nr = ncclCommInitRank(&sh.comm, world_size, id, rank);
+        if (nr != ncclSuccess) {
+            shard_free(sh);
             delete st;
             return set_error(HQ_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(nr));
         }
@@ -901,8 +961,14 @@ static hq_status circuit_compile(hq_state *st, hq_circuit *c, const std::vector<
             c->permutes++;
         }
     }
-    for (char *p : c->dev_U) if (p) cudaFree(p);
+    for (size_t r = 0; r < c->dev_U.size(); ++r)
+        if (c->dev_U[r]) {
+            cudaSetDevice(c->dev_of[r]);
+            cudaFree(c->dev_U[r]);
+        }
     c->dev_U.assign(st->sh.size(), nullptr);
+    c->dev_of.resize(st->sh.size());
+    for (size_t r = 0; r < st->sh.size(); ++r) c->dev_of[r] = st->sh[r].device;
     if (total == 0) return HQ_OK;
     std::vector<char> blob(total, 0);
     for (size_t i = 0; i < c->ops.size(); ++i) {
@@ -1048,12 +1114,15 @@ extern "C" hq_status hq_circuit_info(const hq_circuit *c, uint64_t *passes, uint
 extern "C" hq_status hq_circuit_destroy(hq_circuit *c) {
     if (!c) return HQ_OK;
     if (c->graph) cudaGraphExecDestroy(c->graph);
+    // the owning state may already be gone (destroy order is the caller's):
+    // use the devices recorded at compile time, never c->owner
     for (size_t r = 0; r < c->dev_U.size(); ++r)
         if (c->dev_U[r]) {
-            if (c->owner && r < c->owner->sh.size()) cudaSetDevice(c->owner->sh[r].device);
+            cudaSetDevice(c->dev_of[r]);
             cudaFree(c->dev_U[r]);
         }
     delete c;
+    cudaGetLastError();
     return HQ_OK;
 }
 

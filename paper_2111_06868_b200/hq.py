@@ -64,6 +64,8 @@ def lib():
                                      ctypes.c_int, P, ctypes.POINTER(P)],
             "hq_state_create_virtual": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(P)],
             "hq_state_create_from_buffers": [ctypes.c_int, ctypes.c_int, P, P, ctypes.POINTER(P)],
+            "hq_state_create_rank_from_buffers": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P, P, P,
+                                                  ctypes.POINTER(P)],
             "hq_nccl_unique_id": [P],
             "hq_state_destroy": [P],
             "hq_state_set_stream": [P, P],
@@ -207,6 +209,21 @@ def hq_state_create_from_buffers(n, dtype, psi_device_ptr, stream_ptr=None):
     out = P()
     _check(lib().hq_state_create_from_buffers(int(n), d, P(psi_device_ptr), P(stream_ptr or 0),
                                               ctypes.byref(out)))
+    return State(out, n, d)
+
+
+def hq_state_create_rank_from_buffers(n, dtype, world_size, rank, psi_device_ptr, buf_device_ptr=None,
+                                      stream_ptr=None, nccl_id=None):
+    """One rank's state on caller-owned device buffers (e.g. torch.empty):
+    psi (and buf, the receive buffer, when world_size > 1) must outlive it."""
+    d = _dt(dtype)
+    out = P()
+    idbuf = None
+    if nccl_id is not None:
+        idbuf = (ctypes.c_char * 128).from_buffer_copy(nccl_id)
+    _check(lib().hq_state_create_rank_from_buffers(int(n), d, int(world_size), int(rank), idbuf,
+                                                   P(psi_device_ptr), P(buf_device_ptr or 0),
+                                                   P(stream_ptr or 0), ctypes.byref(out)))
     return State(out, n, d)
 
 

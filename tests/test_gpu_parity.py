@@ -366,3 +366,32 @@ def test_circuit_graph_replay(dtype):
     t = hq.hq_kernel_times(s)
     assert t["count"] == len(gates)
     assert _err(hq.hq_get_amplitudes(s), want) <= TOL[dtype]
+
+
+# ---------------------------------------------------------------- torch-owned memory
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_rank_state_on_torch_buffers(dtype):
+    """hq_state_create_rank_from_buffers (the bench's constructor): PyTorch owns
+    the shard and the stream; results match the oracle and the amplitudes are
+    visible through the torch tensor."""
+    import torch
+    n = 18
+    gates = hq.hq_fuse(sycamore_circuit(n, 8, 21), 6)
+    want = O.simulate(n, [Gate("F", q, U) for q, U in gates])
+    cdt = torch.complex64 if dtype == "c64" else torch.complex128
+    psi_t = torch.empty(2 ** n, dtype=cdt, device="cuda")
+    stream = torch.cuda.Stream()
+    s = hq.hq_state_create_rank_from_buffers(n, dtype, 1, 0, psi_t.data_ptr(), None, stream.cuda_stream)
+    hq.hq_state_init_basis(s, 0)
+    c = hq.hq_circuit_create(s, gates)
+    hq.hq_circuit_run(s, c)
+    hq.hq_sync(s)
+    got = psi_t.cpu().numpy().astype(np.complex128)      # default layout: physical = logical
+    assert np.linalg.norm(got - want) < (1e-4 if dtype == "c64" else 1e-10)
+    with pytest.raises(hq.HQError) as e:
+        hq.hq_state_create_rank_from_buffers(n, dtype, 1, 0, psi_t.data_ptr() + 8, None, None)
+    assert e.value.status == "HQ_ERR_ARG"
+    with pytest.raises(hq.HQError) as e:                # world 2 needs a receive buffer and an id
+        hq.hq_state_create_rank_from_buffers(n, dtype, 2, 0, psi_t.data_ptr(), None, None)
+    assert e.value.status == "HQ_ERR_ARG"
