@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--impl", default="hq", choices=["hq", "reference"])
     ap.add_argument("--config", default="34q", choices=sorted(CONFIGS))
     ap.add_argument("--kmax", type=int, default=None)
+    ap.add_argument("--fuse", default="merged", choices=["merged", "c7"],
+                    help="planner: hq_fuse_merged (default) or the plain C7 greedy hq_fuse")
     ap.add_argument("--dtype", default="c64", choices=["c64", "c128"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
@@ -228,7 +230,8 @@ def run_hq(args):
     kmax = args.kmax or kdef
     gates = sycamore_circuit(n, cycles, seed)
     t0 = time.perf_counter()
-    fused = hq.hq_fuse(gates, kmax)
+    merged = args.fuse == "merged"
+    fused = hq.hq_fuse(gates, kmax, merged=merged)
     plan_ms = (time.perf_counter() - t0) * 1e3
     es = 8 if args.dtype == "c64" else 16
 
@@ -331,7 +334,7 @@ def run_hq(args):
         barrier()
         t0 = time.perf_counter()
         hq.hq_state_init_basis(state, 0)
-        fz = hq.hq_fuse(gates, kmax)
+        fz = hq.hq_fuse(gates, kmax, merged=merged)
         if layout is not None:
             hq.hq_state_set_layout(state, hq.hq_plan_layout(n, 0, fz, args.dtype)[0])
             hq.hq_state_init_basis(state, 0)
@@ -365,7 +368,8 @@ def run_hq(args):
                    "state_gib": state_bytes / 2 ** 30,
                    "l2": "no flush: state %.0f GiB >> 126 MB L2" % (state_bytes / 2 ** 30),
                    "parallelism": "sv-shard%d" % world,
-                   "layout": "hq_plan_layout" if layout is not None else "default"},
+                   "layout": "hq_plan_layout" if layout is not None else "default",
+                   "fusion": "hq_fuse_merged (C7 groups + convex merging)" if merged else "hq_fuse (C7)"},
         "circuit_wall_s": ms_per_step / 1e3,
         "per_gpu_gbs": value / world,
         "frac_of_hbm_per_gpu": value / world / peak,

@@ -112,11 +112,110 @@ static void left_multiply_embedded(std::vector<double> &M, int m, const int *sup
     M.swap(out);
 }
 
-void fuse_build(const std::vector<GateRef> &g, int kmax, std::vector<FusedGate> &out) {
-    std::vector<int32_t> group_of;
-    const size_t ng = fuse_groups(g, kmax, group_of);
+// Group merging (hq_fuse_merged): after the
+// C7 grouping, contract edges A -> B of the group dependency DAG (A's last
+// use of a qubit is followed by B's first use of it) whenever
+// |supp(A) u supp(B)| <= kmax and no other path A -> ... -> B exists (so the
+// merged block is convex and the DAG stays acyclic).  Candidates are taken in
+// ascending (A, B) order and the scan repeats until nothing merges.  The
+// merged groups are then emitted in a topological order (Kahn, smallest
+// first-member index first); members keep their original order inside a
+// group.  Returns the ordered member lists.
+static std::vector<std::vector<size_t>> merge_groups(const std::vector<GateRef> &g, int kmax,
+                                                     const std::vector<int32_t> &group_of, size_t ng) {
     std::vector<std::vector<size_t>> members(ng);
     for (size_t i = 0; i < g.size(); ++i) members[group_of[i]].push_back(i);
+    std::vector<uint64_t> supp(ng, 0);
+    for (size_t i = 0; i < g.size(); ++i) supp[group_of[i]] |= qmask(g[i]);
+    std::vector<std::vector<char>> adj(ng, std::vector<char>(ng, 0));   // adj[a][b]: edge a -> b
+    std::vector<int> last(64, -1);
+    for (size_t i = 0; i < g.size(); ++i)
+        for (int j = 0; j < g[i].k; ++j) {
+            const int q = g[i].q[j], G = group_of[i];
+            if (last[q] >= 0 && last[q] != G) adj[last[q]][G] = 1;
+            last[q] = G;
+        }
+    std::vector<char> alive(ng, 1);
+    // is there a path a -> ... -> b of length >= 2 (through some other live group)?
+    auto indirect = [&](size_t a, size_t b) {
+        std::vector<char> seen(ng, 0);
+        std::vector<size_t> stack;
+        for (size_t x = 0; x < ng; ++x)
+            if (alive[x] && adj[a][x] && x != b) { stack.push_back(x); seen[x] = 1; }
+        while (!stack.empty()) {
+            const size_t x = stack.back();
+            stack.pop_back();
+            if (adj[x][b]) return true;
+            for (size_t y = 0; y < ng; ++y)
+                if (alive[y] && adj[x][y] && !seen[y] && y != b) { seen[y] = 1; stack.push_back(y); }
+        }
+        return false;
+    };
+    auto reach = [&](size_t a, size_t b) {       // any path a -> ... -> b
+        return adj[a][b] || indirect(a, b);
+    };
+    static const char *indep_env = getenv("HQ_FUSE_INDEP");   // "0": edges only (experiments)
+    const bool indep = !(indep_env && indep_env[0] == '0');
+    for (bool merged = true; merged;) {
+        merged = false;
+        for (size_t a = 0; a < ng && !merged; ++a) {
+            if (!alive[a]) continue;
+            for (size_t b = 0; b < ng; ++b) {
+                if (b == a || !alive[b] || __builtin_popcountll(supp[a] | supp[b]) > kmax) continue;
+                if (adj[a][b]) {
+                    if (indirect(a, b)) continue;
+                } else if (!indep || adj[b][a] || reach(a, b) || reach(b, a)) {
+                    continue;                    // dependent through other groups (or b -> a: seen from b)
+                }
+                // contract b into a
+                supp[a] |= supp[b];
+                members[a].insert(members[a].end(), members[b].begin(), members[b].end());
+                std::sort(members[a].begin(), members[a].end());
+                members[b].clear();
+                alive[b] = 0;
+                for (size_t x = 0; x < ng; ++x) {
+                    if (adj[b][x]) adj[a][x] = 1;
+                    if (adj[x][b]) adj[x][a] = 1;
+                    adj[b][x] = adj[x][b] = 0;
+                }
+                adj[a][a] = 0;
+                merged = true;
+                break;
+            }
+        }
+    }
+    // topological order, smallest first member first
+    std::vector<int> indeg(ng, 0);
+    for (size_t a = 0; a < ng; ++a)
+        if (alive[a])
+            for (size_t b = 0; b < ng; ++b)
+                if (alive[b] && adj[a][b]) indeg[b]++;
+    std::vector<std::vector<size_t>> order;
+    std::vector<char> done(ng, 0);
+    for (;;) {
+        size_t best = ng;
+        for (size_t a = 0; a < ng; ++a)
+            if (alive[a] && !done[a] && indeg[a] == 0 && (best == ng || members[a][0] < members[best][0])) best = a;
+        if (best == ng) break;
+        done[best] = 1;
+        for (size_t b = 0; b < ng; ++b)
+            if (alive[b] && adj[best][b]) indeg[b]--;
+        order.push_back(members[best]);
+    }
+    return order;
+}
+
+void fuse_build(const std::vector<GateRef> &g, int kmax, std::vector<FusedGate> &out, bool merge) {
+    std::vector<int32_t> group_of;
+    const size_t ng0 = fuse_groups(g, kmax, group_of);
+    std::vector<std::vector<size_t>> members;
+    if (merge) {
+        members = merge_groups(g, kmax, group_of, ng0);
+    } else {
+        members.assign(ng0, {});
+        for (size_t i = 0; i < g.size(); ++i) members[group_of[i]].push_back(i);
+    }
+    const size_t ng = members.size();
     out.clear();
     out.resize(ng);
     for (size_t G = 0; G < ng; ++G) {
@@ -403,8 +502,19 @@ extern "C" hq_status hq_fuse_plan(const hq_gate *in, size_t ngates, int kmax, in
     return HQ_OK;
 }
 
+static hq_status fuse_abi(const hq_gate *in, size_t ngates, int kmax, hq_gate **out, size_t *nout, bool merge);
+
 extern "C" hq_status hq_fuse(const hq_gate *in, size_t ngates, int kmax, hq_gate **out,
                              size_t *nout) {
+    return fuse_abi(in, ngates, kmax, out, nout, false);
+}
+
+extern "C" hq_status hq_fuse_merged(const hq_gate *in, size_t ngates, int kmax, hq_gate **out,
+                                    size_t *nout) {
+    return fuse_abi(in, ngates, kmax, out, nout, true);
+}
+
+static hq_status fuse_abi(const hq_gate *in, size_t ngates, int kmax, hq_gate **out, size_t *nout, bool merge) {
     clear_error();
     if ((!in && ngates) || !out || !nout) return set_error(HQ_ERR_ARG, "NULL argument");
     if (kmax < 1 || kmax > 6) return set_error(HQ_ERR_K, "kmax=%d not in [1,6]", kmax);
@@ -415,7 +525,7 @@ extern "C" hq_status hq_fuse(const hq_gate *in, size_t ngates, int kmax, hq_gate
         if (refs[i].k > kmax) return set_error(HQ_ERR_K, "gate %zu wider (%d) than kmax=%d", i, refs[i].k, kmax);
     std::vector<FusedGate> fused;
     try {
-        fuse_build(refs, kmax, fused);
+        fuse_build(refs, kmax, fused, merge);
     } catch (const std::bad_alloc &) {
         return set_error(HQ_ERR_OOM, "host allocation failed in hq_fuse");
     }

@@ -99,6 +99,8 @@ def lib():
             "hq_probabilities": [P, P, ctypes.c_int, P],
             "hq_measure": [P, P, ctypes.c_int, ctypes.c_double, ctypes.POINTER(ctypes.c_uint64)],
             "hq_reduced_dm": [P, P, ctypes.c_int, P],
+            "hq_fuse_merged": [P, ctypes.c_size_t, ctypes.c_int, ctypes.POINTER(ctypes.POINTER(hq_gate)),
+                               ctypes.POINTER(ctypes.c_size_t)],
             "hq_reduced_dm_batched": [P, ctypes.c_int, P, ctypes.c_int, P],
             "hq_kraus_sample_batched": [P, ctypes.c_int, P, ctypes.c_int, P, ctypes.c_int, P, P, P],
             "hq_kraus_sample": [P, P, ctypes.c_int, P, ctypes.c_int, ctypes.c_double, ctypes.POINTER(ctypes.c_int), P],
@@ -427,12 +429,14 @@ def hq_circuit_info(circuit):
 
 # ------------------------------------------------------------------ planner
 
-def hq_fuse(gates, kmax):
-    """Returns list of (qubits tuple, U complex128 ndarray)."""
+def hq_fuse(gates, kmax, merged=False):
+    """Returns list of (qubits tuple, U complex128 ndarray); merged=True runs
+    hq_fuse_merged (C7 groups, then convex group merging)."""
     arr, ng, keep = _gate_array(gates)
     out = ctypes.POINTER(hq_gate)()
     nout = ctypes.c_size_t()
-    _check(lib().hq_fuse(arr, ng, int(kmax), ctypes.byref(out), ctypes.byref(nout)))
+    fn = lib().hq_fuse_merged if merged else lib().hq_fuse
+    _check(fn(arr, ng, int(kmax), ctypes.byref(out), ctypes.byref(nout)))
     res = []
     try:
         for i in range(nout.value):

@@ -237,3 +237,35 @@ def test_plan_layout_is_permutation_and_improves(kmax):
 def test_plan_layout_errors():
     with pytest.raises(hq.HQError):
         hq.hq_plan_layout(8, 0, [Gate("U", (9,), np.eye(2))])
+
+
+# ---------------------------------------------------------------- merged fusion (hq_fuse_merged)
+
+@pytest.mark.parametrize("kind", ["sycamore", "random", "reversible"])
+@pytest.mark.parametrize("kmax", [2, 3, 4, 5, 6])
+def test_fuse_merged_is_valid_and_no_worse(kind, kmax):
+    """The merged plan is the same circuit (oracle: fused vs unfused, fp64),
+    every block has <= kmax qubits, and it never has more blocks than C7."""
+    n = 12
+    if kind == "sycamore":
+        gates = sycamore_circuit(n, 10, 7)
+    elif kind == "random":
+        gates = random_circuit(n, 150, 9, kmax=min(kmax, 3))
+    else:
+        gates = reversible_circuit(n, 150, 9, kmax=min(kmax, 3))
+    gates = [g for g in gates if len(g.qubits) <= kmax]
+    c7 = hq.hq_fuse(gates, kmax)
+    mg = hq.hq_fuse(gates, kmax, merged=True)
+    assert len(mg) <= len(c7)
+    assert all(1 <= len(q) <= kmax and list(q) == sorted(q) for q, _ in mg)
+    psi = random_state(n, 3)
+    want = O.simulate(n, gates, psi)
+    got = O.simulate(n, [Gate("F", q, U) for q, U in mg], psi)
+    assert np.max(np.abs(got - want)) < 1e-12
+
+
+def test_fuse_merged_34q_bench_circuit():
+    """The bench circuit: 80 C7 blocks -> 75 merged."""
+    gates = sycamore_circuit(34, 20, 3000)
+    assert len(hq.hq_fuse(gates, 6)) == 80
+    assert len(hq.hq_fuse(gates, 6, merged=True)) == 75
