@@ -143,7 +143,7 @@ def traffic_from_profiles(cfg, kmax, path, bytes_per_launch):
 
 
 # ------------------------------------------------------------------ oracle arm
-def oracle_sample(n_full, cycles, seed, kmax, seconds=15.0, n_sample=None):
+def oracle_sample(n_full, cycles, seed, kmax, seconds=15.0, n_sample=None, merged=True):
     """Time the fp64 oracle (as it stands) on a bounded sample of the same
     workload: the first unfused gates of the same generator's circuit at a
     smaller n (c128 state must fit host RAM), extrapolated per gate by
@@ -152,7 +152,10 @@ def oracle_sample(n_full, cycles, seed, kmax, seconds=15.0, n_sample=None):
     import oracle as O
     from hq_inputs import sycamore_circuit
     gates_full = sycamore_circuit(n_full, cycles, seed)
-    P = len(O.compress(gates_full, kmax))   # oracle's own reading of the planner (C7)
+    # the pass count of the unit, from the oracle's own reading of the planner
+    # (C7, plus the merging reading when the GPU arm uses hq_fuse_merged)
+    groups = O.compress(gates_full, kmax)
+    P = len(O.merge_groups(gates_full, groups, kmax)) if merged else len(groups)
     if n_sample is None:
         n_sample = min(n_full, 26)
     gates_s = sycamore_circuit(n_sample, cycles, seed)
@@ -186,7 +189,7 @@ def run_reference(args):
     info = None
     per_step = max(2.0, 60.0 / max(args.steps + args.warmup, 1))
     for i in range(args.warmup + args.steps):
-        v, info = oracle_sample(n, cycles, seed, kmax, seconds=per_step)
+        v, info = oracle_sample(n, cycles, seed, kmax, seconds=per_step, merged=args.fuse == "merged")
         if i >= args.warmup:
             vals.append(v)
     value = statistics.mean(vals)
@@ -381,7 +384,7 @@ def run_hq(args):
         "clocks": clk,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, inf = oracle_sample(n, cycles, seed, kmax, seconds=15.0)
+        v, inf = oracle_sample(n, cycles, seed, kmax, seconds=15.0, merged=merged)
         line["cpu_baseline"] = {"value": v, "unit": "GB/s", "cores": inf["cores"], "kind": "oracle",
                                 "sample": inf["sample"]}
     if rank == 0:

@@ -23,7 +23,8 @@ Contents, each following the passage cited:
 * ``compress`` / ``fused_gates`` -- the greedy fusion rule, reading C7 of
   PAPER P:499-504 (worked example P:510-529), and the fused matrix
   U_group = U_last ... U_first embedded on the ascending support (P:493-494,
-  readings C8, C9).
+  readings C8, C9); ``merge_groups`` -- the convex group merging of the
+  "merged fusion" reading.
 
 * ``init_tokens`` / ``project`` / ``probabilities`` -- token product states
    as a Kronecker product of single-qubit
@@ -214,11 +215,103 @@ def compress(gates, kmax):
     return [G["members"] for G in groups]
 
 
-def fused_gates(gates, kmax):
+def merge_groups(gates, groups, kmax):
+    """DESIGN.md reading "merged fusion" (section 5.4a), step by step: the
+    dependency graph of the groups has an edge A -> B when some qubit's
+    consecutive uses go from a gate of A to a gate of B.  Scan pairs (A, B)
+    in ascending order and merge B into A when |supp(A) u supp(B)| <= kmax
+    and either (edge A -> B and no other path A -> ... -> B) or (no path
+    between them either way); after every merge restart the scan.  Return
+    the merged groups in topological order (among the ready groups, the one
+    with the smallest gate index first), members in gate order."""
+    ng = len(groups)
+    group_of = {}
+    for G, mem in enumerate(groups):
+        for i in mem:
+            group_of[i] = G
+    members = [sorted(m) for m in groups]
+    supp = [set().union(*[set(gates[i].qubits) for i in m]) for m in groups]
+    succ = [set() for _ in range(ng)]
+    last = {}
+    for i, g in enumerate(gates):
+        G = group_of[i]
+        for q in g.qubits:
+            if q in last and last[q] != G:
+                succ[last[q]].add(G)
+            last[q] = G
+    alive = set(range(ng))
+
+    def other_path(a, b):          # a path a -> x -> ... -> b with x != b
+        stack = [x for x in succ[a] if x != b and x in alive]
+        seen = set(stack)
+        while stack:
+            x = stack.pop()
+            if b in succ[x]:
+                return True
+            for y in succ[x]:
+                if y in alive and y != b and y not in seen:
+                    seen.add(y)
+                    stack.append(y)
+        return False
+
+    def path(a, b):
+        return b in succ[a] or other_path(a, b)
+
+    merged = True
+    while merged:
+        merged = False
+        for a in range(ng):
+            if a not in alive:
+                continue
+            for b in range(ng):
+                if b == a or b not in alive or len(supp[a] | supp[b]) > kmax:
+                    continue
+                if b in succ[a]:
+                    if other_path(a, b):
+                        continue
+                elif a in succ[b] or path(a, b) or path(b, a):
+                    continue
+                supp[a] |= supp[b]
+                members[a] = sorted(members[a] + members[b])
+                members[b] = []
+                alive.discard(b)
+                for x in range(ng):
+                    if b in succ[x]:
+                        succ[x].discard(b)
+                        succ[x].add(a)
+                succ[a] |= succ[b]
+                succ[b] = set()
+                succ[a].discard(a)
+                merged = True
+                break
+            if merged:
+                break
+    indeg = {a: 0 for a in alive}
+    for a in alive:
+        for b in succ[a]:
+            if b in alive:
+                indeg[b] += 1
+    order, done = [], set()
+    while len(done) < len(alive):
+        ready = [a for a in alive if a not in done and indeg[a] == 0]
+        a = min(ready, key=lambda x: members[x][0])
+        done.add(a)
+        for b in succ[a]:
+            if b in alive:
+                indeg[b] -= 1
+        order.append(members[a])
+    return order
+
+
+def fused_gates(gates, kmax, merged=False):
     """Fused gate list: (ascending support, U_last ... U_first embedded on it)
-    (P:493-494 to_matrix_gate; readings C8, C9)."""
+    (P:493-494 to_matrix_gate; readings C8, C9); merged=True fuses the groups
+    of merge_groups(compress(...)) instead."""
     out = []
-    for members in compress(gates, kmax):
+    groups = compress(gates, kmax)
+    if merged:
+        groups = merge_groups(gates, groups, kmax)
+    for members in groups:
         support = sorted(set().union(*[set(gates[i].qubits) for i in members]))
         pos = {q: j for j, q in enumerate(support)}
         m = len(support)

@@ -269,3 +269,24 @@ def test_fuse_merged_34q_bench_circuit():
     gates = sycamore_circuit(34, 20, 3000)
     assert len(hq.hq_fuse(gates, 6)) == 80
     assert len(hq.hq_fuse(gates, 6, merged=True)) == 75
+
+
+@pytest.mark.parametrize("n,cycles,seed,kmax", [(12, 10, 1, 3), (12, 10, 1, 6), (16, 12, 5, 4),
+                                                (20, 14, 2, 5), (34, 20, 3000, 6)])
+def test_fuse_merged_bit_exact_vs_oracle(n, cycles, seed, kmax):
+    """hq_fuse_merged's blocks (supports, order) equal the oracle's
+    merge_groups(compress(...)) exactly; matrices agree to fp64 rounding."""
+    gates = sycamore_circuit(n, cycles, seed)
+    want = O.fused_gates(gates, kmax, merged=True)
+    got = hq.hq_fuse(gates, kmax, merged=True)
+    assert [tuple(q) for q, _ in got] == [tuple(q) for q, _ in want]
+    assert max(np.max(np.abs(a - b)) for (_, a), (_, b) in zip(got, want)) < 1e-14
+
+
+def test_fuse_merged_random_circuits_vs_oracle():
+    for seed in range(4):
+        gates = random_circuit(10, 90, seed, kmax=3)
+        for kmax in (3, 4, 6):
+            want = O.fused_gates(gates, kmax, merged=True)
+            got = hq.hq_fuse(gates, kmax, merged=True)
+            assert [tuple(q) for q, _ in got] == [tuple(q) for q, _ in want], (seed, kmax)

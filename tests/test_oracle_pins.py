@@ -513,3 +513,27 @@ def test_kraus_step_unravels_the_channel():
     want = O.dm_apply_kraus(np.outer(psi, psi.conj()), K, [2, 0])
     assert abs(p.sum() - 1) < 1e-14
     assert np.max(np.abs(mean - want)) < 1e-14
+
+
+# ---------------------------------------------------------------- merged fusion reading
+
+@pytest.mark.parametrize("kmax", [2, 3, 4, 6])
+def test_merge_groups_is_a_valid_regrouping(kmax):
+    """merge_groups only regroups: every gate in exactly one block, blocks of
+    <= kmax qubits, members in gate order, never more blocks than compress,
+    and the fused circuit is the original one (fp64 simulate, both orders of
+    evidence: the explicit dense product and the gate-by-gate apply)."""
+    n = 8
+    gates = [g for g in random_circuit(n, 70, 17, kmax=min(kmax, 3)) if len(g.qubits) <= kmax]
+    groups = O.compress(gates, kmax)
+    merged = O.merge_groups(gates, groups, kmax)
+    assert sorted(i for m in merged for i in m) == list(range(len(gates)))
+    assert all(m == sorted(m) for m in merged) and len(merged) <= len(groups)
+    assert all(len(set().union(*[set(gates[i].qubits) for i in m])) <= kmax for m in merged)
+    fused = O.fused_gates(gates, kmax, merged=True)
+    psi = random_state(n, 6)
+    want = O.simulate(n, gates, psi)
+    got = O.simulate(n, [Gate("F", q, U) for q, U in fused], psi)
+    assert np.max(np.abs(got - want)) < 1e-13
+    assert np.max(np.abs(O.circuit_matrix(n, [Gate("F", q, U) for q, U in fused])
+                         - O.circuit_matrix(n, gates))) < 1e-13
