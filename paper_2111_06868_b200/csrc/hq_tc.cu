@@ -521,6 +521,7 @@ struct ParamsB {
     int ns;                // ring depth (template parameter NS)
     int np;                // producer warps (template parameter NP)
     int spin;              // 1: spin-wait instead of try_wait with a suspend hint
+    int l2hint;            // bit 0: evict-first bulk loads, bit 1: streaming stores (experiments)
 };
 
 __device__ __forceinline__ void mbar_arrive_tx(uint32_t bar, uint32_t bytes) {
@@ -531,6 +532,23 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t
     asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                  "l"(src), "r"(bytes), "r"(bar)
                  : "memory");
+}
+
+// cp.async.bulk with an L2 cache policy (createpolicy ... evict_first):
+// the state is streamed once per pass, so its lines need not stay in L2
+__device__ __forceinline__ void bulk_g2s_ef(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar,
+                                            uint64_t pol) {
+    asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void st_cs_f2(void *p, float2 v) {     // streaming store (evict-first)
+    asm volatile("st.global.cs.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v.x), "f"(v.y) : "memory");
 }
 
 __device__ __forceinline__ uint64_t f2_as_u64(float2 v) {
@@ -625,6 +643,7 @@ apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
         constexpr int NPH = NP == 1 ? 1 : NP / 2;
         constexpr int NB = C::NBLK / NPH;
         const int sub = NP == 1 ? 0 : p / 2;
+        const uint64_t pol = policy_evict_first();
         uint32_t it = 0;
         for (uint64_t t = blockIdx.x; t < ntiles; t += G, ++it) {
             const float2 *tb = psi + tile_base<NPOS>(t, P.h);
@@ -637,7 +656,11 @@ apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
                 __syncwarp();
                 if (lane < NB) {
                     const int j = sub * NB + lane;
-                    bulk_g2s(sbase + C::RING + s * C::SLOT_BYTES + j * 1024, tb + P.boff[h][j], 1024, rfull(s));
+                    if (P.l2hint & 1)
+                        bulk_g2s_ef(sbase + C::RING + s * C::SLOT_BYTES + j * 1024, tb + P.boff[h][j], 1024,
+                                    rfull(s), pol);
+                    else
+                        bulk_g2s(sbase + C::RING + s * C::SLOT_BYTES + j * 1024, tb + P.boff[h][j], 1024, rfull(s));
                 }
             }
         }
@@ -769,7 +792,9 @@ apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
                     const uint64_t x = (uint64_t)v[2 * i] | ((uint64_t)v[2 * i + 1] << 32);
-                    *reinterpret_cast<float2 *>(pb + P.off8[16 * ch + i]) = u64_as_f2(mul_f32x2(mul_f32x2(x, f1), f2));
+                    const float2 o = u64_as_f2(mul_f32x2(mul_f32x2(x, f1), f2));
+                    if (P.l2hint & 2) st_cs_f2(pb + P.off8[16 * ch + i], o);
+                    else *reinterpret_cast<float2 *>(pb + P.off8[16 * ch + i]) = o;
                 }
             }
         }
@@ -1055,6 +1080,7 @@ struct ParamsLB {
     ParamsL l;
     uint64_t boff[32];     // amplitude offset of 1 KB block j of a tile (tile bits >= 7 of j << 7)
     int spin;
+    int l2hint;            // unused in mode L
 };
 
 __global__ void __launch_bounds__(LB_THREADS, 1)
@@ -1405,6 +1431,8 @@ static void tc_prepare_l(const ApplyDesc &d, const double *Ucanon, std::vector<c
         }
         static const char *spin = getenv("HQ_TC_SPIN");
         B.spin = spin && spin[0] == '1';
+        static const char *l2 = getenv("HQ_TC_L2HINT");
+        B.l2hint = l2 ? atoi(l2) : 0;
         pb.back() = 'M';
         params.swap(pb);
     }
@@ -1519,6 +1547,10 @@ void tc_prepare(const ApplyDesc &d, const double *Ucanon, std::vector<char> &pay
         B.np = np;
         static const char *spin = getenv("HQ_TC_SPIN");
         B.spin = spin && spin[0] == '1';
+        // default: streaming (evict-first) epilogue stores, 1.2% on the sustained
+        // 34q circuit (tools/pass_times.py, same box); evict-first bulk loads: no gain
+        static const char *l2 = getenv("HQ_TC_L2HINT");
+        B.l2hint = l2 ? atoi(l2) : 2;
         pb.back() = 'B';
         params.swap(pb);
     }
