@@ -227,7 +227,48 @@ void fuse_build(const std::vector<GateRef> &g, int kmax, std::vector<FusedGate> 
         const int D = 1 << f.k;
         f.U.assign((size_t)2 * D * D, 0.0);
         for (int i = 0; i < D; ++i) f.U[(size_t)2 * (i * D + i)] = 1.0;
-        for (size_t i : members[G]) left_multiply_embedded(f.U, f.k, f.q, g[i]);
+        // Consecutive members whose joint support stays <= 3 qubits are first
+        // multiplied together in that small space (8 x 8 at most), so the
+        // 2^k x 2^k group matrix sees a few embeddings instead of one per
+        // member (same product, same order: U_last ... U_first).
+        GateRef pend;
+        std::vector<double> pendU;
+        pend.k = 0;
+        auto flush = [&]() {
+            if (pend.k == 0) return;
+            pend.U = pendU.data();
+            left_multiply_embedded(f.U, f.k, f.q, pend);
+            pend.k = 0;
+        };
+        for (size_t i : members[G]) {
+            const GateRef &m = g[i];
+            int uq[6], un = 0;
+            for (int j = 0; j < pend.k; ++j) uq[un++] = pend.q[j];
+            for (int j = 0; j < m.k; ++j) {
+                bool have = false;
+                for (int t = 0; t < un; ++t) have |= uq[t] == m.q[j];
+                if (!have && un < 6) uq[un++] = m.q[j];
+            }
+            if (pend.k > 0 && un > 3) flush();
+            if (pend.k == 0) {
+                pend.k = m.k;
+                for (int j = 0; j < m.k; ++j) pend.q[j] = m.q[j];
+                pendU.assign(m.U, m.U + ((size_t)2 << (2 * m.k)));
+                continue;
+            }
+            // pend <- m * pend on the joint support (ascending)
+            std::sort(uq, uq + un);
+            const int d = 1 << un;
+            std::vector<double> P((size_t)2 * d * d, 0.0);
+            for (int r = 0; r < d; ++r) P[(size_t)2 * (r * d + r)] = 1.0;
+            pend.U = pendU.data();
+            left_multiply_embedded(P, un, uq, pend);
+            left_multiply_embedded(P, un, uq, m);
+            pend.k = un;
+            for (int j = 0; j < un; ++j) pend.q[j] = uq[j];
+            pendU.swap(P);
+        }
+        flush();
     }
 }
 
