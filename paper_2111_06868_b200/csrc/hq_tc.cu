@@ -522,6 +522,7 @@ struct ParamsB {
     int np;                // producer warps (template parameter NP)
     int spin;              // 1: spin-wait instead of try_wait with a suspend hint
     int l2hint;            // bit 0: evict-first bulk loads, bit 1: streaming stores (experiments)
+    int diag;              // diagnostics (HQ_TC_DIAG, WRONG results): 1 no MMA, 2 no conversion, 4 no stores
 };
 
 __device__ __forceinline__ void mbar_arrive_tx(uint32_t bar, uint32_t bytes) {
@@ -568,7 +569,7 @@ __device__ __forceinline__ uint64_t sub_f32x2(uint64_t a, uint64_t b) {
     return r;
 }
 
-template <int K, int NS, int NP>
+template <int K, int NS, int NP, bool DIAG = false>
 __global__ void __launch_bounds__(bk_threads(NP), 1)
 apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
           const __half *__restrict__ Breal /* [2][N][KD]: hi then lo, row n = output real */) {
@@ -681,7 +682,8 @@ apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
             mbar_wait(afull(d, 0), ph);
             tc_fence_after();
             // correction terms first, main terms last (see apply_tc)
-            if (elect_one()) {
+            const bool no_mma = DIAG && (P.diag & 1);   // diagnostics only: wrong results
+            if (elect_one() && !no_mma) {
 #pragma unroll 1
                 for (int jj = 0; jj < JH; ++jj) {
                     const uint32_t jk = jj * DSTEP;
@@ -693,19 +695,23 @@ apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
             mbar_wait(afull(d, 1), ph);
             tc_fence_after();
             if (elect_one()) {
+                if (!no_mma) {
 #pragma unroll 1
-                for (int jj = 0; jj < JH; ++jj) {
-                    const uint32_t jk = (JH + jj) * DSTEP;
-                    mma_ts(Dt, a1 + KD / 4 + 8 * jj, dbhi + jk, idesc, 1);
-                    mma_ts(Dt, a1 + 8 * jj, dblo + jk, idesc, 1);
+                    for (int jj = 0; jj < JH; ++jj) {
+                        const uint32_t jk = (JH + jj) * DSTEP;
+                        mma_ts(Dt, a1 + KD / 4 + 8 * jj, dbhi + jk, idesc, 1);
+                        mma_ts(Dt, a1 + 8 * jj, dblo + jk, idesc, 1);
+                    }
+#pragma unroll 1
+                    for (int jj = 0; jj < JH; ++jj)
+                        mma_ts(Dt, a0 + 8 * jj, dbhi + jj * DSTEP, idesc, 1);
                 }
-#pragma unroll 1
-                for (int jj = 0; jj < JH; ++jj)
-                    mma_ts(Dt, a0 + 8 * jj, dbhi + jj * DSTEP, idesc, 1);
                 mma_commit(aempty(d, 0));
+                if (!no_mma) {
 #pragma unroll 1
-                for (int jj = 0; jj < JH; ++jj)
-                    mma_ts(Dt, a1 + 8 * jj, dbhi + (JH + jj) * DSTEP, idesc, 1);
+                    for (int jj = 0; jj < JH; ++jj)
+                        mma_ts(Dt, a1 + 8 * jj, dbhi + (JH + jj) * DSTEP, idesc, 1);
+                }
                 mma_commit(aempty(d, 1));
                 mma_commit(tfull(d));
             }
@@ -743,6 +749,11 @@ apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
                 uint32_t hi[CH], lo[CH];
 #pragma unroll
                 for (int i = 0; i < CH; ++i) {
+                    if (DIAG && (P.diag & 2)) {         // diagnostics only: raw bits, no conversion
+                        hi[i] = (uint32_t)v[c0 + i];
+                        lo[i] = (uint32_t)(v[c0 + i] >> 32);
+                        continue;
+                    }
                     const uint64_t x = mul_f32x2(v[c0 + i], sA2);
                     const float2 xf = u64_as_f2(x);
                     const __half2 h2 = __floats2half2_rn(xf.x, xf.y);
@@ -793,6 +804,7 @@ apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
                 for (int i = 0; i < 16; ++i) {
                     const uint64_t x = (uint64_t)v[2 * i] | ((uint64_t)v[2 * i + 1] << 32);
                     const float2 o = u64_as_f2(mul_f32x2(mul_f32x2(x, f1), f2));
+                    if (DIAG && (P.diag & 4)) continue; // diagnostics only: no stores
                     if (P.l2hint & 2) st_cs_f2(pb + P.off8[16 * ch + i], o);
                     else *reinterpret_cast<float2 *>(pb + P.off8[16 * ch + i]) = o;
                 }
@@ -1551,6 +1563,8 @@ void tc_prepare(const ApplyDesc &d, const double *Ucanon, std::vector<char> &pay
         // 34q circuit (tools/pass_times.py, same box); evict-first bulk loads: no gain
         static const char *l2 = getenv("HQ_TC_L2HINT");
         B.l2hint = l2 ? atoi(l2) : 2;
+        static const char *dg = getenv("HQ_TC_DIAG");
+        B.diag = dg ? atoi(dg) : 0;
         pb.back() = 'B';
         params.swap(pb);
     }
@@ -1574,12 +1588,12 @@ static int tc_launch_k(void *psi, const tc::Params &P, const void *dev_payload, 
     return (int)cudaGetLastError();
 }
 
-template <int K, int NS, int NP>
+template <int K, int NS, int NP, bool DIAG = false>
 static int tc_launch_b(void *psi, const tc::ParamsB &P, const void *dev_payload, cudaStream_t st) {
     using C = tc::CfgB<K, NS>;
     static bool attr_done = false;
     if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(tc::apply_tcb<K, NS, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        cudaError_t e = cudaFuncSetAttribute(tc::apply_tcb<K, NS, NP, DIAG>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
         if (e != cudaSuccess) return (int)e;
         attr_done = true;
     }
@@ -1587,7 +1601,7 @@ static int tc_launch_b(void *psi, const tc::ParamsB &P, const void *dev_payload,
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const uint64_t grid = P.h.ntiles < (uint64_t)sms ? P.h.ntiles : (uint64_t)sms;
-    tc::apply_tcb<K, NS, NP><<<(unsigned)grid, tc::bk_threads(NP), C::SMEM, st>>>(
+    tc::apply_tcb<K, NS, NP, DIAG><<<(unsigned)grid, tc::bk_threads(NP), C::SMEM, st>>>(
         reinterpret_cast<float2 *>(psi), P, reinterpret_cast<const __half *>(dev_payload));
     return (int)cudaGetLastError();
 }
@@ -1597,6 +1611,7 @@ template <int K>
 static int tc_launch_bk(void *psi, const tc::ParamsB &P, const void *dev_payload, cudaStream_t st) {
     const int v = P.ns * 10 + P.np;
     if constexpr (K == 6) {
+        if (P.diag) return tc_launch_b<6, 4, 2, true>(psi, P, dev_payload, st);   // HQ_TC_DIAG timing runs
         if (v == 21) return tc_launch_b<6, 2, 1>(psi, P, dev_payload, st);
         if (v == 42) return tc_launch_b<6, 4, 2>(psi, P, dev_payload, st);
         if (v == 44) return tc_launch_b<6, 4, 4>(psi, P, dev_payload, st);
