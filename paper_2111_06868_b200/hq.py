@@ -388,21 +388,35 @@ def hq_apply_matrix(state, U, qubits):
     _check(lib().hq_apply_matrix(state.ptr, Uf.ctypes.data, q.ctypes.data, int(q.size)))
 
 
+_GATE_DT = np.dtype({"names": ["k", "q", "U"], "formats": ["<i4", ("<i4", 6), "<u8"],
+                     "offsets": [hq_gate.k.offset, hq_gate.qubits.offset, hq_gate.U.offset],
+                     "itemsize": ctypes.sizeof(hq_gate)})
+
+
 def _gate_array(gates):
-    """gates: iterable of (qubits, U) or objects with .qubits/.U."""
+    """gates: iterable of (qubits, U) or objects with .qubits/.U.  Builds the
+    hq_gate array in one numpy structured buffer (all matrices in one
+    complex128 buffer) instead of one ctypes object per gate."""
     gates = list(gates)
-    arr = (hq_gate * max(len(gates), 1))()
-    keep = []
+    ng = len(gates)
+    recs = np.zeros(max(ng, 1), dtype=_GATE_DT)
+    mats = []
+    offs = np.zeros(ng + 1, dtype=np.int64)
     for i, g in enumerate(gates):
         qs = g.qubits if hasattr(g, "qubits") else g[0]
         U = g.U if hasattr(g, "U") else g[1]
-        U, Uf = _u_buffer(U)
-        keep.append(Uf)
-        arr[i].k = len(qs)
-        for j in range(6):
-            arr[i].qubits[j] = int(qs[j]) if j < len(qs) else -1
-        arr[i].U = Uf.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
-    return arr, len(gates), keep
+        k = len(qs)
+        recs["k"][i] = k
+        recs["q"][i, :] = -1
+        recs["q"][i, :k] = qs
+        mats.append(np.asarray(U, dtype=np.complex128).reshape(-1))
+        offs[i + 1] = offs[i] + mats[-1].size
+    buf = np.concatenate(mats) if mats else np.zeros(1, dtype=np.complex128)
+    base = buf.ctypes.data
+    if ng:
+        recs["U"][:ng] = base + 16 * offs[:ng]
+    arr = ctypes.cast(recs.ctypes.data, ctypes.POINTER(hq_gate))
+    return arr, ng, (recs, buf)
 
 
 def hq_apply_circuit(state, gates):
