@@ -38,10 +38,14 @@ def main():
         peak = float(json.load(f)["hbm_gbs"])
     n = args.n
     es = 8 if args.dtype == "c64" else 16
-    s = hq.hq_state_create(n, args.dtype, 1)
+    from hq_inputs.states import random_state_torch
+    # dense random-normal state (config [2]): every amplitude non-zero, so the
+    # tensor cores see generic operand activity (a |0>-derived state is mostly
+    # zeros and draws less power under the 1 kW cap)
+    psi_t = random_state_torch(n, "cuda", seed=32, dtype=args.dtype)
+    torch.cuda.synchronize()
     stream = torch.cuda.Stream()
-    hq.hq_state_set_stream(s, stream.cuda_stream)
-    hq.hq_state_init_basis(s, 0)
+    s = hq.hq_state_create_from_buffers(n, args.dtype, psi_t.data_ptr(), stream.cuda_stream)
     nbytes = 2 * es * 2 ** n
     summary = {}
     for k in [int(x) for x in args.ks.split(",")]:

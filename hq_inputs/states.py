@@ -62,3 +62,23 @@ def hash_state_torch(n, device, chunk=1 << 26):
         view[s:s + i.numel(), 0] = (((a >> 20) & 2047) - 1024).to(torch.float32)
         view[s:s + i.numel(), 1] = (((b >> 24) & 2047) - 1024).to(torch.float32)
     return out
+
+
+def random_state_torch(n, device, seed=0, dtype="c64"):
+    """torch: a dense random-normal state of 2^n amplitudes on `device`,
+    normalised (SURVEY §8(d) config [2]: "random-normal normalized state,
+    device fill").  Every amplitude is non-zero, so timed passes see the
+    operand activity of a generic state, not of a sparse |0>-derived one."""
+    import torch
+    dt = torch.complex64 if dtype == "c64" else torch.complex128
+    out = torch.empty(1 << n, dtype=dt, device=device)
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    flat = torch.view_as_real(out).reshape(-1)
+    flat.normal_(generator=g)
+    chunk = 1 << 27
+    nrm2 = torch.zeros((), dtype=torch.float64, device=device)
+    for i in range(0, flat.numel(), chunk):
+        nrm2 += flat[i:i + chunk].double().square().sum()
+    flat.div_(nrm2.sqrt().to(flat.dtype))
+    return out

@@ -23,8 +23,10 @@ def main():
     import torch
     import paper_2111_06868_b200 as hq
     from hq_inputs import haar_sweep_gate
-    s = hq.hq_state_create(a.n, a.dtype, 1)
-    hq.hq_state_init_basis(s, 0)
+    from hq_inputs.states import random_state_torch
+    psi_t = random_state_torch(a.n, "cuda", seed=32, dtype=a.dtype)     # dense state (see bench_sweep.py)
+    torch.cuda.synchronize()
+    s = hq.hq_state_create_from_buffers(a.n, a.dtype, psi_t.data_ptr(), None)
     g = haar_sweep_gate(a.n, a.k, a.placement, 2000 + a.k)
     for _ in range(a.reps):
         hq.hq_apply_matrix(s, g.U, g.qubits)

@@ -31,10 +31,11 @@ def main():
     from hq_inputs import haar_sweep_gate
     pynvml.nvmlInit()
     h = pynvml.nvmlDeviceGetHandleByIndex(0)
-    s = hq.hq_state_create(a.n, "c64", 1)
+    from hq_inputs.states import random_state_torch
+    psi_t = random_state_torch(a.n, "cuda", seed=32)        # dense state: generic operand activity
     st = torch.cuda.Stream()
-    hq.hq_state_set_stream(s, st.cuda_stream)
-    hq.hq_state_init_basis(s, 0)
+    torch.cuda.synchronize()
+    s = hq.hq_state_create_from_buffers(a.n, "c64", psi_t.data_ptr(), st.cuda_stream)
     for case in a.cases.split(","):
         k, pl = case.split(":", 1)
         g = haar_sweep_gate(a.n, int(k), pl, seed=7)
