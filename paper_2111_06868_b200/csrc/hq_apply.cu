@@ -565,6 +565,96 @@ bool apply_needs_dev_U(int dtype, const ApplyDesc &d) {
     return !plan_reg(dtype, d, rp, VEC, T0, KL);
 }
 
+// ------------------------------------------------------------------ small states: whole circuit in shared memory
+// For n_local <= 12 (c64) / 11 (c128) the whole shard fits in shared memory
+// twice (64 KB), so one CTA runs every pass of a compiled circuit with the
+// state resident: out[x] = sum_c U[r(x)][c] in[base(x) | off[c]] per op,
+// ping-ponging between two shared buffers, one HBM read and one write in
+// total.  The launch-bound small-n case then costs one launch instead of one
+// per pass (CUDA graph replay was ~16 us per pass at 12 qubits).
+template <typename R>
+__global__ void __launch_bounds__(1024, 1)
+circuit_smem(typename C2<R>::T *__restrict__ psi, int nl, const SmemOp *__restrict__ ops, int nops,
+             const typename C2<R>::T *__restrict__ mats) {
+    using V = typename C2<R>::T;
+    extern __shared__ __align__(16) unsigned char zbuf[];
+    const int N = 1 << nl;
+    V *a = reinterpret_cast<V *>(zbuf);
+    V *b = a + N;
+    V *Ut = b + N;                                    // U^T of the current op: Ut[c * D + r]
+    int *offs = reinterpret_cast<int *>(Ut + 64 * 64);
+    for (int i = threadIdx.x; i < N; i += blockDim.x) a[i] = psi[i];
+    for (int o = 0; o < nops; ++o) {
+        const SmemOp op = ops[o];
+        const int K = op.k, D = 1 << K;
+        const V *U = mats + op.uoff;
+        __syncthreads();                              // previous op done with Ut / offs / a
+        for (int i = threadIdx.x; i < D * D; i += blockDim.x) Ut[(i % D) * D + i / D] = U[i];
+        for (int c = threadIdx.x; c < D; c += blockDim.x) {
+            int off = 0;
+            for (int i = 0; i < K; ++i) off |= ((c >> i) & 1) << op.p[i];
+            offs[c] = off;
+        }
+        __syncthreads();
+        // output j = set * D + r: lanes run over r, so the inputs of a set are
+        // warp broadcasts and U^T columns are consecutive
+        for (int j = threadIdx.x; j < N; j += blockDim.x) {
+            const int r = j & (D - 1);
+            int base = j >> K;
+            for (int i = 0; i < K; ++i) {
+                const int s = op.p[i];
+                base = ((base >> s) << (s + 1)) | (base & ((1 << s) - 1));
+            }
+            R re = 0, im = 0;
+            for (int c = 0; c < D; ++c) {
+                const V u = Ut[c * D + r];
+                const V v = a[base | offs[c]];
+                re = fma(u.x, v.x, re);
+                re = fma(-u.y, v.y, re);
+                im = fma(u.x, v.y, im);
+                im = fma(u.y, v.x, im);
+            }
+            V y;
+            y.x = re;
+            y.y = im;
+            b[base | offs[r]] = y;
+        }
+        V *t = a;
+        a = b;
+        b = t;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < N; i += blockDim.x) psi[i] = a[i];
+}
+
+int launch_circuit_smem(int dtype, void *psi, int nl, const SmemOp *dev_ops, int nops, const void *dev_mats,
+                        void *stream) {
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const size_t es = dtype == HQ_C64 ? 8 : 16;
+    const size_t smem = (2 * es << nl) + es * 64 * 64 + 64 * sizeof(int);
+    const int threads = nl >= 10 ? 1024 : (1 << nl) < 32 ? 32 : (1 << nl);
+    if (dtype == HQ_C64) {
+        static bool attr = false;
+        if (!attr) {
+            cudaError_t e = cudaFuncSetAttribute(circuit_smem<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)((2 * 8 << SMEM_CIRCUIT_MAX_NL_C64) + 8 * 64 * 64 + 256));
+            if (e != cudaSuccess) return (int)e;
+            attr = true;
+        }
+        circuit_smem<float><<<1, threads, smem, st>>>((float2 *)psi, nl, dev_ops, nops, (const float2 *)dev_mats);
+    } else {
+        static bool attr = false;
+        if (!attr) {
+            cudaError_t e = cudaFuncSetAttribute(circuit_smem<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)((2 * 16 << SMEM_CIRCUIT_MAX_NL_C128) + 16 * 64 * 64 + 256));
+            if (e != cudaSuccess) return (int)e;
+            attr = true;
+        }
+        circuit_smem<double><<<1, threads, smem, st>>>((double2 *)psi, nl, dev_ops, nops, (const double2 *)dev_mats);
+    }
+    return (int)cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ small kernels
 
 template <typename V>

@@ -82,6 +82,21 @@ int launch_apply(int dtype, void *psi, const ApplyDesc &d, const void *host_U,
 // parameter for this (dtype, k, placement)).
 bool apply_needs_dev_U(int dtype, const ApplyDesc &d);
 
+// Whole compiled circuit in one CTA with the shard resident in shared memory
+// (n_local <= 12 for c64, <= 11 for c128).  ops[i]: k canonical targets at
+// ascending physical bits p[], mask = OR of their bits, U at mats + uoff
+// (canonical D x D, state dtype).
+struct SmemOp {
+    int k;
+    int p[6];
+    int mask;
+    int uoff;              // in complex elements
+};
+constexpr int SMEM_CIRCUIT_MAX_NL_C64 = 12;
+constexpr int SMEM_CIRCUIT_MAX_NL_C128 = 11;
+int launch_circuit_smem(int dtype, void *psi, int nl, const SmemOp *dev_ops, int nops, const void *dev_mats,
+                        void *stream);
+
 // tcgen05 tensor-core path (hq_tc.cu): complex64, k = 5 or 6 (5 is widened to
 // 6 exactly as U (x) I).  tc_prepare builds the device payload (real-embedded
 // A hi/lo, 128 KB) and the kernel parameter block from the canonical fp64 U.

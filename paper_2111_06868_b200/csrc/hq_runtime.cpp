@@ -132,6 +132,11 @@ struct hq_circuit {
     std::vector<std::vector<long long>> cuoff;
     std::vector<double> cgnorm;            // spectral bound of the whole U
     std::vector<char *> dev_U;             // per shard: all payloads
+    // small single-shard states: the whole op stream in one shared-memory CTA
+    SmemOp *small_ops = nullptr;
+    void *small_mats = nullptr;
+    int small_nops = 0;
+    int small_dev = 0;
     std::vector<int> dev_of;               // per shard: its device (destroy must not read the state)
     uint64_t passes = 0, remaps = 0, permutes = 0;
     // CUDA graph of the whole op stream (single-shard states, profiling off):
@@ -969,6 +974,39 @@ static hq_status circuit_compile(hq_state *st, hq_circuit *c, const std::vector<
     c->dev_U.assign(st->sh.size(), nullptr);
     c->dev_of.resize(st->sh.size());
     for (size_t r = 0; r < st->sh.size(); ++r) c->dev_of[r] = st->sh[r].device;
+    // small states: one CTA runs every pass with the shard in shared memory
+    {
+        // measured (tools/small_timing.py): one CTA beats the per-pass graph
+        // for n_local <= 10 with >= 2 passes (8q: 16.5 vs 28.7 us, 10q: 45 vs
+        // 55 us); at 11-12 qubits the multi-SM passes win (12q: 132 vs 237 us)
+        const int maxnl = std::min(10, st->dtype == HQ_C64 ? SMEM_CIRCUIT_MAX_NL_C64 : SMEM_CIRCUIT_MAX_NL_C128);
+        bool ok = st->sh.size() == 1 && st->m == 0 && st->nl <= maxnl && c->ops.size() >= 2 && c->remaps == 0 &&
+                  c->permutes == 0;
+        static const char *off = getenv("HQ_SMEM_CIRCUIT");   // "0": per-pass kernels (experiments)
+        if (off && off[0] == '0') ok = false;
+        if (ok) {
+            std::vector<SmemOp> ops;
+            std::vector<char> mats;
+            for (size_t i = 0; i < c->ops.size(); ++i) {
+                const Prep &p = c->prep[i];
+                SmemOp o{};
+                o.k = p.d.k;
+                o.mask = 0;
+                for (int j = 0; j < p.d.k; ++j) { o.p[j] = p.d.p[j]; o.mask |= 1 << p.d.p[j]; }
+                o.uoff = (int)(mats.size() / st->es);
+                mats.insert(mats.end(), p.hostU.begin(), p.hostU.end());
+                ops.push_back(o);
+            }
+            Shard &s0 = st->sh[0];
+            CUDA_TRY(cudaSetDevice(s0.device));
+            CUDA_TRY(cudaMalloc((void **)&c->small_ops, sizeof(SmemOp) * ops.size()));
+            CUDA_TRY(cudaMalloc(&c->small_mats, mats.size()));
+            CUDA_TRY(cudaMemcpy(c->small_ops, ops.data(), sizeof(SmemOp) * ops.size(), cudaMemcpyHostToDevice));
+            CUDA_TRY(cudaMemcpy(c->small_mats, mats.data(), mats.size(), cudaMemcpyHostToDevice));
+            c->small_nops = (int)ops.size();
+            c->small_dev = s0.device;
+        }
+    }
     if (total == 0) return HQ_OK;
     std::vector<char> blob(total, 0);
     for (size_t i = 0; i < c->ops.size(); ++i) {
@@ -1036,6 +1074,20 @@ extern "C" hq_status hq_circuit_run(hq_state *st, hq_circuit *c) {
     if (st->pi != c->pi_start)
         return set_error(HQ_ERR_STATE, "state qubit layout differs from the one the circuit was compiled for");
     hq_status rc;
+    if (c->small_ops && !st->profiling) {
+        Shard &s0 = st->sh[0];
+        CUDA_TRY(cudaSetDevice(s0.device));
+        int e = launch_circuit_smem((int)st->dtype, s0.psi, st->nl, c->small_ops, c->small_nops, c->small_mats,
+                                    s0.stream);
+        if (e) return set_error(HQ_ERR_CUDA, "circuit_smem launch: %s", cudaGetErrorString((cudaError_t)e));
+        for (size_t i = 0; i < c->ops.size(); ++i)
+            if (st->amp_bound >= 0) st->amp_bound *= c->prep[i].gnorm;
+        st->stats.passes += c->passes;
+        st->stats.kernel_launches += 1;
+        st->stats.hbm_bytes += (uint64_t)2 * (st->es << st->nl);
+        st->pi = c->pi_end;
+        return HQ_OK;
+    }
     const bool graphable = st->sh.size() == 1 && !st->profiling && c->remaps == 0 && c->permutes == 0 &&
                            !c->ops.empty();
     if (!graphable) {
@@ -1114,6 +1166,11 @@ extern "C" hq_status hq_circuit_info(const hq_circuit *c, uint64_t *passes, uint
 extern "C" hq_status hq_circuit_destroy(hq_circuit *c) {
     if (!c) return HQ_OK;
     if (c->graph) cudaGraphExecDestroy(c->graph);
+    if (c->small_ops || c->small_mats) {
+        cudaSetDevice(c->small_dev);
+        if (c->small_ops) cudaFree(c->small_ops);
+        if (c->small_mats) cudaFree(c->small_mats);
+    }
     // the owning state may already be gone (destroy order is the caller's):
     // use the devices recorded at compile time, never c->owner
     for (size_t r = 0; r < c->dev_U.size(); ++r)

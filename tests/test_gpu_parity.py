@@ -415,3 +415,33 @@ def test_merged_plan_20q_tensor_cores_vs_oracle(kmax):
     hq.hq_circuit_run(s, c)
     got = hq.hq_get_amplitudes(s)
     assert _err(got, want) <= TOL["c64"]
+
+
+# ---------------------------------------------------------------- small states: whole circuit in shared memory
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("n", [1, 2, 5, 8, 10, 11, 12])
+def test_small_state_circuit_in_shared_memory(dtype, n):
+    """hq_circuit_run for n_local <= 10 (and >= 2 passes) runs every pass in
+    one CTA with the state in shared memory (11-12 qubits: per-pass kernels);
+    results against the oracle, for
+    fused gates of every k the state allows, twice in a row (re-run of the
+    same compiled circuit) and with a random layout."""
+    kmax = min(6, n)
+    gates = [Gate("F", q, U) for q, U in hq.hq_fuse(random_circuit(n, 40, 7, kmax=min(kmax, 3)), kmax)]
+    psi0 = random_state(n, 11)
+    want1 = O.simulate(n, gates, psi0)
+    want2 = O.simulate(n, gates, want1)
+    for layout in (None, [int(x) for x in np.random.default_rng(n).permutation(n)]):
+        s = _gpu_state(n, dtype)
+        if layout is not None:
+            hq.hq_state_set_layout(s, layout)
+        hq.hq_set_amplitudes(s, psi0.astype(s.np_dtype))
+        c = hq.hq_circuit_create(s, gates)
+        hq.hq_stats_reset(s)
+        hq.hq_circuit_run(s, c)
+        assert _err(hq.hq_get_amplitudes(s), want1) <= TOL[dtype]
+        hq.hq_circuit_run(s, c)
+        assert _err(hq.hq_get_amplitudes(s), want2) <= TOL[dtype]
+        st = hq.hq_stats_get(s)
+        assert st["passes"] == 2 * len(gates)
