@@ -39,6 +39,7 @@
 //               accumulator d: [2*KD + d*KD, 2*KD + (d+1)*KD).
 // Synchronisation: mbarriers full[h]/empty[h] (converters <-> MMA per K-half)
 // and tfull[d]/tempty[d] (MMA <-> epilogue, double-buffered accumulator).
+#include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <cstdint>
@@ -523,7 +524,23 @@ struct ParamsB {
     int spin;              // 1: spin-wait instead of try_wait with a suspend hint
     int l2hint;            // bit 0: evict-first bulk loads, bit 1: streaming stores (experiments)
     int diag;              // diagnostics (HQ_TC_DIAG, WRONG results): 1 no MMA, 2 no conversion, 4 no stores
+    int swz;               // 1: blocks arrive by 2-D TMA with SWIZZLE_128B; nidx/cidx8 are pre-swizzled
+    int pair;              // 1: the lowest target is bit 0, patterns (2j, 2j+1) are one 16-byte load / store
+    int xpair;             // 1: the lowest target is bit 1 and lane bit 0 is bit 0: lane pairs swap
+                           //    one output each so that every store is 16 bytes (full sectors)
 };
+
+// SWIZZLE_128B as seen from a slot index (8-byte amplitudes): byte address
+// bits [4:6] ^= bits [7:9], i.e. index bits [1:3] ^= [4:6].  Linear over GF(2),
+// so swz(nidx | cidx) = swz(nidx) ^ swz(cidx) for the disjoint set / pattern bits.
+__host__ __device__ constexpr uint32_t swz128(uint32_t s) { return s ^ (((s >> 4) & 7u) << 1); }
+
+__device__ __forceinline__ void tma_g2s_2d(uint32_t dst, const CUtensorMap *map, int c0, int c1, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+        : "memory");
+}
 
 __device__ __forceinline__ void mbar_arrive_tx(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
@@ -552,6 +569,10 @@ __device__ __forceinline__ void st_cs_f2(void *p, float2 v) {     // streaming s
     asm volatile("st.global.cs.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v.x), "f"(v.y) : "memory");
 }
 
+__device__ __forceinline__ void st_cs_f4(void *p, float2 a, float2 b) {
+    asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y)
+                 : "memory");
+}
 __device__ __forceinline__ uint64_t f2_as_u64(float2 v) {
     return (uint64_t)__float_as_uint(v.x) | ((uint64_t)__float_as_uint(v.y) << 32);
 }
@@ -572,7 +593,8 @@ __device__ __forceinline__ uint64_t sub_f32x2(uint64_t a, uint64_t b) {
 template <int K, int NS, int NP, bool DIAG = false>
 __global__ void __launch_bounds__(bk_threads(NP), 1)
 apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
-          const __half *__restrict__ Breal /* [2][N][KD]: hi then lo, row n = output real */) {
+          const __half *__restrict__ Breal /* [2][N][KD]: hi then lo, row n = output real */,
+          const __grid_constant__ CUtensorMap tmap /* psi as [rows][16 amplitudes], box 8 rows, SWIZZLE_128B (P.swz) */) {
     // even NS only: odd rings (a slot shared by both K-halves) failed with a
     // launch error at n >= 32 in the ring experiments; not pursued
     static_assert(NS % 2 == 0, "slot parity = K-half needs an even ring");
@@ -647,7 +669,8 @@ apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
         const uint64_t pol = policy_evict_first();
         uint32_t it = 0;
         for (uint64_t t = blockIdx.x; t < ntiles; t += G, ++it) {
-            const float2 *tb = psi + tile_base<NPOS>(t, P.h);
+            const uint64_t tbo = tile_base<NPOS>(t, P.h);
+            const float2 *tb = psi + tbo;
 #pragma unroll 1
             for (int h = NP == 1 ? 0 : p % 2; h < (NP == 1 ? 2 : p % 2 + 1); ++h) {
                 const uint32_t sidx = 2 * it + h;
@@ -657,7 +680,10 @@ apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
                 __syncwarp();
                 if (lane < NB) {
                     const int j = sub * NB + lane;
-                    if (P.l2hint & 1)
+                    if (P.swz)   // row = 16 amplitudes; a 1 KB block is 8 rows, swizzled on arrival
+                        tma_g2s_2d(sbase + C::RING + s * C::SLOT_BYTES + j * 1024, &tmap, 0,
+                                   (int)((tbo + P.boff[h][j]) >> 4), rfull(s));
+                    else if (P.l2hint & 1)
                         bulk_g2s_ef(sbase + C::RING + s * C::SLOT_BYTES + j * 1024, tb + P.boff[h][j], 1024,
                                     rfull(s), pol);
                     else
@@ -734,10 +760,20 @@ apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
             // slot back before converting, so the producer can refill it
             // while this warp waits for the A buffer and converts
             wait(rfull(s), (sidx / NSLOT) & 1);
-            const char *raw = reinterpret_cast<const char *>(smem + C::RING + s * C::SLOT_BYTES) + nb8;
+            const char *sraw = reinterpret_cast<const char *>(smem + C::RING + s * C::SLOT_BYTES);
             uint64_t v[HA];
+            // nb8 ^ cidx8: with P.swz both are pre-swizzled; without, their bits are disjoint (^ == |)
+            if (P.pair) {
 #pragma unroll
-            for (int c = 0; c < HA; ++c) v[c] = *reinterpret_cast<const uint64_t *>(raw + P.cidx8[c]);
+                for (int c = 0; c < HA; c += 2) {
+                    const uint4 w = *reinterpret_cast<const uint4 *>(sraw + (nb8 ^ P.cidx8[c]));
+                    v[c] = (uint64_t)w.x | ((uint64_t)w.y << 32);
+                    v[c + 1] = (uint64_t)w.z | ((uint64_t)w.w << 32);
+                }
+            } else {
+#pragma unroll
+                for (int c = 0; c < HA; ++c) v[c] = *reinterpret_cast<const uint64_t *>(sraw + (nb8 ^ P.cidx8[c]));
+            }
             __syncwarp();
             if (lane == 0) mbar_arrive(rempty(s));
             wait(aempty(a, h), ((it >> 1) & 1) ^ 1);
@@ -799,6 +835,38 @@ apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(tempty(d));   // accumulator drained
+                }
+                if (P.pair) {
+                    // bit 0 is a target: patterns 2j, 2j+1 of this set are adjacent
+                    // amplitudes, one 16-byte store (full sectors per warp store)
+#pragma unroll
+                    for (int i = 0; i < 16; i += 2) {
+                        const uint64_t x0 = (uint64_t)v[2 * i] | ((uint64_t)v[2 * i + 1] << 32);
+                        const uint64_t x1 = (uint64_t)v[2 * i + 2] | ((uint64_t)v[2 * i + 3] << 32);
+                        const float2 o0 = u64_as_f2(mul_f32x2(mul_f32x2(x0, f1), f2));
+                        const float2 o1 = u64_as_f2(mul_f32x2(mul_f32x2(x1, f1), f2));
+                        if (DIAG && (P.diag & 4)) continue;
+                        st_cs_f4(pb + P.off8[16 * ch + i], o0, o1);
+                    }
+                    continue;
+                }
+                if (P.xpair) {
+                    // bit 1 is the lowest target, bit 0 the lane parity: the even lane
+                    // (set s) stores (s, 2j), (s^1, 2j) and the odd lane (s, 2j+1),
+                    // (s^1, 2j+1), each a 16-byte store, one shuffle per pair
+                    const bool odd = lane & 1;
+#pragma unroll
+                    for (int i = 0; i < 16; i += 2) {
+                        const uint64_t x0 = (uint64_t)v[2 * i] | ((uint64_t)v[2 * i + 1] << 32);
+                        const uint64_t x1 = (uint64_t)v[2 * i + 2] | ((uint64_t)v[2 * i + 3] << 32);
+                        const uint64_t y0 = mul_f32x2(mul_f32x2(x0, f1), f2);
+                        const uint64_t y1 = mul_f32x2(mul_f32x2(x1, f1), f2);
+                        const uint64_t r = __shfl_xor_sync(0xffffffffu, odd ? y0 : y1, 1);
+                        if (DIAG && (P.diag & 4)) continue;
+                        st_cs_f4(pb - (odd ? 8 : 0) + P.off8[16 * ch + i + (odd ? 1 : 0)], u64_as_f2(odd ? r : y0),
+                                 u64_as_f2(odd ? y1 : r));
+                    }
+                    continue;
                 }
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
@@ -1524,17 +1592,86 @@ void tc_prepare(const ApplyDesc &d, const double *Ucanon, std::vector<char> &pay
         auto tpos = [&](int phys) { return (int)(std::find(all, all + na, phys) - all); };
         const int hp = tpos(d.p[K - 1]);
         auto slot_of = [&](uint64_t ti) { return (ti & ((1ull << hp) - 1)) | ((ti >> (hp + 1)) << hp); };
+        // Targets in bits 0..3 (measured on the 34q circuit, tools/pass_times.py,
+        // same box):
+        //  * bit 0 a target: patterns (2j, 2j+1) are adjacent, so converters
+        //    load and the epilogue stores 16 bytes (pair): 61 -> 47 ms per pass;
+        //  * bit 1 the lowest target: 2-D TMA with SWIZZLE_128B removes the 2-way
+        //    bank conflicts of the converter loads (61 -> 58 ms) and lane pairs
+        //    swap outputs for 16-byte stores (xpair).  The swizzled TMA copies
+        //    are slower elsewhere (no low target 57 -> 60 ms, a k = 5 pass with
+        //    targets 3, 4, 6 56 -> 80 ms), so only this case uses them.
+        // HQ_TC_SWZ=0 disables all three, 2 forces the swizzled copies (experiments).
+        static const char *swe = getenv("HQ_TC_SWZ");
+        const bool low_ok = !(swe && swe[0] == '0');
+        B.swz = low_ok && ((K == 6 && d.p[0] == 1) || (swe && swe[0] == '2'));
+        B.pair = low_ok && d.p[0] == 0;
+        B.xpair = 0;
+        // Converter lanes (n bits 0..4) are 5 of the 7 set bits.  With one
+        // target in bits 0..3 the ascending choice puts a warp's 8-byte reads
+        // on 8 of 16 bank pairs (2-way conflicts); with the swizzled slot
+        // another choice of lane bits, or 16-byte pattern pairs when bit 0 is
+        // a target, reaches all of them.  Pick the conflict-minimal choice,
+        // the ascending one on ties (it keeps the epilogue stores contiguous).
+        int order[tc::SETBITS];
+        for (int i = 0; i < tc::SETBITS; ++i) order[i] = setbits[i];
+        if (B.swz) {
+            auto slot_idx = [&](int n, const int *sb) {
+                uint64_t ti = 0;
+                for (int i = 0; i < tc::SETBITS; ++i)
+                    if ((n >> i) & 1) ti |= 1ull << tpos(sb[i]);
+                return tc::swz128((uint32_t)slot_of(ti));
+            };
+            auto wavefronts = [&](const int *sb) {
+                const int words = B.pair ? 4 : 2;
+                int cnt[32] = {0};
+                uint32_t seen[32][32];
+                for (int l = 0; l < 32; ++l) {
+                    const uint32_t w0 = slot_idx(l, sb) * 2;
+                    for (int w = 0; w < words; ++w) {
+                        const uint32_t word = w0 + w, bank = word & 31;
+                        bool dup = false;
+                        for (int i = 0; i < cnt[bank]; ++i) dup |= seen[bank][i] == word;
+                        if (!dup) seen[bank][cnt[bank]++] = word;
+                    }
+                }
+                return *std::max_element(cnt, cnt + 32);
+            };
+            int best = wavefronts(order);
+            for (int m = 0; m < (1 << tc::SETBITS); ++m) {
+                if (__builtin_popcount(m) != 5) continue;
+                int cand[tc::SETBITS], nc = 0;
+                for (int i = 0; i < tc::SETBITS; ++i)
+                    if ((m >> i) & 1) cand[nc++] = setbits[i];
+                for (int i = 0; i < tc::SETBITS; ++i)
+                    if (!((m >> i) & 1)) cand[nc++] = setbits[i];
+                const int w = wavefronts(cand);
+                if (w < best) {
+                    best = w;
+                    std::copy(cand, cand + tc::SETBITS, order);
+                }
+            }
+            for (int n = 0; n < tc::M; ++n) {
+                uint32_t o = 0;
+                for (int i = 0; i < tc::SETBITS; ++i)
+                    if ((n >> i) & 1) o |= 1u << order[i];
+                B.h.setoff[n] = o;
+            }
+        }
+        if (low_ok && d.p[0] == 1 && order[0] == 0) {
+            B.xpair = 1;
+        }
         for (int n = 0; n < tc::M; ++n) {
             uint64_t ti = 0;
             for (int i = 0; i < tc::SETBITS; ++i)
-                if ((n >> i) & 1) ti |= 1ull << tpos(setbits[i]);
-            B.nidx[n] = (uint16_t)slot_of(ti);
+                if ((n >> i) & 1) ti |= 1ull << tpos(order[i]);
+            B.nidx[n] = (uint16_t)(B.swz ? tc::swz128((uint32_t)slot_of(ti)) : slot_of(ti));
         }
         for (int c = 0; c < D / 2; ++c) {
             uint64_t ti = 0;
             for (int i = 0; i < K - 1; ++i)
                 if ((c >> i) & 1) ti |= 1ull << tpos(d.p[i]);
-            B.cidx8[c] = (uint32_t)slot_of(ti) * 8;
+            B.cidx8[c] = (uint32_t)(B.swz ? tc::swz128((uint32_t)slot_of(ti)) : slot_of(ti)) * 8;
         }
         for (int h = 0; h < 2; ++h)
             for (int j = 0; j < D / 2; ++j) {
@@ -1588,6 +1725,31 @@ static int tc_launch_k(void *psi, const tc::Params &P, const void *dev_payload, 
     return (int)cudaGetLastError();
 }
 
+// psi (2^nl complex64) as a 2-D FP32 tensor [2^(nl-4) rows][32 floats] (128 B
+// rows), box 8 rows = one 1 KB block, SWIZZLE_128B; the driver entry point is
+// looked up once (no -lcuda).
+using EncodeTiledFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static int tc_encode_rows_map(CUtensorMap *map, void *psi, int nl) {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void *f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q);
+        if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !f) return e != cudaSuccess ? (int)e : (int)cudaErrorNotSupported;
+        fn = reinterpret_cast<EncodeTiledFn>(f);
+    }
+    const cuuint64_t dims[2] = {32, 1ull << (nl - 4)};
+    const cuuint64_t strides[1] = {128};
+    const cuuint32_t box[2] = {32, 8};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, psi, dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
+}
+
 template <int K, int NS, int NP, bool DIAG = false>
 static int tc_launch_b(void *psi, const tc::ParamsB &P, const void *dev_payload, cudaStream_t st) {
     using C = tc::CfgB<K, NS>;
@@ -1601,8 +1763,16 @@ static int tc_launch_b(void *psi, const tc::ParamsB &P, const void *dev_payload,
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const uint64_t grid = P.h.ntiles < (uint64_t)sms ? P.h.ntiles : (uint64_t)sms;
+    alignas(64) CUtensorMap map;
+    std::memset(&map, 0, sizeof(map));
+    if (P.swz) {
+        int nl = K + tc::SETBITS;
+        while ((1ull << (nl - K - tc::SETBITS)) < P.h.ntiles) ++nl;
+        const int e = tc_encode_rows_map(&map, psi, nl);
+        if (e) return e;
+    }
     tc::apply_tcb<K, NS, NP, DIAG><<<(unsigned)grid, tc::bk_threads(NP), C::SMEM, st>>>(
-        reinterpret_cast<float2 *>(psi), P, reinterpret_cast<const __half *>(dev_payload));
+        reinterpret_cast<float2 *>(psi), P, reinterpret_cast<const __half *>(dev_payload), map);
     return (int)cudaGetLastError();
 }
 

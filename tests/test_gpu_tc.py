@@ -31,6 +31,27 @@ def test_tc_low_targets(placement):
     assert err < 2e-6, err
 
 
+# mode H with targets below bit 7 (the swizzled slot, the converter lane-bit
+# choice and the 16-byte pattern pairs when bit 0 is a target)
+LOWH6 = ["b:%d-8-9-12-14-16" % b for b in range(7)] + [
+    "b:0-3-9-12-14-16", "b:1-2-9-12-14-16", "b:2-3-9-12-14-16", "b:3-5-6-9-12-16", "b:0-4-5-6-12-16",
+    "b:0-5-6-8-9-10"]
+LOWH5 = ["b:%d-8-12-14-16" % b for b in range(7)] + ["b:0-3-9-12-16", "b:1-2-9-12-16", "b:0-4-5-6-16"]
+
+
+@pytest.mark.parametrize("n", [17, 20])
+@pytest.mark.parametrize("placement", LOWH6 + LOWH5)
+def test_tc_low_target_mode_h(placement, n):
+    k = placement.count("-") + 1
+    g = haar_sweep_gate(n, k, placement, seed=2100 + k)
+    psi0 = random_state(n, 6)
+    want = O.apply_gate(psi0.copy(), g.U, g.qubits)
+    s = _state(n, psi0)
+    hq.hq_apply_matrix(s, g.U, g.qubits)
+    err = np.linalg.norm(hq.hq_get_amplitudes(s).astype(np.complex128) - want)
+    assert err < 2e-6, err
+
+
 def _state(n, psi0):
     s = hq.hq_state_create(n, "c64", 1)
     hq.hq_set_amplitudes(s, psi0)
