@@ -526,8 +526,8 @@ struct ParamsB {
     int diag;              // diagnostics (HQ_TC_DIAG, WRONG results): 1 no MMA, 2 no conversion, 4 no stores
     int swz;               // 1: blocks arrive by 2-D TMA with SWIZZLE_128B; nidx/cidx8 are pre-swizzled
     int pair;              // 1: the lowest target is bit 0, patterns (2j, 2j+1) are one 16-byte load / store
-    int xpair;             // 1: the lowest target is bit 1 and lane bit 0 is bit 0: lane pairs swap
-                           //    one output each so that every store is 16 bytes (full sectors)
+    int xpair;             // 1: bit 0 is not a target and is lane bit 0: lane pairs swap one
+                           //    output each so that every store is 16 bytes
 };
 
 // SWIZZLE_128B as seen from a slot index (8-byte amplitudes): byte address
@@ -851,9 +851,10 @@ apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
                     continue;
                 }
                 if (P.xpair) {
-                    // bit 1 is the lowest target, bit 0 the lane parity: the even lane
-                    // (set s) stores (s, 2j), (s^1, 2j) and the odd lane (s, 2j+1),
-                    // (s^1, 2j+1), each a 16-byte store, one shuffle per pair
+                    // bit 0 is a set bit and the lane parity: for the pattern pair
+                    // (2j, 2j+1) the even lane (set s) stores (s, 2j), (s^1, 2j) and
+                    // the odd lane (s, 2j+1), (s^1, 2j+1), adjacent amplitudes, one
+                    // 16-byte store each after one 64-bit shuffle
                     const bool odd = lane & 1;
 #pragma unroll
                     for (int i = 0; i < 16; i += 2) {
@@ -1658,7 +1659,13 @@ void tc_prepare(const ApplyDesc &d, const double *Ucanon, std::vector<char> &pay
                 B.h.setoff[n] = o;
             }
         }
-        if (low_ok && d.p[0] == 1 && order[0] == 0) {
+        // xpair for every pass with bit 0 free (the set bit of lane bit 0):
+        // halving the epilogue's store instructions is what speeds the pair
+        // passes up, full sectors or not; HQ_TC_XPAIR=0: only
+        // when bit 1 is the lowest target (experiments)
+        static const char *xpe = getenv("HQ_TC_XPAIR");
+        const bool xall = !(xpe && xpe[0] == '0');
+        if (low_ok && d.p[0] != 0 && order[0] == 0 && (xall || d.p[0] == 1)) {
             B.xpair = 1;
         }
         for (int n = 0; n < tc::M; ++n) {
