@@ -439,7 +439,11 @@ double layout_pass_cost(int dtype, int k, const int *bits) {
         // tensor-core pass, measured per pass on the sustained 34q circuit
         // (tools/pass_times.py): mode H with <= 1 target in bits 0..3 is the
         // baseline; 2 such targets cost 1.19x; mode L (bits 0 and 1, or >= 3
-        // targets in bits 0..3) 1.29x
+        // targets in bits 0..3) 1.29x.  Since the 16-byte pattern pairs and
+        // lane-pair stores every measured mode-H pass with
+        // <= 1 low target runs at the same ~47 ms, whichever bit it is; a
+        // bit-0 bonus (tried: 4037 vs 4050 ms before the lane-pair stores)
+        // no longer applies.
         int lo = 0;
         bool b0 = false, b1 = false;
         for (int j = 0; j < k; ++j) {
@@ -447,18 +451,10 @@ double layout_pass_cost(int dtype, int k, const int *bits) {
             b0 |= bits[j] == 0;
             b1 |= bits[j] == 1;
         }
-        // Since the 16-byte pattern pairs a mode-H pass with a
-        // target at bit 0 is the cheapest (47 vs 57 ms), one at bit 1 (swizzled
-        // TMA) about baseline, one at bit 2 or 3 ~1.06x; HQ_LAYOUT_PAIR=0 keeps
-        // the earlier weights (experiments).
         static const char *old_model = getenv("HQ_LAYOUT_V4");   // "1": the round-1 v4 model (experiments)
-        static const char *pair_env = getenv("HQ_LAYOUT_PAIR");
-        const bool pair = !(pair_env && pair_env[0] == '0');
         if (old_model && old_model[0] == '1') c += lo ? 0.06 + 0.02 * lo : 0.0;
         else if ((b0 && b1) || lo >= 3) c += 0.29;
-        else if (lo == 2) c += pair && b0 ? -0.08 : 0.19;
-        else if (pair && b0) c -= 0.18;
-        else if (pair && lo == 1 && !b1) c += 0.06;
+        else if (lo == 2) c += 0.19;
     } else {
         const int lane_lo = dtype == HQ_C64 ? 1 : 0, lane_hi = lane_lo + 5;
         for (int j = 0; j < k; ++j)

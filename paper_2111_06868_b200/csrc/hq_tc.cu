@@ -528,6 +528,7 @@ struct ParamsB {
     int pair;              // 1: the lowest target is bit 0, patterns (2j, 2j+1) are one 16-byte load / store
     int xpair;             // 1: bit 0 is not a target and is lane bit 0: lane pairs swap one
                            //    output each so that every store is 16 bytes
+    int xquad;             // 1: bits 0, 1 are lane bits 0, 1: lane quads transpose, 32-byte stores
 };
 
 // SWIZZLE_128B as seen from a slot index (8-byte amplitudes): byte address
@@ -572,6 +573,9 @@ __device__ __forceinline__ void st_cs_f2(void *p, float2 v) {     // streaming s
 __device__ __forceinline__ void st_cs_f4(void *p, float2 a, float2 b) {
     asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y)
                  : "memory");
+}
+__device__ __forceinline__ void st_cs_f8(void *p, uint64_t a, uint64_t b, uint64_t c, uint64_t d) {
+    asm volatile("st.global.cs.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(a), "l"(b), "l"(c), "l"(d) : "memory");
 }
 __device__ __forceinline__ uint64_t f2_as_u64(float2 v) {
     return (uint64_t)__float_as_uint(v.x) | ((uint64_t)__float_as_uint(v.y) << 32);
@@ -847,6 +851,34 @@ apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
                         const float2 o1 = u64_as_f2(mul_f32x2(mul_f32x2(x1, f1), f2));
                         if (DIAG && (P.diag & 4)) continue;
                         st_cs_f4(pb + P.off8[16 * ch + i], o0, o1);
+                    }
+                    continue;
+                }
+                if (P.xquad) {
+                    // bits 0 and 1 are set bits, lane bits 0 and 1: a 4x4 transpose of
+                    // (set, pattern) over the lane quad (two shuffle stages) gives each
+                    // lane 4 adjacent amplitudes of one pattern, one 32-byte store
+                    const bool b0 = lane & 1, b1 = lane & 2;
+                    const int q = lane & 3;
+                    char *qb = pb - 8 * (q);
+#pragma unroll
+                    for (int i = 0; i < 16; i += 4) {
+                        uint64_t y[4];
+#pragma unroll
+                        for (int m = 0; m < 4; ++m) {
+                            const uint64_t x = (uint64_t)v[2 * (i + m)] | ((uint64_t)v[2 * (i + m) + 1] << 32);
+                            y[m] = mul_f32x2(mul_f32x2(x, f1), f2);
+                        }
+                        const uint64_t ra = __shfl_xor_sync(0xffffffffu, b0 ? y[0] : y[1], 1);
+                        const uint64_t rb = __shfl_xor_sync(0xffffffffu, b0 ? y[2] : y[3], 1);
+                        const uint64_t u00 = b0 ? ra : y[0], u10 = b0 ? y[1] : ra;
+                        const uint64_t u01 = b0 ? rb : y[2], u11 = b0 ? y[3] : rb;
+                        const uint64_t r0 = __shfl_xor_sync(0xffffffffu, b1 ? u00 : u01, 2);
+                        const uint64_t r1 = __shfl_xor_sync(0xffffffffu, b1 ? u10 : u11, 2);
+                        const uint64_t k0 = b1 ? u01 : u00, k1 = b1 ? u11 : u10;
+                        if (DIAG && (P.diag & 4)) continue;
+                        st_cs_f8(qb + P.off8[16 * ch + i + q], b1 ? r0 : k0, b1 ? r1 : k1, b1 ? k0 : r0,
+                                 b1 ? k1 : r1);
                     }
                     continue;
                 }
@@ -1668,6 +1700,12 @@ void tc_prepare(const ApplyDesc &d, const double *Ucanon, std::vector<char> &pay
         if (low_ok && d.p[0] != 0 && order[0] == 0 && (xall || d.p[0] == 1)) {
             B.xpair = 1;
         }
+        // HQ_TC_XQUAD=1 (experiments): 32-byte stores when bits 0 and 1 are both
+        // free, after a two-stage quad transpose.  Measured slower on the 34q
+        // circuit (3870 vs 3708 ms same box: passes with no low target 54 vs
+        // 48 ms), so the 16-byte pairs stay the default.
+        static const char *xqe = getenv("HQ_TC_XQUAD");
+        B.xquad = B.xpair && d.p[0] > 1 && order[1] == 1 && xqe && xqe[0] == '1';
         for (int n = 0; n < tc::M; ++n) {
             uint64_t ti = 0;
             for (int i = 0; i < tc::SETBITS; ++i)
