@@ -1434,10 +1434,13 @@ static bool tc_use_mode_l(const ApplyDesc &d) {
     static const char *force = getenv("HQ_TC_MODE");
     if (force && force[0] == 'H') return false;
     if (force && force[0] == 'L') return true;
-    // measured on a B200 (bench_sweep.py, n = 32): mode H needs the low bits
-    // to hold gather-set bits; when both bits 0 and 1, or three of bits 0..3,
-    // are targets, mode L is faster (0.91-0.93 vs 0.28-0.81 of HBM peak);
-    // otherwise mode H is (0.85-0.99 vs 0.83-0.91).
+    // measured on a B200 (bench_sweep.py, n = 32 dense state, same box,
+    // scripts/ab_modesel.sh): since the mode-H pattern pairs and lane-pair
+    // stores, mode H wins with bits 0 and 1 as the only low targets (0.82-0.87
+    // vs 0.63-0.66 of HBM peak) and with three low targets that leave bit 0 or
+    // bit 1 free (0.65-0.74 vs 0.65-0.68); mode L wins with four or more
+    // targets in bits 0..3 (0.65-0.71 vs 0.28-0.42) and with bits 0, 1 and a
+    // third low bit (0.66 vs 0.60).
     int low = 0;
     bool b0 = false, b1 = false;
     for (int i = 0; i < d.k; ++i) {
@@ -1445,7 +1448,9 @@ static bool tc_use_mode_l(const ApplyDesc &d) {
         b0 |= d.p[i] == 0;
         b1 |= d.p[i] == 1;
     }
-    return (b0 && b1) || low >= 3;
+    static const char *sel = getenv("HQ_TC_MODESEL_V5");   // "1": the earlier rule (experiments)
+    if (sel && sel[0] == '1') return (b0 && b1) || low >= 3;
+    return low >= 4 || (b0 && b1 && low >= 3);
 }
 
 static void tc_prepare_l(const ApplyDesc &d, const double *Ucanon, std::vector<char> &payload,

@@ -16,6 +16,9 @@ PLACEMENTS = ["low", "high", "spread", "random0", "random1", "random2", "random3
 # explicit low-bit placements (mode L of the tensor-core kernel: lowest target < 3)
 LOW6 = ["b:0-1-2-3-4-5", "b:0-7-8-9-10-11", "b:2-3-4-12-13-14", "b:1-5-6-9-14-15", "b:0-2-4-6-8-10"]
 LOW5 = ["b:0-1-2-3-4", "b:0-7-8-9-10", "b:2-3-4-12-13", "b:1-5-6-9-14"]
+# still mode L: four or more targets in bits 0..3, or bits 0, 1 and a third low bit
+LOW6 += ["b:0-1-2-9-12-16", "b:0-1-3-8-12-14", "b:0-1-2-3-12-14", "b:0-1-3-4-5-6"]
+LOW5 += ["b:0-1-2-9-12", "b:0-1-3-12-14", "b:0-1-2-3-14"]
 
 
 @pytest.mark.parametrize("placement", LOW6 + LOW5)
@@ -37,6 +40,11 @@ LOWH6 = ["b:%d-8-9-12-14-16" % b for b in range(7)] + [
     "b:0-3-9-12-14-16", "b:1-2-9-12-14-16", "b:2-3-9-12-14-16", "b:3-5-6-9-12-16", "b:0-4-5-6-12-16",
     "b:0-5-6-8-9-10"]
 LOWH5 = ["b:%d-8-12-14-16" % b for b in range(7)] + ["b:0-3-9-12-16", "b:1-2-9-12-16", "b:0-4-5-6-16"]
+# routed to mode H by the current rule (bits 0 and 1 as the only low targets,
+# or three low targets with bit 0 or bit 1 free; scripts/ab_modesel.sh)
+LOWH6 += ["b:0-1-10-12-14-16", "b:0-1-4-5-6-12", "b:0-1-8-9-10-11", "b:1-2-3-12-14-16",
+          "b:0-2-3-9-12-16", "b:0-2-3-4-5-6", "b:1-2-3-7-8-9"]
+LOWH5 += ["b:0-1-12-14-16", "b:0-1-5-6-9", "b:1-2-3-9-14", "b:0-2-3-9-16", "b:0-2-3-4-5"]
 
 
 @pytest.mark.parametrize("n", [17, 20])
