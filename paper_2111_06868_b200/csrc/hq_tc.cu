@@ -1537,7 +1537,9 @@ static void tc_prepare_l(const ApplyDesc &d, const double *Ucanon, std::vector<c
     static const char *lbulk = getenv("HQ_TC_LBULK");   // "0": cp.async mode L only (experiments)
     // (measured: 0.95 vs 0.83-0.91 of peak for split placements; for a fully
     // contiguous tile, bits 0..11, the cp.async kernel is 1% ahead)
-    if (P.pos[6] == 6 && P.pos[11] != 11 && !(bulk && bulk[0] == '0') && !(lbulk && lbulk[0] == '0')) {
+    // "2": the bulk producer for the fully contiguous tile too (experiments)
+    const bool contig_ok = P.pos[11] != 11 || (lbulk && lbulk[0] == '2');
+    if (P.pos[6] == 6 && contig_ok && !(bulk && bulk[0] == '0') && !(lbulk && lbulk[0] == '0')) {
         std::vector<char> pb(sizeof(tc::ParamsLB) + 1, 0);
         tc::ParamsLB &B = *reinterpret_cast<tc::ParamsLB *>(pb.data());
         B.l = P;
