@@ -438,8 +438,10 @@ double layout_pass_cost(int dtype, int k, const int *bits) {
     if (dtype == HQ_C64 && k >= 5) {
         // tensor-core pass, measured per pass on the sustained 34q circuit
         // (tools/pass_times.py): mode H with <= 1 target in bits 0..3 is the
-        // baseline; 2 such targets cost 1.19x; mode L (bits 0 and 1, or >= 3
-        // targets in bits 0..3) 1.29x.  Since the 16-byte pattern pairs and
+        // baseline; 2 such targets cost 1.19x; 3 or more 1.29x, in mode L
+        // (>= 4 low targets, or bits 0, 1 and a third) as in mode H (the
+        // executor's rule, tc_use_mode_l; bits {0,1} alone now run mode H
+        // and cost like any other pair).  Since the 16-byte pattern pairs and
         // lane-pair stores every measured mode-H pass with
         // <= 1 low target runs at the same ~47 ms, whichever bit it is; a
         // bit-0 bonus (tried: 4037 vs 4050 ms before the lane-pair stores)
@@ -453,8 +455,9 @@ double layout_pass_cost(int dtype, int k, const int *bits) {
         }
         static const char *old_model = getenv("HQ_LAYOUT_V4");   // "1": the round-1 v4 model (experiments)
         if (old_model && old_model[0] == '1') c += lo ? 0.06 + 0.02 * lo : 0.0;
-        else if ((b0 && b1) || lo >= 3) c += 0.29;
-        else if (lo == 2) c += 0.19;
+        else if (lo >= 4 || (b0 && b1 && lo >= 3)) c += 0.29;   // mode L
+        else if (lo == 3) c += 0.29;   // mode H, 0.65-0.79 of peak
+        else if (lo == 2) c += 0.19;   // mode H, incl. bits {0,1} (0.75-0.86)
     } else {
         const int lane_lo = dtype == HQ_C64 ? 1 : 0, lane_hi = lane_lo + 5;
         for (int j = 0; j < k; ++j)
