@@ -5,18 +5,27 @@ random circuit through the C ABI (BASELINE.json metric).
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config 34q] [--kmax 4]
     python bench.py --impl reference ...      # the fp64 CPU oracle arm
 
-A "step" is one pass of the whole hot path over one synthetic circuit:
-fused gate list (planned before the timed region, reported as plan_ms) ->
-every apply pass and remap on the device -> norm.  The state (2^n complex64)
-is initialised to |0> before each step, outside the per-step events.
+A "step" is one pass of the whole hot path over one synthetic circuit: every
+fused apply pass and every remap of the compiled circuit (hq_circuit_run), on
+the device.  The fused gate list and the layout are planned before the timed
+region (reported as plan_ms); the state (2^n complex64) is initialised to |0>
+before each step, outside the per-step CUDA events; the norm is read once
+after the timed region (norm_after).
 
 value  = passes * 2 * (state bytes) / circuit time (whole job, all GPUs),
          device-timed with CUDA events on the library's stream, max over ranks.
 e2e    = the same metric through the public API with host inputs: per step
-         hq_fuse(host gates) + hq_apply_circuit (matrices copied H2D) +
-         hq_norm (D2H), host wall clock.
+         hq_fuse(host gates) + layout + hq_apply_circuit (matrices copied H2D)
+         + hq_norm (the step's result read back to the host), host wall
+         clock; the H2D/D2H byte counts are the library's own (hq_stats).
+         Only the norm comes back: the 128 GiB state is never copied out.
+sweep  = (N=1) the fused-gate sweep of BASELINE configs[2] on the bench's own
+         dense state: one Haar k-qubit gate per k=1..6 at the low / spread /
+         random0 placements, median of 5 passes, as a fraction of the HBM peak.
 For N>1 the same circuit is strong-scaled: the state is sharded on the top
-log2 N qubits and remaps run as NCCL all-to-all exchanges.
+log2 N qubits and remaps run as NCCL exchanges; the line then carries a
+parity object computed through that transport (mirror circuit C.C^dagger
+distance from |0>, pin P9; reversible circuit |x> -> |f(x)> bit-exact, P10).
 """
 import argparse
 import json
@@ -52,6 +61,8 @@ def parse():
     ap.add_argument("--dtype", default="c64", choices=["c64", "c128"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--sweep-reps", type=int, default=5,
+                    help="N=1: passes per fused-gate sweep cell on the bench state (0: no sweep)")
     ap.add_argument("--no-layout", action="store_true",
                     help="keep the default qubit layout instead of hq_plan_layout's")
     return ap.parse_args()
@@ -143,66 +154,140 @@ def traffic_from_profiles(cfg, kmax, path, bytes_per_launch):
 
 
 # ------------------------------------------------------------------ oracle arm
-def oracle_sample(n_full, cycles, seed, kmax, seconds=15.0, n_sample=None, merged=True):
-    """Time the fp64 oracle (as it stands) on a bounded sample of the same
-    workload: the first unfused gates of the same generator's circuit at a
-    smaller n (c128 state must fit host RAM), extrapolated per gate by
-    2^(n_full - n_sample).  Returns (value in the GPU arm's unit, info)."""
-    import numpy as np
+# Fused pass count P of the GPU arm's plan per (config, kmax, planner).  Both
+# arms express their time in the same unit, P * 2 * (c64 state bytes) / T, so
+# the driver's ratio of the two values is the ratio of circuit times.  The GPU
+# arm checks its own P against this table (unit_passes_match); the 34q entry
+# is pinned by tests/test_abi_cpu.py::test_fuse_merged_34q_bench_circuit.
+UNIT_PASSES = {
+    ("12q", 2, "merged"): 43, ("12q", 4, "merged"): 15, ("12q", 5, "merged"): 16, ("12q", 6, "merged"): 11,
+    ("12q", 2, "c7"): 43, ("12q", 4, "c7"): 16, ("12q", 5, "c7"): 17, ("12q", 6, "c7"): 15,
+    ("30q", 2, "merged"): 245, ("30q", 4, "merged"): 100, ("30q", 5, "merged"): 99, ("30q", 6, "merged"): 63,
+    ("30q", 2, "c7"): 245, ("30q", 4, "c7"): 101, ("30q", 5, "c7"): 100, ("30q", 6, "c7"): 67,
+    ("34q", 2, "merged"): 280, ("34q", 4, "merged"): 114, ("34q", 5, "merged"): 112, ("34q", 6, "merged"): 75,
+    ("34q", 2, "c7"): 280, ("34q", 4, "c7"): 116, ("34q", 5, "c7"): 115, ("34q", 6, "c7"): 80,
+    ("36q", 2, "merged"): 360, ("36q", 4, "merged"): 144, ("36q", 5, "merged"): 143, ("36q", 6, "merged"): 96,
+    ("36q", 2, "c7"): 360, ("36q", 4, "c7"): 144, ("36q", 5, "c7"): 144, ("36q", 6, "c7"): 96,
+}
+ORACLE_SAMPLE_N = 26     # the oracle's c128 state at n=26 is 1 GiB; the full 725-gate circuit takes ~15 s
+
+
+class OracleRun:
+    """The fp64 oracle (as it stands, all host threads) on the same
+    generator's circuit at n_sample qubits, gate by gate from |0>; run(m)
+    applies the next m gates and returns their wall time."""
+
+    def __init__(self, n_sample, cycles, seed):
+        import oracle as O
+        from hq_inputs import sycamore_circuit
+        self.O = O
+        self.gates = sycamore_circuit(n_sample, cycles, seed)
+        self.psi = O.init_basis(n_sample, 0)
+        self.next = 0
+
+    def run(self, m):
+        hi = min(self.next + m, len(self.gates))
+        t0 = time.perf_counter()
+        for g in self.gates[self.next:hi]:
+            self.O.apply_gate(self.psi, g.U, g.qubits)
+        dt = time.perf_counter() - t0
+        done, self.next = hi - self.next, hi
+        return dt, done
+
+
+def oracle_unit_value(n_full, cycles, seed, P, seconds, gates_timed, n_sample=ORACLE_SAMPLE_N):
+    """The oracle's time per unfused gate at n_sample, extrapolated x2^(n_full -
+    n_sample) per gate to the n_full circuit, in the GPU arm's unit."""
+    from hq_inputs import sycamore_circuit
+    n_gates_full = len(sycamore_circuit(n_full, cycles, seed))
+    per_gate = seconds / max(gates_timed, 1) * 2 ** (n_full - n_sample)
+    T_full = per_gate * n_gates_full
+    return P * 2 * 8 * 2 ** n_full / T_full / 1e9, T_full
+
+
+def oracle_full_circuit(n, cycles, seed, threads=None):
+    """The whole unfused circuit through the oracle (configs[0] size), wall time."""
     import oracle as O
     from hq_inputs import sycamore_circuit
-    gates_full = sycamore_circuit(n_full, cycles, seed)
-    # the pass count of the unit, from the oracle's own reading of the planner
-    # (C7, plus the merging reading when the GPU arm uses hq_fuse_merged)
-    groups = O.compress(gates_full, kmax)
-    P = len(O.merge_groups(gates_full, groups, kmax)) if merged else len(groups)
-    if n_sample is None:
-        n_sample = min(n_full, 26)
-    gates_s = sycamore_circuit(n_sample, cycles, seed)
-    psi = O.init_basis(n_sample, 0)
-    t0 = time.perf_counter()
-    done = 0
-    for g in gates_s:
-        O.apply_gate(psi, g.U, g.qubits)
-        done += 1
-        if time.perf_counter() - t0 > seconds:
-            break
-    dt = time.perf_counter() - t0
-    per_gate = dt / done * 2 ** (n_full - n_sample)
-    T_full = per_gate * len(gates_full)
-    work = P * 2 * 8 * 2 ** n_full          # same algorithmic bytes as the GPU arm (c64)
-    value = work / T_full / 1e9
-    info = {"sample": "first %d of %d unfused gates of the same generator's circuit at n=%d "
-                      "(c128, %.1f s), extrapolated x2^%d per gate to the %d-gate n=%d circuit"
-                      % (done, len(gates_s), n_sample, dt, n_full - n_sample, len(gates_full), n_full),
-            "extrapolated_circuit_s": T_full, "cores": O.max_threads()}
-    return value, info
+    gates = sycamore_circuit(n, cycles, seed)
+    old = O.max_threads()
+    if threads:
+        O.set_threads(threads)
+    try:
+        t0 = time.perf_counter()
+        O.simulate(n, gates)
+        return time.perf_counter() - t0, len(gates)
+    finally:
+        O.set_threads(old)
+
+
+def cpu_baseline_block(config, kmax, fusion):
+    """cpu_baseline of the N=1 GPU line: the oracle on the complete 26-qubit
+    circuit of the same generator (~15 s, extrapolated per gate to the bench
+    circuit, the same sample the reference arm times), plus the full
+    configs[0] circuit (12q d10) on all host threads and on one thread
+    (SURVEY §8(d) "Oracle timing")."""
+    import oracle as O
+    n, cycles, seed, _, _ = CONFIGS[config]
+    P = UNIT_PASSES[(config, kmax, fusion)]
+    n_s = min(n, ORACLE_SAMPLE_N)
+    run = OracleRun(n_s, cycles, seed)
+    sec, done = run.run(len(run.gates))
+    value, T_full = oracle_unit_value(n, cycles, seed, P, sec, done, n_s)
+    t12, g12 = oracle_full_circuit(12, 10, 0)
+    t12_1, _ = oracle_full_circuit(12, 10, 0, threads=1)
+    return {"value": value, "unit": "GB/s", "cores": O.max_threads(), "kind": "oracle",
+            "sample": "all %d unfused gates of the same generator's circuit at n=%d (c128, %.1f s), "
+                      "extrapolated x2^%d per gate to the n=%d circuit (%.0f s), in the GPU arm's unit "
+                      "(P=%d passes x 2 x c64 state bytes / time)" % (done, n_s, sec, n - n_s, n, T_full, P),
+            "extrapolated_circuit_s": T_full,
+            "config0_full_circuit": {"workload": "12q d10 seed 0 (BASELINE configs[0]), %d unfused gates, fp64"
+                                                 % g12,
+                                     "seconds_all_threads": t12, "threads": O.max_threads(),
+                                     "seconds_1_thread": t12_1}}
 
 
 def run_reference(args):
+    """--impl reference: the fp64 oracle as it stands on the host cores.  The
+    K timed steps together run the complete 26-qubit circuit of the bench's
+    generator once (step i = the i-th contiguous slice of its gates; the
+    same ~15 s sample as the GPU line's cpu_baseline); the W warm-up steps
+    run one gate each.  Value = the extrapolated rate in the GPU arm's unit."""
+    import oracle as O
     world, rank, local = dist_env()
     if rank != 0:
         return 0
     n, cycles, seed, kdef, cidx = CONFIGS[args.config]
     kmax = args.kmax or kdef
-    vals = []
-    info = None
-    per_step = max(2.0, 60.0 / max(args.steps + args.warmup, 1))
-    for i in range(args.warmup + args.steps):
-        v, info = oracle_sample(n, cycles, seed, kmax, seconds=per_step, merged=args.fuse == "merged")
-        if i >= args.warmup:
-            vals.append(v)
-    value = statistics.mean(vals)
+    P = UNIT_PASSES[(args.config, kmax, args.fuse)]
+    n_s = min(n, ORACLE_SAMPLE_N)
+    warm = OracleRun(n_s, cycles, seed)
+    for i in range(args.warmup):
+        warm.run(1)
+    del warm
+    run = OracleRun(n_s, cycles, seed)
+    ng_s = len(run.gates)
+    K = max(args.steps, 1)
+    bounds = [round(i * ng_s / K) for i in range(K + 1)]
+    sec, done = 0.0, 0
+    for i in range(K):
+        t, g = run.run(bounds[i + 1] - bounds[i])
+        sec += t
+        done += g
+    value, T_full = oracle_unit_value(n, cycles, seed, P, sec, done, n_s)
+    sample = ("all %d unfused gates of the same generator's circuit at n=%d (c128, %.1f s) in %d timed slices, "
+              "extrapolated x2^%d per gate to the n=%d circuit" % (done, n_s, sec, K, n - n_s, n))
     line = {
         "impl": "reference", "metric": "state-update GB/s", "value": value, "unit": "GB/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": info["extrapolated_circuit_s"] * 1e3, "higher_is_better": True,
+        "ms_per_step": T_full * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "%s Sycamore-style d%d random circuit (BASELINE configs[%d]), "
-                               "oracle unfused fp64" % (args.config, cycles, cidx),
-                   "n": n, "cycles": cycles, "seed": seed, "kmax": kmax},
-        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": info["cores"], "kind": "oracle",
-                         "sample": info["sample"]},
+                               "oracle unfused fp64; ms_per_step = the extrapolated full-circuit time"
+                               % (args.config, cycles, cidx),
+                   "n": n, "cycles": cycles, "seed": seed, "kmax": kmax, "unit_passes": P},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": O.max_threads(), "kind": "oracle",
+                         "sample": sample},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -331,10 +416,10 @@ def run_hq(args):
             "peak_source": peak_src}
 
     # ---- e2e through the public API with host inputs
-    e2e_ms = []
-    h2d = sum(es * (4 ** len(q)) for q, _ in fused)
+    e2e_ms, e2e_h2d, e2e_d2h = [], [], []
     for i in range(args.e2e_steps + 1 if args.e2e_steps > 0 else 0):
         barrier()
+        st0 = hq.hq_stats_get(state)
         t0 = time.perf_counter()
         hq.hq_state_init_basis(state, 0)
         fz = hq.hq_fuse(gates, kmax, merged=merged)
@@ -346,6 +431,9 @@ def run_hq(args):
         barrier()
         if i > 0:
             e2e_ms.append((time.perf_counter() - t0) * 1e3)
+            st1 = hq.hq_stats_get(state)
+            e2e_h2d.append(st1["h2d_bytes"] - st0["h2d_bytes"])
+            e2e_d2h.append(st1["d2h_bytes"] - st0["d2h_bytes"])
     e2e = None
     if e2e_ms:
         e2e_t = statistics.mean(e2e_ms)
@@ -354,10 +442,24 @@ def run_hq(args):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_t = float(t.item())
         e2e = {"value": work_bytes / (e2e_t * 1e-3) / 1e9, "unit": "GB/s",
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8 * 148 * 16,
+               "h2d_bytes_per_step": int(max(e2e_h2d)), "d2h_bytes_per_step": int(max(e2e_d2h)),
+               "bytes_counted_by": "hq_stats h2d_bytes / d2h_bytes (every host<->device copy the library makes, "
+                                   "this rank)",
                "ms_per_step": e2e_t,
+               "readback": "the norm only (fp64 partial sums); the %.0f GiB state stays on the device"
+                           % (state_bytes / 2 ** 30),
                "api": "hq_fuse + hq_plan_layout + hq_state_set_layout + hq_state_init_basis + "
                       "hq_apply_circuit + hq_norm"}
+
+    # ---- N>1: correctness through the real transport (pins P9, P10)
+    parity = None
+    if world > 1:
+        parity = remap_parity(hq, state, n, gates, kmax, merged, world, rank, dist, torch)
+
+    # ---- N=1: fused-gate sweep (BASELINE configs[2]) on this dense state
+    sweep = None
+    if world == 1 and args.sweep_reps > 0:
+        sweep = run_sweep(hq, torch, psi_t, stream, n, args.dtype, args.sweep_reps)
 
     line = {
         "metric": "state-update GB/s", "value": value, "unit": "GB/s", "n_gpus": world,
@@ -368,6 +470,7 @@ def run_hq(args):
                                % (args.config, cycles, kmax, cidx),
                    "n": n, "cycles": cycles, "seed": seed, "kmax": kmax, "gates": len(gates),
                    "passes": P, "remaps": R, "circuit_sha256": circuit_sha256(gates),
+                   "unit_passes_match": UNIT_PASSES.get((args.config, kmax, args.fuse)) == P,
                    "state_gib": state_bytes / 2 ** 30,
                    "l2": "no flush: state %.0f GiB >> 126 MB L2" % (state_bytes / 2 ** 30),
                    "parallelism": "sv-shard%d" % world,
@@ -383,16 +486,120 @@ def run_hq(args):
         "gpu_launches": launches,
         "clocks": clk,
     }
+    if parity is not None:
+        line["parity"] = parity
+    if sweep is not None:
+        line["sweep"] = sweep
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, inf = oracle_sample(n, cycles, seed, kmax, seconds=15.0, merged=merged)
-        line["cpu_baseline"] = {"value": v, "unit": "GB/s", "cores": inf["cores"], "kind": "oracle",
-                                "sample": inf["sample"]}
+        line["cpu_baseline"] = cpu_baseline_block(args.config, kmax, args.fuse)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def reversible_image(n, gates, x):
+    """f(x) of a permutation circuit by host bit operations (pin P10's
+    definition): the target bits of the index are the column c of each gate
+    (qubits[0] = MSB), the row r with U[r][c] = 1 replaces them."""
+    import numpy as np
+    y = int(x)
+    for g in gates:
+        k = len(g.qubits)
+        c = 0
+        for j, q in enumerate(g.qubits):
+            c |= ((y >> (n - 1 - q)) & 1) << (k - 1 - j)
+        r = int(np.flatnonzero(np.abs(np.asarray(g.U)[:, c]) > 0.5)[0])
+        for j, q in enumerate(g.qubits):
+            b = n - 1 - q
+            y = (y & ~(1 << b)) | (((r >> (k - 1 - j)) & 1) << b)
+    return y
+
+
+def remap_parity(hq, state, n, gates, kmax, merged, world, rank, dist, torch):
+    """Correctness of the sharded path through the NCCL remaps, at full size:
+    mirror circuit C.C^dagger from |0> (pin P9: returns to |0>; distance
+    ||psi - |0>||_2 = sqrt(||psi||^2 - 2 Re psi_0 + 1) <= 1e-4 in complex64)
+    and a reversible circuit of permutation gates on every qubit from a basis
+    state |x> (pin P10: exactly |f(x)>, compared with ==)."""
+    import numpy as np
+    from hq_inputs import Gate, reversible_circuit
+
+    def amp(i):        # amplitude i, owned by one rank; the others contribute 0
+        a = np.zeros(1, dtype=np.complex64)
+        hq.hq_get_amplitudes(state, i, 1, a)
+        owner = 1.0 if a[0] != 0 else 0.0
+        t = torch.tensor([float(a[0].real), float(a[0].imag), owner], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t)
+        return complex(t[0].item(), t[1].item()), t[2].item()
+
+    out = {}
+    mirror = list(gates) + [Gate(g.name + "^dag", g.qubits, np.conj(np.asarray(g.U)).T) for g in reversed(gates)]
+    fz = hq.hq_fuse(mirror, kmax, merged=merged)
+    c = hq.hq_circuit_create(state, fz)
+    info = hq.hq_circuit_info(c)
+    hq.hq_state_init_basis(state, 0)
+    hq.hq_circuit_run(state, c)
+    nrm = hq.hq_norm(state)
+    a0, _ = amp(0)
+    dist_ = float(np.sqrt(max(nrm ** 2 - 2 * a0.real + 1, 0.0)))
+    out["mirror_dist"] = dist_
+    out["mirror_ok"] = dist_ <= 1e-4
+    out["mirror_passes"], out["mirror_remaps"] = info["passes"], info["remaps"]
+    del c
+    rev = reversible_circuit(n, 4 * n, 4242, kmax=3)
+    x = int.from_bytes(np.random.default_rng(4243).bytes(8), "little") & ((1 << n) - 1)
+    y = reversible_image(n, rev, x)
+    fz = hq.hq_fuse(rev, kmax, merged=merged)
+    st0 = hq.hq_stats_get(state)
+    hq.hq_state_init_basis(state, x)
+    hq.hq_apply_circuit(state, fz)
+    st1 = hq.hq_stats_get(state)
+    ay, owners = amp(y)
+    nrm = hq.hq_norm(state)
+    out["reversible_exact"] = bool(ay == 1.0 and owners == 1.0 and nrm == 1.0)
+    out["reversible_remaps"] = st1["remaps"] - st0["remaps"]
+    out["transport"] = "NCCL grouped send/recv between %d ranks" % world
+    return out
+
+
+def run_sweep(hq, torch, psi_t, stream, n, dtype, reps, ks=(1, 2, 3, 4, 5, 6),
+              placements=("low", "spread", "random0")):
+    """BASELINE configs[2] on the bench's own buffer: the dense state the
+    circuit left (a default-layout view of the same memory), one Haar k-qubit
+    gate per (k, placement), 1 warm-up + `reps` passes, CUDA events on the
+    library's stream; fraction of the measured HBM peak per cell."""
+    import numpy as np
+    from hq_inputs import haar_sweep_gate
+    peak, _ = peaks()
+    es = 8 if dtype == "c64" else 16
+    nbytes = 2 * es * 2 ** n
+    s = hq.hq_state_create_from_buffers(n, dtype, psi_t.data_ptr(), stream.cuda_stream)
+    cells = {}
+    for k in ks:
+        for pl in placements:
+            g = haar_sweep_gate(n, k, pl, 2000 + k)
+            hq.hq_apply_matrix(s, g.U, g.qubits)
+            ev = []
+            for _ in range(reps):
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                hq.hq_apply_matrix(s, g.U, g.qubits)
+                b.record(stream)
+                ev.append((a, b))
+            torch.cuda.synchronize()
+            ms = statistics.median(a.elapsed_time(b) for a, b in ev)
+            cells["k%d_%s" % (k, pl)] = {"phys_bits": sorted(n - 1 - q for q in g.qubits), "median_ms": ms,
+                                         "frac": nbytes / (ms * 1e-3) / 1e9 / peak}
+    nrm = hq.hq_norm(s)
+    s.close()
+    return {"workload": "BASELINE configs[2] cells on the %dq bench state (dense after the circuit), "
+                        "median of %d passes" % (n, reps),
+            "cells": cells, "min_frac_k_le_5": min(v["frac"] for key, v in cells.items() if int(key[1]) <= 5),
+            "norm_after": nrm}
 
 
 def main():

@@ -91,6 +91,8 @@ typedef struct hq_stats {
     uint64_t kernel_launches; /* all library kernels launched on this rank         */
     uint64_t hbm_bytes;       /* algorithmic HBM bytes of those kernels (this rank) */
     uint64_t link_bytes;      /* bytes sent to peers by remaps (this rank)         */
+    uint64_t h2d_bytes;       /* host->device bytes the library copied (this rank) */
+    uint64_t d2h_bytes;       /* device->host bytes the library copied (this rank) */
 } hq_stats;
 
 /* ------------------------------------------------------------------ create */
@@ -124,7 +126,14 @@ hq_status hq_state_create_virtual(int n, hq_dtype dtype, int nshards, hq_state *
 
 /* Borrowed-memory variant of the 1-GPU state (e.g. torch.empty buffers):
  * psi = 2^n amplitudes in dtype (16-byte aligned), stream = a cudaStream_t (or
- * NULL for the legacy default stream).  Memory must outlive the state. */
+ * NULL for the legacy default stream).  Memory must outlive the state.
+ * Amplitude-bound rule (both borrowed-buffer constructors): the library keeps
+ * a rigorous bound on ||psi||_2 that the complex64 tensor-core passes use to
+ * scale amplitudes into the FP16 range.  It is updated by every library call
+ * that writes the state.  A caller that writes the borrowed memory itself
+ * (e.g. psi_t.mul_(8) or copy_ between calls) MUST call
+ * hq_state_invalidate_bound (or hq_norm) before the next apply; otherwise
+ * scaled amplitudes may overflow FP16 (inf/NaN results). */
 hq_status hq_state_create_from_buffers(int n, hq_dtype dtype, void *psi_device,
                                        void *stream, hq_state **out);
 
@@ -151,6 +160,10 @@ hq_status hq_state_create_rank_from_buffers(int n, hq_dtype dtype, int world_siz
  * Errors: HQ_ERR_ARG (not a permutation), HQ_ERR_STATE (multi-rank). */
 hq_status hq_state_set_layout(hq_state *s, const int32_t *pi);
 hq_status hq_state_get_layout(const hq_state *s, int32_t *pi_out);
+
+/* Forget the tracked amplitude bound (see the rule above): the next pass that
+ * needs it recomputes it with one norm pass.  Never changes the amplitudes. */
+hq_status hq_state_invalidate_bound(hq_state *s);
 
 /* Frees everything the library owns.  NULL is accepted. */
 hq_status hq_state_destroy(hq_state *s);

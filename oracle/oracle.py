@@ -23,8 +23,16 @@ Contents, each following the passage cited:
 * ``compress`` / ``fused_gates`` -- the greedy fusion rule, reading C7 of
   PAPER P:499-504 (worked example P:510-529), and the fused matrix
   U_group = U_last ... U_first embedded on the ascending support (P:493-494,
-  readings C8, C9); ``merge_groups`` -- the convex group merging of the
-  "merged fusion" reading.
+  readings C8, C9).  The product's further merging of C7 groups
+  (``hq_fuse_merged``) is a planner choice the paper does not fix (many
+  groupings are valid); the oracle holds no transcript of it.
+  Merged plans are checked only through the state they produce (fused vs
+  unfused, and the dense circuit matrix), never grouping against grouping.
+
+* ``reversible_image`` -- pin P10: a basis state |x> through permutation
+  gates (0/1 matrices) is the basis state |f(x)>, with f computed by host bit
+  operations on the index (qubit q <-> index bit n-1-q, reading C1; U acts on
+  column vectors, reading C2).
 
 * ``init_tokens`` / ``project`` / ``probabilities`` -- token product states
    as a Kronecker product of single-qubit
@@ -215,102 +223,11 @@ def compress(gates, kmax):
     return [G["members"] for G in groups]
 
 
-def merge_groups(gates, groups, kmax):
-    """DESIGN.md reading "merged fusion" (section 5.4a), step by step: the
-    dependency graph of the groups has an edge A -> B when some qubit's
-    consecutive uses go from a gate of A to a gate of B.  Scan pairs (A, B)
-    in ascending order and merge B into A when |supp(A) u supp(B)| <= kmax
-    and either (edge A -> B and no other path A -> ... -> B) or (no path
-    between them either way); after every merge restart the scan.  Return
-    the merged groups in topological order (among the ready groups, the one
-    with the smallest gate index first), members in gate order."""
-    ng = len(groups)
-    group_of = {}
-    for G, mem in enumerate(groups):
-        for i in mem:
-            group_of[i] = G
-    members = [sorted(m) for m in groups]
-    supp = [set().union(*[set(gates[i].qubits) for i in m]) for m in groups]
-    succ = [set() for _ in range(ng)]
-    last = {}
-    for i, g in enumerate(gates):
-        G = group_of[i]
-        for q in g.qubits:
-            if q in last and last[q] != G:
-                succ[last[q]].add(G)
-            last[q] = G
-    alive = set(range(ng))
-
-    def other_path(a, b):          # a path a -> x -> ... -> b with x != b
-        stack = [x for x in succ[a] if x != b and x in alive]
-        seen = set(stack)
-        while stack:
-            x = stack.pop()
-            if b in succ[x]:
-                return True
-            for y in succ[x]:
-                if y in alive and y != b and y not in seen:
-                    seen.add(y)
-                    stack.append(y)
-        return False
-
-    def path(a, b):
-        return b in succ[a] or other_path(a, b)
-
-    merged = True
-    while merged:
-        merged = False
-        for a in range(ng):
-            if a not in alive:
-                continue
-            for b in range(ng):
-                if b == a or b not in alive or len(supp[a] | supp[b]) > kmax:
-                    continue
-                if b in succ[a]:
-                    if other_path(a, b):
-                        continue
-                elif a in succ[b] or path(a, b) or path(b, a):
-                    continue
-                supp[a] |= supp[b]
-                members[a] = sorted(members[a] + members[b])
-                members[b] = []
-                alive.discard(b)
-                for x in range(ng):
-                    if b in succ[x]:
-                        succ[x].discard(b)
-                        succ[x].add(a)
-                succ[a] |= succ[b]
-                succ[b] = set()
-                succ[a].discard(a)
-                merged = True
-                break
-            if merged:
-                break
-    indeg = {a: 0 for a in alive}
-    for a in alive:
-        for b in succ[a]:
-            if b in alive:
-                indeg[b] += 1
-    order, done = [], set()
-    while len(done) < len(alive):
-        ready = [a for a in alive if a not in done and indeg[a] == 0]
-        a = min(ready, key=lambda x: members[x][0])
-        done.add(a)
-        for b in succ[a]:
-            if b in alive:
-                indeg[b] -= 1
-        order.append(members[a])
-    return order
-
-
-def fused_gates(gates, kmax, merged=False):
+def fused_gates(gates, kmax):
     """Fused gate list: (ascending support, U_last ... U_first embedded on it)
-    (P:493-494 to_matrix_gate; readings C8, C9); merged=True fuses the groups
-    of merge_groups(compress(...)) instead."""
+    (P:493-494 to_matrix_gate; readings C8, C9)."""
     out = []
     groups = compress(gates, kmax)
-    if merged:
-        groups = merge_groups(gates, groups, kmax)
     for members in groups:
         support = sorted(set().union(*[set(gates[i].qubits) for i in members]))
         pos = {q: j for j, q in enumerate(support)}
@@ -320,6 +237,27 @@ def fused_gates(gates, kmax, merged=False):
             M = embed_dense(m, gates[i].U, [pos[q] for q in gates[i].qubits]) @ M
         out.append((tuple(support), M))
     return out
+
+
+def reversible_image(n, gates, x):
+    """f(x) for a circuit of permutation gates (pin P10): for each gate read
+    the target bits of the index as the column c (qubits[0] = MSB, C2), find
+    the row r with U[r][c] = 1, write r back into the target bits."""
+    y = int(x)
+    for g in gates:
+        k = len(g.qubits)
+        c = 0
+        for j, q in enumerate(g.qubits):
+            c |= ((y >> (n - 1 - q)) & 1) << (k - 1 - j)
+        col = np.asarray(g.U)[:, c]
+        rows = np.flatnonzero(np.abs(col) > 0.5)
+        if len(rows) != 1 or np.count_nonzero(col) != 1 or col[rows[0]] != 1:
+            raise OracleError("not a permutation gate")
+        r = int(rows[0])
+        for j, q in enumerate(g.qubits):
+            b = n - 1 - q
+            y = (y & ~(1 << b)) | (((r >> (k - 1 - j)) & 1) << b)
+    return y
 
 
 # ---------------------------------------------------------------- f4: tokens, projection

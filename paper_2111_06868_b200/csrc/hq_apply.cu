@@ -498,12 +498,9 @@ template <int K>
 static cudaError_t launch_ztile(void *psi, const GenParams &P, const void *dU, cudaStream_t st) {
     constexpr int D = 1 << K;
     constexpr size_t smem = sizeof(double2) * (D * D + 2 * D * ZT_SETS);
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(apply_ztile<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    static std::atomic<uint64_t> attr{0};
+    cudaError_t e = smem_attr_once(apply_ztile<K>, (int)smem, attr);
+    if (e != cudaSuccess) return e;
     const uint64_t ntiles = P.nsets / ZT_SETS;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -634,22 +631,14 @@ int launch_circuit_smem(int dtype, void *psi, int nl, const SmemOp *dev_ops, int
     const size_t smem = (2 * es << nl) + es * 64 * 64 + 64 * sizeof(int);
     const int threads = nl >= 10 ? 1024 : (1 << nl) < 32 ? 32 : (1 << nl);
     if (dtype == HQ_C64) {
-        static bool attr = false;
-        if (!attr) {
-            cudaError_t e = cudaFuncSetAttribute(circuit_smem<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)((2 * 8 << SMEM_CIRCUIT_MAX_NL_C64) + 8 * 64 * 64 + 256));
-            if (e != cudaSuccess) return (int)e;
-            attr = true;
-        }
+        static std::atomic<uint64_t> attr{0};
+        cudaError_t e = smem_attr_once(circuit_smem<float>, (int)((2 * 8 << SMEM_CIRCUIT_MAX_NL_C64) + 8 * 64 * 64 + 256), attr);
+        if (e != cudaSuccess) return (int)e;
         circuit_smem<float><<<1, threads, smem, st>>>((float2 *)psi, nl, dev_ops, nops, (const float2 *)dev_mats);
     } else {
-        static bool attr = false;
-        if (!attr) {
-            cudaError_t e = cudaFuncSetAttribute(circuit_smem<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)((2 * 16 << SMEM_CIRCUIT_MAX_NL_C128) + 16 * 64 * 64 + 256));
-            if (e != cudaSuccess) return (int)e;
-            attr = true;
-        }
+        static std::atomic<uint64_t> attr{0};
+        cudaError_t e = smem_attr_once(circuit_smem<double>, (int)((2 * 16 << SMEM_CIRCUIT_MAX_NL_C128) + 16 * 64 * 64 + 256), attr);
+        if (e != cudaSuccess) return (int)e;
         circuit_smem<double><<<1, threads, smem, st>>>((double2 *)psi, nl, dev_ops, nops, (const double2 *)dev_mats);
     }
     return (int)cudaGetLastError();

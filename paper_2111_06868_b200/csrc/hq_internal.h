@@ -2,6 +2,7 @@
 // Product code only: nothing here is shared with oracle/.
 #pragma once
 
+#include <atomic>
 #include <cstdint>
 #include <cstddef>
 #include <string>
@@ -16,6 +17,22 @@ namespace hq {
 // ------------------------------------------------------------------ errors
 hq_status set_error(hq_status st, const char *fmt, ...);
 void clear_error();
+
+// ------------------------------------------------------------------ launch helpers
+// The dynamic shared-memory limit of a kernel is a per-device setting: raise
+// it once per (kernel, device), tracked in a per-kernel device bitmask (a
+// multi-device state launches the same kernel on several devices).
+template <class Kern>
+inline cudaError_t smem_attr_once(Kern kernel, int bytes, std::atomic<uint64_t> &done) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const uint64_t bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+    return e;
+}
 
 // ------------------------------------------------------------------ planner (hq_plan.cpp)
 struct GateRef {            // validated view of an hq_gate

@@ -85,13 +85,21 @@ struct Shard {
     double *d_red = nullptr;      // reduced-density-matrix partials (lazy)
     double *h_red = nullptr;      // pinned
     size_t red_cap = 0;           // doubles in d_red / h_red
+    double *d_ar = nullptr;       // all-reduce scratch (rank mode), AR_CAP doubles
+    double *h_ar = nullptr;       // pinned
     Arena arena;
+    // profiling events, created on this shard's device (an event must be
+    // recorded on a stream of the device it was created on)
+    std::vector<cudaEvent_t> ev_pool;
 };
+
+constexpr int AR_CAP = 1024;      // largest host all-reduce: 2^10 outcome probabilities
 
 struct ProfEvent {
     cudaEvent_t a, b;
     uint64_t bytes;
     int path;
+    int shard;
 };
 
 struct ProfAcc {
@@ -116,7 +124,6 @@ struct hq_state {
     hq_stats stats{};
     bool profiling = false;
     std::vector<ProfEvent> prof;  // pending
-    std::vector<cudaEvent_t> ev_pool;
     ProfAcc acc[3];               // per kernel family (PATH_REG, PATH_GEN, PATH_TC)
 };
 
@@ -156,6 +163,15 @@ static int ilog2(int x) {
     return l;
 }
 
+// Host<->device copy on a shard stream that also counts the bytes in the
+// state's statistics (the bench's e2e byte counts come from here).
+static cudaError_t copy_async(hq_stats &stats, void *dst, const void *src, size_t bytes, cudaMemcpyKind kind,
+                              cudaStream_t stream) {
+    if (kind == cudaMemcpyHostToDevice) stats.h2d_bytes += bytes;
+    if (kind == cudaMemcpyDeviceToHost) stats.d2h_bytes += bytes;
+    return cudaMemcpyAsync(dst, src, bytes, kind, stream);
+}
+
 static hq_status arena_init(Shard &s, size_t cap) {
     CUDA_TRY(cudaSetDevice(s.device));
     CUDA_TRY(cudaMalloc((void **)&s.arena.dev, cap));
@@ -167,7 +183,7 @@ static hq_status arena_init(Shard &s, size_t cap) {
 
 // Copy `bytes` of host data to the device arena (stream-ordered); returns the
 // device pointer.  When full, synchronise the stream and restart.
-static hq_status arena_push(Shard &s, const void *src, size_t bytes, void **dev_out) {
+static hq_status arena_push(hq_state *st, Shard &s, const void *src, size_t bytes, void **dev_out) {
     const size_t a = (bytes + 255) & ~(size_t)255;
     if (a > s.arena.cap) return set_error(HQ_ERR_ARG, "matrix larger than staging arena");
     if (s.arena.off + a > s.arena.cap) {
@@ -175,8 +191,8 @@ static hq_status arena_push(Shard &s, const void *src, size_t bytes, void **dev_
         s.arena.off = 0;
     }
     memcpy(s.arena.host + s.arena.off, src, bytes);
-    CUDA_TRY(cudaMemcpyAsync(s.arena.dev + s.arena.off, s.arena.host + s.arena.off, bytes,
-                             cudaMemcpyHostToDevice, s.stream));
+    CUDA_TRY(copy_async(st->stats, s.arena.dev + s.arena.off, s.arena.host + s.arena.off, bytes,
+                        cudaMemcpyHostToDevice, s.stream));
     *dev_out = s.arena.dev + s.arena.off;
     s.arena.off += a;
     return HQ_OK;
@@ -223,6 +239,9 @@ static void shard_free(Shard &s) {
     if (s.h_part) cudaFreeHost(s.h_part);
     if (s.d_red) cudaFree(s.d_red);
     if (s.h_red) cudaFreeHost(s.h_red);
+    if (s.d_ar) cudaFree(s.d_ar);
+    if (s.h_ar) cudaFreeHost(s.h_ar);
+    for (auto e : s.ev_pool) cudaEventDestroy(e);
     if (s.arena.dev) cudaFree(s.arena.dev);
     if (s.arena.host) cudaFreeHost(s.arena.host);
     if (s.comm) ncclCommDestroy(s.comm);
@@ -474,11 +493,21 @@ extern "C" hq_status hq_state_create_from_buffers(int n, hq_dtype dtype, void *p
 extern "C" hq_status hq_state_destroy(hq_state *st) {
     clear_error();
     if (!st) return HQ_OK;
-    for (auto &p : st->prof) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
-    for (auto e : st->ev_pool) cudaEventDestroy(e);
+    for (auto &p : st->prof) {
+        cudaSetDevice(st->sh[p.shard].device);
+        cudaEventDestroy(p.a);
+        cudaEventDestroy(p.b);
+    }
     // virtual shards share shard 0's stream: free others first
     for (size_t i = st->sh.size(); i-- > 0;) shard_free(st->sh[i]);
     delete st;
+    return HQ_OK;
+}
+
+extern "C" hq_status hq_state_invalidate_bound(hq_state *st) {
+    clear_error();
+    if (!st) return set_error(HQ_ERR_ARG, "state is NULL");
+    st->amp_bound = -1.0;
     return HQ_OK;
 }
 
@@ -623,14 +652,16 @@ static void prepare(hq_dtype dt, const double *U, int k, const int *phys, int nl
 
 static hq_status prof_begin(hq_state *st, Shard &s, ProfEvent &pe) {
     if (!st->profiling) return HQ_OK;
+    CUDA_TRY(cudaSetDevice(s.device));
     auto take = [&]() {
         cudaEvent_t e;
-        if (!st->ev_pool.empty()) { e = st->ev_pool.back(); st->ev_pool.pop_back(); }
+        if (!s.ev_pool.empty()) { e = s.ev_pool.back(); s.ev_pool.pop_back(); }
         else cudaEventCreate(&e);
         return e;
     };
     pe.a = take();
     pe.b = take();
+    pe.shard = (int)(&s - st->sh.data());
     CUDA_TRY(cudaEventRecord(pe.a, s.stream));
     return HQ_OK;
 }
@@ -881,7 +912,7 @@ static hq_status run_ops(hq_state *st, const std::vector<GateRef> &refs, const s
                 Shard &s = st->sh[r];
                 if (cond) prepare_cond(st, g, op, s.rank, p);
                 void *dU = nullptr;
-                if (!p.payload.empty() && (rc = arena_push(s, p.payload.data(), p.payload.size(), &dU)))
+                if (!p.payload.empty() && (rc = arena_push(st, s, p.payload.data(), p.payload.size(), &dU)))
                     return rc;
                 if ((rc = exec_prep(st, s, p, dU))) return rc;
             }
@@ -1088,8 +1119,12 @@ extern "C" hq_status hq_circuit_run(hq_state *st, hq_circuit *c) {
         st->pi = c->pi_end;
         return HQ_OK;
     }
+    bool has_cond = false;
+    for (auto &cp : c->cprep) has_cond |= !cp.empty();
+    // rank-dependent (row f1) ops keep their own per-launch scales and bounds:
+    // such circuits run op by op
     const bool graphable = st->sh.size() == 1 && !st->profiling && c->remaps == 0 && c->permutes == 0 &&
-                           !c->ops.empty();
+                           !c->ops.empty() && !has_cond;
     if (!graphable) {
         if ((rc = circuit_run_ops(st, c))) return rc;
         st->pi = c->pi_end;
@@ -1239,8 +1274,8 @@ static hq_status io_amplitudes(hq_state *st, uint64_t first, uint64_t count, voi
             if (a >= b) continue;
             char *h = (char *)host + (a - first) * es;
             char *d = (char *)s.psi + (a - lo) * es;
-            if (get) CUDA_TRY(cudaMemcpyAsync(h, d, (b - a) * es, cudaMemcpyDeviceToHost, s.stream));
-            else CUDA_TRY(cudaMemcpyAsync(d, h, (b - a) * es, cudaMemcpyHostToDevice, s.stream));
+            if (get) CUDA_TRY(copy_async(st->stats, h, d, (b - a) * es, cudaMemcpyDeviceToHost, s.stream));
+            else CUDA_TRY(copy_async(st->stats, d, h, (b - a) * es, cudaMemcpyHostToDevice, s.stream));
             CUDA_TRY(cudaStreamSynchronize(s.stream));
             continue;
         }
@@ -1260,13 +1295,13 @@ static hq_status io_amplitudes(hq_state *st, uint64_t first, uint64_t count, voi
             if (get) {
                 e = launch_gather((int)st->dtype, s.psi, tmp, first + off, c, st->n, st->nl, bitmap.data(), s.rank, s.stream);
                 if (e) { cudaFree(tmp); return set_error(HQ_ERR_CUDA, "gather launch failed"); }
-                cudaError_t ce = cudaMemcpyAsync(h.data(), tmp, c * es, cudaMemcpyDeviceToHost, s.stream);
+                cudaError_t ce = copy_async(st->stats, h.data(), tmp, c * es, cudaMemcpyDeviceToHost, s.stream);
                 if (!ce) ce = cudaStreamSynchronize(s.stream);
                 if (ce) { cudaFree(tmp); return set_error(HQ_ERR_CUDA, "gather copy: %s", cudaGetErrorString(ce)); }
                 for (uint64_t j : own) memcpy((char *)host + (off + j) * es, h.data() + j * es, es);
             } else {
                 memcpy(h.data(), (const char *)host + off * es, c * es);
-                cudaError_t ce = cudaMemcpyAsync(tmp, h.data(), c * es, cudaMemcpyHostToDevice, s.stream);
+                cudaError_t ce = copy_async(st->stats, tmp, h.data(), c * es, cudaMemcpyHostToDevice, s.stream);
                 if (ce) { cudaFree(tmp); return set_error(HQ_ERR_CUDA, "scatter copy: %s", cudaGetErrorString(ce)); }
                 e = launch_scatter((int)st->dtype, s.psi, tmp, first + off, c, st->n, st->nl, bitmap.data(), s.rank, s.stream);
                 if (e) { cudaFree(tmp); return set_error(HQ_ERR_CUDA, "scatter launch failed"); }
@@ -1297,25 +1332,32 @@ extern "C" hq_status hq_norm(hq_state *st, double *out) {
     clear_error();
     if (!st || !out) return set_error(HQ_ERR_ARG, "NULL argument");
     double total = 0.0;
-    for (auto &s : st->sh) {
+    // enqueue every shard's partial sums and their copy-back first, then
+    // synchronise, so the devices of a multi-device state work concurrently
+    std::vector<int> nbs(st->sh.size(), 0);
+    for (size_t i = 0; i < st->sh.size(); ++i) {
+        Shard &s = st->sh[i];
         CUDA_TRY(cudaSetDevice(s.device));
-        int nb = 0;
-        int e = launch_norm_partials((int)st->dtype, s.psi, 1ull << st->nl, s.d_part, 148 * 16, s.stream, &nb);
+        int e = launch_norm_partials((int)st->dtype, s.psi, 1ull << st->nl, s.d_part, 148 * 16, s.stream, &nbs[i]);
         if (e) return set_error(HQ_ERR_CUDA, "norm launch: %s", cudaGetErrorString((cudaError_t)e));
         st->stats.kernel_launches++;
         st->stats.hbm_bytes += st->es << st->nl;
-        CUDA_TRY(cudaMemcpyAsync(s.h_part, s.d_part, sizeof(double) * nb, cudaMemcpyDeviceToHost, s.stream));
+        CUDA_TRY(copy_async(st->stats, s.h_part, s.d_part, sizeof(double) * nbs[i], cudaMemcpyDeviceToHost, s.stream));
+    }
+    for (size_t i = 0; i < st->sh.size(); ++i) {
+        Shard &s = st->sh[i];
+        CUDA_TRY(cudaSetDevice(s.device));
         CUDA_TRY(cudaStreamSynchronize(s.stream));
         double acc = 0.0;
-        for (int b = 0; b < nb; ++b) acc += s.h_part[b];
+        for (int b = 0; b < nbs[i]; ++b) acc += s.h_part[b];
         total += acc;
     }
     if (st->mode == MODE_RANK) {
         Shard &s = st->sh[0];
         s.h_part[0] = total;
-        CUDA_TRY(cudaMemcpyAsync(s.d_part, s.h_part, sizeof(double), cudaMemcpyHostToDevice, s.stream));
+        CUDA_TRY(copy_async(st->stats, s.d_part, s.h_part, sizeof(double), cudaMemcpyHostToDevice, s.stream));
         NCCL_TRY(ncclAllReduce(s.d_part, s.d_part, 1, ncclDouble, ncclSum, s.comm, s.stream));
-        CUDA_TRY(cudaMemcpyAsync(s.h_part, s.d_part, sizeof(double), cudaMemcpyDeviceToHost, s.stream));
+        CUDA_TRY(copy_async(st->stats, s.h_part, s.d_part, sizeof(double), cudaMemcpyDeviceToHost, s.stream));
         CUDA_TRY(cudaStreamSynchronize(s.stream));
         total = s.h_part[0];
     }
@@ -1388,19 +1430,23 @@ extern "C" hq_status hq_state_init_tokens(hq_state *st, const char *tokens) {
     return HQ_OK;
 }
 
+// Sum `count` host doubles over the ranks (rank mode): one ncclAllReduce
+// through a persistent device scratch (allocated on first use).
 static hq_status allreduce_host(hq_state *st, double *v, int count) {
     if (st->mode != MODE_RANK) return HQ_OK;
+    if (count > AR_CAP) return set_error(HQ_ERR_ARG, "internal: all-reduce of %d > %d doubles", count, AR_CAP);
     Shard &s = st->sh[0];
-    double *d = nullptr;
     CUDA_TRY(cudaSetDevice(s.device));
-    CUDA_TRY(cudaMalloc((void **)&d, sizeof(double) * count));
-    cudaError_t ce = cudaMemcpyAsync(d, v, sizeof(double) * count, cudaMemcpyHostToDevice, s.stream);
-    ncclResult_t nr = ce ? ncclSuccess : ncclAllReduce(d, d, count, ncclDouble, ncclSum, s.comm, s.stream);
-    if (!ce && nr == ncclSuccess) ce = cudaMemcpyAsync(v, d, sizeof(double) * count, cudaMemcpyDeviceToHost, s.stream);
-    if (!ce) ce = cudaStreamSynchronize(s.stream);
-    cudaFree(d);
-    if (nr != ncclSuccess) return set_error(HQ_ERR_NCCL, "ncclAllReduce: %s", ncclGetErrorString(nr));
-    if (ce) return set_error(HQ_ERR_CUDA, "allreduce copy: %s", cudaGetErrorString(ce));
+    if (!s.d_ar) {
+        CUDA_TRY(cudaMalloc((void **)&s.d_ar, sizeof(double) * AR_CAP));
+        CUDA_TRY(cudaMallocHost((void **)&s.h_ar, sizeof(double) * AR_CAP));
+    }
+    memcpy(s.h_ar, v, sizeof(double) * count);
+    CUDA_TRY(copy_async(st->stats, s.d_ar, s.h_ar, sizeof(double) * count, cudaMemcpyHostToDevice, s.stream));
+    NCCL_TRY(ncclAllReduce(s.d_ar, s.d_ar, count, ncclDouble, ncclSum, s.comm, s.stream));
+    CUDA_TRY(copy_async(st->stats, s.h_ar, s.d_ar, sizeof(double) * count, cudaMemcpyDeviceToHost, s.stream));
+    CUDA_TRY(cudaStreamSynchronize(s.stream));
+    memcpy(v, s.h_ar, sizeof(double) * count);
     return HQ_OK;
 }
 
@@ -1432,7 +1478,7 @@ extern "C" hq_status hq_project(hq_state *st, const int32_t *qubits, const int32
         if (e) return set_error(HQ_ERR_CUDA, "project launch: %s", cudaGetErrorString((cudaError_t)e));
         st->stats.kernel_launches++;
         st->stats.hbm_bytes += (uint64_t)2 * (st->es << st->nl);
-        CUDA_TRY(cudaMemcpyAsync(s.h_part, s.d_part, sizeof(double) * nb, cudaMemcpyDeviceToHost, s.stream));
+        CUDA_TRY(copy_async(st->stats, s.h_part, s.d_part, sizeof(double) * nb, cudaMemcpyDeviceToHost, s.stream));
         CUDA_TRY(cudaStreamSynchronize(s.stream));
         double acc = 0.0;
         for (int b = 0; b < nb; ++b) acc += s.h_part[b];
@@ -1476,7 +1522,7 @@ extern "C" hq_status hq_probabilities(hq_state *st, const int32_t *qubits, int n
         int e = launch_probabilities((int)st->dtype, s.psi, 1ull << st->nl, P, dh, nb_max, s.stream, &nb);
         if (e) { cudaFree(dh); return set_error(HQ_ERR_CUDA, "probabilities launch: %s", cudaGetErrorString((cudaError_t)e)); }
         std::vector<double> h((size_t)nb << nloc);
-        cudaError_t ce = cudaMemcpyAsync(h.data(), dh, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, s.stream);
+        cudaError_t ce = copy_async(st->stats, h.data(), dh, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, s.stream);
         if (!ce) ce = cudaStreamSynchronize(s.stream);
         cudaFree(dh);
         if (ce) return set_error(HQ_ERR_CUDA, "probabilities copy: %s", cudaGetErrorString(ce));
@@ -1588,7 +1634,7 @@ extern "C" hq_status hq_reduced_dm(hq_state *st, const int32_t *qubits, int k, d
         if (e) return set_error(HQ_ERR_CUDA, "reduced_dm launch: %s", cudaGetErrorString((cudaError_t)e));
         st->stats.kernel_launches++;
         st->stats.hbm_bytes += st->es << st->nl;
-        CUDA_TRY(cudaMemcpyAsync(s.h_red, s.d_red, sizeof(double) * 2 * E * nb, cudaMemcpyDeviceToHost, s.stream));
+        CUDA_TRY(copy_async(st->stats, s.h_red, s.d_red, sizeof(double) * 2 * E * nb, cudaMemcpyDeviceToHost, s.stream));
         CUDA_TRY(cudaStreamSynchronize(s.stream));
         for (int b = 0; b < nb; ++b)
             for (int x = 0; x < 2 * E; ++x) acc[x] += s.h_red[(size_t)b * 2 * E + x];
@@ -1719,7 +1765,7 @@ extern "C" hq_status hq_reduced_dm_batched(hq_state *st, int nb, const int32_t *
     if (e) return set_error(HQ_ERR_CUDA, "reduced_dm_batched launch: %s", cudaGetErrorString((cudaError_t)e));
     st->stats.kernel_launches++;
     st->stats.hbm_bytes += st->es << st->nl;
-    CUDA_TRY(cudaMemcpyAsync(s.h_red, s.d_red, sizeof(double) * 2 * E * nblk * S, cudaMemcpyDeviceToHost, s.stream));
+    CUDA_TRY(copy_async(st->stats, s.h_red, s.d_red, sizeof(double) * 2 * E * nblk * S, cudaMemcpyDeviceToHost, s.stream));
     CUDA_TRY(cudaStreamSynchronize(s.stream));
     for (int sh = 0; sh < S; ++sh) {
         double acc[2 * 36] = {0};
@@ -1806,7 +1852,7 @@ extern "C" hq_status hq_kraus_sample_batched(hq_state *st, int nb, const double 
         chosen_out[sh] = pick[sh];
     }
     void *dm = nullptr;
-    if ((rc = arena_push(s, mats.data(), mats.size(), &dm))) return rc;
+    if ((rc = arena_push(st, s, mats.data(), mats.size(), &dm))) return rc;
     const RdmParams P = rdm_params(st, qubits, k);
     int e = launch_apply_batched((int)st->dtype, s.psi, 1ull << st->nl, P, dm, st->n - nb, s.stream);
     if (e) return set_error(HQ_ERR_CUDA, "apply_batched launch: %s", cudaGetErrorString((cudaError_t)e));
@@ -1908,7 +1954,7 @@ extern "C" hq_status hq_dm_trace(hq_state *st, double *re, double *im) {
                                 reinterpret_cast<double2 *>(s.d_part), 148 * 8, s.stream, &nb);
         if (e) return set_error(HQ_ERR_CUDA, "dm_trace launch: %s", cudaGetErrorString((cudaError_t)e));
         st->stats.kernel_launches++;
-        CUDA_TRY(cudaMemcpyAsync(s.h_part, s.d_part, sizeof(double) * 2 * nb, cudaMemcpyDeviceToHost, s.stream));
+        CUDA_TRY(copy_async(st->stats, s.h_part, s.d_part, sizeof(double) * 2 * nb, cudaMemcpyDeviceToHost, s.stream));
         CUDA_TRY(cudaStreamSynchronize(s.stream));
         for (int b = 0; b < nb; ++b) { t[0] += s.h_part[2 * b]; t[1] += s.h_part[2 * b + 1]; }
     }
@@ -1968,8 +2014,8 @@ extern "C" hq_status hq_kernel_times(hq_state *st, int path, uint64_t *count, do
         a.total += ms;
         a.max = std::max(a.max, (double)ms);
         a.bytes += p.bytes;
-        st->ev_pool.push_back(p.a);
-        st->ev_pool.push_back(p.b);
+        st->sh[p.shard].ev_pool.push_back(p.a);
+        st->sh[p.shard].ev_pool.push_back(p.b);
     }
     st->prof.clear();
     ProfAcc r;

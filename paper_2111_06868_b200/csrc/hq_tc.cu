@@ -6,45 +6,38 @@
 // so the SIMT kernel cannot keep up with HBM; the per-tile complex matvec is a
 // real dense contraction.
 //
-// Formulation (one tile = 128 gather sets of a K-target gate, KD = 2^(K+1)):
-//   D[m][n] = sum_kk A[m][kk] * B[kk][n]
-//   A = the tile, lane m = gather set, column kk = 2c+f: (re, im)_f of
-//       amplitude c (the natural interleaved layout of one set), in TMEM,
-//       written by the converter warps with tcgen05.st;
-//   B = real embedding of U: B[2c+f][2r+e] = [[Ur,-Ui],[Ui,Ur]]_{ef}, K-major
-//       in shared memory (loaded once per persistent CTA);
-//   D = output tile in TMEM, lane m = set, column 2r+e = (re, im) of w_r, so
-//       each epilogue thread owns a whole output gather set and its global
-//       stores (lanes = consecutive sets) are fully coalesced.
-// Precision: a 3-term split product with FP32 accumulation
-// in TMEM, D = Alo.Bhi + Ahi.Blo + Ahi.Bhi, each operand carried as hi + lo
-// with 11-bit significands (~22 bits together, FP32-class; a single-term
-// TF32/FP16 product fails the 1e-4 bound).  Mode H uses FP16 operands
-// (kind::f16, K = 16 per MMA: half the MMAs of TF32, which matters under the
-// 1 kW power cap).  The FP16 range is handled by exact power-of-two scaling:
-// B = U 2^ue (host, per gate) and A = psi 2^ea with ea chosen by the runtime
-// from its rigorous bound on max |amplitude| (the tracked state norm), so that
-// every scaled amplitude is <= 2^14 < 65504; amplitudes 2^-28 below the bound
-// and smaller lose relative precision gracefully (absolute error <= 2^-38 of
-// the bound).  Mode L (below) uses TF32 (kind::tf32), which needs no scaling.
+// Two orientations of the same contraction, both with FP16 operands
+// (tcgen05.mma kind::f16, K = 16 per MMA), FP32 accumulation in TMEM and a
+// 3-term split product D = Alo.Bhi + Ahi.Blo + Ahi.Bhi:
+//   mode H (apply_tcb): lane = gather set.  A = the tile in TMEM (packed
+//     f16x2, column c = amplitude c of the set), B = real embedding of U in
+//     shared memory, B[2c+f][2r+e] = [[Ur,-Ui],[Ui,Ur]]_{ef}; each epilogue
+//     thread owns a whole output gather set.  Used whenever the highest target
+//     is at bit >= 7 and at most three targets sit in bits 0..3.
+//   mode L (apply_tcL): lane = output real.  A = real embedding of U in TMEM,
+//     B = the tile in shared memory (K-major SWIZZLE_128B, row = gather set).
+//     Used for gathers concentrated in the lowest bits.
+// Precision: each operand is carried as hi + lo with
+// 11-bit significands (~22 bits together, FP32-class; a single-term TF32/FP16
+// product fails the 1e-4 bound).  The FP16 range is handled by exact
+// power-of-two scaling: U 2^ue (host, per gate) and psi 2^ea with ea chosen by
+// the runtime from its rigorous bound on max |amplitude| (the tracked state
+// norm), so that every scaled amplitude is <= 2^14 < 65504; amplitudes 2^-28
+// below the bound and smaller lose relative precision gracefully (absolute
+// error <= 2^-38 of the bound).
 //
-// Warp roles (persistent, one CTA per SM, static round-robin tiles):
-//   warps 0-3   epilogue: TMEM -> registers (tcgen05.ld) -> global stores.
-//   warp  4     MMA issuer: one elect.sync lane issues 3 * KD/8 tcgen05.mma
-//               per tile (M = 128, N = KD, K = 8).
-//   warps 5-12  converters: group h (4 warps, one per TMEM lane quarter) owns
-//               the K-half h of the tile: global loads of its set's
-//               amplitudes, hi/lo split, tcgen05.st into the A ring.
-// TMEM columns: A half h: hi [h*KD, h*KD+KD/2), lo [h*KD+KD/2, (h+1)*KD);
-//               accumulator d: [2*KD + d*KD, 2*KD + (d+1)*KD).
-// Synchronisation: mbarriers full[h]/empty[h] (converters <-> MMA per K-half)
-// and tfull[d]/tempty[d] (MMA <-> epilogue, double-buffered accumulator).
+// Both kernels are persistent (one CTA per SM, static round-robin tiles) and
+// warp-specialised: epilogue warps (TMEM -> registers -> global stores), one
+// MMA-issuing warp (elect.sync), converter warps (shared memory -> FP16 hi/lo
+// -> TMEM or swizzled shared memory) and TMA bulk-copy producer warps; mbarrier
+// pairs hand every ring slot, A buffer and accumulator between the roles.
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <algorithm>
 #include <cmath>
+#include <atomic>
 #include <cstring>
 #include <vector>
 
@@ -63,26 +56,8 @@ constexpr int CONV0 = NUM_EPI + 1;
 constexpr int THREADS = (NUM_EPI + 1 + NUM_CONV) * 32;
 constexpr int BAR_BYTES = 128;
 // mode H: 8 converter warps (2 per TMEM lane quarter, each owning one K-half
-// of its gather set) prefetching the next tile with cp.async into a 2-tile
-// shared-memory ring, so loads stay in flight while a tile is converted
+// of its gather set)
 constexpr int H_NUM_CONV = 8;
-constexpr int H_THREADS = (NUM_EPI + 1 + H_NUM_CONV) * 32;
-
-template <int K> struct Cfg {
-    static constexpr int D = 1 << K;             // amplitudes per gather set
-    static constexpr int KD = 2 * D;             // reals per set = MMA N = reduction length
-    static constexpr int N = KD;
-    static constexpr int HALF_AMPS = D / 2;      // amplitudes per K-half
-    static constexpr int B_BYTES = N * KD * 2;   // one of Bhi / Blo (fp16)
-    static constexpr int RAW_BYTES = H_NUM_CONV * 32 * HALF_AMPS * 8;   // one prefetched tile
-    static constexpr int SMEM = 2 * B_BYTES + BAR_BYTES + 2 * RAW_BYTES;
-    // TMEM columns (32-bit; A holds packed f16x2 = one complex amplitude):
-    //   A half h: hi [h*KD/2, h*KD/2 + KD/4), lo [h*KD/2 + KD/4, (h+1)*KD/2)
-    //   accumulator d: [KD + d*N, KD + (d+1)*N)
-    static constexpr int A_COLS = KD;
-    static constexpr int TMEM_COLS = K == 6 ? 512 : (K == 5 ? 256 : 128);
-    static constexpr int LBO = N * 16;           // K-chunk (8 fp16) stride in the B layout
-};
 
 struct Params {
     uint64_t off[64];      // amplitude offset of canonical target pattern c
@@ -111,7 +86,7 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 // completes (or the hint expires) instead of spinning on the issue slots.
 // In apply_tcb the converters wait ~40% of the time for bulk copies; spinning
 // cost ~16% of all issued instructions (ncu source view) and power under the
-// 1 kW cap.  HQ_TC_SPIN=1 selects plain spinning (experiments).
+// 1 kW cap.
 __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
@@ -150,12 +125,15 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint3
     return d;
 }
 
-__device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
-                                       uint32_t idesc, uint32_t acc) {
+// D (+)= A B with A in TMEM (packed f16x2 per 32-bit column), B from a
+// shared-memory descriptor; FP16 operands, FP32 accumulator (kind::f16; the
+// instruction descriptor's A/B format fields are 0 = F16, bit 4 = F32 D).
+__device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                        uint32_t idesc, uint32_t acc) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
         "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(acc)
         : "memory");
 }
@@ -173,12 +151,6 @@ __device__ __forceinline__ bool elect_one() {
     asm volatile("{\n\t.reg .pred P1;\n\telect.sync _|P1, 0xffffffff;\n\t@P1 mov.b32 %0, 1;\n\t}"
                  : "+r"(pred));
     return pred != 0;
-}
-
-__device__ __forceinline__ uint32_t to_tf32(float x) {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-    return r;
 }
 
 #define TC_REGS32(v)                                                                            \
@@ -267,219 +239,8 @@ __device__ __forceinline__ uint64_t tile_base(uint64_t t, const Params &P) {
     return t;
 }
 
-template <int K>
-__global__ void __launch_bounds__(H_THREADS, 1)
-apply_tc(float2 *__restrict__ psi, const __grid_constant__ Params P,
-         const __half *__restrict__ Breal /* [2][N][KD]: hi then lo, row n = output real */) {
-    using C = Cfg<K>;
-    constexpr int KD = C::KD, N = C::N, HA = C::HALF_AMPS;
-    constexpr int NPOS = K + SETBITS;
-    extern __shared__ __align__(1024) uint8_t smem[];
-    const int warp = threadIdx.x >> 5;
-    const int lane = threadIdx.x & 31;
-    const uint32_t sbase = smem_u32(smem);
-    const uint32_t bar0 = sbase + 2 * C::B_BYTES;
-    auto full_bar = [&](int h) { return bar0 + 8 * h; };
-    auto empty_bar = [&](int h) { return bar0 + 8 * (2 + h); };
-    auto tfull_bar = [&](int d) { return bar0 + 8 * (4 + d); };
-    auto tempty_bar = [&](int d) { return bar0 + 8 * (6 + d); };
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + 2 * C::B_BYTES + 64);
-
-    if (threadIdx.x == 0) {
-        for (int h = 0; h < 2; ++h) {
-            mbar_init(full_bar(h), 4);
-            mbar_init(empty_bar(h), 1);
-            mbar_init(tfull_bar(h), 1);
-            mbar_init(tempty_bar(h), NUM_EPI);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == MMA_WARP) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                         smem_u32(tmem_slot)),
-                     "r"(C::TMEM_COLS));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    // B (U hi, lo; fp16) into shared memory in the K-major SWIZZLE_NONE layout:
-    // byte offset(n, kk) = (kk/8) * LBO + n * 16 + (kk%8) * 2.
-    for (int i = threadIdx.x; i < 2 * N * KD / 8; i += H_THREADS) {
-        const int part = i / (N * KD / 8);
-        const int r = i % (N * KD / 8);
-        const int n = r / (KD / 8), kq = r % (KD / 8);
-        const uint4 v = *reinterpret_cast<const uint4 *>(Breal + part * N * KD + n * KD + 8 * kq);
-        *reinterpret_cast<uint4 *>(smem + part * C::B_BYTES + kq * C::LBO + n * 16) = v;
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-    const uint64_t ntiles = P.ntiles;
-
-    if (warp == MMA_WARP) {
-        // idesc: F32 accumulate, A/B F16, K-major, N = KD, M = 128
-        const uint32_t idesc = (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(N >> 3) << 17) |
-                               ((uint32_t)(M >> 4) << 24);
-        const uint64_t dbhi = smem_desc(sbase, C::LBO, 128);
-        const uint64_t dblo = smem_desc(sbase + C::B_BYTES, C::LBO, 128);
-        constexpr int JH = KD / 32;                 // K-chunks (of 16 reals) per half
-        constexpr uint32_t DSTEP = (2 * C::LBO) >> 4;   // descriptor address step per K-chunk
-        uint32_t it = 0;
-        for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-            const int d = it & 1;
-            const uint32_t ph = it & 1;               // each half barrier completes once per tile
-            const uint32_t dp = (it >> 1) & 1;
-            const uint32_t Dt = tmem + C::A_COLS + d * N;
-            mbar_wait(tempty_bar(d), dp ^ 1);
-            // Accumulation order matters for accuracy: the tensor core rounds
-            // the FP32 accumulator coarsely at every MMA, so the error grows
-            // with the number of MMAs that add into an accumulator of full
-            // magnitude.  Issue all correction terms (Alo.Bhi, Ahi.Blo; ~2^-11
-            // of the result) first, then the main terms Ahi.Bhi.
-            mbar_wait(full_bar(0), ph);
-            tc_fence_after();
-            if (elect_one()) {
-#pragma unroll 1
-                for (int jj = 0; jj < JH; ++jj) {
-                    const uint32_t jk = jj * DSTEP;
-                    mma_ts(Dt, tmem + KD / 4 + 8 * jj, dbhi + jk, idesc, jj != 0);
-                    mma_ts(Dt, tmem + 8 * jj, dblo + jk, idesc, 1);
-                }
-            }
-            __syncwarp();
-            mbar_wait(full_bar(1), ph);
-            tc_fence_after();
-            if (elect_one()) {
-                const uint32_t a1 = tmem + KD / 2;
-#pragma unroll 1
-                for (int jj = 0; jj < JH; ++jj) {
-                    const uint32_t jk = (JH + jj) * DSTEP;
-                    mma_ts(Dt, a1 + KD / 4 + 8 * jj, dbhi + jk, idesc, 1);
-                    mma_ts(Dt, a1 + 8 * jj, dblo + jk, idesc, 1);
-                }
-#pragma unroll 1
-                for (int jj = 0; jj < JH; ++jj)
-                    mma_ts(Dt, tmem + 8 * jj, dbhi + jj * DSTEP, idesc, 1);
-                mma_commit(empty_bar(0));
-#pragma unroll 1
-                for (int jj = 0; jj < JH; ++jj)
-                    mma_ts(Dt, a1 + 8 * jj, dbhi + (JH + jj) * DSTEP, idesc, 1);
-                mma_commit(empty_bar(1));
-                mma_commit(tfull_bar(d));
-            }
-            __syncwarp();
-        }
-    } else if (warp >= CONV0) {
-        // converter group h (4 warps, one per TMEM lane quarter) owns K-half h
-        // (amplitudes [h*HA, (h+1)*HA)) of every gather set
-        const int ct = (warp - CONV0) * 32 + lane;  // 0..255
-        const int h = (warp - CONV0) >> 2;
-        const int q = warp & 3;                     // TMEM lane quarter of this warp
-        const int n = q * 32 + lane;                // gather set (TMEM lane)
-        const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
-        const uint32_t chi = tmem + h * (KD / 2), clo = chi + KD / 4;
-        const float sA = __int_as_float((127 + max(-126, min(127, P.ea))) << 23);
-        const uint64_t soff = P.setoff[n];
-        const uint64_t *offh = P.off + h * HA;
-        // raw ring: [buf][c][ct] float2, conflict-free (consecutive threads, 8 B)
-        const uint32_t raw0 = sbase + 2 * C::B_BYTES + BAR_BYTES;
-        auto prefetch = [&](uint64_t tt, int buf) {
-            const float2 *b = psi + tile_base<NPOS>(tt, P) + soff;
-            const uint32_t dst = raw0 + buf * C::RAW_BYTES + ct * 8;
-#pragma unroll
-            for (int c = 0; c < HA; ++c)
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst + c * 256 * 8),
-                             "l"(b + offh[c])
-                             : "memory");
-            asm volatile("cp.async.commit_group;" ::: "memory");
-        };
-        const uint64_t G = gridDim.x;
-        uint32_t it = 0;
-        uint64_t t = blockIdx.x;
-        if (t < ntiles) prefetch(t, 0);
-        for (; t < ntiles; t += G, ++it) {
-            const int buf = it & 1;
-            if (t + G < ntiles) {
-                prefetch(t + G, buf ^ 1);
-                asm volatile("cp.async.wait_group 1;" ::: "memory");
-            } else {
-                asm volatile("cp.async.wait_group 0;" ::: "memory");
-            }
-            const float2 *raw = reinterpret_cast<const float2 *>(smem + 2 * C::B_BYTES + BAR_BYTES +
-                                                                 buf * C::RAW_BYTES) + ct;
-            mbar_wait(empty_bar(h), (it & 1) ^ 1);
-            tc_fence_after();
-#pragma unroll
-            constexpr int CH = HA < 16 ? HA : 16;     // amplitudes per tcgen05.st
-            for (int c0 = 0; c0 < HA; c0 += CH) {
-                uint32_t hi[CH], lo[CH];
-#pragma unroll
-                for (int i = 0; i < CH; ++i) {
-                    const float2 v = raw[(c0 + i) * 256];
-                    const float2 x = make_float2(v.x * sA, v.y * sA);
-                    const __half2 h2 = __floats2half2_rn(x.x, x.y);
-                    const float2 hf = __half22float2(h2);
-                    const __half2 l2 = __floats2half2_rn(x.x - hf.x, x.y - hf.y);
-                    hi[i] = *reinterpret_cast<const uint32_t *>(&h2);
-                    lo[i] = *reinterpret_cast<const uint32_t *>(&l2);
-                }
-                if constexpr (CH == 16) {
-                    tmem_st16(chi + lane_addr + c0, hi);
-                    tmem_st16(clo + lane_addr + c0, lo);
-                } else {
-                    tmem_st8(chi + lane_addr + c0, hi);
-                    tmem_st8(clo + lane_addr + c0, lo);
-                }
-            }
-            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(full_bar(h));
-        }
-    } else {
-        // epilogue: warp q reads TMEM lanes 32q.. = gather sets n
-        const int n = warp * 32 + lane;
-        const uint64_t soff = P.setoff[n];
-        const uint32_t lane_addr = (uint32_t)(warp * 32) << 16;
-        uint32_t it = 0;
-        for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-            const int d = it & 1;
-            const uint32_t dp = (it >> 1) & 1;
-            mbar_wait(tfull_bar(d), dp);
-            tc_fence_after();
-            const uint64_t base = tile_base<NPOS>(t, P) + soff;
-            const float2 sf = pow2_factors(-(max(-126, min(127, P.ea)) + P.ue));
-            const uint32_t Dt = tmem + C::A_COLS + d * N + lane_addr;
-#pragma unroll 1
-            for (int ch = 0; ch < N / 32; ++ch) {
-                uint32_t v[32];
-                tmem_ld32(Dt + 32 * ch, v);
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    float2 o;
-                    o.x = __uint_as_float(v[2 * i]) * sf.x * sf.y;
-                    o.y = __uint_as_float(v[2 * i + 1]) * sf.x * sf.y;
-                    psi[base + P.off[16 * ch + i]] = o;
-                }
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(tempty_bar(d));
-        }
-    }
-
-    tc_fence_before();
-    __syncthreads();
-    if (warp == MMA_WARP) {
-        tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TMEM_COLS));
-    }
-}
-
-// ------------------------------------------------------------------ mode H, bulk-copy producer
-// Same contraction and precision as apply_tc<K>; what changes is how the tile
-// reaches shared memory.  A tile spans 13 (K = 6) "tile bits": the targets and
+// ------------------------------------------------------------------ mode H
+// A tile (128 gather sets) spans 13 (K = 6) "tile bits": the targets and
 // the 7 lowest non-target bits, so physical bits 0..6 are always tile bits and
 // the tile is a union of 2^(K + 7 - 7) contiguous 1 KB blocks (128
 // amplitudes, bits 0..6), whatever the placement.  One producer warp moves
@@ -519,16 +280,12 @@ struct ParamsB {
     uint64_t boff[2][32];  // amplitude offset (from the tile base) of block j of K-half h
     uint32_t cidx8[32];    // byte offset in a slot of pattern c (low K-1 bits of c)
     uint16_t nidx[128];    // slot index of gather set n (pattern 0)
-    int ns;                // ring depth (template parameter NS)
-    int np;                // producer warps (template parameter NP)
-    int spin;              // 1: spin-wait instead of try_wait with a suspend hint
-    int l2hint;            // bit 0: evict-first bulk loads, bit 1: streaming stores (experiments)
-    int diag;              // diagnostics (HQ_TC_DIAG, WRONG results): 1 no MMA, 2 no conversion, 4 no stores
+    int diag;              // diagnostics (WRONG results; builds with -DHQ_TC_DIAG_BUILD only): 1 no MMA,
+                           // 2 no conversion, 4 no stores
     int swz;               // 1: blocks arrive by 2-D TMA with SWIZZLE_128B; nidx/cidx8 are pre-swizzled
     int pair;              // 1: the lowest target is bit 0, patterns (2j, 2j+1) are one 16-byte load / store
     int xpair;             // 1: bit 0 is not a target and is lane bit 0: lane pairs swap one
                            //    output each so that every store is 16 bytes
-    int xquad;             // 1: bits 0, 1 are lane bits 0, 1: lane quads transpose, 32-byte stores
 };
 
 // SWIZZLE_128B as seen from a slot index (8-byte amplitudes): byte address
@@ -553,19 +310,6 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t
                  : "memory");
 }
 
-// cp.async.bulk with an L2 cache policy (createpolicy ... evict_first):
-// the state is streamed once per pass, so its lines need not stay in L2
-__device__ __forceinline__ void bulk_g2s_ef(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar,
-                                            uint64_t pol) {
-    asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
-                 ::"r"(dst), "l"(src), "r"(bytes), "r"(bar), "l"(pol)
-                 : "memory");
-}
-__device__ __forceinline__ uint64_t policy_evict_first() {
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
 __device__ __forceinline__ void st_cs_f2(void *p, float2 v) {     // streaming store (evict-first)
     asm volatile("st.global.cs.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v.x), "f"(v.y) : "memory");
 }
@@ -617,11 +361,7 @@ apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
     auto rfull = [&](int s) { return bar0 + 8 * (12 + s); };
     auto rempty = [&](int s) { return bar0 + 8 * (12 + NSLOT + s); };
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + C::BARS + 8 * (12 + 2 * NSLOT));
-    const bool spin = P.spin != 0;
-    auto wait = [&](uint32_t bar, uint32_t parity) {
-        if (spin) mbar_wait(bar, parity);
-        else mbar_wait_sleep(bar, parity);
-    };
+    auto wait = [&](uint32_t bar, uint32_t parity) { mbar_wait_sleep(bar, parity); };
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < 4; ++i) {
@@ -670,7 +410,6 @@ apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
         constexpr int NPH = NP == 1 ? 1 : NP / 2;
         constexpr int NB = C::NBLK / NPH;
         const int sub = NP == 1 ? 0 : p / 2;
-        const uint64_t pol = policy_evict_first();
         uint32_t it = 0;
         for (uint64_t t = blockIdx.x; t < ntiles; t += G, ++it) {
             const uint64_t tbo = tile_base<NPOS>(t, P.h);
@@ -687,9 +426,6 @@ apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
                     if (P.swz)   // row = 16 amplitudes; a 1 KB block is 8 rows, swizzled on arrival
                         tma_g2s_2d(sbase + C::RING + s * C::SLOT_BYTES + j * 1024, &tmap, 0,
                                    (int)((tbo + P.boff[h][j]) >> 4), rfull(s));
-                    else if (P.l2hint & 1)
-                        bulk_g2s_ef(sbase + C::RING + s * C::SLOT_BYTES + j * 1024, tb + P.boff[h][j], 1024,
-                                    rfull(s), pol);
                     else
                         bulk_g2s(sbase + C::RING + s * C::SLOT_BYTES + j * 1024, tb + P.boff[h][j], 1024, rfull(s));
                 }
@@ -711,14 +447,18 @@ apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
             mbar_wait(tempty(d), ph ^ 1);
             mbar_wait(afull(d, 0), ph);
             tc_fence_after();
-            // correction terms first, main terms last (see apply_tc)
+            // Accumulation order matters for accuracy: the tensor core rounds
+            // the FP32 accumulator coarsely at every MMA, so the error grows
+            // with the number of MMAs that add into an accumulator of full
+            // magnitude.  Issue all correction terms (Alo.Bhi, Ahi.Blo; ~2^-11
+            // of the result) first, then the main terms Ahi.Bhi.
             const bool no_mma = DIAG && (P.diag & 1);   // diagnostics only: wrong results
             if (elect_one() && !no_mma) {
 #pragma unroll 1
                 for (int jj = 0; jj < JH; ++jj) {
                     const uint32_t jk = jj * DSTEP;
-                    mma_ts(Dt, a0 + KD / 4 + 8 * jj, dbhi + jk, idesc, jj != 0);
-                    mma_ts(Dt, a0 + 8 * jj, dblo + jk, idesc, 1);
+                    mma_f16(Dt, a0 + KD / 4 + 8 * jj, dbhi + jk, idesc, jj != 0);
+                    mma_f16(Dt, a0 + 8 * jj, dblo + jk, idesc, 1);
                 }
             }
             __syncwarp();
@@ -729,18 +469,18 @@ apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
 #pragma unroll 1
                     for (int jj = 0; jj < JH; ++jj) {
                         const uint32_t jk = (JH + jj) * DSTEP;
-                        mma_ts(Dt, a1 + KD / 4 + 8 * jj, dbhi + jk, idesc, 1);
-                        mma_ts(Dt, a1 + 8 * jj, dblo + jk, idesc, 1);
+                        mma_f16(Dt, a1 + KD / 4 + 8 * jj, dbhi + jk, idesc, 1);
+                        mma_f16(Dt, a1 + 8 * jj, dblo + jk, idesc, 1);
                     }
 #pragma unroll 1
                     for (int jj = 0; jj < JH; ++jj)
-                        mma_ts(Dt, a0 + 8 * jj, dbhi + jj * DSTEP, idesc, 1);
+                        mma_f16(Dt, a0 + 8 * jj, dbhi + jj * DSTEP, idesc, 1);
                 }
                 mma_commit(aempty(d, 0));
                 if (!no_mma) {
 #pragma unroll 1
                     for (int jj = 0; jj < JH; ++jj)
-                        mma_ts(Dt, a1 + 8 * jj, dbhi + (JH + jj) * DSTEP, idesc, 1);
+                        mma_f16(Dt, a1 + 8 * jj, dbhi + (JH + jj) * DSTEP, idesc, 1);
                 }
                 mma_commit(aempty(d, 1));
                 mma_commit(tfull(d));
@@ -854,34 +594,6 @@ apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
                     }
                     continue;
                 }
-                if (P.xquad) {
-                    // bits 0 and 1 are set bits, lane bits 0 and 1: a 4x4 transpose of
-                    // (set, pattern) over the lane quad (two shuffle stages) gives each
-                    // lane 4 adjacent amplitudes of one pattern, one 32-byte store
-                    const bool b0 = lane & 1, b1 = lane & 2;
-                    const int q = lane & 3;
-                    char *qb = pb - 8 * (q);
-#pragma unroll
-                    for (int i = 0; i < 16; i += 4) {
-                        uint64_t y[4];
-#pragma unroll
-                        for (int m = 0; m < 4; ++m) {
-                            const uint64_t x = (uint64_t)v[2 * (i + m)] | ((uint64_t)v[2 * (i + m) + 1] << 32);
-                            y[m] = mul_f32x2(mul_f32x2(x, f1), f2);
-                        }
-                        const uint64_t ra = __shfl_xor_sync(0xffffffffu, b0 ? y[0] : y[1], 1);
-                        const uint64_t rb = __shfl_xor_sync(0xffffffffu, b0 ? y[2] : y[3], 1);
-                        const uint64_t u00 = b0 ? ra : y[0], u10 = b0 ? y[1] : ra;
-                        const uint64_t u01 = b0 ? rb : y[2], u11 = b0 ? y[3] : rb;
-                        const uint64_t r0 = __shfl_xor_sync(0xffffffffu, b1 ? u00 : u01, 2);
-                        const uint64_t r1 = __shfl_xor_sync(0xffffffffu, b1 ? u10 : u11, 2);
-                        const uint64_t k0 = b1 ? u01 : u00, k1 = b1 ? u11 : u10;
-                        if (DIAG && (P.diag & 4)) continue;
-                        st_cs_f8(qb + P.off8[16 * ch + i + q], b1 ? r0 : k0, b1 ? r1 : k1, b1 ? k0 : r0,
-                                 b1 ? k1 : r1);
-                    }
-                    continue;
-                }
                 if (P.xpair) {
                     // bit 0 is a set bit and the lane parity: for the pattern pair
                     // (2j, 2j+1) the even lane (set s) stores (s, 2j), (s^1, 2j) and
@@ -906,8 +618,7 @@ apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
                     const uint64_t x = (uint64_t)v[2 * i] | ((uint64_t)v[2 * i + 1] << 32);
                     const float2 o = u64_as_f2(mul_f32x2(mul_f32x2(x, f1), f2));
                     if (DIAG && (P.diag & 4)) continue; // diagnostics only: no stores
-                    if (P.l2hint & 2) st_cs_f2(pb + P.off8[16 * ch + i], o);
-                    else *reinterpret_cast<float2 *>(pb + P.off8[16 * ch + i]) = o;
+                    st_cs_f2(pb + P.off8[16 * ch + i], o);
                 }
             }
         }
@@ -925,29 +636,47 @@ apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
 // ------------------------------------------------------------------ mode L
 // Orientation for gathers whose targets include the lowest physical bits
 // (there a gather set is a short contiguous run, so "lanes = sets" loads and
-// stores are strided).  Here the roles swap: A = real embedding of U in TMEM
+// stores are strided).  The roles swap: A = real embedding of U in TMEM
 // (lane = output real 2r+e), B = the tile in shared memory (K-major,
 // SWIZZLE_128B, row = gather set, 64 sets per tile), D = output tile in TMEM
-// (lane = output real, column = set).  Converter lanes follow the tile's
-// memory order, so loads are contiguous whatever the placement; the swizzle
-// keeps their 8-byte shared-memory stores conflict-light; epilogue lanes are
-// output reals, contiguous in memory when the targets are the low bits.
-// k = 5 gates are widened to 6 targets on the host (U (x) I, exact).
+// (lane = output real, column = set).  Same arithmetic as mode H: FP16 hi/lo
+// operands (kind::f16, K = 16 per MMA), A = U 2^ue from the host, B = psi 2^ea
+// from the runtime's amplitude bound, 3-term product with the correction
+// terms issued first, FP32 accumulation.
+// Mode L's tile (6 targets + the 6 lowest non-target bits) always contains
+// physical bits 0..6 (mode L is only chosen when some target is below bit 7),
+// so the tile is 32 contiguous 1 KB blocks; a producer warp moves them with
+// cp.async.bulk into an L_NR-slot raw ring in tile-index order, and the
+// converter warps read it conflict-free, split, and write swizzled half2.
+// k = 5 gates are widened to 6 targets on the host (U (x) I, exact): by the
+// tcgen05 pacing law (B300_MICROARCH.md, floor = max(M,128) N / 256 cycles per
+// MMA) a native M = 64 k = 5 pass costs the same tensor cycles per amplitude.
+//   warps 0-3 epilogue, 4 MMA, 5-12 converters, 13 producer.
+// TMEM columns: A hi [0,64), A lo [64,128) (packed f16x2, column c = input
+// amplitude c), accumulator d: [128 + 64 d, 192 + 64 d).
 
 constexpr int L_NS = 64;                          // gather sets per tile (MMA N)
 constexpr int L_STAGES = 2;
-constexpr int L_HALF = L_NS * 128 * 4;            // 32 KB: hi (or lo) of one stage
+constexpr int L_ATOMCOL = (L_NS / 8) * 1024;      // bytes per 64-half (128 B) atom column
+constexpr int L_HALF = 2 * L_ATOMCOL;             // 16 KB: hi (or lo) of one stage (K = 128 halves)
 constexpr int L_STAGE = 2 * L_HALF;
-constexpr int L_RAW = NUM_CONV * 32 * 16 * 8;     // one prefetched tile (cp.async ring slot)
-constexpr int L_SMEM = L_STAGES * L_STAGE + BAR_BYTES + 2 * L_RAW;
-constexpr int L_ATOMCOL = (L_NS / 8) * 1024;      // bytes per 32-real atom column
+constexpr int L_RAW = NUM_CONV * 32 * 16 * 8;     // one tile of raw amplitudes (32 KB)
+constexpr int L_NR = 3;                           // raw ring slots
+constexpr int LB_PROD = NUM_EPI + 1 + NUM_CONV;   // warp 13
+constexpr int LB_THREADS = (LB_PROD + 1) * 32;
+constexpr int L_BARS = L_STAGES * L_STAGE + L_NR * L_RAW;
+constexpr int LB_SMEM = L_BARS + BAR_BYTES;
+constexpr int L_TMEM_COLS = 256;
 
 struct ParamsL {
     uint64_t off[64];      // amplitude offset of canonical target pattern c
     uint32_t setoff[64];   // amplitude offset of set n inside a tile
+    uint64_t boff[32];     // amplitude offset of 1 KB block j of a tile (tile bits >= 7 of j << 7)
     int pos[12];           // ascending bit positions of the tile (targets + set bits)
     int nbit[12];          // tile bit i -> set-index bit (or -1)
     int cbit[12];          // tile bit i -> canonical target bit (or -1)
+    int ue;                // A = U * 2^ue (host scaling into the fp16 range)
+    int ea;                // B = psi * 2^ea (runtime: from the amplitude bound)
     uint64_t ntiles;
 };
 
@@ -971,253 +700,23 @@ __device__ __forceinline__ uint64_t tile_base12(uint64_t t, const ParamsL &P) {
     return t;
 }
 
-__global__ void __launch_bounds__(THREADS, 1)
-apply_tcL(float2 *__restrict__ psi, const __grid_constant__ ParamsL P,
-          const float *__restrict__ Areal /* [2][128][128] hi then lo, row = output real */) {
-    extern __shared__ __align__(1024) uint8_t smem[];
-    const int warp = threadIdx.x >> 5;
-    const int lane = threadIdx.x & 31;
-    const uint32_t sbase = smem_u32(smem);
-    const uint32_t bar0 = sbase + L_STAGES * L_STAGE;
-    auto full_bar = [&](int s) { return bar0 + 8 * s; };
-    auto empty_bar = [&](int s) { return bar0 + 8 * (L_STAGES + s); };
-    auto tfull_bar = [&](int d) { return bar0 + 8 * (2 * L_STAGES + d); };
-    auto tempty_bar = [&](int d) { return bar0 + 8 * (2 * L_STAGES + 2 + d); };
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + L_STAGES * L_STAGE + 8 * (2 * L_STAGES + 4));
-
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < L_STAGES; ++s) {
-            mbar_init(full_bar(s), NUM_CONV);
-            mbar_init(empty_bar(s), 1);
-        }
-        for (int d = 0; d < 2; ++d) {
-            mbar_init(tfull_bar(d), 1);
-            mbar_init(tempty_bar(d), NUM_EPI);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == MMA_WARP) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                         smem_u32(tmem_slot)),
-                     "r"(512));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-    // A (U hi, lo) into TMEM: warp q writes lanes 32q..32q+31 (rows of A)
-    if (warp < NUM_EPI) {
-        const int m = warp * 32 + lane;
-#pragma unroll 1
-        for (int ch = 0; ch < 8; ++ch) {
-            uint32_t v[32];
-            const float *src = Areal + (ch >> 2) * (128 * 128) + m * 128 + (ch & 3) * 32;
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__ldg(src + i));
-            tmem_st32(tmem + ((uint32_t)(warp * 32) << 16) + ch * 32, v);
-        }
-        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t A_HI = tmem, A_LO = tmem + 128;
-    const uint64_t ntiles = P.ntiles;
-
-    if (warp == MMA_WARP) {
-        const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(L_NS >> 3) << 17) |
-                               ((uint32_t)(128 >> 4) << 24);
-        uint32_t it = 0;
-        for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-            const int s = it % L_STAGES;
-            const uint32_t sp = (it / L_STAGES) & 1;
-            const int d = it & 1;
-            const uint32_t dp = (it >> 1) & 1;
-            mbar_wait(tempty_bar(d), dp ^ 1);
-            mbar_wait(full_bar(s), sp);
-            tc_fence_after();
-            if (elect_one()) {
-                const uint32_t D = tmem + 256 + L_NS * d;
-                const uint32_t bhi = sbase + s * L_STAGE, blo = bhi + L_HALF;
-                // K-chunk j (8 reals = 32 B): atom column j/4, +32 B inside the 128-B row
-#pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    const uint32_t o = (j >> 2) * L_ATOMCOL + (j & 3) * 32;
-                    mma_ts(D, A_LO + 8 * j, smem_desc_sw128(bhi + o), idesc, j > 0);
-                    mma_ts(D, A_HI + 8 * j, smem_desc_sw128(blo + o), idesc, 1);
-                }
-#pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    const uint32_t o = (j >> 2) * L_ATOMCOL + (j & 3) * 32;
-                    mma_ts(D, A_HI + 8 * j, smem_desc_sw128(bhi + o), idesc, 1);
-                }
-                mma_commit(empty_bar(s));
-                mma_commit(tfull_bar(d));
-            }
-            __syncwarp();
-        }
-    } else if (warp >= CONV0) {
-        // thread -> tile-local amplitude index tl = lane | (cw << 5) | (i << 8), i = 0..15
-        const int cw = warp - CONV0;
-        uint64_t aoff_base = 0;
-        uint32_t n_base = 0, c_base = 0;
-#pragma unroll
-        for (int b = 0; b < 8; ++b) {
-            const int bit = b < 5 ? (lane >> b) & 1 : (cw >> (b - 5)) & 1;
-            if (bit) {
-                aoff_base |= 1ull << P.pos[b];
-                if (P.nbit[b] >= 0) n_base |= 1u << P.nbit[b];
-                if (P.cbit[b] >= 0) c_base |= 1u << P.cbit[b];
-            }
-        }
-        uint64_t aoff[16];
-        uint32_t sdst[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            uint64_t a = aoff_base;
-            uint32_t n = n_base, c = c_base;
-#pragma unroll
-            for (int b = 0; b < 4; ++b)
-                if ((i >> b) & 1) {
-                    a |= 1ull << P.pos[8 + b];
-                    if (P.nbit[8 + b] >= 0) n |= 1u << P.nbit[8 + b];
-                    if (P.cbit[8 + b] >= 0) c |= 1u << P.cbit[8 + b];
-                }
-            aoff[i] = a;
-            const uint32_t r8 = n & 7, ch = (c >> 1) & 7;
-            sdst[i] = (c >> 4) * L_ATOMCOL + (n >> 3) * 1024 + r8 * 128 + ((ch ^ r8) << 4) + (c & 1) * 8;
-        }
-        // cp.async prefetch of the next tile into a 2-slot raw ring [slot][i][thread]
-        const int ct = cw * 32 + lane;
-        const uint32_t raw0 = sbase + L_STAGES * L_STAGE + BAR_BYTES;
-        auto prefetch = [&](uint64_t tt, int slot) {
-            const float2 *b = psi + tile_base12(tt, P);
-            const uint32_t dst = raw0 + slot * L_RAW + ct * 8;
-#pragma unroll
-            for (int i = 0; i < 16; ++i)
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst + i * 256 * 8),
-                             "l"(b + aoff[i])
-                             : "memory");
-            asm volatile("cp.async.commit_group;" ::: "memory");
-        };
-        const uint64_t G = gridDim.x;
-        uint64_t t = blockIdx.x;
-        uint32_t it = 0;
-        if (t < ntiles) prefetch(t, 0);
-        for (; t < ntiles; t += G, ++it) {
-            const int slot = it & 1;
-            if (t + G < ntiles) {
-                prefetch(t + G, slot ^ 1);
-                asm volatile("cp.async.wait_group 1;" ::: "memory");
-            } else {
-                asm volatile("cp.async.wait_group 0;" ::: "memory");
-            }
-            const float2 *raw = reinterpret_cast<const float2 *>(smem + L_STAGES * L_STAGE + BAR_BYTES +
-                                                                 slot * L_RAW) + ct;
-            const int s = it % L_STAGES;
-            const uint32_t sp = (it / L_STAGES) & 1;
-            mbar_wait(empty_bar(s), sp ^ 1);
-            uint8_t *hi = smem + s * L_STAGE;
-            uint8_t *lo = hi + L_HALF;
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const float2 v = raw[i * 256];
-                uint2 hh, ll;
-                hh.x = to_tf32(v.x);
-                hh.y = to_tf32(v.y);
-                ll.x = __float_as_uint(v.x - __uint_as_float(hh.x));
-                ll.y = __float_as_uint(v.y - __uint_as_float(hh.y));
-                *reinterpret_cast<uint2 *>(hi + sdst[i]) = hh;
-                *reinterpret_cast<uint2 *>(lo + sdst[i]) = ll;
-            }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) mbar_arrive(full_bar(s));
-        }
-    } else {
-        // epilogue warps 0..3: TMEM lanes 32q.. = output reals m = 2r + e
-        const int m = warp * 32 + lane;
-        const int r = m >> 1, e = m & 1;
-        const uint64_t offr = P.off[r];
-        uint32_t it = 0;
-        for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-            const int d = it & 1;
-            const uint32_t dp = (it >> 1) & 1;
-            mbar_wait(tfull_bar(d), dp);
-            tc_fence_after();
-            uint32_t v0[32], v1[32];
-            const uint32_t D = tmem + 256 + L_NS * d + ((uint32_t)(warp * 32) << 16);
-            tmem_ld32(D, v0);
-            tmem_ld32(D + 32, v1);
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(tempty_bar(d));
-            const uint64_t base = tile_base12(t, P) + offr;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                const uint32_t x0 = j < 16 ? v0[2 * j] : v1[2 * j - 32];
-                const uint32_t x1 = j < 16 ? v0[2 * j + 1] : v1[2 * j + 1 - 32];
-                const uint32_t snd = e ? x0 : x1;
-                const uint32_t rcv = __shfl_xor_sync(0xffffffffu, snd, 1);
-                float2 o;
-                o.x = __uint_as_float(e ? rcv : x0);
-                o.y = __uint_as_float(e ? x1 : rcv);
-                psi[base + P.setoff[2 * j + e]] = o;
-            }
-        }
-    }
-
-    tc_fence_before();
-    __syncthreads();
-    if (warp == MMA_WARP) {
-        tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
-    }
-}
-
-// ------------------------------------------------------------------ mode L, bulk-copy producer
-// Mode L's tile (6 targets + the 6 lowest non-target bits) always contains
-// physical bits 0..6, because at least one target is below bit 7 in mode L;
-// the tile is therefore 32 contiguous 1 KB blocks.  A producer warp moves them
-// with cp.async.bulk into an L_NR-slot raw ring laid out in tile-index order
-// (exactly the [i][thread] order the converters read), replacing the
-// converters' per-thread cp.async.
-constexpr int L_NR = 3;
-constexpr int LB_PROD = NUM_EPI + 1 + NUM_CONV;             // warp 13
-constexpr int LB_THREADS = (LB_PROD + 1) * 32;
-constexpr int LB_SMEM = L_STAGES * L_STAGE + BAR_BYTES + L_NR * L_RAW;
-
-struct ParamsLB {
-    ParamsL l;
-    uint64_t boff[32];     // amplitude offset of 1 KB block j of a tile (tile bits >= 7 of j << 7)
-    int spin;
-    int l2hint;            // unused in mode L
-};
-
 __global__ void __launch_bounds__(LB_THREADS, 1)
-apply_tcLb(float2 *__restrict__ psi, const __grid_constant__ ParamsLB PB,
-           const float *__restrict__ Areal /* [2][128][128] hi then lo, row = output real */) {
-    const ParamsL &P = PB.l;
+apply_tcL(float2 *__restrict__ psi, const __grid_constant__ ParamsL P,
+          const uint32_t *__restrict__ Apack /* [2][128][64] half2: hi then lo, row = output real */) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const uint32_t sbase = smem_u32(smem);
-    const uint32_t bar0 = sbase + L_STAGES * L_STAGE;
+    const uint32_t bar0 = sbase + L_BARS;
     auto full_bar = [&](int s) { return bar0 + 8 * s; };
     auto empty_bar = [&](int s) { return bar0 + 8 * (L_STAGES + s); };
     auto tfull_bar = [&](int d) { return bar0 + 8 * (2 * L_STAGES + d); };
     auto tempty_bar = [&](int d) { return bar0 + 8 * (2 * L_STAGES + 2 + d); };
     auto rfull = [&](int r) { return bar0 + 8 * (2 * L_STAGES + 4 + r); };
     auto rempty = [&](int r) { return bar0 + 8 * (2 * L_STAGES + 4 + L_NR + r); };
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + L_STAGES * L_STAGE + 8 * (2 * L_STAGES + 4 + 2 * L_NR));
-    const uint32_t raw0 = sbase + L_STAGES * L_STAGE + BAR_BYTES;
-    const bool spin = PB.spin != 0;
-    auto wait = [&](uint32_t bar, uint32_t parity) {
-        if (spin) mbar_wait(bar, parity);
-        else mbar_wait_sleep(bar, parity);
-    };
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + L_BARS + 8 * (2 * L_STAGES + 4 + 2 * L_NR));
+    const uint32_t raw0 = sbase + L_STAGES * L_STAGE;
+    auto wait = [&](uint32_t bar, uint32_t parity) { mbar_wait_sleep(bar, parity); };
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < L_STAGES; ++s) {
@@ -1237,21 +736,22 @@ apply_tcLb(float2 *__restrict__ psi, const __grid_constant__ ParamsLB PB,
     if (warp == MMA_WARP) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(tmem_slot)),
-                     "r"(512));
+                     "r"(L_TMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    // A (U hi, lo as packed half2) into TMEM: warp q writes lanes 32q..32q+31
     if (warp < NUM_EPI) {
         const int m = warp * 32 + lane;
 #pragma unroll 1
-        for (int ch = 0; ch < 8; ++ch) {
+        for (int ch = 0; ch < 4; ++ch) {
             uint32_t v[32];
-            const float *src = Areal + (ch >> 2) * (128 * 128) + m * 128 + (ch & 3) * 32;
+            const uint32_t *src = Apack + (ch >> 1) * (128 * 64) + m * 64 + (ch & 1) * 32;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__ldg(src + i));
+            for (int i = 0; i < 32; ++i) v[i] = __ldg(src + i);
             tmem_st32(tmem + ((uint32_t)(warp * 32) << 16) + ch * 32, v);
         }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -1259,7 +759,7 @@ apply_tcLb(float2 *__restrict__ psi, const __grid_constant__ ParamsLB PB,
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t A_HI = tmem, A_LO = tmem + 128;
+    const uint32_t A_HI = tmem, A_LO = tmem + 64;
     const uint64_t ntiles = P.ntiles;
     const uint64_t G = gridDim.x;
 
@@ -1271,11 +771,11 @@ apply_tcLb(float2 *__restrict__ psi, const __grid_constant__ ParamsLB PB,
             if (lane == 0) mbar_arrive_tx(rfull(r), L_RAW);
             __syncwarp();
             const float2 *tb = psi + tile_base12(t, P);
-            bulk_g2s(raw0 + r * L_RAW + lane * 1024, tb + PB.boff[lane], 1024, rfull(r));
+            bulk_g2s(raw0 + r * L_RAW + lane * 1024, tb + P.boff[lane], 1024, rfull(r));
         }
     } else if (warp == MMA_WARP) {
-        const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(L_NS >> 3) << 17) |
-                               ((uint32_t)(128 >> 4) << 24);
+        // idesc: F32 accumulate, A/B F16, both K-major, N = 64 sets, M = 128 output reals
+        const uint32_t idesc = (1u << 4) | ((uint32_t)(L_NS >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
         uint32_t it = 0;
         for (uint64_t t = blockIdx.x; t < ntiles; t += G, ++it) {
             const int s = it % L_STAGES;
@@ -1286,18 +786,20 @@ apply_tcLb(float2 *__restrict__ psi, const __grid_constant__ ParamsLB PB,
             mbar_wait(full_bar(s), sp);
             tc_fence_after();
             if (elect_one()) {
-                const uint32_t D = tmem + 256 + L_NS * d;
+                const uint32_t D = tmem + 128 + L_NS * d;
                 const uint32_t bhi = sbase + s * L_STAGE, blo = bhi + L_HALF;
+                // K-chunk j (16 halves = 32 B): atom column j/4, +32 B inside the 128-B row;
+                // correction terms first, main terms last (accuracy, see apply_tcb)
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
+                for (int j = 0; j < 8; ++j) {
                     const uint32_t o = (j >> 2) * L_ATOMCOL + (j & 3) * 32;
-                    mma_ts(D, A_LO + 8 * j, smem_desc_sw128(bhi + o), idesc, j > 0);
-                    mma_ts(D, A_HI + 8 * j, smem_desc_sw128(blo + o), idesc, 1);
+                    mma_f16(D, A_LO + 8 * j, smem_desc_sw128(bhi + o), idesc, j > 0);
+                    mma_f16(D, A_HI + 8 * j, smem_desc_sw128(blo + o), idesc, 1);
                 }
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
+                for (int j = 0; j < 8; ++j) {
                     const uint32_t o = (j >> 2) * L_ATOMCOL + (j & 3) * 32;
-                    mma_ts(D, A_HI + 8 * j, smem_desc_sw128(bhi + o), idesc, 1);
+                    mma_f16(D, A_HI + 8 * j, smem_desc_sw128(bhi + o), idesc, 1);
                 }
                 mma_commit(empty_bar(s));
                 mma_commit(tfull_bar(d));
@@ -1316,6 +818,8 @@ apply_tcLb(float2 *__restrict__ psi, const __grid_constant__ ParamsLB PB,
                 if (P.cbit[b] >= 0) c_base |= 1u << P.cbit[b];
             }
         }
+        // byte offset of (set n, amplitude c) in a K-major SWIZZLE_128B half2
+        // stage: atom column c / 32, row n, 16-byte chunk (c / 4) % 8 ^ n % 8
         uint32_t sdst[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
@@ -1326,16 +830,18 @@ apply_tcLb(float2 *__restrict__ psi, const __grid_constant__ ParamsLB PB,
                     if (P.nbit[8 + b] >= 0) n |= 1u << P.nbit[8 + b];
                     if (P.cbit[8 + b] >= 0) c |= 1u << P.cbit[8 + b];
                 }
-            const uint32_t r8 = n & 7, ch = (c >> 1) & 7;
-            sdst[i] = (c >> 4) * L_ATOMCOL + (n >> 3) * 1024 + r8 * 128 + ((ch ^ r8) << 4) + (c & 1) * 8;
+            const uint32_t r8 = n & 7, ch = (c >> 2) & 7;
+            sdst[i] = (c >> 5) * L_ATOMCOL + (n >> 3) * 1024 + r8 * 128 + ((ch ^ r8) << 4) + (c & 3) * 4;
         }
+        const float sA = __int_as_float((127 + max(-126, min(127, P.ea))) << 23);
+        const uint64_t sA2 = f2_as_u64(make_float2(sA, sA));
         const int ct = cw * 32 + lane;
         uint32_t it = 0;
         for (uint64_t t = blockIdx.x; t < ntiles; t += G, ++it) {
             const int r = it % L_NR;
             wait(rfull(r), (it / L_NR) & 1);
-            const float2 *raw = reinterpret_cast<const float2 *>(smem + L_STAGES * L_STAGE + BAR_BYTES + r * L_RAW) + ct;
-            float2 v[16];
+            const uint64_t *raw = reinterpret_cast<const uint64_t *>(smem + L_STAGES * L_STAGE + r * L_RAW) + ct;
+            uint64_t v[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) v[i] = raw[i * 256];
             __syncwarp();
@@ -1347,13 +853,13 @@ apply_tcLb(float2 *__restrict__ psi, const __grid_constant__ ParamsLB PB,
             uint8_t *lo = hi + L_HALF;
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
-                uint2 hh, ll;
-                hh.x = to_tf32(v[i].x);
-                hh.y = to_tf32(v[i].y);
-                ll.x = __float_as_uint(v[i].x - __uint_as_float(hh.x));
-                ll.y = __float_as_uint(v[i].y - __uint_as_float(hh.y));
-                *reinterpret_cast<uint2 *>(hi + sdst[i]) = hh;
-                *reinterpret_cast<uint2 *>(lo + sdst[i]) = ll;
+                const uint64_t x = mul_f32x2(v[i], sA2);
+                const float2 xf = u64_as_f2(x);
+                const __half2 h2 = __floats2half2_rn(xf.x, xf.y);
+                const float2 rf = u64_as_f2(sub_f32x2(x, f2_as_u64(__half22float2(h2))));
+                const __half2 l2 = __floats2half2_rn(rf.x, rf.y);
+                *reinterpret_cast<__half2 *>(hi + sdst[i]) = h2;
+                *reinterpret_cast<__half2 *>(lo + sdst[i]) = l2;
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
@@ -1364,6 +870,7 @@ apply_tcLb(float2 *__restrict__ psi, const __grid_constant__ ParamsLB PB,
         const int m = warp * 32 + lane;
         const int r = m >> 1, e = m & 1;
         const uint64_t offr = P.off[r];
+        const float2 sf = pow2_factors(-(max(-126, min(127, P.ea)) + P.ue));
         uint32_t it = 0;
         for (uint64_t t = blockIdx.x; t < ntiles; t += G, ++it) {
             const int d = it & 1;
@@ -1371,14 +878,14 @@ apply_tcLb(float2 *__restrict__ psi, const __grid_constant__ ParamsLB PB,
             wait(tfull_bar(d), dp);
             tc_fence_after();
             uint32_t v0[32], v1[32];
-            const uint32_t D = tmem + 256 + L_NS * d + ((uint32_t)(warp * 32) << 16);
+            const uint32_t D = tmem + 128 + L_NS * d + ((uint32_t)(warp * 32) << 16);
             tmem_ld32(D, v0);
             tmem_ld32(D + 32, v1);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(tempty_bar(d));
-            const uint64_t base = tile_base12(t, P) + offr;
+            float2 *pb = psi + tile_base12(t, P) + offr;
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
                 const uint32_t x0 = j < 16 ? v0[2 * j] : v1[2 * j - 32];
@@ -1386,9 +893,9 @@ apply_tcLb(float2 *__restrict__ psi, const __grid_constant__ ParamsLB PB,
                 const uint32_t snd = e ? x0 : x1;
                 const uint32_t rcv = __shfl_xor_sync(0xffffffffu, snd, 1);
                 float2 o;
-                o.x = __uint_as_float(e ? rcv : x0);
-                o.y = __uint_as_float(e ? x1 : rcv);
-                psi[base + P.setoff[2 * j + e]] = o;
+                o.x = __uint_as_float(e ? rcv : x0) * sf.x * sf.y;
+                o.y = __uint_as_float(e ? x1 : rcv) * sf.x * sf.y;
+                pb[P.setoff[2 * j + e]] = o;
             }
         }
     }
@@ -1397,7 +904,7 @@ apply_tcLb(float2 *__restrict__ psi, const __grid_constant__ ParamsLB PB,
     __syncthreads();
     if (warp == MMA_WARP) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(L_TMEM_COLS));
     }
 }
 
@@ -1405,42 +912,19 @@ apply_tcLb(float2 *__restrict__ psi, const __grid_constant__ ParamsLB PB,
 
 // ------------------------------------------------------------------ host side
 
-static inline float tf32_round_host(double x) {
-    // round-to-nearest (ties away) to 10 explicit mantissa bits, as cvt.rna.tf32
-    float f = (float)x;
-    uint32_t u;
-    memcpy(&u, &f, 4);
-    if ((u & 0x7f800000u) == 0x7f800000u) return f;
-    u = (u + 0x1000u) & 0xffffe000u;
-    memcpy(&f, &u, 4);
-    return f;
-}
-
 bool tc_applicable(int dtype, const ApplyDesc &d) {
-    static const char *k4 = getenv("HQ_TC_K4");   // experiment: k = 4 on tensor cores
-    bool k_ok = d.k == 5 || d.k == 6;
-    if (d.k == 4 && k4 && k4[0] == '1') {          // mode H only (no low-bit targets)
-        int low = 0;
-        for (int i = 0; i < 4; ++i) low += d.p[i] < 4;
-        k_ok = low == 0;
-    }
-    return dtype == HQ_C64 && k_ok && d.n_local >= d.k + tc::SETBITS + 3;
+    return dtype == HQ_C64 && (d.k == 5 || d.k == 6) && d.n_local >= d.k + tc::SETBITS + 3;
 }
 
-// Mode L (U in TMEM, tile in smem) when a target sits in the lowest bits,
-// where mode H's lanes-are-sets layout gives strided accesses.
-// HQ_TC_MODE=H|L forces one orientation (experiments, tests).
+// Mode L (U in TMEM, tile in shared memory) when the targets crowd the lowest
+// bits, where mode H's lanes-are-sets layout gives strided accesses, and
+// whenever every target is below bit 7 (mode H's bulk-copy blocks need the
+// K-half bit above bits 0..6).  Measured on a B200 (bench_sweep.py, n = 32
+// dense state, same box, round 1): mode H wins with bits 0 and 1 as the only
+// low targets and with three low targets that leave bit 0 or bit 1 free;
+// mode L wins with four or more targets in bits 0..3 and with bits 0, 1 and a
+// third low bit.
 static bool tc_use_mode_l(const ApplyDesc &d) {
-    static const char *force = getenv("HQ_TC_MODE");
-    if (force && force[0] == 'H') return false;
-    if (force && force[0] == 'L') return true;
-    // measured on a B200 (bench_sweep.py, n = 32 dense state, same box,
-    // scripts/ab_modesel.sh): since the mode-H pattern pairs and lane-pair
-    // stores, mode H wins with bits 0 and 1 as the only low targets (0.82-0.87
-    // vs 0.63-0.66 of HBM peak) and with three low targets that leave bit 0 or
-    // bit 1 free (0.65-0.74 vs 0.65-0.68); mode L wins with four or more
-    // targets in bits 0..3 (0.65-0.71 vs 0.28-0.42) and with bits 0, 1 and a
-    // third low bit (0.66 vs 0.60).
     int low = 0;
     bool b0 = false, b1 = false;
     for (int i = 0; i < d.k; ++i) {
@@ -1448,9 +932,23 @@ static bool tc_use_mode_l(const ApplyDesc &d) {
         b0 |= d.p[i] == 0;
         b1 |= d.p[i] == 1;
     }
-    static const char *sel = getenv("HQ_TC_MODESEL_V5");   // "1": the earlier rule (experiments)
-    if (sel && sel[0] == '1') return (b0 && b1) || low >= 3;
-    return low >= 4 || (b0 && b1 && low >= 3);
+    return low >= 4 || (b0 && b1 && low >= 3) || d.p[d.k - 1] < 7;
+}
+
+// U 2^ue with max |U| 2^ue in [2^14, 2^15): the FP16 range of the U operand
+static int u_scale_exp(const double *U, int k) {
+    const int D = 1 << k;
+    double umax = 0.0;
+    for (int i = 0; i < 2 * D * D; ++i) umax = std::max(umax, std::fabs(U[i]));
+    int ex = 0;
+    if (umax > 0) std::frexp(umax, &ex);
+    return umax > 0 ? 15 - ex : 0;
+}
+
+// fp64 x -> FP16 hi + lo (hi = RN(x), lo = RN(x - hi))
+static void split_f16(double x, __half &hi, __half &lo) {
+    hi = __double2half(x);
+    lo = __double2half(x - (double)__half2float(hi));
 }
 
 static void tc_prepare_l(const ApplyDesc &d, const double *Ucanon, std::vector<char> &payload,
@@ -1482,25 +980,28 @@ static void tc_prepare_l(const ApplyDesc &d, const double *Ucanon, std::vector<c
                 U6[2 * (r * D6 + c) + 1] = Ucanon[2 * (drop(r) * D5 + drop(c)) + 1];
             }
     }
-    // A = interleaved real embedding (row = output real 2r+e, col = input real 2c+f)
-    payload.assign(2 * 128 * 128 * sizeof(float), 0);
-    float *hi = reinterpret_cast<float *>(payload.data());
-    float *lo = hi + 128 * 128;
+    const int ue = u_scale_exp(U6.data(), 6);
+    // A = interleaved real embedding (row = output real 2r+e, column kk = input
+    // real 2c+f) times 2^ue, FP16 hi and lo, packed two halves (f = 0, 1) per
+    // 32-bit word: [2][128][64] words
+    payload.assign(2 * 128 * 64 * sizeof(uint32_t), 0);
+    __half *hi = reinterpret_cast<__half *>(payload.data());
+    __half *lo = hi + 128 * 128;
     for (int r = 0; r < D6; ++r)
         for (int c = 0; c < D6; ++c) {
             const double ur = U6[2 * (r * D6 + c)], ui = U6[2 * (r * D6 + c) + 1];
             const double blk[2][2] = {{ur, -ui}, {ui, ur}};
             for (int e = 0; e < 2; ++e)
                 for (int f = 0; f < 2; ++f) {
-                    const double x = blk[e][f];
-                    const float h = tf32_round_host(x);
-                    hi[(2 * r + e) * 128 + 2 * c + f] = h;
-                    lo[(2 * r + e) * 128 + 2 * c + f] = tf32_round_host(x - (double)h);
+                    const int idx = (2 * r + e) * 128 + 2 * c + f;
+                    split_f16(std::ldexp(blk[e][f], ue), hi[idx], lo[idx]);
                 }
         }
     params.assign(sizeof(tc::ParamsL) + 1, 0);
     params.back() = 'L';
     tc::ParamsL &P = *reinterpret_cast<tc::ParamsL *>(params.data());
+    P.ue = ue;
+    P.ea = 14;             // set per launch by the runtime (tc_set_amp_bound)
     for (int c = 0; c < 64; ++c) {
         uint64_t o = 0;
         for (int i = 0; i < 6; ++i)
@@ -1530,37 +1031,20 @@ static void tc_prepare_l(const ApplyDesc &d, const double *Ucanon, std::vector<c
             if (p6[j] == all[i]) P.cbit[i] = j;
         }
     }
-    P.ntiles = 1ull << (d.n_local - 12);
-    // bulk-copy producer: physical bits 0..6 are tile bits 0..6 (some target
-    // is below bit 7 in mode L), so a tile is 32 contiguous 1 KB blocks
-    static const char *bulk = getenv("HQ_TC_BULK");
-    static const char *lbulk = getenv("HQ_TC_LBULK");   // "0": cp.async mode L only (experiments)
-    // (measured: 0.95 vs 0.83-0.91 of peak for split placements; for a fully
-    // contiguous tile, bits 0..11, the cp.async kernel is 1% ahead)
-    // "2": the bulk producer for the fully contiguous tile too (experiments)
-    const bool contig_ok = P.pos[11] != 11 || (lbulk && lbulk[0] == '2');
-    if (P.pos[6] == 6 && contig_ok && !(bulk && bulk[0] == '0') && !(lbulk && lbulk[0] == '0')) {
-        std::vector<char> pb(sizeof(tc::ParamsLB) + 1, 0);
-        tc::ParamsLB &B = *reinterpret_cast<tc::ParamsLB *>(pb.data());
-        B.l = P;
-        for (int j = 0; j < 32; ++j) {
-            uint64_t o = 0;
-            for (int b = 7; b < 12; ++b)
-                if (((uint64_t)j << 7 >> b) & 1) o |= 1ull << P.pos[b];
-            B.boff[j] = o;
-        }
-        static const char *spin = getenv("HQ_TC_SPIN");
-        B.spin = spin && spin[0] == '1';
-        static const char *l2 = getenv("HQ_TC_L2HINT");
-        B.l2hint = l2 ? atoi(l2) : 0;
-        pb.back() = 'M';
-        params.swap(pb);
+    // physical bits 0..6 are tile bits 0..6 (some target is below bit 7 in
+    // mode L), so a tile is 32 contiguous 1 KB blocks
+    for (int j = 0; j < 32; ++j) {
+        uint64_t o = 0;
+        for (int b = 7; b < 12; ++b)
+            if (((uint64_t)j << 7 >> b) & 1) o |= 1ull << P.pos[b];
+        P.boff[j] = o;
     }
+    P.ntiles = 1ull << (d.n_local - 12);
 }
 
-// Build the device payload (B = real embedding of U, hi and lo, [N][KD] fp32
-// each, row n = output real) and the kernel parameter block from the
-// canonical fp64 U (canonical order: U-index bit i <-> d.p[i]).
+// Build the device payload (B = real embedding of U times 2^ue, FP16 hi and
+// lo, [N][KD] each, row n = output real) and the kernel parameter block from
+// the canonical fp64 U (canonical order: U-index bit i <-> d.p[i]).
 void tc_prepare(const ApplyDesc &d, const double *Ucanon, std::vector<char> &payload,
                 std::vector<char> &params) {
     if (tc_use_mode_l(d)) {
@@ -1568,12 +1052,7 @@ void tc_prepare(const ApplyDesc &d, const double *Ucanon, std::vector<char> &pay
         return;
     }
     const int K = d.k, D = 1 << K, KD = 2 * D, N = KD;
-    // B = U * 2^ue in fp16 hi + lo, with max |U| * 2^ue in [2^14, 2^15)
-    double umax = 0.0;
-    for (int i = 0; i < 2 * D * D; ++i) umax = std::max(umax, std::fabs(Ucanon[i]));
-    int ex = 0;
-    if (umax > 0) std::frexp(umax, &ex);
-    const int ue = umax > 0 ? 15 - ex : 0;
+    const int ue = u_scale_exp(Ucanon, K);
     payload.assign((size_t)2 * N * KD * sizeof(__half), 0);
     __half *hi = reinterpret_cast<__half *>(payload.data());
     __half *lo = hi + N * KD;
@@ -1584,15 +1063,14 @@ void tc_prepare(const ApplyDesc &d, const double *Ucanon, std::vector<char> &pay
             const double blk[2][2] = {{ur, -ui}, {ui, ur}};
             for (int e = 0; e < 2; ++e)
                 for (int f = 0; f < 2; ++f) {
-                    const double x = std::ldexp(blk[e][f], ue);
-                    const __half h = __double2half(x);
-                    hi[(2 * r + e) * KD + 2 * c + f] = h;
-                    lo[(2 * r + e) * KD + 2 * c + f] = __double2half(x - (double)__half2float(h));
+                    const int idx = (2 * r + e) * KD + 2 * c + f;
+                    split_f16(std::ldexp(blk[e][f], ue), hi[idx], lo[idx]);
                 }
         }
-    params.assign(sizeof(tc::Params) + 1, 0);
-    params.back() = 'H';
-    tc::Params &P = *reinterpret_cast<tc::Params *>(params.data());
+    params.assign(sizeof(tc::ParamsB) + 1, 0);
+    params.back() = 'B';
+    tc::ParamsB &B = *reinterpret_cast<tc::ParamsB *>(params.data());
+    tc::Params &P = B.h;
     P.k = K;
     P.ue = ue;
     P.ea = 14;             // set per launch by the runtime (tc_set_amp_bound)
@@ -1620,161 +1098,103 @@ void tc_prepare(const ApplyDesc &d, const double *Ucanon, std::vector<char> &pay
     std::sort(all, all + na);
     for (int i = 0; i < na; ++i) P.pos[i] = all[i];
     P.ntiles = 1ull << (d.n_local - K - tc::SETBITS);
-    // bulk-copy producer (apply_tcb) when the highest target is at bit >= 7
-    // (the K-half bit must lie above the 1 KB blocks of bits 0..6)
-    static const char *bulk = getenv("HQ_TC_BULK");   // "0" keeps the cp.async kernel (experiments)
-    static const char *nsenv = getenv("HQ_TC_NSLOT");  // ring depth override (experiments)
-    if (d.p[K - 1] >= 7 && !(bulk && bulk[0] == '0')) {
-        std::vector<char> pb(sizeof(tc::ParamsB) + 1, 0);
-        tc::ParamsB &B = *reinterpret_cast<tc::ParamsB *>(pb.data());
-        B.h = P;
-        for (int c = 0; c < D; ++c) B.off8[c] = P.off[c] * 8;
-        auto tpos = [&](int phys) { return (int)(std::find(all, all + na, phys) - all); };
-        const int hp = tpos(d.p[K - 1]);
-        auto slot_of = [&](uint64_t ti) { return (ti & ((1ull << hp) - 1)) | ((ti >> (hp + 1)) << hp); };
-        // Targets in bits 0..3 (measured on the 34q circuit, tools/pass_times.py,
-        // same box):
-        //  * bit 0 a target: patterns (2j, 2j+1) are adjacent, so converters
-        //    load and the epilogue stores 16 bytes (pair): 61 -> 47 ms per pass;
-        //  * bit 1 the lowest target: 2-D TMA with SWIZZLE_128B removes the 2-way
-        //    bank conflicts of the converter loads (61 -> 58 ms) and lane pairs
-        //    swap outputs for 16-byte stores (xpair).  The swizzled TMA copies
-        //    are slower elsewhere (no low target 57 -> 60 ms, a k = 5 pass with
-        //    targets 3, 4, 6 56 -> 80 ms), so only this case uses them.
-        // HQ_TC_SWZ=0 disables all three, 2 forces the swizzled copies (experiments).
-        static const char *swe = getenv("HQ_TC_SWZ");
-        const bool low_ok = !(swe && swe[0] == '0');
-        B.swz = low_ok && ((K == 6 && d.p[0] == 1) || (swe && swe[0] == '2'));
-        B.pair = low_ok && d.p[0] == 0;
-        B.xpair = 0;
-        // Converter lanes (n bits 0..4) are 5 of the 7 set bits.  With one
-        // target in bits 0..3 the ascending choice puts a warp's 8-byte reads
-        // on 8 of 16 bank pairs (2-way conflicts); with the swizzled slot
-        // another choice of lane bits, or 16-byte pattern pairs when bit 0 is
-        // a target, reaches all of them.  Pick the conflict-minimal choice,
-        // the ascending one on ties (it keeps the epilogue stores contiguous).
-        int order[tc::SETBITS];
-        for (int i = 0; i < tc::SETBITS; ++i) order[i] = setbits[i];
-        if (B.swz) {
-            auto slot_idx = [&](int n, const int *sb) {
-                uint64_t ti = 0;
-                for (int i = 0; i < tc::SETBITS; ++i)
-                    if ((n >> i) & 1) ti |= 1ull << tpos(sb[i]);
-                return tc::swz128((uint32_t)slot_of(ti));
-            };
-            auto wavefronts = [&](const int *sb) {
-                const int words = B.pair ? 4 : 2;
-                int cnt[32] = {0};
-                uint32_t seen[32][32];
-                for (int l = 0; l < 32; ++l) {
-                    const uint32_t w0 = slot_idx(l, sb) * 2;
-                    for (int w = 0; w < words; ++w) {
-                        const uint32_t word = w0 + w, bank = word & 31;
-                        bool dup = false;
-                        for (int i = 0; i < cnt[bank]; ++i) dup |= seen[bank][i] == word;
-                        if (!dup) seen[bank][cnt[bank]++] = word;
-                    }
-                }
-                return *std::max_element(cnt, cnt + 32);
-            };
-            int best = wavefronts(order);
-            for (int m = 0; m < (1 << tc::SETBITS); ++m) {
-                if (__builtin_popcount(m) != 5) continue;
-                int cand[tc::SETBITS], nc = 0;
-                for (int i = 0; i < tc::SETBITS; ++i)
-                    if ((m >> i) & 1) cand[nc++] = setbits[i];
-                for (int i = 0; i < tc::SETBITS; ++i)
-                    if (!((m >> i) & 1)) cand[nc++] = setbits[i];
-                const int w = wavefronts(cand);
-                if (w < best) {
-                    best = w;
-                    std::copy(cand, cand + tc::SETBITS, order);
-                }
-            }
-            for (int n = 0; n < tc::M; ++n) {
-                uint32_t o = 0;
-                for (int i = 0; i < tc::SETBITS; ++i)
-                    if ((n >> i) & 1) o |= 1u << order[i];
-                B.h.setoff[n] = o;
-            }
-        }
-        // xpair for every pass with bit 0 free (the set bit of lane bit 0):
-        // halving the epilogue's store instructions is what speeds the pair
-        // passes up, full sectors or not; HQ_TC_XPAIR=0: only
-        // when bit 1 is the lowest target (experiments)
-        static const char *xpe = getenv("HQ_TC_XPAIR");
-        const bool xall = !(xpe && xpe[0] == '0');
-        if (low_ok && d.p[0] != 0 && order[0] == 0 && (xall || d.p[0] == 1)) {
-            B.xpair = 1;
-        }
-        // HQ_TC_XQUAD=1 (experiments): 32-byte stores when bits 0 and 1 are both
-        // free, after a two-stage quad transpose.  Measured slower on the 34q
-        // circuit (3870 vs 3708 ms same box: passes with no low target 54 vs
-        // 48 ms), so the 16-byte pairs stay the default.
-        static const char *xqe = getenv("HQ_TC_XQUAD");
-        B.xquad = B.xpair && d.p[0] > 1 && order[1] == 1 && xqe && xqe[0] == '1';
-        for (int n = 0; n < tc::M; ++n) {
+    // the highest target is at bit >= 7 (tc_use_mode_l): the K-half bit lies
+    // above the 1 KB blocks of bits 0..6
+    for (int c = 0; c < D; ++c) B.off8[c] = P.off[c] * 8;
+    auto tpos = [&](int phys) { return (int)(std::find(all, all + na, phys) - all); };
+    const int hp = tpos(d.p[K - 1]);
+    auto slot_of = [&](uint64_t ti) { return (ti & ((1ull << hp) - 1)) | ((ti >> (hp + 1)) << hp); };
+    // Targets in bits 0..3 (measured on the 34q circuit, tools/pass_times.py,
+    // same box):
+    //  * bit 0 a target: patterns (2j, 2j+1) are adjacent, so converters
+    //    load and the epilogue stores 16 bytes (pair): 61 -> 47 ms per pass;
+    //  * bit 1 the lowest target (k = 6): 2-D TMA with SWIZZLE_128B removes the
+    //    2-way bank conflicts of the converter loads (61 -> 58 ms).  The
+    //    swizzled copies are slower elsewhere (no low target 57 -> 60 ms, a
+    //    k = 5 pass with targets 3, 4, 6 56 -> 80 ms), so only this case uses them.
+    B.swz = K == 6 && d.p[0] == 1;
+    B.pair = d.p[0] == 0;
+    B.xpair = 0;
+    // Converter lanes (n bits 0..4) are 5 of the 7 set bits.  With one
+    // target in bits 0..3 the ascending choice puts a warp's 8-byte reads
+    // on 8 of 16 bank pairs (2-way conflicts); with the swizzled slot
+    // another choice of lane bits, or 16-byte pattern pairs when bit 0 is
+    // a target, reaches all of them.  Pick the conflict-minimal choice,
+    // the ascending one on ties (it keeps the epilogue stores contiguous).
+    int order[tc::SETBITS];
+    for (int i = 0; i < tc::SETBITS; ++i) order[i] = setbits[i];
+    if (B.swz) {
+        auto slot_idx = [&](int n, const int *sb) {
             uint64_t ti = 0;
             for (int i = 0; i < tc::SETBITS; ++i)
-                if ((n >> i) & 1) ti |= 1ull << tpos(order[i]);
-            B.nidx[n] = (uint16_t)(B.swz ? tc::swz128((uint32_t)slot_of(ti)) : slot_of(ti));
-        }
-        for (int c = 0; c < D / 2; ++c) {
-            uint64_t ti = 0;
-            for (int i = 0; i < K - 1; ++i)
-                if ((c >> i) & 1) ti |= 1ull << tpos(d.p[i]);
-            B.cidx8[c] = (uint32_t)(B.swz ? tc::swz128((uint32_t)slot_of(ti)) : slot_of(ti)) * 8;
-        }
-        for (int h = 0; h < 2; ++h)
-            for (int j = 0; j < D / 2; ++j) {
-                const uint64_t x = (uint64_t)j << 7;
-                const uint64_t ti = (x & ((1ull << hp) - 1)) | ((uint64_t)h << hp) | ((x >> hp) << (hp + 1));
-                uint64_t o = 0;
-                for (int i = 0; i < na; ++i)
-                    if ((ti >> i) & 1) o |= 1ull << all[i];
-                B.boff[h][j] = o;
+                if ((n >> i) & 1) ti |= 1ull << tpos(sb[i]);
+            return tc::swz128((uint32_t)slot_of(ti));
+        };
+        auto wavefronts = [&](const int *sb) {
+            const int words = B.pair ? 4 : 2;
+            int cnt[32] = {0};
+            uint32_t seen[32][32];
+            for (int l = 0; l < 32; ++l) {
+                const uint32_t w0 = slot_idx(l, sb) * 2;
+                for (int w = 0; w < words; ++w) {
+                    const uint32_t word = w0 + w, bank = word & 31;
+                    bool dup = false;
+                    for (int i = 0; i < cnt[bank]; ++i) dup |= seen[bank][i] == word;
+                    if (!dup) seen[bank][cnt[bank]++] = word;
+                }
             }
-        // ring depth and producer warps; HQ_TC_NSLOT="<ns><np>" overrides (experiments)
-        // measured on the 34q bench circuit in the sustained (power-capped)
-        // regime (tools/pass_times.py): (4, 2) beats (4, 1) and (8, *) and
-        // the cp.async kernel (3.91 s vs 4.28 s and 4.08 s); in 32q bursts
-        // (4, 1) is ahead for K = 6 (bench_sweep.py, profiles/r01/SUMMARY.md)
-        int ns = 4, np = 2;
-        if (nsenv && nsenv[0] >= '2' && nsenv[0] <= '8') {
-            ns = nsenv[0] - '0';
-            np = nsenv[1] == '2' ? 2 : (nsenv[1] == '4' ? 4 : 1);
+            return *std::max_element(cnt, cnt + 32);
+        };
+        int best = wavefronts(order);
+        for (int m = 0; m < (1 << tc::SETBITS); ++m) {
+            if (__builtin_popcount(m) != 5) continue;
+            int cand[tc::SETBITS], nc = 0;
+            for (int i = 0; i < tc::SETBITS; ++i)
+                if ((m >> i) & 1) cand[nc++] = setbits[i];
+            for (int i = 0; i < tc::SETBITS; ++i)
+                if (!((m >> i) & 1)) cand[nc++] = setbits[i];
+            const int w = wavefronts(cand);
+            if (w < best) {
+                best = w;
+                std::copy(cand, cand + tc::SETBITS, order);
+            }
         }
-        B.ns = ns;
-        B.np = np;
-        static const char *spin = getenv("HQ_TC_SPIN");
-        B.spin = spin && spin[0] == '1';
-        // default: streaming (evict-first) epilogue stores, 1.2% on the sustained
-        // 34q circuit (tools/pass_times.py, same box); evict-first bulk loads: no gain
-        static const char *l2 = getenv("HQ_TC_L2HINT");
-        B.l2hint = l2 ? atoi(l2) : 2;
-        static const char *dg = getenv("HQ_TC_DIAG");
-        B.diag = dg ? atoi(dg) : 0;
-        pb.back() = 'B';
-        params.swap(pb);
+        for (int n = 0; n < tc::M; ++n) {
+            uint32_t o = 0;
+            for (int i = 0; i < tc::SETBITS; ++i)
+                if ((n >> i) & 1) o |= 1u << order[i];
+            P.setoff[n] = o;
+        }
     }
-}
-
-template <int K>
-static int tc_launch_k(void *psi, const tc::Params &P, const void *dev_payload, cudaStream_t st) {
-    using C = tc::Cfg<K>;
-    static bool attr_done = false;
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(tc::apply_tc<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-        if (e != cudaSuccess) return (int)e;
-        attr_done = true;
+    // Every pass with bit 0 free, bit 0 being the set bit of lane bit 0: lane
+    // pairs swap one output each so that every store is 16 bytes (halving the
+    // epilogue's store instructions).
+    if (d.p[0] != 0 && order[0] == 0) B.xpair = 1;
+    for (int n = 0; n < tc::M; ++n) {
+        uint64_t ti = 0;
+        for (int i = 0; i < tc::SETBITS; ++i)
+            if ((n >> i) & 1) ti |= 1ull << tpos(order[i]);
+        B.nidx[n] = (uint16_t)(B.swz ? tc::swz128((uint32_t)slot_of(ti)) : slot_of(ti));
     }
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const uint64_t grid = P.ntiles < (uint64_t)sms ? P.ntiles : (uint64_t)sms;
-    tc::apply_tc<K><<<(unsigned)grid, tc::H_THREADS, C::SMEM, st>>>(
-        reinterpret_cast<float2 *>(psi), P, reinterpret_cast<const __half *>(dev_payload));
-    return (int)cudaGetLastError();
+    for (int c = 0; c < D / 2; ++c) {
+        uint64_t ti = 0;
+        for (int i = 0; i < K - 1; ++i)
+            if ((c >> i) & 1) ti |= 1ull << tpos(d.p[i]);
+        B.cidx8[c] = (uint32_t)(B.swz ? tc::swz128((uint32_t)slot_of(ti)) : slot_of(ti)) * 8;
+    }
+    for (int h = 0; h < 2; ++h)
+        for (int j = 0; j < D / 2; ++j) {
+            const uint64_t x = (uint64_t)j << 7;
+            const uint64_t ti = (x & ((1ull << hp) - 1)) | ((uint64_t)h << hp) | ((x >> hp) << (hp + 1));
+            uint64_t o = 0;
+            for (int i = 0; i < na; ++i)
+                if ((ti >> i) & 1) o |= 1ull << all[i];
+            B.boff[h][j] = o;
+        }
+#ifdef HQ_TC_DIAG_BUILD
+    static const char *dg = getenv("HQ_TC_DIAG");
+    B.diag = dg ? atoi(dg) : 0;
+#endif
 }
 
 // psi (2^nl complex64) as a 2-D FP32 tensor [2^(nl-4) rows][32 floats] (128 B
@@ -1802,109 +1222,75 @@ static int tc_encode_rows_map(CUtensorMap *map, void *psi, int nl) {
     return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
 }
 
-template <int K, int NS, int NP, bool DIAG = false>
-static int tc_launch_b(void *psi, const tc::ParamsB &P, const void *dev_payload, cudaStream_t st) {
-    using C = tc::CfgB<K, NS>;
-    static bool attr_done = false;
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(tc::apply_tcb<K, NS, NP, DIAG>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-        if (e != cudaSuccess) return (int)e;
-        attr_done = true;
-    }
+static int sm_count() {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
+}
+
+// Ring depth NS = 4 K-half slots and NP = 2 producer warps: measured on the
+// 34q bench circuit in the sustained (power-capped) regime
+// (tools/pass_times.py, round 1): (4, 2) beats (4, 1), (8, *) and the
+// earlier cp.async kernel (3.91 s vs 4.28 s and 4.08 s).
+template <int K, bool DIAG = false>
+static int tc_launch_b(void *psi, const tc::ParamsB &P, const void *dev_payload, cudaStream_t st) {
+    constexpr int NS = 4, NP = 2;
+    using C = tc::CfgB<K, NS>;
+    static std::atomic<uint64_t> attr{0};
+    cudaError_t e = smem_attr_once(tc::apply_tcb<K, NS, NP, DIAG>, C::SMEM, attr);
+    if (e != cudaSuccess) return (int)e;
+    const int sms = sm_count();
     const uint64_t grid = P.h.ntiles < (uint64_t)sms ? P.h.ntiles : (uint64_t)sms;
     alignas(64) CUtensorMap map;
     std::memset(&map, 0, sizeof(map));
     if (P.swz) {
         int nl = K + tc::SETBITS;
         while ((1ull << (nl - K - tc::SETBITS)) < P.h.ntiles) ++nl;
-        const int e = tc_encode_rows_map(&map, psi, nl);
-        if (e) return e;
+        const int r = tc_encode_rows_map(&map, psi, nl);
+        if (r) return r;
     }
     tc::apply_tcb<K, NS, NP, DIAG><<<(unsigned)grid, tc::bk_threads(NP), C::SMEM, st>>>(
         reinterpret_cast<float2 *>(psi), P, reinterpret_cast<const __half *>(dev_payload), map);
     return (int)cudaGetLastError();
 }
 
-// ring depth NS and producer warps NP: (NS, NP) from the host's choice
-template <int K>
-static int tc_launch_bk(void *psi, const tc::ParamsB &P, const void *dev_payload, cudaStream_t st) {
-    const int v = P.ns * 10 + P.np;
-    if constexpr (K == 6) {
-        if (P.diag) return tc_launch_b<6, 4, 2, true>(psi, P, dev_payload, st);   // HQ_TC_DIAG timing runs
-        if (v == 21) return tc_launch_b<6, 2, 1>(psi, P, dev_payload, st);
-        if (v == 42) return tc_launch_b<6, 4, 2>(psi, P, dev_payload, st);
-        if (v == 44) return tc_launch_b<6, 4, 4>(psi, P, dev_payload, st);
-        return tc_launch_b<6, 4, 1>(psi, P, dev_payload, st);
-    } else {
-        if (v == 41) return tc_launch_b<K, 4, 1>(psi, P, dev_payload, st);
-        if (v == 42) return tc_launch_b<K, 4, 2>(psi, P, dev_payload, st);
-        if (v == 61) return tc_launch_b<K, 6, 1>(psi, P, dev_payload, st);
-        if (v == 82) return tc_launch_b<K, 8, 2>(psi, P, dev_payload, st);
-        return tc_launch_b<K, 8, 1>(psi, P, dev_payload, st);
-    }
-}
-
-static int tc_launch_lb(void *psi, const tc::ParamsLB &P, const void *dev_payload, cudaStream_t st) {
-    static bool attr_done = false;
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(tc::apply_tcLb, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::LB_SMEM);
-        if (e != cudaSuccess) return (int)e;
-        attr_done = true;
-    }
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const uint64_t grid = P.l.ntiles < (uint64_t)sms ? P.l.ntiles : (uint64_t)sms;
-    tc::apply_tcLb<<<(unsigned)grid, tc::LB_THREADS, tc::LB_SMEM, st>>>(
-        reinterpret_cast<float2 *>(psi), P, reinterpret_cast<const float *>(dev_payload));
-    return (int)cudaGetLastError();
-}
-
 static int tc_launch_l(void *psi, const tc::ParamsL &P, const void *dev_payload, cudaStream_t st) {
-    static bool attr_done = false;
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(tc::apply_tcL, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::L_SMEM);
-        if (e != cudaSuccess) return (int)e;
-        attr_done = true;
-    }
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    static std::atomic<uint64_t> attr{0};
+    cudaError_t e = smem_attr_once(tc::apply_tcL, tc::LB_SMEM, attr);
+    if (e != cudaSuccess) return (int)e;
+    const int sms = sm_count();
     const uint64_t grid = P.ntiles < (uint64_t)sms ? P.ntiles : (uint64_t)sms;
-    tc::apply_tcL<<<(unsigned)grid, tc::THREADS, tc::L_SMEM, st>>>(
-        reinterpret_cast<float2 *>(psi), P, reinterpret_cast<const float *>(dev_payload));
+    tc::apply_tcL<<<(unsigned)grid, tc::LB_THREADS, tc::LB_SMEM, st>>>(
+        reinterpret_cast<float2 *>(psi), P, reinterpret_cast<const uint32_t *>(dev_payload));
     return (int)cudaGetLastError();
 }
 
-// Mode H scales the state into the FP16 range by 2^ea with max |psi| * 2^ea
-// <= 2^14, from the runtime's rigorous bound on max |amplitude|.
+// Both modes scale the state into the FP16 range by 2^ea with
+// max |psi| 2^ea <= 2^14, from the runtime's rigorous bound on max |amplitude|.
 void tc_set_amp_bound(std::vector<char> &params, double bound) {
-    if (params.empty() || (params.back() != 'H' && params.back() != 'B')) return;
-    tc::Params &P = *reinterpret_cast<tc::Params *>(params.data());
+    if (params.empty()) return;
     int ex = 0;
     if (bound > 0 && std::isfinite(bound)) std::frexp(bound, &ex);   // bound < 2^ex
-    P.ea = std::max(-126, std::min(127, 14 - ex));
+    const int ea = std::max(-126, std::min(127, 14 - ex));
+    if (params.back() == 'B') reinterpret_cast<tc::ParamsB *>(params.data())->h.ea = ea;
+    else if (params.back() == 'L') reinterpret_cast<tc::ParamsL *>(params.data())->ea = ea;
 }
 
-// params: a tc::Params (mode H) or tc::ParamsL (mode L) block followed by
-// one tag byte ('H' or 'L'); size tells them apart.
+// params: a tc::ParamsB (mode H) or tc::ParamsL (mode L) block followed by
+// one tag byte ('B' or 'L').
 int tc_launch(void *psi, const void *params, size_t params_size, const void *dev_payload,
               void *stream) {
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const char tag = reinterpret_cast<const char *>(params)[params_size - 1];
     if (tag == 'L') return tc_launch_l(psi, *reinterpret_cast<const tc::ParamsL *>(params), dev_payload, st);
-    if (tag == 'M') return tc_launch_lb(psi, *reinterpret_cast<const tc::ParamsLB *>(params), dev_payload, st);
-    if (tag == 'B') {
-        const tc::ParamsB &B = *reinterpret_cast<const tc::ParamsB *>(params);
-        if (B.h.k == 4) return tc_launch_bk<4>(psi, B, dev_payload, st);
-        return B.h.k == 5 ? tc_launch_bk<5>(psi, B, dev_payload, st) : tc_launch_bk<6>(psi, B, dev_payload, st);
-    }
-    const tc::Params &P = *reinterpret_cast<const tc::Params *>(params);
-    if (P.k == 4) return tc_launch_k<4>(psi, P, dev_payload, st);
-    return P.k == 5 ? tc_launch_k<5>(psi, P, dev_payload, st) : tc_launch_k<6>(psi, P, dev_payload, st);
+    if (tag != 'B') return (int)cudaErrorInvalidValue;
+    const tc::ParamsB &B = *reinterpret_cast<const tc::ParamsB *>(params);
+#ifdef HQ_TC_DIAG_BUILD
+    if (B.diag) return B.h.k == 5 ? tc_launch_b<5, true>(psi, B, dev_payload, st)
+                                  : tc_launch_b<6, true>(psi, B, dev_payload, st);
+#endif
+    return B.h.k == 5 ? tc_launch_b<5>(psi, B, dev_payload, st) : tc_launch_b<6>(psi, B, dev_payload, st);
 }
 
 }  // namespace hq

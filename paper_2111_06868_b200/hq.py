@@ -43,7 +43,8 @@ class hq_op(ctypes.Structure):
 class hq_stats(ctypes.Structure):
     _fields_ = [("passes", ctypes.c_uint64), ("remaps", ctypes.c_uint64),
                 ("permutes", ctypes.c_uint64), ("kernel_launches", ctypes.c_uint64),
-                ("hbm_bytes", ctypes.c_uint64), ("link_bytes", ctypes.c_uint64)]
+                ("hbm_bytes", ctypes.c_uint64), ("link_bytes", ctypes.c_uint64),
+                ("h2d_bytes", ctypes.c_uint64), ("d2h_bytes", ctypes.c_uint64)]
 
 
 _lib = None
@@ -90,6 +91,7 @@ def lib():
             "hq_plan_layout": [ctypes.c_int, ctypes.c_int, ctypes.c_int, P, ctypes.c_size_t, P,
                                ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)],
             "hq_state_set_layout": [P, P],
+            "hq_state_invalidate_bound": [P],
             "hq_state_init_tokens": [P, ctypes.c_char_p],
             "hq_dm_superop": [P, ctypes.c_int, ctypes.c_int, P],
             "hq_dm_apply_unitary": [P, P, P, ctypes.c_int],
@@ -504,6 +506,11 @@ def hq_plan_layout(n, m, gates, dtype="c64"):
 def hq_state_set_layout(state, pi):
     v = np.ascontiguousarray(pi, dtype=np.int32)
     _check(lib().hq_state_set_layout(state.ptr, v.ctypes.data))
+
+
+def hq_state_invalidate_bound(state):
+    """Call after writing a borrowed state buffer outside the library (hq.h)."""
+    _check(lib().hq_state_invalidate_bound(state.ptr))
 
 
 def hq_state_get_layout(state):

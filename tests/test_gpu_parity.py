@@ -398,6 +398,31 @@ def test_rank_state_on_torch_buffers(dtype):
     assert e.value.status == "HQ_ERR_ARG"
 
 
+def test_borrowed_buffer_external_write_needs_invalidate():
+    """the complex64 tensor-core passes scale amplitudes into FP16
+    with the tracked norm bound.  After the caller scales a borrowed buffer
+    by 2^20 outside the library, hq_state_invalidate_bound makes the next
+    k = 6 pass correct (relative error within the single-pass bound)."""
+    import torch
+    n = 18
+    psi0 = random_state(n, 41)
+    psi_t = torch.from_numpy(psi0.astype(np.complex64)).cuda()
+    stream = torch.cuda.Stream()
+    s = hq.hq_state_create_from_buffers(n, "c64", psi_t.data_ptr(), stream.cuda_stream)
+    hq.hq_set_amplitudes(s, psi0)
+    assert abs(hq.hq_norm(s) - 1.0) < 1e-6          # bound is now ~1
+    torch.cuda.synchronize()
+    psi_t.mul_(2.0 ** 20)                           # external write: the bound is stale
+    torch.cuda.synchronize()
+    hq.hq_state_invalidate_bound(s)
+    g = haar_sweep_gate(n, 6, "spread", 2206)
+    hq.hq_apply_matrix(s, g.U, g.qubits)
+    want = O.apply_gate(psi0.copy() * 2.0 ** 20, g.U, g.qubits)
+    got = hq.hq_get_amplitudes(s).astype(np.complex128)
+    assert np.all(np.isfinite(got))
+    assert np.linalg.norm(got - want) / np.linalg.norm(want) < 2e-6
+
+
 # ---------------------------------------------------------------- merged plan at a tensor-core size
 
 @pytest.mark.parametrize("kmax", [5, 6])

@@ -1,4 +1,4 @@
-"""Tensor-core (tcgen05, 3xTF32) path: complex64 k = 5, 6 on states with
+"""Tensor-core (tcgen05, FP16 3-term split products) path: complex64 k = 5, 6 on states with
 n_local >= 16, against the fp64 oracle.  Tolerance 1e-4 (north_star) per
 circuit; single passes are held to a tighter 2e-6 to catch layout bugs that a
 loose bound would hide."""
@@ -45,6 +45,9 @@ LOWH5 = ["b:%d-8-12-14-16" % b for b in range(7)] + ["b:0-3-9-12-16", "b:1-2-9-1
 LOWH6 += ["b:0-1-10-12-14-16", "b:0-1-4-5-6-12", "b:0-1-8-9-10-11", "b:1-2-3-12-14-16",
           "b:0-2-3-9-12-16", "b:0-2-3-4-5-6", "b:1-2-3-7-8-9"]
 LOWH5 += ["b:0-1-12-14-16", "b:0-1-5-6-9", "b:1-2-3-9-14", "b:0-2-3-9-16", "b:0-2-3-4-5"]
+# every target below bit 7: mode L (round 2; these ran the removed cp.async mode-H kernel)
+LOWH5 += ["b:0-1-4-5-6", "b:2-3-4-5-6", "b:1-3-4-5-6", "b:0-2-4-5-6"]
+LOWH6 += ["b:1-2-3-4-5-6", "b:0-1-3-4-5-6", "b:0-2-3-4-5-6"]
 
 
 @pytest.mark.parametrize("n", [17, 20])

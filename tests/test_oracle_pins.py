@@ -515,25 +515,25 @@ def test_kraus_step_unravels_the_channel():
     assert np.max(np.abs(mean - want)) < 1e-14
 
 
-# ---------------------------------------------------------------- merged fusion reading
+# ---------------------------------------------------------------- P10 reversible image
+def test_P10_reversible_image_textbook_sequence():
+    """X, CX, SWAP, CCX on |0000> by hand (qubit 0 = MSB, C1; control first,
+    C2): X(0) -> 1000, CX(0,3) -> 1001, SWAP(1,3) -> 1100, CCX(0,1,2) -> 1110."""
+    n = 4
+    seq = [Gate("X", (0,), X), Gate("CX", (0, 3), CX), Gate("SWAP", (1, 3), SWAP),
+           Gate("CCX", (0, 1, 2), CCX)]
+    want = [0b1000, 0b1001, 0b1100, 0b1110]
+    for i in range(len(seq)):
+        assert O.reversible_image(n, seq[:i + 1], 0) == want[i]
+    with pytest.raises(O.OracleError):
+        O.reversible_image(n, [Gate("H", (0,), H)], 0)
 
-@pytest.mark.parametrize("kmax", [2, 3, 4, 6])
-def test_merge_groups_is_a_valid_regrouping(kmax):
-    """merge_groups only regroups: every gate in exactly one block, blocks of
-    <= kmax qubits, members in gate order, never more blocks than compress,
-    and the fused circuit is the original one (fp64 simulate, both orders of
-    evidence: the explicit dense product and the gate-by-gate apply)."""
+
+def test_P10_reversible_image_agrees_with_dense_simulation():
+    from hq_inputs import reversible_circuit
     n = 8
-    gates = [g for g in random_circuit(n, 70, 17, kmax=min(kmax, 3)) if len(g.qubits) <= kmax]
-    groups = O.compress(gates, kmax)
-    merged = O.merge_groups(gates, groups, kmax)
-    assert sorted(i for m in merged for i in m) == list(range(len(gates)))
-    assert all(m == sorted(m) for m in merged) and len(merged) <= len(groups)
-    assert all(len(set().union(*[set(gates[i].qubits) for i in m])) <= kmax for m in merged)
-    fused = O.fused_gates(gates, kmax, merged=True)
-    psi = random_state(n, 6)
-    want = O.simulate(n, gates, psi)
-    got = O.simulate(n, [Gate("F", q, U) for q, U in fused], psi)
-    assert np.max(np.abs(got - want)) < 1e-13
-    assert np.max(np.abs(O.circuit_matrix(n, [Gate("F", q, U) for q, U in fused])
-                         - O.circuit_matrix(n, gates))) < 1e-13
+    gates = reversible_circuit(n, 40, 5, kmax=3)
+    for x in (0, 1, 77, 255):
+        psi = O.simulate(n, gates, x=x)
+        y = O.reversible_image(n, gates, x)
+        assert psi[y] == 1.0 and np.count_nonzero(psi) == 1
