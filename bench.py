@@ -338,14 +338,18 @@ def run_hq(args):
                                                  buf_t.data_ptr() if buf_t is not None else None,
                                                  stream.cuda_stream, nid[0])
     layout = None
-    if world == 1 and not args.no_layout:
+    if not args.no_layout:
+        # the same planned layout on every rank: local bits by the pass cost
+        # model, and (world > 1) the first global set outside the schedule's
+        # first segment, so that segment needs no remap
         t0 = time.perf_counter()
-        layout, cost0, cost1 = hq.hq_plan_layout(n, 0, fused, args.dtype)
+        layout, cost0, cost1 = hq.hq_plan_layout(n, m_bits, fused, args.dtype)
         plan_ms += (time.perf_counter() - t0) * 1e3
         hq.hq_state_set_layout(state, layout)
     circ = hq.hq_circuit_create(state, fused)
     info = hq.hq_circuit_info(circ)
     P, R = info["passes"], info["remaps"]
+    standalone_permutes = info["permutes"]
     state_bytes = es * 2 ** n                     # whole job
     work_bytes = P * 2 * state_bytes              # algorithmic HBM bytes per step (all ranks)
 
@@ -424,7 +428,7 @@ def run_hq(args):
         hq.hq_state_init_basis(state, 0)
         fz = hq.hq_fuse(gates, kmax, merged=merged)
         if layout is not None:
-            hq.hq_state_set_layout(state, hq.hq_plan_layout(n, 0, fz, args.dtype)[0])
+            hq.hq_state_set_layout(state, hq.hq_plan_layout(n, m_bits, fz, args.dtype)[0])
             hq.hq_state_init_basis(state, 0)
         hq.hq_apply_circuit(state, fz)
         nv = hq.hq_norm(state)           # D2H of the result, synchronises
@@ -469,7 +473,8 @@ def run_hq(args):
         "config": {"workload": "%s Sycamore-style d%d random circuit, fused k<=%d (BASELINE configs[%d])"
                                % (args.config, cycles, kmax, cidx),
                    "n": n, "cycles": cycles, "seed": seed, "kmax": kmax, "gates": len(gates),
-                   "passes": P, "remaps": R, "circuit_sha256": circuit_sha256(gates),
+                   "passes": P, "remaps": R, "standalone_permutes": standalone_permutes,
+                   "circuit_sha256": circuit_sha256(gates),
                    "unit_passes_match": UNIT_PASSES.get((args.config, kmax, args.fuse)) == P,
                    "state_gib": state_bytes / 2 ** 30,
                    "l2": "no flush: state %.0f GiB >> 126 MB L2" % (state_bytes / 2 ** 30),

@@ -87,12 +87,13 @@ typedef struct hq_circuit hq_circuit;
 typedef struct hq_stats {
     uint64_t passes;          /* apply kernels launched (all shards)              */
     uint64_t remaps;          /* global<->local qubit swaps (all-to-all exchanges) */
-    uint64_t permutes;        /* local bit-permutation passes                      */
+    uint64_t permutes;        /* standalone local bit-permutation passes           */
     uint64_t kernel_launches; /* all library kernels launched on this rank         */
     uint64_t hbm_bytes;       /* algorithmic HBM bytes of those kernels (this rank) */
     uint64_t link_bytes;      /* bytes sent to peers by remaps (this rank)         */
     uint64_t h2d_bytes;       /* host->device bytes the library copied (this rank) */
     uint64_t d2h_bytes;       /* device->host bytes the library copied (this rank) */
+    uint64_t packs;           /* PERMUTEs folded into an apply pass (apply+pack)   */
 } hq_stats;
 
 /* ------------------------------------------------------------------ create */
@@ -155,9 +156,9 @@ hq_status hq_state_create_rank_from_buffers(int n, hq_dtype dtype, int world_siz
  * the amplitudes live in HBM, never what get/set_amplitudes return (always
  * logical order, C14).  hq_state_set_layout makes the given layout the one
  * hq_state_init_basis restores; the amplitudes are UNDEFINED after the call
- * until hq_state_init_basis or a full hq_set_amplitudes.  Single-rank states
- * only (distributed states start from the default and change by remaps).
- * Errors: HQ_ERR_ARG (not a permutation), HQ_ERR_STATE (multi-rank). */
+ * until hq_state_init_basis or a full hq_set_amplitudes.  In a multi-rank
+ * state every rank must set the same layout (the top log2 G physical bits are
+ * the rank bits).  Errors: HQ_ERR_ARG (not a permutation). */
 hq_status hq_state_set_layout(hq_state *s, const int32_t *pi);
 hq_status hq_state_get_layout(const hq_state *s, int32_t *pi_out);
 
@@ -365,6 +366,11 @@ hq_status hq_fuse_plan(const hq_gate *in, size_t ngates, int kmax, int32_t *grou
 
 /* Host-only view of the distributed schedule (for tests): for an n-qubit
  * state on G = 2^m ranks, the op stream hq_apply_circuit would execute.
+ * The stream is cut into segments, each a maximal run of gates whose
+ * must-be-local qubits fit on the n - m local bits; one REMAP at each segment
+ * boundary swaps the incoming globals with the local qubits of furthest next
+ * use (Belady), which a PERMUTE first packs onto the top local bits (the
+ * executor folds that PERMUTE into the preceding apply pass: apply+pack).
  * ops[i] = {kind, gate, nbits, bits[12]}:
  *   kind 0 APPLY  : gate index `gate`, bits[0..k-1] = physical target bits of
  *                   qubits[0..k-1]; a bit >= n - m is a global target of a
@@ -382,6 +388,10 @@ typedef struct hq_op {
 } hq_op;
 hq_status hq_schedule(int n, int m, const hq_gate *gates, size_t ngates,
                       hq_op **ops, size_t *nops, int32_t *pi_out);
+/* The same from a given initial layout pi_in (n entries, a permutation; e.g.
+ * hq_plan_layout's), as a state with that layout would execute it. */
+hq_status hq_schedule_from(int n, int m, const hq_gate *gates, size_t ngates, const int32_t *pi_in,
+                           hq_op **ops, size_t *nops, int32_t *pi_out);
 hq_status hq_free_ops(hq_op *ops);
 
 /* Layout planner (the GPU counterpart of the paper's "qubits are swapped to
@@ -390,6 +400,9 @@ hq_status hq_free_ops(hq_op *ops);
  * estimated pass cost of `gates` for dtype (HQ_C64 / HQ_C128).  The cost model
  * penalises targets in the warp-lane bits of the
  * SIMT kernel and tensor-core gathers spanning more than 16 8-MB regions.
+ * With m > 0 it also picks the m qubits that start global: those outside the
+ * first segment of the distributed schedule with the furthest next use, so
+ * the first segment needs no remap.
  * pi_out receives n entries; cost_before / cost_after (may be NULL) the
  * model's totals for the default and the returned layout. */
 hq_status hq_plan_layout(int n, int m, int dtype, const hq_gate *gates, size_t ngates,

@@ -48,6 +48,11 @@ struct RegParams {
     uint64_t nunits;     // number of threads with work (= 32 * warps)
     int S[6];            // ascending insertion positions in warp space (count K-T0)
     int la[5];           // lane bit (0..4) of each lane target, canonical order
+    // out-of-place output (om.active): positions in load units; pvoff[v] =
+    // om_swap(voff[v]) without the selector bits, tv[v] = its selector bits
+    OutMap om;
+    uint64_t pvoff[32];
+    uint8_t tv[32];
 };
 
 template <typename R, int K> struct UParam {
@@ -176,6 +181,25 @@ apply_reg(typename C2<R>::T *__restrict__ psi, const __grid_constant__ RegParams
 #pragma unroll
     for (int i = KL - 1; i >= 0; --i) lane_transpose<V, NR>(x, P.la[i], T0 + i, lane);
 
+    if (P.om.active) {
+        // apply+pack: out-of-place, bit-permuted (and buffer-selected) output
+        const uint64_t yb = om_swap(base, P.om);
+        const uint32_t tb = (uint32_t)(yb >> P.om.tsh) & P.om.tmask;
+        const uint64_t lb = (yb & ~((uint64_t)P.om.tmask << P.om.tsh)) | P.om.add;
+        if constexpr (VEC == 2) {
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                const int j0 = ((v >> P0) << (P0 + 1)) | (v & ((1 << P0) - 1));
+                const int j1 = j0 | (1 << P0);
+                float4 *dst = reinterpret_cast<float4 *>(P.om.dst[tb | P.tv[v]]);
+                dst[lb | P.pvoff[v]] = make_float4(x[j0].x, x[j0].y, x[j1].x, x[j1].y);
+            }
+        } else {
+#pragma unroll
+            for (int v = 0; v < NV; ++v) reinterpret_cast<V *>(P.om.dst[tb | P.tv[v]])[lb | P.pvoff[v]] = x[v];
+        }
+        return;
+    }
     if constexpr (VEC == 2) {
         float4 *dst = reinterpret_cast<float4 *>(psi);
 #pragma unroll
@@ -196,7 +220,17 @@ struct GenParams {
     uint64_t off[64];    // amplitude offset of U-index c (canonical order)
     uint64_t nsets;      // 2^(n_l - k)
     int s[6];            // ascending target bits
+    OutMap om;           // out-of-place output (om.active), amplitude units
 };
+
+// output element for amplitude index x (in place, or through the output map)
+template <typename V>
+__device__ __forceinline__ V *gen_out(V *psi, uint64_t x, const OutMap &om) {
+    if (!om.active) return psi + x;
+    const uint64_t y = om_swap(x, om);
+    const uint32_t t = (uint32_t)(y >> om.tsh) & om.tmask;
+    return reinterpret_cast<V *>(om.dst[t]) + ((y & ~((uint64_t)om.tmask << om.tsh)) | om.add);
+}
 
 template <typename R, int K>
 __global__ void __launch_bounds__(128)
@@ -225,7 +259,7 @@ apply_gen(typename C2<R>::T *__restrict__ psi, const __grid_constant__ GenParams
             V w;
             w.x = ar;
             w.y = ai;
-            psi[base + P.off[r]] = w;
+            *gen_out(psi, base + P.off[r], P.om) = w;
         }
     }
 }
@@ -261,7 +295,7 @@ apply_gen_warp(typename C2<R>::T *__restrict__ psi, const __grid_constant__ GenP
         V out;
         out.x = ar;
         out.y = ai;
-        psi[base + P.off[r]] = out;
+        *gen_out(psi, base + P.off[r], P.om) = out;
     }
 }
 
@@ -512,13 +546,59 @@ static cudaError_t launch_ztile(void *psi, const GenParams &P, const void *dU, c
     return cudaGetLastError();
 }
 
+// OutSpec (amplitude bit positions) -> OutMap in units of 2^lb amplitudes.
+// False when a swapped bit, the selector or the added offset falls inside a
+// unit (such a map would split a vector).
+static bool out_map(const OutSpec &o, int lb, OutMap &m) {
+    m = OutMap{};
+    if (!o.active) return true;
+    m.active = 1;
+    m.npairs = o.npairs;
+    for (int i = 0; i < o.npairs; ++i) {
+        if (o.pa[i] < lb || o.pb[i] < lb) return false;
+        m.pa[i] = o.pa[i] - lb;
+        m.pb[i] = o.pb[i] - lb;
+    }
+    if (o.tmask && o.tsh < lb) return false;
+    if (o.add & ((1ull << lb) - 1)) return false;
+    m.tsh = o.tmask ? o.tsh - lb : 0;
+    m.tmask = o.tmask;
+    m.add = o.add >> lb;
+    for (int t = 0; t < 8; ++t) m.dst[t] = reinterpret_cast<uint64_t>(o.dst[t]);
+    return true;
+}
+
+static bool reg_out_tables(RegParams &rp, int VEC, int K, int T0, const OutSpec *out) {
+    const int LB = VEC == 2 ? 1 : 0;
+    if (!out_map(out ? *out : OutSpec{}, LB, rp.om)) return false;
+    if (!rp.om.active) return true;
+    const int NB0 = (VEC == 2 && !T0) ? 1 : 0;
+    const int NV = (1 << (K + NB0)) / VEC;
+    for (int v = 0; v < NV; ++v) {
+        const uint64_t y = om_swap(rp.voff[v], rp.om);
+        rp.tv[v] = (uint8_t)((y >> rp.om.tsh) & rp.om.tmask);
+        rp.pvoff[v] = y & ~((uint64_t)rp.om.tmask << rp.om.tsh);
+    }
+    return true;
+}
+
+bool apply_supports_out(int dtype, const ApplyDesc &d, const OutSpec &o) {
+    RegParams rp;
+    int VEC = 1, T0 = 0, KL = 0;
+    if (plan_reg(dtype, d, rp, VEC, T0, KL)) return reg_out_tables(rp, VEC, d.k, T0, &o);
+    if (dtype == HQ_C128 && d.k >= 5 && (1ull << (d.n_local - d.k)) >= (1ull << 12)) return false;   // apply_ztile
+    OutMap m;
+    return out_map(o, 0, m);
+}
+
 int launch_apply(int dtype, void *psi, const ApplyDesc &d, const void *host_U, const void *dev_U,
-                 void *stream, int *launches) {
+                 void *stream, int *launches, const OutSpec *out) {
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     RegParams rp;
     int VEC = 1, T0 = 0, KL = 0;
     cudaError_t e;
     if (host_U && plan_reg(dtype, d, rp, VEC, T0, KL)) {
+        if (!reg_out_tables(rp, VEC, d.k, T0, out)) return (int)cudaErrorInvalidValue;
         if (dtype == HQ_C64) {
             switch (d.k) {
                 case 1: e = launch_reg_f<1>(VEC, T0, KL, psi, rp, host_U, st); break;
@@ -545,9 +625,11 @@ int launch_apply(int dtype, void *psi, const ApplyDesc &d, const void *host_U, c
         for (int i = 0; i < d.k; ++i) gp.s[i] = d.p[i];
         gp.nsets = 1ull << (d.n_local - d.k);
         if (!dev_U) return (int)cudaErrorInvalidValue;
-        static const char *zt = getenv("HQ_ZTILE");     // "0": generic kernel (experiments)
-        if (dtype == HQ_C128 && d.k >= 5 && gp.nsets >= (1ull << 12) && !(zt && zt[0] == '0'))
+        if (!out_map(out ? *out : OutSpec{}, 0, gp.om)) return (int)cudaErrorInvalidValue;
+        if (dtype == HQ_C128 && d.k >= 5 && gp.nsets >= (1ull << 12)) {
+            if (gp.om.active) return (int)cudaErrorInvalidValue;     // in place only
             e = d.k == 5 ? launch_ztile<5>(psi, gp, dev_U, st) : launch_ztile<6>(psi, gp, dev_U, st);
+        }
         else
             e = dtype == HQ_C64 ? launch_gen<float>(d.k, psi, gp, dev_U, st)
                                 : launch_gen<double>(d.k, psi, gp, dev_U, st);

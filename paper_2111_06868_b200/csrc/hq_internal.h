@@ -66,7 +66,11 @@ struct Op {
 // applies the block selected by its rank bits to the local targets (row f1).
 void schedule(int n, int m, const std::vector<GateRef> &g, std::vector<int> &pi,
               std::vector<Op> &ops);
+// Lowest physical bit a scheduler PERMUTE (pack) may move: bits 0 and 1 stay in
+// place so that every apply+pack write still fills whole 32-byte sectors.
+constexpr int PACK_MIN_BIT = 2;
 bool block_diag_in(const double *U, int k, int umask);
+uint64_t local_need(const GateRef &gt);
 
 // Layout planner: logical->physical map of the local qubits minimising the
 // estimated pass cost of `g` (hq_plan_layout).
@@ -83,6 +87,43 @@ struct ApplyDesc {
     int n_local;
 };
 
+// Out-of-place output of an apply pass (apply+pack): the
+// amplitude computed for input index x is written at output index
+//   y = x with the bit pairs (pa[i], pb[i]) exchanged,
+//   t = (y >> tsh) & tmask            (selects the output buffer dst[t]),
+//   dst[t][(y & ~(tmask << tsh)) | add].
+// apply+pack alone: one buffer (tmask = 0, add = 0).  The kernels take the
+// positions in their own index units (amplitudes, or 16-byte vectors for the
+// complex64 SIMT kernel).  active = 0: in place.
+struct OutMap {
+    uint64_t dst[8];
+    uint64_t add;
+    int active;
+    int npairs;
+    int pa[6], pb[6];
+    int tsh;
+    uint32_t tmask;
+};
+
+__host__ __device__ inline uint64_t om_swap(uint64_t x, const OutMap &m) {
+    for (int i = 0; i < m.npairs; ++i) {
+        const uint64_t d = ((x >> m.pa[i]) ^ (x >> m.pb[i])) & 1;
+        x ^= (d << m.pa[i]) | (d << m.pb[i]);
+    }
+    return x;
+}
+
+// Host description of an out-of-place output (amplitude bit positions).
+struct OutSpec {
+    bool active = false;
+    int npairs = 0;
+    int pa[6] = {0}, pb[6] = {0};
+    int tsh = 0;
+    uint32_t tmask = 0;
+    void *dst[8] = {nullptr};
+    uint64_t add = 0;
+};
+
 // Device-side matrix: U in dtype, row-major, interleaved, 4^k complex.
 // host_U (dtype, same layout) is also given so small matrices travel in the
 // kernel's parameter space; dev_U may be null if host path suffices.
@@ -93,7 +134,10 @@ struct KernelStatus {
 // Launch one apply pass on `psi` (2^n_local amplitudes).  Returns cudaError_t
 // as int.  stream is a cudaStream_t.
 int launch_apply(int dtype, void *psi, const ApplyDesc &d, const void *host_U,
-                 const void *dev_U, void *stream, int *launches);
+                 const void *dev_U, void *stream, int *launches, const OutSpec *out = nullptr);
+// Whether launch_apply can write this pass out of place through an OutSpec
+// (every kernel but the complex128 k = 5, 6 tile kernel).
+bool apply_supports_out(int dtype, const ApplyDesc &d, const OutSpec &o);
 
 // Whether launch_apply needs dev_U (true when U cannot travel as a kernel
 // parameter for this (dtype, k, placement)).
@@ -122,6 +166,9 @@ void tc_prepare(const ApplyDesc &d, const double *Ucanon, std::vector<char> &pay
                 std::vector<char> &params);
 int tc_launch(void *psi, const void *params, size_t params_size, const void *dev_payload,
               void *stream);
+// Fill the output-map tables of a tensor-core parameter block (apply+pack);
+// returns false when this block cannot write out of place with that map.
+bool tc_set_output(std::vector<char> &params, const OutSpec &o);
 // Set the FP16 input scale of a mode-H parameter block from a rigorous upper
 // bound on max |amplitude| of the state the pass will read.
 void tc_set_amp_bound(std::vector<char> &params, double bound);

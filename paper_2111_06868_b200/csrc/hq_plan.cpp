@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <tuple>
 #include <vector>
 #include <limits>
 #include <new>
@@ -287,6 +288,28 @@ bool block_diag_in(const double *U, int k, int umask) {
     return true;
 }
 
+// Qubits gate gt must hold on local bits: every target in which U is not
+// block-diagonal (row f1: a target in which U is block-diagonal may stay
+// global; block-diagonality in each of several bits implies it in their union).
+uint64_t local_need(const GateRef &gt) {
+    uint64_t need = 0;
+    for (int j = 0; j < gt.k; ++j)
+        if (!block_diag_in(gt.U, gt.k, 1 << (gt.k - 1 - j))) need |= 1ull << gt.q[j];
+    return need;
+}
+
+// Distributed schedule.  The op stream is cut into segments, each a maximal
+// run of gates whose local-need qubits fit on the n - m local bits together
+// (greedy furthest reach, which minimises the number of segments, hence of
+// remaps, for a given first global set).  At each segment boundary one REMAP
+// makes the new global set S: the current globals the segment does not need
+// stay global, and the incoming ones trade places with the local qubits of the
+// complement whose next use lies furthest ahead (Belady), preferring bits >=
+// PACK_MIN_BIT.  Those evictees are first packed onto the top local bits by a
+// PERMUTE (swap pairs), unless they already lie in the top RUNWIN bits; the
+// executor folds a PERMUTE into the preceding apply pass as a bit-permuting
+// out-of-place write (apply+pack: no extra HBM pass), so every peer's data is
+// one contiguous chunk (or a few long runs).
 void schedule(int n, int m, const std::vector<GateRef> &g, std::vector<int> &pi,
               std::vector<Op> &ops) {
     const int nl = n - m;
@@ -297,128 +320,105 @@ void schedule(int n, int m, const std::vector<GateRef> &g, std::vector<int> &pi,
     std::vector<int> inv(n);
     for (int q = 0; q < n; ++q) inv[pi[q]] = q;
     ops.clear();
-    // next_use[i][q] computed lazily: for each qubit, list of gate indices using it
+    const size_t N = g.size();
+    std::vector<uint64_t> need(N, 0);
+    if (m > 0)
+        for (size_t i = 0; i < N; ++i) need[i] = local_need(g[i]);
+    // uses[q] = gates that need logical qubit q local (ascending)
     std::vector<std::vector<uint32_t>> uses(n);
-    for (size_t i = 0; i < g.size(); ++i)
-        for (int j = 0; j < g[i].k; ++j) uses[g[i].q[j]].push_back((uint32_t)i);
-    std::vector<size_t> cursor(n, 0);
-    auto next_use = [&](int q, size_t after) -> size_t {
-        auto &u = uses[q];
-        size_t &c = cursor[q];
-        while (c < u.size() && u[c] <= after) ++c;
-        return c < u.size() ? u[c] : std::numeric_limits<size_t>::max();
+    for (size_t i = 0; i < N; ++i)
+        for (int q = 0; q < n; ++q)
+            if ((need[i] >> q) & 1) uses[q].push_back((uint32_t)i);
+    auto next_use = [&](int q, size_t from) -> size_t {     // first use at index >= from
+        auto it = std::lower_bound(uses[q].begin(), uses[q].end(), (uint32_t)from);
+        return it == uses[q].end() ? std::numeric_limits<size_t>::max() : *it;
     };
-    // Evictees (local qubits that become global) are taken from the top
-    // RUNWIN local bits: there a remap's per-peer data is at most
-    // 2^(RUNWIN - m') contiguous runs, which the executor sends as grouped
-    // point-to-point transfers with no packing pass.  Only when that window
-    // cannot supply enough candidates do we fall back to a PERMUTE pass.
+    auto swap_phys = [&](int a, int b) {           // exchange the qubits at physical bits a, b
+        const int qa = inv[a], qb = inv[b];
+        std::swap(pi[qa], pi[qb]);
+        inv[a] = qb;
+        inv[b] = qa;
+    };
+    auto globals = [&]() {
+        uint64_t G = 0;
+        for (int p = nl; p < n; ++p) G |= 1ull << inv[p];
+        return G;
+    };
     const int RUNWIN = std::min(nl, 7);
-    for (size_t i = 0; i < g.size(); ++i) {
+    for (size_t i = 0; i < N; ++i) {
         const GateRef &gt = g[i];
-        if (m > 0) {
-            uint64_t Q = qmask(gt);
-            int need[6], nneed = 0, umask = 0;
-            for (int j = 0; j < gt.k; ++j)
-                if (pi[gt.q[j]] >= nl) {
-                    need[nneed++] = gt.q[j];
-                    umask |= 1 << (gt.k - 1 - j);
-                }
-            // Row f1: a gate block-diagonal in its global targets needs no
-            // remap; every rank applies the block its rank bits select
-            // (an APPLY whose bits include global positions >= nl).
-            if (nneed > 0 && block_diag_in(gt.U, gt.k, umask)) nneed = 0;
-            if (nneed > 0) {
-                // candidates in the run window, furthest next use first (Belady)
-                std::vector<std::pair<size_t, int>> cand;   // (next use, phys bit)
-                for (int p = nl - RUNWIN; p < nl; ++p) {
-                    const int q = inv[p];
-                    if ((Q >> q) & 1) continue;
-                    cand.push_back({next_use(q, i), p});
-                }
-                std::sort(cand.begin(), cand.end(), [](const auto &a, const auto &b) {
-                    if (a.first != b.first) return a.first > b.first;
-                    return a.second > b.second;
-                });
-                if ((int)cand.size() < nneed) {
-                    // fallback: permute the best evictees from anywhere into the window
-                    std::vector<std::pair<size_t, int>> all;
-                    for (int p = 0; p < nl; ++p) {
-                        const int q = inv[p];
-                        if ((Q >> q) & 1) continue;
-                        all.push_back({next_use(q, i), p});
-                    }
-                    std::sort(all.begin(), all.end(), [](const auto &a, const auto &b) {
-                        if (a.first != b.first) return a.first > b.first;
-                        return a.second > b.second;
-                    });
-                    Op perm{OP_PERMUTE, -1, 0, {0}};
-                    int used = 0;
-                    for (auto &c : all) {
-                        if ((int)cand.size() >= nneed) break;
-                        if (c.second >= nl - RUNWIN) continue;     // already in the window
-                        // swap into a window slot holding a target-free... any non-Q slot
-                        // is already a candidate, so the free slots hold Q qubits: swap
-                        // with the lowest window slot not yet used as a candidate
-                        int slot = -1;
-                        for (int p = nl - RUNWIN; p < nl && slot < 0; ++p) {
-                            bool taken = false;
-                            for (auto &cc : cand) taken |= cc.second == p;
-                            if (!taken) slot = p;
-                        }
-                        if (slot < 0 || used >= 6) break;
-                        perm.bits[2 * perm.nbits] = c.second;
-                        perm.bits[2 * perm.nbits + 1] = slot;
-                        perm.nbits++;
-                        ++used;
-                        const int qa = inv[c.second], qb = inv[slot];
-                        std::swap(pi[qa], pi[qb]);
-                        inv[c.second] = qb;
-                        inv[slot] = qa;
-                        cand.push_back({c.first, slot});
-                    }
-                    if (perm.nbits > 0) ops.push_back(perm);
-                }
-                // also bring in other global qubits needed sooner than the local
-                // qubits the window would keep (one exchange instead of several)
-                std::vector<std::pair<size_t, int>> gl;       // (next use, logical q)
-                for (int p = nl; p < n; ++p) {
-                    const int q = inv[p];
-                    bool in_need = false;
-                    for (int t = 0; t < nneed; ++t) in_need |= need[t] == q;
-                    if (!in_need) gl.push_back({next_use(q, i), q});
-                }
-                std::sort(gl.begin(), gl.end());
-                int nb = nneed;
-                int bring[6];
-                for (int t = 0; t < nneed; ++t) bring[t] = need[t];
-                for (auto &x : gl) {
-                    if (nb >= (int)cand.size() || nb >= 6) break;
-                    if (x.first >= cand[nb].first) break;   // evicting cand[nb] would cost more
-                    bring[nb++] = x.second;
-                }
-                int gb[6], lb[6];
-                for (int t = 0; t < nb; ++t) {
-                    gb[t] = pi[bring[t]];
-                    lb[t] = cand[t].second;
-                }
-                std::sort(gb, gb + nb);
-                std::sort(lb, lb + nb);
-                Op rem{OP_REMAP, -1, nb, {0}};
-                for (int t = 0; t < nb; ++t) {
-                    const int a = gb[t], b = lb[t];
-                    rem.bits[2 * t] = a;
-                    rem.bits[2 * t + 1] = b;
-                    const int qa = inv[a], qb = inv[b];
-                    std::swap(pi[qa], pi[qb]);
-                    inv[a] = qb;
-                    inv[b] = qa;
-                }
-                ops.push_back(rem);
+        if (m > 0 && (need[i] & globals())) {
+            // the segment starting at gate i; it also ends early when the
+            // incoming globals would outnumber the local qubits outside it
+            // that a folded pack can move (bits >= PACK_MIN_BIT)
+            const uint64_t Gm = globals();
+            uint64_t Lp = 0;
+            for (int p = std::min(PACK_MIN_BIT, nl); p < nl; ++p) Lp |= 1ull << inv[p];
+            uint64_t U = 0;
+            size_t j = i;
+            while (j < N) {
+                const uint64_t U2 = U | need[j];
+                if (__builtin_popcountll(U2) > nl) break;
+                if (j > i && __builtin_popcountll(U2 & Gm) > __builtin_popcountll(Lp & ~U2)) break;
+                U = U2;
+                ++j;
             }
+            // incoming: current globals the segment needs
+            int in_bits[6], nin = 0;
+            for (int p = nl; p < n; ++p)
+                if ((U >> inv[p]) & 1) in_bits[nin++] = p;
+            // outgoing: local qubits outside the segment's union, furthest next use
+            // after the segment first, bits >= PACK_MIN_BIT before bits below it
+            std::vector<std::tuple<int, size_t, int>> cand;   // (packable, next use, phys bit)
+            for (int p = 0; p < nl; ++p) {
+                const int q = inv[p];
+                if ((U >> q) & 1) continue;
+                cand.push_back({p >= PACK_MIN_BIT ? 1 : 0, next_use(q, j), p});
+            }
+            std::sort(cand.begin(), cand.end(), [](const auto &a, const auto &b) {
+                if (std::get<0>(a) != std::get<0>(b)) return std::get<0>(a) > std::get<0>(b);
+                if (std::get<1>(a) != std::get<1>(b)) return std::get<1>(a) > std::get<1>(b);
+                return std::get<2>(a) > std::get<2>(b);
+            });
+            int ev[6];
+            bool in_window = true;
+            for (int t = 0; t < nin; ++t) {
+                ev[t] = std::get<2>(cand[t]);
+                in_window &= ev[t] >= nl - RUNWIN;
+            }
+            int lb[6];
+            if (in_window) {
+                for (int t = 0; t < nin; ++t) lb[t] = ev[t];
+            } else {
+                // pack: the evictees onto the top nin local bits
+                Op perm{OP_PERMUTE, -1, 0, {0}};
+                bool is_ev[64] = {false};
+                for (int t = 0; t < nin; ++t) is_ev[ev[t]] = true;
+                int slot = nl - 1;
+                for (int t = 0; t < nin; ++t) {
+                    if (ev[t] >= nl - nin) { lb[t] = ev[t]; continue; }
+                    while (is_ev[slot]) --slot;      // a top slot not holding an evictee
+                    perm.bits[2 * perm.nbits] = ev[t];
+                    perm.bits[2 * perm.nbits + 1] = slot;
+                    perm.nbits++;
+                    swap_phys(ev[t], slot);
+                    is_ev[slot] = true;
+                    lb[t] = slot--;
+                }
+                if (perm.nbits > 0) ops.push_back(perm);
+            }
+            std::sort(in_bits, in_bits + nin);
+            std::sort(lb, lb + nin);
+            Op rem{OP_REMAP, -1, nin, {0}};
+            for (int t = 0; t < nin; ++t) {
+                rem.bits[2 * t] = in_bits[t];
+                rem.bits[2 * t + 1] = lb[t];
+                swap_phys(in_bits[t], lb[t]);
+            }
+            ops.push_back(rem);
         }
         Op ap{OP_APPLY, (int)i, gt.k, {0}};
-        for (int j = 0; j < gt.k; ++j) ap.bits[j] = pi[gt.q[j]];
+        for (int jj = 0; jj < gt.k; ++jj) ap.bits[jj] = pi[gt.q[jj]];
         ops.push_back(ap);
     }
 }
@@ -473,6 +473,44 @@ void plan_layout(int n, int m, int dtype, const std::vector<GateRef> &g, std::ve
     pi.resize(n);
     for (int q = 0; q < n; ++q) pi[q] = n - 1 - q;
     const int nl = n - m;
+    if (m > 0 && !g.empty()) {
+        // the first global set: m qubits outside the first segment (the
+        // schedule's maximal gate run whose local-need qubits fit on nl
+        // bits), furthest first use after it first; they take the global bits
+        // in place of the default globals (logical 0..m-1)
+        std::vector<uint64_t> need(g.size());
+        for (size_t i = 0; i < g.size(); ++i) need[i] = local_need(g[i]);
+        uint64_t U = 0;
+        size_t j = 0;
+        while (j < g.size() && __builtin_popcountll(U | need[j]) <= nl) U |= need[j++];
+        std::vector<std::pair<size_t, int>> cand;     // (first use at >= j, logical q)
+        for (int q = 0; q < n; ++q) {
+            if ((U >> q) & 1) continue;
+            size_t first = std::numeric_limits<size_t>::max();
+            for (size_t i = j; i < g.size() && first == std::numeric_limits<size_t>::max(); ++i)
+                if ((need[i] >> q) & 1) first = i;
+            cand.push_back({first, q});
+        }
+        std::stable_sort(cand.begin(), cand.end(), [](const auto &a, const auto &b) { return a.first > b.first; });
+        std::vector<int> inv(n);
+        for (int q = 0; q < n; ++q) inv[pi[q]] = q;
+        for (int t = 0; t < m && t < (int)cand.size(); ++t) {
+            const int q = cand[t].second;
+            if (pi[q] >= nl) continue;                  // already global
+            // swap with a global qubit that is not itself chosen
+            for (int p = nl; p < n; ++p) {
+                const int o = inv[p];
+                bool chosen = false;
+                for (int u = 0; u < m && u < (int)cand.size(); ++u) chosen |= cand[u].second == o;
+                if (chosen) continue;
+                const int pq = pi[q];
+                std::swap(pi[q], pi[o]);
+                inv[p] = q;
+                inv[pq] = o;
+                break;
+            }
+        }
+    }
     std::vector<std::vector<int>> uses(n);
     for (size_t i = 0; i < g.size(); ++i)
         for (int j = 0; j < g[i].k; ++j) uses[g[i].q[j]].push_back((int)i);
@@ -605,6 +643,11 @@ extern "C" hq_status hq_free_gates(hq_gate *gates, size_t ngates) {
 
 extern "C" hq_status hq_schedule(int n, int m, const hq_gate *gates, size_t ngates, hq_op **ops,
                                  size_t *nops, int32_t *pi_out) {
+    return hq_schedule_from(n, m, gates, ngates, nullptr, ops, nops, pi_out);
+}
+
+extern "C" hq_status hq_schedule_from(int n, int m, const hq_gate *gates, size_t ngates, const int32_t *pi_in,
+                                      hq_op **ops, size_t *nops, int32_t *pi_out) {
     clear_error();
     if ((!gates && ngates) || !ops || !nops) return set_error(HQ_ERR_ARG, "NULL argument");
     if (n < 1 || n > 63 || m < 0 || m > 16) return set_error(HQ_ERR_ARG, "bad n=%d / m=%d", n, m);
@@ -615,6 +658,12 @@ extern "C" hq_status hq_schedule(int n, int m, const hq_gate *gates, size_t ngat
     for (size_t i = 0; i < ngates; ++i)
         if (refs[i].k > n - m) return set_error(HQ_ERR_K, "gate %zu: k=%d > local qubits %d", i, refs[i].k, n - m);
     std::vector<int> pi;
+    if (pi_in) {
+        std::vector<int> seen(n, 0);
+        pi.assign(pi_in, pi_in + n);
+        for (int q = 0; q < n; ++q)
+            if (pi[q] < 0 || pi[q] >= n || seen[pi[q]]++) return set_error(HQ_ERR_ARG, "pi_in is not a permutation");
+    }
     std::vector<Op> v;
     schedule(n, m, refs, pi, v);
     hq_op *arr = new (std::nothrow) hq_op[v.size() ? v.size() : 1];

@@ -138,6 +138,7 @@ struct hq_circuit {
     std::vector<std::vector<struct Prep>> cprep;
     std::vector<std::vector<long long>> cuoff;
     std::vector<double> cgnorm;            // spectral bound of the whole U
+    std::vector<OutSpec> pack;             // per APPLY op: apply+pack output map (active: folds op i+1)
     std::vector<char *> dev_U;             // per shard: all payloads
     // small single-shard states: the whole op stream in one shared-memory CTA
     SmemOp *small_ops = nullptr;
@@ -145,7 +146,7 @@ struct hq_circuit {
     int small_nops = 0;
     int small_dev = 0;
     std::vector<int> dev_of;               // per shard: its device (destroy must not read the state)
-    uint64_t passes = 0, remaps = 0, permutes = 0;
+    uint64_t passes = 0, remaps = 0, permutes = 0, packs = 0;
     // CUDA graph of the whole op stream (single-shard states, profiling off):
     // captured on the first run, replayed while the capture key matches.
     cudaGraphExec_t graph = nullptr;
@@ -514,7 +515,6 @@ extern "C" hq_status hq_state_invalidate_bound(hq_state *st) {
 extern "C" hq_status hq_state_set_layout(hq_state *st, const int32_t *pi) {
     clear_error();
     if (!st || !pi) return set_error(HQ_ERR_ARG, "NULL argument");
-    if (st->world > 1) return set_error(HQ_ERR_STATE, "layout can only be chosen for single-rank states");
     std::vector<int> seen(st->n, 0), v(st->n);
     for (int q = 0; q < st->n; ++q) {
         if (pi[q] < 0 || pi[q] >= st->n || seen[pi[q]]++)
@@ -677,15 +677,44 @@ static hq_status prof_end(hq_state *st, Shard &s, ProfEvent &pe, uint64_t bytes,
 
 static hq_status ensure_bound(hq_state *st);
 
-static hq_status exec_apply(hq_state *st, Shard &s, const Prep &p, const void *dU) {
+// apply+pack: the scheduler's PERMUTE right after an APPLY is
+// folded into that pass, which then reads psi and writes the bit-permuted
+// result into the exchange buffer (no extra HBM pass).  True when the
+// prepared pass can do so; o receives the output map (dst set per shard).
+static bool pack_spec(const hq_state *st, const Prep &p, const Op &perm, OutSpec &o) {
+    if (p.scalar || perm.kind != OP_PERMUTE || perm.nbits < 1 || perm.nbits > 6) return false;
+    o = OutSpec{};
+    o.active = true;
+    o.npairs = perm.nbits;
+    for (int i = 0; i < perm.nbits; ++i) {
+        o.pa[i] = perm.bits[2 * i];
+        o.pb[i] = perm.bits[2 * i + 1];
+        if (o.pa[i] < PACK_MIN_BIT || o.pb[i] < PACK_MIN_BIT) return false;
+    }
+    for (auto &sh : st->sh)
+        if (!sh.buf) return false;
+    if (p.path == PATH_TC) {
+        std::vector<char> tmp = p.params;
+        return tc_set_output(tmp, o);
+    }
+    return apply_supports_out((int)st->dtype, p.d, o);
+}
+
+static hq_status exec_apply(hq_state *st, Shard &s, const Prep &p, const void *dU, const OutSpec *pack = nullptr) {
     CUDA_TRY(cudaSetDevice(s.device));
     ProfEvent pe{};
     hq_status rc = HQ_OK;
     std::vector<char> params;
+    OutSpec o;
+    if (pack) {
+        o = *pack;
+        o.dst[0] = s.buf;
+    }
     if (p.path == PATH_TC) {
         if ((rc = ensure_bound(st))) return rc;
         params = p.params;
         tc_set_amp_bound(params, st->amp_bound);
+        if (pack && !tc_set_output(params, o)) return set_error(HQ_ERR_STATE, "internal: pack not supported");
     }
     if ((rc = prof_begin(st, s, pe))) return rc;
     int launches = 0;
@@ -694,12 +723,16 @@ static hq_status exec_apply(hq_state *st, Shard &s, const Prep &p, const void *d
         e = tc_launch(s.psi, params.data(), params.size(), dU, s.stream);
         launches = 1;
     } else {
-        e = launch_apply((int)st->dtype, s.psi, p.d, p.hostU.data(), dU, s.stream, &launches);
+        e = launch_apply((int)st->dtype, s.psi, p.d, p.hostU.data(), dU, s.stream, &launches, pack ? &o : nullptr);
     }
     if (e != cudaSuccess)
         return set_error(HQ_ERR_CUDA, "apply kernel launch failed: %s", cudaGetErrorString((cudaError_t)e));
     const uint64_t bytes = (uint64_t)2 * (st->es << st->nl);
     if ((rc = prof_end(st, s, pe, bytes, p.path))) return rc;
+    if (pack) {
+        std::swap(s.psi, s.buf);
+        std::swap(s.own_psi, s.own_buf);
+    }
     st->stats.passes++;
     st->stats.kernel_launches += launches;
     st->stats.hbm_bytes += bytes;
@@ -754,8 +787,8 @@ static void prepare_cond(const hq_state *st, const GateRef &g, const Op &op, int
     prepare(st->dtype, V.data(), kl, lb, st->nl, p);
 }
 
-static hq_status exec_prep(hq_state *st, Shard &s, const Prep &p, const void *dU) {
-    if (!p.scalar) return exec_apply(st, s, p, dU);
+static hq_status exec_prep(hq_state *st, Shard &s, const Prep &p, const void *dU, const OutSpec *pack = nullptr) {
+    if (!p.scalar) return exec_apply(st, s, p, dU, pack);
     if (p.sre == 1.0 && p.sim == 0.0) return HQ_OK;
     CUDA_TRY(cudaSetDevice(s.device));
     int e = launch_scale_complex((int)st->dtype, s.psi, 1ull << st->nl, p.sre, p.sim, s.stream);
@@ -902,19 +935,26 @@ static hq_status validate_gates(const hq_state *st, const hq_gate *g, size_t ng,
 // staged through the arena) or precompiled (circuit).
 static hq_status run_ops(hq_state *st, const std::vector<GateRef> &refs, const std::vector<Op> &ops) {
     Prep p;
-    for (const Op &op : ops) {
+    for (size_t i = 0; i < ops.size(); ++i) {
+        const Op &op = ops[i];
         hq_status rc = HQ_OK;
         if (op.kind == OP_APPLY) {
             const GateRef &g = refs[op.gate];
             const bool cond = op_conditioned(st, op);
             if (!cond) prepare(st->dtype, g.U, g.k, op.bits, st->nl, p);
+            OutSpec pk;
+            const bool fold = !cond && i + 1 < ops.size() && pack_spec(st, p, ops[i + 1], pk);
             for (size_t r = 0; r < st->sh.size(); ++r) {
                 Shard &s = st->sh[r];
                 if (cond) prepare_cond(st, g, op, s.rank, p);
                 void *dU = nullptr;
                 if (!p.payload.empty() && (rc = arena_push(st, s, p.payload.data(), p.payload.size(), &dU)))
                     return rc;
-                if ((rc = exec_prep(st, s, p, dU))) return rc;
+                if ((rc = exec_prep(st, s, p, dU, fold ? &pk : nullptr))) return rc;
+            }
+            if (fold) {
+                st->stats.packs++;
+                ++i;                       // the PERMUTE is done
             }
             if (st->amp_bound >= 0) st->amp_bound *= cond ? spectral_bound(g.U, g.k) : p.gnorm;
         } else if (op.kind == OP_REMAP) {
@@ -964,10 +1004,12 @@ static hq_status circuit_compile(hq_state *st, hq_circuit *c, const std::vector<
     c->cprep.assign(c->ops.size(), {});
     c->cuoff.assign(c->ops.size(), {});
     c->cgnorm.assign(c->ops.size(), 1.0);
+    c->pack.assign(c->ops.size(), OutSpec{});
     size_t total = 0;
-    c->passes = c->remaps = c->permutes = 0;
+    c->passes = c->remaps = c->permutes = c->packs = 0;
     for (size_t i = 0; i < c->ops.size(); ++i) {
         const Op &op = c->ops[i];
+        if (op.kind == OP_PERMUTE && i > 0 && c->pack[i - 1].active) continue;    // folded (apply+pack)
         if (op.kind == OP_APPLY) {
             const GateRef &g = refs[op.gate];
             if (op_conditioned(st, op)) {
@@ -990,6 +1032,8 @@ static hq_status circuit_compile(hq_state *st, hq_circuit *c, const std::vector<
                 c->op_uoff[i] = (long long)total;
                 total += (c->prep[i].payload.size() + 255) & ~(size_t)255;
             }
+            if (i + 1 < c->ops.size() && pack_spec(st, c->prep[i], c->ops[i + 1], c->pack[i])) c->packs++;
+            else c->pack[i] = OutSpec{};
             c->passes++;
         } else if (op.kind == OP_REMAP) {
             c->remaps++;
@@ -1081,11 +1125,16 @@ static hq_status circuit_run_ops(hq_state *st, hq_circuit *c) {
         hq_status rc = HQ_OK;
         if (op.kind == OP_APPLY) {
             const bool cond = !c->cprep[i].empty();
+            const OutSpec *pk = c->pack[i].active ? &c->pack[i] : nullptr;
             for (size_t r = 0; r < st->sh.size(); ++r) {
                 const char *base = c->dev_U[st->mode == MODE_VIRTUAL ? 0 : r];
                 const long long off = cond ? c->cuoff[i][r] : c->op_uoff[i];
                 const void *dU = (base && off >= 0) ? base + off : nullptr;
-                if ((rc = exec_prep(st, st->sh[r], cond ? c->cprep[i][r] : c->prep[i], dU))) return rc;
+                if ((rc = exec_prep(st, st->sh[r], cond ? c->cprep[i][r] : c->prep[i], dU, pk))) return rc;
+            }
+            if (pk) {
+                st->stats.packs++;
+                ++i;                       // the folded PERMUTE
             }
             if (st->amp_bound >= 0) st->amp_bound *= cond ? c->cgnorm[i] : c->prep[i].gnorm;
         } else if (op.kind == OP_REMAP) {
@@ -1194,7 +1243,7 @@ extern "C" hq_status hq_circuit_info(const hq_circuit *c, uint64_t *passes, uint
     if (!c) return set_error(HQ_ERR_ARG, "NULL circuit");
     if (passes) *passes = c->passes;
     if (remaps) *remaps = c->remaps;
-    if (permutes) *permutes = c->permutes;
+    if (permutes) *permutes = c->permutes;      // standalone PERMUTE passes (folded ones excluded)
     return HQ_OK;
 }
 

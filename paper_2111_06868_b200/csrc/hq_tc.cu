@@ -286,6 +286,13 @@ struct ParamsB {
     int pair;              // 1: the lowest target is bit 0, patterns (2j, 2j+1) are one 16-byte load / store
     int xpair;             // 1: bit 0 is not a target and is lane bit 0: lane pairs swap one
                            //    output each so that every store is 16 bytes
+    // out-of-place output (apply+pack; om.active): byte offsets of the
+    // permuted pattern / set parts without the selector bits, and those bits
+    OutMap om;
+    uint64_t poff8[64];
+    uint64_t psoff8[128];
+    uint8_t tpat[64];
+    uint8_t tset[128];
 };
 
 // SWIZZLE_128B as seen from a slot index (8-byte amplitudes): byte address
@@ -569,6 +576,19 @@ apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
             wait(tfull(d), (it >> 1) & 1);
             tc_fence_after();
             char *pb = reinterpret_cast<char *>(psi + tile_base<NPOS>(t, P.h)) + soff8;
+            // apply+pack: the output index is om_swap(input index), split into a
+            // buffer selector (tile | set | pattern parts) and an offset
+            uint32_t tsel = 0;
+            uint64_t obase = 0;
+            if (P.om.active) {
+                const uint64_t y = om_swap(tile_base<NPOS>(t, P.h), P.om);
+                tsel = ((uint32_t)(y >> P.om.tsh) & P.om.tmask) | P.tset[n];
+                obase = ((y & ~((uint64_t)P.om.tmask << P.om.tsh)) | P.om.add) * 8 + P.psoff8[n];
+            }
+            auto saddr = [&](int c) -> char * {
+                return P.om.active ? reinterpret_cast<char *>(P.om.dst[tsel | P.tpat[c]]) + obase + P.poff8[c]
+                                   : pb + P.off8[c];
+            };
             const uint32_t Dt = tmem + 2 * KD + d * N + lane_addr;
 #pragma unroll 2
             for (int ch = 0; ch < N / 32; ++ch) {
@@ -590,7 +610,7 @@ apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
                         const float2 o0 = u64_as_f2(mul_f32x2(mul_f32x2(x0, f1), f2));
                         const float2 o1 = u64_as_f2(mul_f32x2(mul_f32x2(x1, f1), f2));
                         if (DIAG && (P.diag & 4)) continue;
-                        st_cs_f4(pb + P.off8[16 * ch + i], o0, o1);
+                        st_cs_f4(saddr(16 * ch + i), o0, o1);
                     }
                     continue;
                 }
@@ -608,7 +628,7 @@ apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
                         const uint64_t y1 = mul_f32x2(mul_f32x2(x1, f1), f2);
                         const uint64_t r = __shfl_xor_sync(0xffffffffu, odd ? y0 : y1, 1);
                         if (DIAG && (P.diag & 4)) continue;
-                        st_cs_f4(pb - (odd ? 8 : 0) + P.off8[16 * ch + i + (odd ? 1 : 0)], u64_as_f2(odd ? r : y0),
+                        st_cs_f4(saddr(16 * ch + i + (odd ? 1 : 0)) - (odd ? 8 : 0), u64_as_f2(odd ? r : y0),
                                  u64_as_f2(odd ? y1 : r));
                     }
                     continue;
@@ -618,7 +638,7 @@ apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
                     const uint64_t x = (uint64_t)v[2 * i] | ((uint64_t)v[2 * i + 1] << 32);
                     const float2 o = u64_as_f2(mul_f32x2(mul_f32x2(x, f1), f2));
                     if (DIAG && (P.diag & 4)) continue; // diagnostics only: no stores
-                    st_cs_f2(pb + P.off8[16 * ch + i], o);
+                    st_cs_f2(saddr(16 * ch + i), o);
                 }
             }
         }
@@ -678,6 +698,13 @@ struct ParamsL {
     int ue;                // A = U * 2^ue (host scaling into the fp16 range)
     int ea;                // B = psi * 2^ea (runtime: from the amplitude bound)
     uint64_t ntiles;
+    // out-of-place output (apply+pack; om.active): amplitude offsets of the
+    // permuted pattern / set parts without the selector bits, and those bits
+    OutMap om;
+    uint64_t poff[64];
+    uint64_t psetoff[64];
+    uint8_t tpat[64];
+    uint8_t tset[64];
 };
 
 __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t addr) {
@@ -886,6 +913,13 @@ apply_tcL(float2 *__restrict__ psi, const __grid_constant__ ParamsL P,
             __syncwarp();
             if (lane == 0) mbar_arrive(tempty_bar(d));
             float2 *pb = psi + tile_base12(t, P) + offr;
+            uint32_t tsel = 0;
+            uint64_t obase = 0;
+            if (P.om.active) {        // apply+pack (see apply_tcb)
+                const uint64_t y = om_swap(tile_base12(t, P), P.om);
+                tsel = ((uint32_t)(y >> P.om.tsh) & P.om.tmask) | P.tpat[r];
+                obase = ((y & ~((uint64_t)P.om.tmask << P.om.tsh)) | P.om.add) + P.poff[r];
+            }
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
                 const uint32_t x0 = j < 16 ? v0[2 * j] : v1[2 * j - 32];
@@ -895,7 +929,11 @@ apply_tcL(float2 *__restrict__ psi, const __grid_constant__ ParamsL P,
                 float2 o;
                 o.x = __uint_as_float(e ? rcv : x0) * sf.x * sf.y;
                 o.y = __uint_as_float(e ? x1 : rcv) * sf.x * sf.y;
-                pb[P.setoff[2 * j + e]] = o;
+                const int sn = 2 * j + e;
+                if (P.om.active)
+                    reinterpret_cast<float2 *>(P.om.dst[tsel | P.tset[sn]])[obase + P.psetoff[sn]] = o;
+                else
+                    pb[P.setoff[sn]] = o;
             }
         }
     }
@@ -1264,6 +1302,60 @@ static int tc_launch_l(void *psi, const tc::ParamsL &P, const void *dev_payload,
     tc::apply_tcL<<<(unsigned)grid, tc::LB_THREADS, tc::LB_SMEM, st>>>(
         reinterpret_cast<float2 *>(psi), P, reinterpret_cast<const uint32_t *>(dev_payload));
     return (int)cudaGetLastError();
+}
+
+// apply+pack: write the pass out of place through the output map o (the
+// tile part is permuted in the kernel, once per tile; the pattern and set
+// parts here).  Bits 0 and 1 must stay in place (16-byte pattern pairs and
+// lane-pair stores, whole 32-byte sectors).
+bool tc_set_output(std::vector<char> &params, const OutSpec &o) {
+    if (params.empty()) return false;
+    OutMap m{};
+    if (o.active) {
+        m.active = 1;
+        m.npairs = o.npairs;
+        for (int i = 0; i < o.npairs; ++i) {
+            if (o.pa[i] < PACK_MIN_BIT || o.pb[i] < PACK_MIN_BIT) return false;
+            m.pa[i] = o.pa[i];
+            m.pb[i] = o.pb[i];
+        }
+        if (o.tmask && o.tsh < PACK_MIN_BIT) return false;
+        m.tsh = o.tmask ? o.tsh : 0;
+        m.tmask = o.tmask;
+        m.add = o.add;
+        for (int t = 0; t < 8; ++t) m.dst[t] = reinterpret_cast<uint64_t>(o.dst[t]);
+    }
+    const uint64_t strip = ~((uint64_t)m.tmask << m.tsh);
+    auto split = [&](uint64_t x, uint64_t &low, uint8_t &sel) {
+        const uint64_t y = om_swap(x, m);
+        sel = (uint8_t)((y >> m.tsh) & m.tmask);
+        low = y & strip;
+    };
+    if (params.back() == 'B') {
+        tc::ParamsB &B = *reinterpret_cast<tc::ParamsB *>(params.data());
+        B.om = m;
+        if (!m.active) return true;
+        for (int c = 0; c < (1 << B.h.k); ++c) {
+            uint64_t lo;
+            split(B.h.off[c], lo, B.tpat[c]);
+            B.poff8[c] = lo * 8;
+        }
+        for (int n = 0; n < tc::M; ++n) {
+            uint64_t lo;
+            split(B.h.setoff[n], lo, B.tset[n]);
+            B.psoff8[n] = lo * 8;
+        }
+        return true;
+    }
+    if (params.back() == 'L') {
+        tc::ParamsL &L = *reinterpret_cast<tc::ParamsL *>(params.data());
+        L.om = m;
+        if (!m.active) return true;
+        for (int c = 0; c < 64; ++c) split(L.off[c], L.poff[c], L.tpat[c]);
+        for (int n = 0; n < 64; ++n) split(L.setoff[n], L.psetoff[n], L.tset[n]);
+        return true;
+    }
+    return false;
 }
 
 // Both modes scale the state into the FP16 range by 2^ea with

@@ -44,7 +44,7 @@ class hq_stats(ctypes.Structure):
     _fields_ = [("passes", ctypes.c_uint64), ("remaps", ctypes.c_uint64),
                 ("permutes", ctypes.c_uint64), ("kernel_launches", ctypes.c_uint64),
                 ("hbm_bytes", ctypes.c_uint64), ("link_bytes", ctypes.c_uint64),
-                ("h2d_bytes", ctypes.c_uint64), ("d2h_bytes", ctypes.c_uint64)]
+                ("h2d_bytes", ctypes.c_uint64), ("d2h_bytes", ctypes.c_uint64), ("packs", ctypes.c_uint64)]
 
 
 _lib = None
@@ -88,6 +88,8 @@ def lib():
             "hq_schedule": [ctypes.c_int, ctypes.c_int, P, ctypes.c_size_t,
                             ctypes.POINTER(ctypes.POINTER(hq_op)), ctypes.POINTER(ctypes.c_size_t), P],
             "hq_free_ops": [P],
+            "hq_schedule_from": [ctypes.c_int, ctypes.c_int, P, ctypes.c_size_t, P,
+                                 ctypes.POINTER(ctypes.POINTER(hq_op)), ctypes.POINTER(ctypes.c_size_t), P],
             "hq_plan_layout": [ctypes.c_int, ctypes.c_int, ctypes.c_int, P, ctypes.c_size_t, P,
                                ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)],
             "hq_state_set_layout": [P, P],
@@ -474,14 +476,15 @@ def hq_fuse_plan(gates, kmax):
     return group_of[:ng].copy(), ngroups.value
 
 
-def hq_schedule(n, m, gates):
-    """Returns (ops list of dict, final pi list)."""
+def hq_schedule(n, m, gates, pi0=None):
+    """Returns (ops list of dict, final pi list); pi0: initial layout (default q -> n-1-q)."""
     arr, ng, keep = _gate_array(gates)
     ops = ctypes.POINTER(hq_op)()
     nops = ctypes.c_size_t()
     pi = np.zeros(max(n, 1), dtype=np.int32)
-    _check(lib().hq_schedule(int(n), int(m), arr, ng, ctypes.byref(ops), ctypes.byref(nops),
-                             pi.ctypes.data))
+    p0 = None if pi0 is None else np.ascontiguousarray(pi0, dtype=np.int32)
+    _check(lib().hq_schedule_from(int(n), int(m), arr, ng, None if p0 is None else p0.ctypes.data,
+                                  ctypes.byref(ops), ctypes.byref(nops), pi.ctypes.data))
     res = []
     try:
         for i in range(nops.value):

@@ -1,0 +1,109 @@
+"""apply+pack (row f1): the scheduler packs the evictees of a
+remap onto the top local bits with a PERMUTE that the executor folds into
+the preceding apply pass (out-of-place, bit-permuted write into the exchange
+buffer).  Checked on virtual shards (the real kernels, scheduler and chunk
+arithmetic on one B200) against the fp64 oracle, for every kernel family that
+can fold (tensor-core modes H and L, SIMT, generic) and through both the
+direct (hq_apply_circuit) and the compiled (hq_circuit_run) executor; the
+reversible circuits are bit-exact (pin P10)."""
+import numpy as np
+import pytest
+
+import oracle as O
+from hq_inputs import Gate, sycamore_circuit, reversible_circuit, integer_state, haar_sweep_gate, random_state
+import paper_2111_06868_b200 as hq
+
+pytestmark = pytest.mark.gpu
+TOL = {"c64": 1e-4, "c128": 1e-10}
+
+
+def _run(n, dtype, G, fused, planned, compiled, psi0=None, x=0):
+    m = G.bit_length() - 1
+    s = hq.hq_state_create_virtual(n, dtype, G)
+    if planned:
+        pi0, _, _ = hq.hq_plan_layout(n, m, fused, dtype)
+        hq.hq_state_set_layout(s, pi0)
+    if psi0 is None:
+        hq.hq_state_init_basis(s, x)
+    else:
+        hq.hq_set_amplitudes(s, psi0)
+    hq.hq_stats_reset(s)
+    if compiled:
+        c = hq.hq_circuit_create(s, fused)
+        hq.hq_circuit_run(s, c)
+    else:
+        hq.hq_apply_circuit(s, fused)
+    return s, hq.hq_stats_get(s)
+
+
+@pytest.mark.parametrize("compiled", [False, True])
+@pytest.mark.parametrize("planned", [False, True])
+@pytest.mark.parametrize("G", [2, 4, 8])
+@pytest.mark.parametrize("kmax", [4, 6])
+def test_pack_sycamore_vs_oracle(kmax, G, planned, compiled):
+    """20 qubits: k<=6 blocks run on the tensor cores (n_local >= 16), k<=4 on
+    the SIMT kernel; every pack is folded (no standalone permute pass)."""
+    n = 20
+    gates = sycamore_circuit(n, 14, 77)
+    fused = hq.hq_fuse(gates, kmax, merged=True)
+    s, st = _run(n, "c64", G, fused, planned, compiled)
+    assert st["remaps"] > 0
+    assert st["packs"] > 0 and st["permutes"] == 0, st
+    err = np.linalg.norm(hq.hq_get_amplitudes(s).astype(np.complex128) - O.simulate(n, gates))
+    assert err <= 1e-4, err
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("n,G,kmax", [(12, 4, 3), (12, 8, 6), (18, 4, 4), (20, 4, 6)])
+def test_pack_every_kernel_family(dtype, n, G, kmax):
+    """Small n (generic kernel), SIMT, complex128 (SIMT; its k = 5, 6 tile
+    kernel cannot fold, so those packs run as standalone permute passes)."""
+    gates = sycamore_circuit(n, 12, 5)
+    fused = hq.hq_fuse(gates, kmax)
+    s, st = _run(n, dtype, G, fused, True, False)
+    assert st["remaps"] > 0
+    assert st["packs"] + st["permutes"] > 0
+    err = np.linalg.norm(hq.hq_get_amplitudes(s).astype(np.complex128) - O.simulate(n, gates))
+    assert err <= TOL[dtype], err
+
+
+@pytest.mark.parametrize("kmax", [3, 6])
+@pytest.mark.parametrize("G", [4, 8])
+def test_pack_reversible_bit_exact(kmax, G):
+    """Permutation gates on an integer-valued state through packs and remaps:
+    every amplitude equal (C11), and a basis state lands exactly on f(x) (P10)."""
+    n = 20
+    gates = reversible_circuit(n, 120, 31, kmax=3)
+    fused = hq.hq_fuse(gates, kmax)
+    psi0 = integer_state(n, 4)
+    s, st = _run(n, "c64", G, fused, True, True, psi0=psi0)
+    assert st["packs"] > 0
+    assert np.array_equal(hq.hq_get_amplitudes(s).astype(np.complex128), O.simulate(n, gates, psi0))
+    x = 0xBEEF5
+    s, st = _run(n, "c64", G, fused, True, False, x=x)
+    y = O.reversible_image(n, gates, x)
+    got = hq.hq_get_amplitudes(s)
+    assert got[y] == 1.0 and np.count_nonzero(got) == 1
+
+
+def test_pack_single_pass_every_tc_mode():
+    """One k = 6 gate at mode-H and mode-L placements, then a segment that
+    needs global qubit 0 and the top local bits 10..17: the remap's evictee
+    lies below the run window, so the k = 6 pass carries the pack
+    (2e-6 single-pass bound)."""
+    from hq_inputs import haar_unitary
+    n, G = 20, 4
+    rng = np.random.default_rng(5)
+    H = np.array([[1, 1], [1, -1]]) / np.sqrt(2)
+    tail = [Gate("H0", (0,), H),
+            Gate("U6", tuple(n - 1 - b for b in range(11, 17)), haar_unitary(6, rng)),
+            Gate("U2", (n - 1 - 17, n - 1 - 10), haar_unitary(2, rng))]
+    for placement in ("low", "b:0-3-7-9-14-15", "b:1-2-3-7-8-9", "b:0-2-5-9-12-15"):
+        g = haar_sweep_gate(n, 6, placement, 2301)
+        gates = [g] + tail
+        psi0 = random_state(n, 12)
+        s, st = _run(n, "c64", G, [(tuple(x.qubits), x.U) for x in gates], False, False, psi0=psi0)
+        assert st["remaps"] == 1 and st["packs"] == 1 and st["permutes"] == 0, (placement, st)
+        want = O.simulate(n, gates, psi0)
+        err = np.linalg.norm(hq.hq_get_amplitudes(s).astype(np.complex128) - want)
+        assert err < 4e-6, (placement, err)
