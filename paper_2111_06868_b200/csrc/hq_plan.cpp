@@ -350,10 +350,17 @@ void schedule(int n, int m, const std::vector<GateRef> &g, std::vector<int> &pi,
         if (m > 0 && (need[i] & globals())) {
             // the segment starting at gate i; it also ends early when the
             // incoming globals would outnumber the local qubits outside it
-            // that a folded pack can move (bits >= PACK_MIN_BIT)
+            // that can be evicted without a standalone pass: those a folded
+            // pack can move (bits >= PACK_MIN_BIT) after an apply; with no
+            // apply right before (circuit start, back-to-back remaps) nothing
+            // can absorb a pack, so those in the top RUNWIN bits (the exchange
+            // then sends a few long runs)
+            bool after_apply = !ops.empty() && ops.back().kind == OP_APPLY;
+            if (after_apply)        // an apply on a global target (row f1) runs per rank: no fold
+                for (int jj = 0; jj < ops.back().nbits; ++jj) after_apply &= ops.back().bits[jj] < nl;
             const uint64_t Gm = globals();
             uint64_t Lp = 0;
-            for (int p = std::min(PACK_MIN_BIT, nl); p < nl; ++p) Lp |= 1ull << inv[p];
+            for (int p = after_apply ? std::min(PACK_MIN_BIT, nl) : nl - RUNWIN; p < nl; ++p) Lp |= 1ull << inv[p];
             uint64_t U = 0;
             size_t j = i;
             while (j < N) {
@@ -370,10 +377,13 @@ void schedule(int n, int m, const std::vector<GateRef> &g, std::vector<int> &pi,
             // outgoing: local qubits outside the segment's union, furthest next use
             // after the segment first, bits >= PACK_MIN_BIT before bits below it
             std::vector<std::tuple<int, size_t, int>> cand;   // (packable, next use, phys bit)
-            for (int p = 0; p < nl; ++p) {
-                const int q = inv[p];
-                if ((U >> q) & 1) continue;
-                cand.push_back({p >= PACK_MIN_BIT ? 1 : 0, next_use(q, j), p});
+            for (int pass = after_apply ? 1 : 0; pass < 2 && (int)cand.size() < nin; ++pass) {
+                cand.clear();
+                for (int p = pass == 0 ? nl - RUNWIN : 0; p < nl; ++p) {
+                    const int q = inv[p];
+                    if ((U >> q) & 1) continue;
+                    cand.push_back({p >= PACK_MIN_BIT ? 1 : 0, next_use(q, j), p});
+                }
             }
             std::sort(cand.begin(), cand.end(), [](const auto &a, const auto &b) {
                 if (std::get<0>(a) != std::get<0>(b)) return std::get<0>(a) > std::get<0>(b);

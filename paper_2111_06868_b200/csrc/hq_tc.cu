@@ -33,6 +33,7 @@
 // pairs hand every ring slot, A buffer and accumulator between the roles.
 #include <cuda.h>
 #include <cuda_fp16.h>
+#include <cstdio>
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <algorithm>
@@ -87,6 +88,7 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 // In apply_tcb the converters wait ~40% of the time for bulk copies; spinning
 // cost ~16% of all issued instructions (ncu source view) and power under the
 // 1 kW cap.
+#ifndef HQ_DEVICE_CHECKS
 __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
@@ -106,6 +108,61 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+#else
+// Checked build (-DHQ_DEVICE_CHECKS, lib/libhq_check.so): every mbarrier wait
+// carries a watchdog.  A phase that does not complete within ~2^33 cycles
+// (several seconds) is a synchronisation bug (a missing arrive, a wrong
+// parity, an expect-tx byte count that never lands): report and trap instead
+// of hanging the GPU.  (compute-sanitizer is not available on the GPU pool.)
+__device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __noinline__ void mbar_watchdog(uint32_t bar, uint32_t parity) {
+    printf("hq device check: mbarrier wait timeout (block %d thread %d smem 0x%x parity %u)\n", blockIdx.x,
+           threadIdx.x, bar, parity);
+    __trap();
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    const long long t0 = clock64();
+    while (!mbar_try(bar, parity))
+        if (clock64() - t0 > (1ll << 33)) mbar_watchdog(bar, parity);
+}
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) { mbar_wait(bar, parity); }
+#endif
+
+// Checked build: every global store / bulk-copy source of the tensor-core
+// kernels must lie inside one of the buffers the pass may touch.
+#ifdef HQ_DEVICE_CHECKS
+__device__ __noinline__ void hq_range_fail(const void *p, uint32_t need, int where) {
+    printf("hq device check %d: %u-byte access at %p outside the pass's buffers (block %d thread %d)\n", where, need,
+           p, blockIdx.x, threadIdx.x);
+    __trap();
+}
+__device__ __forceinline__ bool in_buf(const void *p, uint32_t need, uint64_t base, uint64_t bytes) {
+    const uint64_t a = reinterpret_cast<uint64_t>(p);
+    return base && a >= base && a + need <= base + bytes;
+}
+#define HQ_CHECK_IN(p, need, base, bytes, where) \
+    do { if (!in_buf((p), (need), (uint64_t)(base), (bytes))) hq_range_fail((p), (need), (where)); } while (0)
+#define HQ_CHECK_OUT(p, need, psi, om, bytes, where)                                                     \
+    do {                                                                                                  \
+        bool ok_ = false;                                                                                 \
+        if (!(om).active) ok_ = in_buf((p), (need), (uint64_t)(psi), (bytes));                            \
+        else for (int i_ = 0; i_ < 8; ++i_) ok_ |= in_buf((p), (need), (om).dst[i_], (bytes));            \
+        if (!ok_) hq_range_fail((p), (need), (where));                                                    \
+    } while (0)
+#else
+#define HQ_CHECK_IN(p, need, base, bytes, where) ((void)0)
+#define HQ_CHECK_OUT(p, need, psi, om, bytes, where) ((void)0)
+#endif
 
 __device__ __forceinline__ void tc_fence_before() {
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -239,6 +296,23 @@ __device__ __forceinline__ uint64_t tile_base(uint64_t t, const Params &P) {
     return t;
 }
 
+// Tile bases of a persistent CTA's tiles t, t + G, t + 2G, ...: the base is
+// the tile index deposited into the non-tile bits, so stepping it by G is an
+// addition in that masked space (carries ripple through the tile bits, which
+// are forced to 1): base' = ((base | tilemask) + dep(G)) & ~tilemask.
+struct TileWalk {
+    uint64_t base, step, tmask;
+    __device__ __forceinline__ void next() { base = ((base | tmask) + step) & ~tmask; }
+};
+
+template <int NPOS>
+__device__ __forceinline__ TileWalk tile_walk(const Params &P) {
+    uint64_t tm = 0;
+#pragma unroll
+    for (int i = 0; i < NPOS; ++i) tm |= 1ull << P.pos[i];
+    return TileWalk{tile_base<NPOS>(blockIdx.x, P), tile_base<NPOS>(gridDim.x, P), tm};
+}
+
 // ------------------------------------------------------------------ mode H
 // A tile (128 gather sets) spans 13 (K = 6) "tile bits": the targets and
 // the 7 lowest non-target bits, so physical bits 0..6 are always tile bits and
@@ -317,6 +391,9 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t
                  : "memory");
 }
 
+__device__ __forceinline__ void st_cs_f1(void *p, float v) {       // streaming store (evict-first)
+    asm volatile("st.global.cs.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
 __device__ __forceinline__ void st_cs_f2(void *p, float2 v) {     // streaming store (evict-first)
     asm volatile("st.global.cs.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v.x), "f"(v.y) : "memory");
 }
@@ -418,8 +495,9 @@ apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
         constexpr int NB = C::NBLK / NPH;
         const int sub = NP == 1 ? 0 : p / 2;
         uint32_t it = 0;
-        for (uint64_t t = blockIdx.x; t < ntiles; t += G, ++it) {
-            const uint64_t tbo = tile_base<NPOS>(t, P.h);
+        TileWalk tw = tile_walk<NPOS>(P.h);
+        for (uint64_t t = blockIdx.x; t < ntiles; t += G, ++it, tw.next()) {
+            const uint64_t tbo = tw.base;
             const float2 *tb = psi + tbo;
 #pragma unroll 1
             for (int h = NP == 1 ? 0 : p % 2; h < (NP == 1 ? 2 : p % 2 + 1); ++h) {
@@ -431,10 +509,14 @@ apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
                 if (lane < NB) {
                     const int j = sub * NB + lane;
                     if (P.swz)   // row = 16 amplitudes; a 1 KB block is 8 rows, swizzled on arrival
+                        HQ_CHECK_IN(tb + P.boff[h][j], 1024, psi, P.h.ntiles << (K + SETBITS + 3), 1);
                         tma_g2s_2d(sbase + C::RING + s * C::SLOT_BYTES + j * 1024, &tmap, 0,
                                    (int)((tbo + P.boff[h][j]) >> 4), rfull(s));
                     else
+                    {
+                        HQ_CHECK_IN(tb + P.boff[h][j], 1024, psi, P.h.ntiles << (K + SETBITS + 3), 1);
                         bulk_g2s(sbase + C::RING + s * C::SLOT_BYTES + j * 1024, tb + P.boff[h][j], 1024, rfull(s));
+                    }
                 }
             }
         }
@@ -571,17 +653,18 @@ apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
         const float2 sf = pow2_factors(-(max(-126, min(127, P.h.ea)) + P.h.ue));
         const uint64_t f1 = f2_as_u64(make_float2(sf.x, sf.x)), f2 = f2_as_u64(make_float2(sf.y, sf.y));
         uint32_t it = 0;
-        for (uint64_t t = blockIdx.x; t < ntiles; t += G, ++it) {
+        TileWalk tw = tile_walk<NPOS>(P.h);
+        for (uint64_t t = blockIdx.x; t < ntiles; t += G, ++it, tw.next()) {
             const int d = it & 1;
             wait(tfull(d), (it >> 1) & 1);
             tc_fence_after();
-            char *pb = reinterpret_cast<char *>(psi + tile_base<NPOS>(t, P.h)) + soff8;
+            char *pb = reinterpret_cast<char *>(psi + tw.base) + soff8;
             // apply+pack: the output index is om_swap(input index), split into a
             // buffer selector (tile | set | pattern parts) and an offset
             uint32_t tsel = 0;
             uint64_t obase = 0;
             if (P.om.active) {
-                const uint64_t y = om_swap(tile_base<NPOS>(t, P.h), P.om);
+                const uint64_t y = om_swap(tw.base, P.om);
                 tsel = ((uint32_t)(y >> P.om.tsh) & P.om.tmask) | P.tset[n];
                 obase = ((y & ~((uint64_t)P.om.tmask << P.om.tsh)) | P.om.add) * 8 + P.psoff8[n];
             }
@@ -610,6 +693,7 @@ apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
                         const float2 o0 = u64_as_f2(mul_f32x2(mul_f32x2(x0, f1), f2));
                         const float2 o1 = u64_as_f2(mul_f32x2(mul_f32x2(x1, f1), f2));
                         if (DIAG && (P.diag & 4)) continue;
+                        HQ_CHECK_OUT(saddr(16 * ch + i), 16, psi, P.om, P.h.ntiles << (K + SETBITS + 3), 2);
                         st_cs_f4(saddr(16 * ch + i), o0, o1);
                     }
                     continue;
@@ -628,6 +712,8 @@ apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
                         const uint64_t y1 = mul_f32x2(mul_f32x2(x1, f1), f2);
                         const uint64_t r = __shfl_xor_sync(0xffffffffu, odd ? y0 : y1, 1);
                         if (DIAG && (P.diag & 4)) continue;
+                        HQ_CHECK_OUT(saddr(16 * ch + i + (odd ? 1 : 0)) - (odd ? 8 : 0), 16, psi, P.om,
+                                     P.h.ntiles << (K + SETBITS + 3), 3);
                         st_cs_f4(saddr(16 * ch + i + (odd ? 1 : 0)) - (odd ? 8 : 0), u64_as_f2(odd ? r : y0),
                                  u64_as_f2(odd ? y1 : r));
                     }
@@ -638,6 +724,7 @@ apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
                     const uint64_t x = (uint64_t)v[2 * i] | ((uint64_t)v[2 * i + 1] << 32);
                     const float2 o = u64_as_f2(mul_f32x2(mul_f32x2(x, f1), f2));
                     if (DIAG && (P.diag & 4)) continue; // diagnostics only: no stores
+                    HQ_CHECK_OUT(saddr(16 * ch + i), 8, psi, P.om, P.h.ntiles << (K + SETBITS + 3), 4);
                     st_cs_f2(saddr(16 * ch + i), o);
                 }
             }
@@ -671,7 +758,11 @@ apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
 // k = 5 gates are widened to 6 targets on the host (U (x) I, exact): by the
 // tcgen05 pacing law (B300_MICROARCH.md, floor = max(M,128) N / 256 cycles per
 // MMA) a native M = 64 k = 5 pass costs the same tensor cycles per amplitude.
-//   warps 0-3 epilogue, 4 MMA, 5-12 converters, 13 producer.
+//   warps 0-7 epilogue (two per TMEM lane quarter, one per half of the 64
+//   columns), 8 MMA, 9-16 converters, 17 producer.  The epilogue was the
+//   bottleneck with four warps and re/im shuffles (ncu source view: the MMA
+//   warp waited on the accumulator, the converters on the MMA): now each lane
+//   stores its own real component, one 4-byte store per set.
 // TMEM columns: A hi [0,64), A lo [64,128) (packed f16x2, column c = input
 // amplitude c), accumulator d: [128 + 64 d, 192 + 64 d).
 
@@ -682,7 +773,12 @@ constexpr int L_HALF = 2 * L_ATOMCOL;             // 16 KB: hi (or lo) of one st
 constexpr int L_STAGE = 2 * L_HALF;
 constexpr int L_RAW = NUM_CONV * 32 * 16 * 8;     // one tile of raw amplitudes (32 KB)
 constexpr int L_NR = 3;                           // raw ring slots
-constexpr int LB_PROD = NUM_EPI + 1 + NUM_CONV;   // warp 13
+// warps 0-7 epilogue (warp w: TMEM lane quarter w % 4, columns [32 (w / 4), +32)),
+// 8 MMA, 9-16 converters, 17 producer
+constexpr int L_EPI = 8;
+constexpr int L_MMA = L_EPI;
+constexpr int L_CONV0 = L_EPI + 1;
+constexpr int LB_PROD = L_CONV0 + NUM_CONV;
 constexpr int LB_THREADS = (LB_PROD + 1) * 32;
 constexpr int L_BARS = L_STAGES * L_STAGE + L_NR * L_RAW;
 constexpr int LB_SMEM = L_BARS + BAR_BYTES;
@@ -727,6 +823,7 @@ __device__ __forceinline__ uint64_t tile_base12(uint64_t t, const ParamsL &P) {
     return t;
 }
 
+
 __global__ void __launch_bounds__(LB_THREADS, 1)
 apply_tcL(float2 *__restrict__ psi, const __grid_constant__ ParamsL P,
           const uint32_t *__restrict__ Apack /* [2][128][64] half2: hi then lo, row = output real */) {
@@ -752,7 +849,7 @@ apply_tcL(float2 *__restrict__ psi, const __grid_constant__ ParamsL P,
         }
         for (int d = 0; d < 2; ++d) {
             mbar_init(tfull_bar(d), 1);
-            mbar_init(tempty_bar(d), NUM_EPI);
+            mbar_init(tempty_bar(d), L_EPI);
         }
         for (int r = 0; r < L_NR; ++r) {
             mbar_init(rfull(r), 1);
@@ -760,7 +857,7 @@ apply_tcL(float2 *__restrict__ psi, const __grid_constant__ ParamsL P,
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == MMA_WARP) {
+    if (warp == L_MMA) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(tmem_slot)),
                      "r"(L_TMEM_COLS));
@@ -771,7 +868,7 @@ apply_tcL(float2 *__restrict__ psi, const __grid_constant__ ParamsL P,
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     // A (U hi, lo as packed half2) into TMEM: warp q writes lanes 32q..32q+31
-    if (warp < NUM_EPI) {
+    if (warp < 4) {
         const int m = warp * 32 + lane;
 #pragma unroll 1
         for (int ch = 0; ch < 4; ++ch) {
@@ -789,18 +886,22 @@ apply_tcL(float2 *__restrict__ psi, const __grid_constant__ ParamsL P,
     const uint32_t A_HI = tmem, A_LO = tmem + 64;
     const uint64_t ntiles = P.ntiles;
     const uint64_t G = gridDim.x;
+    uint64_t tmask = 0;
+#pragma unroll
+    for (int i = 0; i < 12; ++i) tmask |= 1ull << P.pos[i];
+    TileWalk tw{tile_base12(blockIdx.x, P), tile_base12(G, P), tmask};
 
     if (warp == LB_PROD) {
         uint32_t it = 0;
-        for (uint64_t t = blockIdx.x; t < ntiles; t += G, ++it) {
+        for (uint64_t t = blockIdx.x; t < ntiles; t += G, ++it, tw.next()) {
             const int r = it % L_NR;
             wait(rempty(r), ((it / L_NR) & 1) ^ 1);
             if (lane == 0) mbar_arrive_tx(rfull(r), L_RAW);
             __syncwarp();
-            const float2 *tb = psi + tile_base12(t, P);
-            bulk_g2s(raw0 + r * L_RAW + lane * 1024, tb + P.boff[lane], 1024, rfull(r));
+            HQ_CHECK_IN(psi + tw.base + P.boff[lane], 1024, psi, P.ntiles << 15, 5);
+            bulk_g2s(raw0 + r * L_RAW + lane * 1024, psi + tw.base + P.boff[lane], 1024, rfull(r));
         }
-    } else if (warp == MMA_WARP) {
+    } else if (warp == L_MMA) {
         // idesc: F32 accumulate, A/B F16, both K-major, N = 64 sets, M = 128 output reals
         const uint32_t idesc = (1u << 4) | ((uint32_t)(L_NS >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
         uint32_t it = 0;
@@ -833,9 +934,9 @@ apply_tcL(float2 *__restrict__ psi, const __grid_constant__ ParamsL P,
             }
             __syncwarp();
         }
-    } else if (warp >= CONV0) {
+    } else if (warp >= L_CONV0) {
         // thread -> tile-local amplitude index tl = lane | (cw << 5) | (i << 8), i = 0..15
-        const int cw = warp - CONV0;
+        const int cw = warp - L_CONV0;
         uint32_t n_base = 0, c_base = 0;
 #pragma unroll
         for (int b = 0; b < 8; ++b) {
@@ -893,54 +994,68 @@ apply_tcL(float2 *__restrict__ psi, const __grid_constant__ ParamsL P,
             if (lane == 0) mbar_arrive(full_bar(s));
         }
     } else {
-        // epilogue warps 0..3: TMEM lanes 32q.. = output reals m = 2r + e
-        const int m = warp * 32 + lane;
+        // epilogue warp w (0..7): TMEM lanes 32 (w % 4).. = output reals m = 2r + e,
+        // columns (sets) [32 (w / 4), +32).  Each lane stores its own component
+        // of output r for every set: a warp's 32 lanes write re, im of 16
+        // patterns, one 4-byte store per set (a full 128-byte line when the
+        // lowest targets are bits 0..3), no re/im shuffles.
+        const int q = warp & 3, hc = warp >> 2;
+        const int m = q * 32 + lane;
         const int r = m >> 1, e = m & 1;
-        const uint64_t offr = P.off[r];
-        const float2 sf = pow2_factors(-(max(-126, min(127, P.ea)) + P.ue));
+        const uint64_t rb = 2 * P.off[r] + e;                  // float offset of (r, e) in a set
+        // set offsets are GF(2)-linear in the set index (disjoint bits), so
+        // setoff[32 hc + j] = setoff[32 hc] + setoff[j], j a compile-time index
+        const uint64_t rbh = rb + 2 * (uint64_t)P.setoff[32 * hc];
+        // 2^-(ea + ue) as one factor when it is a normal float, else two
+        const int se = -(max(-126, min(127, P.ea)) + P.ue);
+        const float2 sf = pow2_factors(se);
+        const bool one = se >= -126 && se <= 127;
+        const float s1 = one ? __int_as_float((127 + se) << 23) : 1.0f;
+        float *const psif = reinterpret_cast<float *>(psi);
         uint32_t it = 0;
-        for (uint64_t t = blockIdx.x; t < ntiles; t += G, ++it) {
+        for (uint64_t t = blockIdx.x; t < ntiles; t += G, ++it, tw.next()) {
             const int d = it & 1;
             const uint32_t dp = (it >> 1) & 1;
             wait(tfull_bar(d), dp);
             tc_fence_after();
-            uint32_t v0[32], v1[32];
-            const uint32_t D = tmem + 128 + L_NS * d + ((uint32_t)(warp * 32) << 16);
-            tmem_ld32(D, v0);
-            tmem_ld32(D + 32, v1);
+            uint32_t v[32];
+            tmem_ld32(tmem + 128 + L_NS * d + 32 * hc + ((uint32_t)(q * 32) << 16), v);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(tempty_bar(d));
-            float2 *pb = psi + tile_base12(t, P) + offr;
-            uint32_t tsel = 0;
-            uint64_t obase = 0;
-            if (P.om.active) {        // apply+pack (see apply_tcb)
-                const uint64_t y = om_swap(tile_base12(t, P), P.om);
-                tsel = ((uint32_t)(y >> P.om.tsh) & P.om.tmask) | P.tpat[r];
-                obase = ((y & ~((uint64_t)P.om.tmask << P.om.tsh)) | P.om.add) + P.poff[r];
-            }
+            if (one) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                const uint32_t x0 = j < 16 ? v0[2 * j] : v1[2 * j - 32];
-                const uint32_t x1 = j < 16 ? v0[2 * j + 1] : v1[2 * j + 1 - 32];
-                const uint32_t snd = e ? x0 : x1;
-                const uint32_t rcv = __shfl_xor_sync(0xffffffffu, snd, 1);
-                float2 o;
-                o.x = __uint_as_float(e ? rcv : x0) * sf.x * sf.y;
-                o.y = __uint_as_float(e ? x1 : rcv) * sf.x * sf.y;
-                const int sn = 2 * j + e;
-                if (P.om.active)
-                    reinterpret_cast<float2 *>(P.om.dst[tsel | P.tset[sn]])[obase + P.psetoff[sn]] = o;
-                else
-                    pb[P.setoff[sn]] = o;
+                for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) * s1);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) * sf.x * sf.y);
+            }
+            if (!P.om.active) {
+                float *pb = psif + 2 * tw.base + rbh;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    HQ_CHECK_IN(pb + 2 * P.setoff[j], 4, psi, P.ntiles << 15, 6);
+                    st_cs_f1(pb + 2 * P.setoff[j], __uint_as_float(v[j]));
+                }
+            } else {                  // apply+pack (see apply_tcb)
+                const uint64_t y = om_swap(tw.base, P.om);
+                const uint32_t tsel = ((uint32_t)(y >> P.om.tsh) & P.om.tmask) | P.tpat[r];
+                const uint64_t ob = ((y & ~((uint64_t)P.om.tmask << P.om.tsh)) | P.om.add) + P.poff[r];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const int sn = 32 * hc + j;
+                    float *dst = reinterpret_cast<float *>(P.om.dst[tsel | P.tset[sn]]);
+                    HQ_CHECK_OUT(dst + 2 * (ob + P.psetoff[sn]) + e, 4, psi, P.om, P.ntiles << 15, 7);
+                    dst[2 * (ob + P.psetoff[sn]) + e] = __uint_as_float(v[j]);
+                }
             }
         }
     }
 
     tc_fence_before();
     __syncthreads();
-    if (warp == MMA_WARP) {
+    if (warp == L_MMA) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(L_TMEM_COLS));
     }

@@ -222,6 +222,9 @@ def test_schedule_remap_counts(n, cycles, seed, kmax, merged):
         lb = _segments_lower_bound(n, m, fused)
         ops, _ = hq.hq_schedule(n, m, gates)
         R0 = sum(o["kind"] == "remap" for o in ops)
+        for i, o in enumerate(ops):
+            if o["kind"] == "permute":
+                assert i > 0 and ops[i - 1]["kind"] == "apply"
         pi0, _, _ = hq.hq_plan_layout(n, m, fused)
         assert sorted(pi0) == list(range(n))
         ops, _ = hq.hq_schedule(n, m, gates, pi0)
@@ -234,6 +237,8 @@ def test_schedule_remap_counts(n, cycles, seed, kmax, merged):
             if o["kind"] == "permute":
                 assert i > 0 and ops[i - 1]["kind"] == "apply"
                 assert all(b >= 2 for b in o["bits"][:2 * o["nbits"]])
+                g = fused[ops[i - 1]["gate"]]
+                assert all(b < n - m for b in ops[i - 1]["bits"][:len(g[0])])
         if n == 34 and kmax == 5 and m == 3:
             assert R <= 11 and R0 <= 12 and R / len(fused) <= 0.106
 
