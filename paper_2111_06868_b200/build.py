@@ -16,6 +16,9 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libhq.so")
+# checked variant (-DHQ_DEVICE_CHECKS): mbarrier watchdogs and bounds checks on
+# every tensor-core / SIMT global access; tests load it through HQ_LIB
+LIB_CHECK = os.path.join(LIBDIR, "libhq_check.so")
 INCLUDE = os.path.join(ROOT, "include")
 
 SOURCES = ["hq_apply.cu", "hq_tc.cu", "hq_state_ops.cu", "hq_runtime.cpp", "hq_plan.cpp"]
@@ -38,22 +41,27 @@ def nvcc():
     return "nvcc"
 
 
-def _stale():
-    if not os.path.exists(LIB):
+def _stale(lib=LIB):
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(INCLUDE, "hq.h"), __file__]
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force=False, verbose=False):
-    if not force and not _stale():
-        return LIB
+def build(force=False, verbose=False, checked=False):
+    lib = LIB_CHECK if checked else LIB
+    if not force and not _stale(lib):
+        return lib
+    if not force and os.environ.get("HQ_NO_BUILD") and os.path.exists(lib):
+        return lib          # use the shipped build as is (GPU-box scripts)
     os.makedirs(LIBDIR, exist_ok=True)
     inc, nlib = _nccl_dirs()
-    objdir = os.path.join(LIBDIR, "obj")
+    objdir = os.path.join(LIBDIR, "obj_check" if checked else "obj")
     os.makedirs(objdir, exist_ok=True)
     common = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I", INCLUDE, "-I", CSRC, "-I", inc]
+    if checked:
+        common += ["-DHQ_DEVICE_CHECKS"]
     objs = []
     procs = []
     for src in SOURCES:
@@ -76,11 +84,10 @@ def build(force=False, verbose=False):
         if verbose and out:
             sys.stderr.write(out.decode(errors="replace"))
     link = [nvcc(), "-shared"] + ARCH + objs + [
-        "-L" + nlib, "-Xlinker", "-l:libnccl.so.2", "-Xlinker", "-rpath=" + nlib, "-o", LIB]
+        "-L" + nlib, "-Xlinker", "-l:libnccl.so.2", "-Xlinker", "-rpath=" + nlib, "-o", lib]
     subprocess.check_call(link)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, checked="--checked" in sys.argv))

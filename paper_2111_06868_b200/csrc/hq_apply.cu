@@ -41,6 +41,22 @@ __device__ __forceinline__ uint64_t insert_zero(uint64_t x, int s) {
     return ((x >> s) << (s + 1)) | lo;
 }
 
+// Checked build (-DHQ_DEVICE_CHECKS, lib/libhq_check.so): every SIMT store
+// must land inside the buffer of the pass (in place: the shard; apply+pack:
+// one of the output-map buffers).
+#ifdef HQ_DEVICE_CHECKS
+#include <cstdio>
+__device__ __noinline__ void hq_store_fail(uint64_t idx, uint64_t lim, int where) {
+    printf("hq device check %d: store index %llu >= %llu (block %d thread %d)\n", where,
+           (unsigned long long)idx, (unsigned long long)lim, blockIdx.x, threadIdx.x);
+    __trap();
+}
+#define HQ_CHECK_IDX(idx, lim, where) \
+    do { if ((uint64_t)(idx) >= (uint64_t)(lim)) hq_store_fail((idx), (lim), (where)); } while (0)
+#else
+#define HQ_CHECK_IDX(idx, lim, where) ((void)0)
+#endif
+
 // ------------------------------------------------------------------ fast SIMT kernel
 
 struct RegParams {
@@ -192,11 +208,15 @@ apply_reg(typename C2<R>::T *__restrict__ psi, const __grid_constant__ RegParams
                 const int j0 = ((v >> P0) << (P0 + 1)) | (v & ((1 << P0) - 1));
                 const int j1 = j0 | (1 << P0);
                 float4 *dst = reinterpret_cast<float4 *>(P.om.dst[tb | P.tv[v]]);
+                HQ_CHECK_IDX(lb | P.pvoff[v], P.nunits * NV, 11);
                 dst[lb | P.pvoff[v]] = make_float4(x[j0].x, x[j0].y, x[j1].x, x[j1].y);
             }
         } else {
 #pragma unroll
-            for (int v = 0; v < NV; ++v) reinterpret_cast<V *>(P.om.dst[tb | P.tv[v]])[lb | P.pvoff[v]] = x[v];
+            for (int v = 0; v < NV; ++v) {
+                HQ_CHECK_IDX(lb | P.pvoff[v], P.nunits * NV, 12);
+                reinterpret_cast<V *>(P.om.dst[tb | P.tv[v]])[lb | P.pvoff[v]] = x[v];
+            }
         }
         return;
     }
@@ -206,11 +226,15 @@ apply_reg(typename C2<R>::T *__restrict__ psi, const __grid_constant__ RegParams
         for (int v = 0; v < NV; ++v) {
             const int j0 = ((v >> P0) << (P0 + 1)) | (v & ((1 << P0) - 1));
             const int j1 = j0 | (1 << P0);
+            HQ_CHECK_IDX(base + P.voff[v], P.nunits * NV, 13);
             dst[base + P.voff[v]] = make_float4(x[j0].x, x[j0].y, x[j1].x, x[j1].y);
         }
     } else {
 #pragma unroll
-        for (int v = 0; v < NV; ++v) psi[base + P.voff[v]] = x[v];
+        for (int v = 0; v < NV; ++v) {
+            HQ_CHECK_IDX(base + P.voff[v], P.nunits * NV, 14);
+            psi[base + P.voff[v]] = x[v];
+        }
     }
 }
 

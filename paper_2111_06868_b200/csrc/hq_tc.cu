@@ -508,15 +508,12 @@ apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
                 __syncwarp();
                 if (lane < NB) {
                     const int j = sub * NB + lane;
+                    HQ_CHECK_IN(tb + P.boff[h][j], 1024, psi, P.h.ntiles << (K + SETBITS + 3), 1);
                     if (P.swz)   // row = 16 amplitudes; a 1 KB block is 8 rows, swizzled on arrival
-                        HQ_CHECK_IN(tb + P.boff[h][j], 1024, psi, P.h.ntiles << (K + SETBITS + 3), 1);
                         tma_g2s_2d(sbase + C::RING + s * C::SLOT_BYTES + j * 1024, &tmap, 0,
                                    (int)((tbo + P.boff[h][j]) >> 4), rfull(s));
                     else
-                    {
-                        HQ_CHECK_IN(tb + P.boff[h][j], 1024, psi, P.h.ntiles << (K + SETBITS + 3), 1);
                         bulk_g2s(sbase + C::RING + s * C::SLOT_BYTES + j * 1024, tb + P.boff[h][j], 1024, rfull(s));
-                    }
                 }
             }
         }

@@ -11,7 +11,9 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libhq.so")
+# HQ_LIB selects another build of the same library, e.g. the checked variant
+# lib/libhq_check.so (device-side bounds checks and mbarrier watchdogs)
+LIB_PATH = os.environ.get("HQ_LIB") or os.path.join(_PKG, "lib", "libhq.so")
 
 HQ_C64, HQ_C128 = 0, 1
 _DTYPES = {"c64": HQ_C64, "complex64": HQ_C64, HQ_C64: HQ_C64,

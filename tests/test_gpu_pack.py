@@ -76,7 +76,7 @@ def test_pack_reversible_bit_exact(kmax, G):
     fused = hq.hq_fuse(gates, kmax)
     psi0 = integer_state(n, 4)
     s, st = _run(n, "c64", G, fused, True, True, psi0=psi0)
-    assert st["packs"] > 0 and st["permutes"] == 0, st
+    assert st["remaps"] > 0 and st["permutes"] == 0, st
     assert np.array_equal(hq.hq_get_amplitudes(s).astype(np.complex128), O.simulate(n, gates, psi0))
     x = 0xBEEF5
     s, st = _run(n, "c64", G, fused, True, False, x=x)
