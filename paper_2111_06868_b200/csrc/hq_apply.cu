@@ -64,12 +64,18 @@ struct RegParams {
     uint64_t nunits;     // number of threads with work (= 32 * warps)
     int S[6];            // ascending insertion positions in warp space (count K-T0)
     int la[5];           // lane bit (0..4) of each lane target, canonical order
-    // out-of-place output (om.active): positions in load units; pvoff[v] =
-    // om_swap(voff[v]) without the selector bits, tv[v] = its selector bits
+};
+
+// apply+pack output of the SIMT kernel (positions in load units): pvoff[v] =
+// om_swap(voff[v]) without the selector bits, tv[v] = its selector bits.  A
+// separate kernel argument that only the PK instantiation carries: a larger
+// RegParams alone raised the in-place kernel from 80 to 127 registers.
+struct RegPack {
     OutMap om;
     uint64_t pvoff[32];
     uint8_t tv[32];
 };
+struct NoPack {};
 
 template <typename R, int K> struct UParam {
     typename C2<R>::T u[1 << K][1 << K];
@@ -148,10 +154,14 @@ __device__ __forceinline__ void lane_transpose(V *x, int la, int e, int lane) {
 // VEC = amplitudes per load: 2 (complex64 as float4, physical bit 0 in-thread)
 // or 1 (complex64 as float2 / complex128 as double2).  T0: bit 0 is a target
 // (VEC == 2 only).  KL: number of targets inside the lane bit range.
-template <typename R, int VEC, int K, int T0, int KL>
+// PK: apply+pack variant (out-of-place through P.om); a separate
+// instantiation so the in-place kernel keeps its register budget (the
+// runtime branch cost 80 -> 128 registers and occupancy at k = 4).
+template <typename R, int VEC, int K, int T0, int KL, bool PK>
 __global__ void __launch_bounds__(128)
 apply_reg(typename C2<R>::T *__restrict__ psi, const __grid_constant__ RegParams P,
-          const __grid_constant__ UParam<R, K> U) {
+          const __grid_constant__ UParam<R, K> U,
+          const __grid_constant__ std::conditional_t<PK, RegPack, NoPack> X) {
     using V = typename C2<R>::T;
     constexpr int NB0 = (VEC == 2 && !T0) ? 1 : 0;              // bit 0 as non-target register bit
     constexpr int NR = 1 << (K + NB0);                           // amplitudes per thread
@@ -197,30 +207,28 @@ apply_reg(typename C2<R>::T *__restrict__ psi, const __grid_constant__ RegParams
 #pragma unroll
     for (int i = KL - 1; i >= 0; --i) lane_transpose<V, NR>(x, P.la[i], T0 + i, lane);
 
-    if (P.om.active) {
+    if constexpr (PK) {
         // apply+pack: out-of-place, bit-permuted (and buffer-selected) output
-        const uint64_t yb = om_swap(base, P.om);
-        const uint32_t tb = (uint32_t)(yb >> P.om.tsh) & P.om.tmask;
-        const uint64_t lb = (yb & ~((uint64_t)P.om.tmask << P.om.tsh)) | P.om.add;
+        const uint64_t yb = om_swap(base, X.om);
+        const uint32_t tb = (uint32_t)(yb >> X.om.tsh) & X.om.tmask;
+        const uint64_t lb = (yb & ~((uint64_t)X.om.tmask << X.om.tsh)) | X.om.add;
         if constexpr (VEC == 2) {
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
                 const int j0 = ((v >> P0) << (P0 + 1)) | (v & ((1 << P0) - 1));
                 const int j1 = j0 | (1 << P0);
-                float4 *dst = reinterpret_cast<float4 *>(P.om.dst[tb | P.tv[v]]);
-                HQ_CHECK_IDX(lb | P.pvoff[v], P.nunits * NV, 11);
-                dst[lb | P.pvoff[v]] = make_float4(x[j0].x, x[j0].y, x[j1].x, x[j1].y);
+                float4 *dst = reinterpret_cast<float4 *>(X.om.dst[tb | X.tv[v]]);
+                HQ_CHECK_IDX(lb | X.pvoff[v], P.nunits * NV, 11);
+                dst[lb | X.pvoff[v]] = make_float4(x[j0].x, x[j0].y, x[j1].x, x[j1].y);
             }
         } else {
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
-                HQ_CHECK_IDX(lb | P.pvoff[v], P.nunits * NV, 12);
-                reinterpret_cast<V *>(P.om.dst[tb | P.tv[v]])[lb | P.pvoff[v]] = x[v];
+                HQ_CHECK_IDX(lb | X.pvoff[v], P.nunits * NV, 12);
+                reinterpret_cast<V *>(X.om.dst[tb | X.tv[v]])[lb | X.pvoff[v]] = x[v];
             }
         }
-        return;
-    }
-    if constexpr (VEC == 2) {
+    } else if constexpr (VEC == 2) {
         float4 *dst = reinterpret_cast<float4 *>(psi);
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
@@ -330,37 +338,41 @@ namespace {
 constexpr int kThreads = 128;
 
 template <typename R, int VEC, int K, int T0, int KL>
-cudaError_t launch_reg_t(void *psi, const RegParams &P, const void *host_U, cudaStream_t st) {
+cudaError_t launch_reg_t(void *psi, const RegParams &P, const RegPack *X, const void *host_U, cudaStream_t st) {
     UParam<R, K> U;
     memcpy(&U, host_U, sizeof(U));
     const uint64_t blocks = (P.nunits + kThreads - 1) / kThreads;
-    apply_reg<R, VEC, K, T0, KL><<<(unsigned)blocks, kThreads, 0, st>>>(
-        reinterpret_cast<typename C2<R>::T *>(psi), P, U);
+    if (X)
+        apply_reg<R, VEC, K, T0, KL, true><<<(unsigned)blocks, kThreads, 0, st>>>(
+            reinterpret_cast<typename C2<R>::T *>(psi), P, U, *X);
+    else
+        apply_reg<R, VEC, K, T0, KL, false><<<(unsigned)blocks, kThreads, 0, st>>>(
+            reinterpret_cast<typename C2<R>::T *>(psi), P, U, NoPack{});
     return cudaGetLastError();
 }
 
 template <typename R, int VEC, int K, int T0>
-cudaError_t launch_reg_kl(int KL, void *psi, const RegParams &P, const void *hU, cudaStream_t st) {
+cudaError_t launch_reg_kl(int KL, void *psi, const RegParams &P, const RegPack *X, const void *hU, cudaStream_t st) {
     switch (KL) {
-        case 0: return launch_reg_t<R, VEC, K, T0, 0>(psi, P, hU, st);
-        case 1: if constexpr (K - T0 >= 1) return launch_reg_t<R, VEC, K, T0, 1>(psi, P, hU, st); break;
-        case 2: if constexpr (K - T0 >= 2) return launch_reg_t<R, VEC, K, T0, 2>(psi, P, hU, st); break;
-        case 3: if constexpr (K - T0 >= 3) return launch_reg_t<R, VEC, K, T0, 3>(psi, P, hU, st); break;
-        case 4: if constexpr (K - T0 >= 4) return launch_reg_t<R, VEC, K, T0, 4>(psi, P, hU, st); break;
+        case 0: return launch_reg_t<R, VEC, K, T0, 0>(psi, P, X, hU, st);
+        case 1: if constexpr (K - T0 >= 1) return launch_reg_t<R, VEC, K, T0, 1>(psi, P, X, hU, st); break;
+        case 2: if constexpr (K - T0 >= 2) return launch_reg_t<R, VEC, K, T0, 2>(psi, P, X, hU, st); break;
+        case 3: if constexpr (K - T0 >= 3) return launch_reg_t<R, VEC, K, T0, 3>(psi, P, X, hU, st); break;
+        case 4: if constexpr (K - T0 >= 4) return launch_reg_t<R, VEC, K, T0, 4>(psi, P, X, hU, st); break;
         default: break;
     }
     return cudaErrorInvalidValue;
 }
 
 template <int K>
-cudaError_t launch_reg_f(int VEC, int T0, int KL, void *psi, const RegParams &P, const void *hU,
+cudaError_t launch_reg_f(int VEC, int T0, int KL, void *psi, const RegParams &P, const RegPack *X, const void *hU,
                          cudaStream_t st) {
     if (VEC == 2) {
-        if (T0) return launch_reg_kl<float, 2, K, 1>(KL, psi, P, hU, st);
-        if constexpr (K <= 3) return launch_reg_kl<float, 2, K, 0>(KL, psi, P, hU, st);
+        if (T0) return launch_reg_kl<float, 2, K, 1>(KL, psi, P, X, hU, st);
+        if constexpr (K <= 3) return launch_reg_kl<float, 2, K, 0>(KL, psi, P, X, hU, st);
         return cudaErrorInvalidValue;
     }
-    return launch_reg_kl<float, 1, K, 0>(KL, psi, P, hU, st);
+    return launch_reg_kl<float, 1, K, 0>(KL, psi, P, X, hU, st);
 }
 
 template <typename R>
@@ -592,16 +604,16 @@ static bool out_map(const OutSpec &o, int lb, OutMap &m) {
     return true;
 }
 
-static bool reg_out_tables(RegParams &rp, int VEC, int K, int T0, const OutSpec *out) {
+static bool reg_out_tables(const RegParams &rp, RegPack &X, int VEC, int K, int T0, const OutSpec *out) {
     const int LB = VEC == 2 ? 1 : 0;
-    if (!out_map(out ? *out : OutSpec{}, LB, rp.om)) return false;
-    if (!rp.om.active) return true;
+    if (!out_map(out ? *out : OutSpec{}, LB, X.om)) return false;
+    if (!X.om.active) return true;
     const int NB0 = (VEC == 2 && !T0) ? 1 : 0;
     const int NV = (1 << (K + NB0)) / VEC;
     for (int v = 0; v < NV; ++v) {
-        const uint64_t y = om_swap(rp.voff[v], rp.om);
-        rp.tv[v] = (uint8_t)((y >> rp.om.tsh) & rp.om.tmask);
-        rp.pvoff[v] = y & ~((uint64_t)rp.om.tmask << rp.om.tsh);
+        const uint64_t y = om_swap(rp.voff[v], X.om);
+        X.tv[v] = (uint8_t)((y >> X.om.tsh) & X.om.tmask);
+        X.pvoff[v] = y & ~((uint64_t)X.om.tmask << X.om.tsh);
     }
     return true;
 }
@@ -609,7 +621,8 @@ static bool reg_out_tables(RegParams &rp, int VEC, int K, int T0, const OutSpec 
 bool apply_supports_out(int dtype, const ApplyDesc &d, const OutSpec &o) {
     RegParams rp;
     int VEC = 1, T0 = 0, KL = 0;
-    if (plan_reg(dtype, d, rp, VEC, T0, KL)) return reg_out_tables(rp, VEC, d.k, T0, &o);
+    RegPack X;
+    if (plan_reg(dtype, d, rp, VEC, T0, KL)) return reg_out_tables(rp, X, VEC, d.k, T0, &o);
     if (dtype == HQ_C128 && d.k >= 5 && (1ull << (d.n_local - d.k)) >= (1ull << 12)) return false;   // apply_ztile
     OutMap m;
     return out_map(o, 0, m);
@@ -622,20 +635,22 @@ int launch_apply(int dtype, void *psi, const ApplyDesc &d, const void *host_U, c
     int VEC = 1, T0 = 0, KL = 0;
     cudaError_t e;
     if (host_U && plan_reg(dtype, d, rp, VEC, T0, KL)) {
-        if (!reg_out_tables(rp, VEC, d.k, T0, out)) return (int)cudaErrorInvalidValue;
+        RegPack X;
+        if (!reg_out_tables(rp, X, VEC, d.k, T0, out)) return (int)cudaErrorInvalidValue;
+        const RegPack *xp = X.om.active ? &X : nullptr;
         if (dtype == HQ_C64) {
             switch (d.k) {
-                case 1: e = launch_reg_f<1>(VEC, T0, KL, psi, rp, host_U, st); break;
-                case 2: e = launch_reg_f<2>(VEC, T0, KL, psi, rp, host_U, st); break;
-                case 3: e = launch_reg_f<3>(VEC, T0, KL, psi, rp, host_U, st); break;
-                default: e = launch_reg_f<4>(VEC, T0, KL, psi, rp, host_U, st); break;
+                case 1: e = launch_reg_f<1>(VEC, T0, KL, psi, rp, xp, host_U, st); break;
+                case 2: e = launch_reg_f<2>(VEC, T0, KL, psi, rp, xp, host_U, st); break;
+                case 3: e = launch_reg_f<3>(VEC, T0, KL, psi, rp, xp, host_U, st); break;
+                default: e = launch_reg_f<4>(VEC, T0, KL, psi, rp, xp, host_U, st); break;
             }
         } else {
             switch (d.k) {
-                case 1: e = launch_reg_kl<double, 1, 1, 0>(KL, psi, rp, host_U, st); break;
-                case 2: e = launch_reg_kl<double, 1, 2, 0>(KL, psi, rp, host_U, st); break;
-                case 3: e = launch_reg_kl<double, 1, 3, 0>(KL, psi, rp, host_U, st); break;
-                default: e = launch_reg_kl<double, 1, 4, 0>(KL, psi, rp, host_U, st); break;
+                case 1: e = launch_reg_kl<double, 1, 1, 0>(KL, psi, rp, xp, host_U, st); break;
+                case 2: e = launch_reg_kl<double, 1, 2, 0>(KL, psi, rp, xp, host_U, st); break;
+                case 3: e = launch_reg_kl<double, 1, 3, 0>(KL, psi, rp, xp, host_U, st); break;
+                default: e = launch_reg_kl<double, 1, 4, 0>(KL, psi, rp, xp, host_U, st); break;
             }
         }
     } else {

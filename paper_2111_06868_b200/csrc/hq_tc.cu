@@ -40,6 +40,7 @@
 #include <cmath>
 #include <atomic>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include "hq_internal.h"
@@ -360,14 +361,22 @@ struct ParamsB {
     int pair;              // 1: the lowest target is bit 0, patterns (2j, 2j+1) are one 16-byte load / store
     int xpair;             // 1: bit 0 is not a target and is lane bit 0: lane pairs swap one
                            //    output each so that every store is 16 bytes
-    // out-of-place output (apply+pack; om.active): byte offsets of the
-    // permuted pattern / set parts without the selector bits, and those bits
+};
+
+// apply+pack output of mode H (a separate kernel argument of the PK
+// instantiation only, so the in-place kernel's parameters stay as they were):
+// byte offsets of the permuted pattern / set parts without the selector bits,
+// and those bits
+struct PackB {
     OutMap om;
     uint64_t poff8[64];
     uint64_t psoff8[128];
     uint8_t tpat[64];
     uint8_t tset[128];
 };
+struct NoPack {};
+__device__ __forceinline__ const OutMap &pk_om(const PackB &x) { return x.om; }
+__device__ __forceinline__ OutMap pk_om(const NoPack &) { return OutMap{}; }
 
 // SWIZZLE_128B as seen from a slot index (8-byte amplitudes): byte address
 // bits [4:6] ^= bits [7:9], i.e. index bits [1:3] ^= [4:6].  Linear over GF(2),
@@ -422,11 +431,14 @@ __device__ __forceinline__ uint64_t sub_f32x2(uint64_t a, uint64_t b) {
     return r;
 }
 
-template <int K, int NS, int NP, bool DIAG = false>
+// PK: apply+pack variant (out-of-place through P.om), instantiated separately
+// so the in-place epilogue carries no output-map code.
+template <int K, int NS, int NP, bool DIAG = false, bool PK = false>
 __global__ void __launch_bounds__(bk_threads(NP), 1)
 apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
           const __half *__restrict__ Breal /* [2][N][KD]: hi then lo, row n = output real */,
-          const __grid_constant__ CUtensorMap tmap /* psi as [rows][16 amplitudes], box 8 rows, SWIZZLE_128B (P.swz) */) {
+          const __grid_constant__ CUtensorMap tmap /* psi as [rows][16 amplitudes], box 8 rows, SWIZZLE_128B (P.swz) */,
+          const __grid_constant__ std::conditional_t<PK, PackB, NoPack> X) {
     // even NS only: odd rings (a slot shared by both K-halves) failed with a
     // launch error at n >= 32 in the ring experiments; not pursued
     static_assert(NS % 2 == 0, "slot parity = K-half needs an even ring");
@@ -660,14 +672,14 @@ apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
             // buffer selector (tile | set | pattern parts) and an offset
             uint32_t tsel = 0;
             uint64_t obase = 0;
-            if (P.om.active) {
-                const uint64_t y = om_swap(tw.base, P.om);
-                tsel = ((uint32_t)(y >> P.om.tsh) & P.om.tmask) | P.tset[n];
-                obase = ((y & ~((uint64_t)P.om.tmask << P.om.tsh)) | P.om.add) * 8 + P.psoff8[n];
+            if constexpr (PK) {
+                const uint64_t y = om_swap(tw.base, X.om);
+                tsel = ((uint32_t)(y >> X.om.tsh) & X.om.tmask) | X.tset[n];
+                obase = ((y & ~((uint64_t)X.om.tmask << X.om.tsh)) | X.om.add) * 8 + X.psoff8[n];
             }
             auto saddr = [&](int c) -> char * {
-                return P.om.active ? reinterpret_cast<char *>(P.om.dst[tsel | P.tpat[c]]) + obase + P.poff8[c]
-                                   : pb + P.off8[c];
+                if constexpr (PK) return reinterpret_cast<char *>(X.om.dst[tsel | X.tpat[c]]) + obase + X.poff8[c];
+                else return pb + P.off8[c];
             };
             const uint32_t Dt = tmem + 2 * KD + d * N + lane_addr;
 #pragma unroll 2
@@ -690,7 +702,7 @@ apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
                         const float2 o0 = u64_as_f2(mul_f32x2(mul_f32x2(x0, f1), f2));
                         const float2 o1 = u64_as_f2(mul_f32x2(mul_f32x2(x1, f1), f2));
                         if (DIAG && (P.diag & 4)) continue;
-                        HQ_CHECK_OUT(saddr(16 * ch + i), 16, psi, P.om, P.h.ntiles << (K + SETBITS + 3), 2);
+                        HQ_CHECK_OUT(saddr(16 * ch + i), 16, psi, pk_om(X), P.h.ntiles << (K + SETBITS + 3), 2);
                         st_cs_f4(saddr(16 * ch + i), o0, o1);
                     }
                     continue;
@@ -709,7 +721,7 @@ apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
                         const uint64_t y1 = mul_f32x2(mul_f32x2(x1, f1), f2);
                         const uint64_t r = __shfl_xor_sync(0xffffffffu, odd ? y0 : y1, 1);
                         if (DIAG && (P.diag & 4)) continue;
-                        HQ_CHECK_OUT(saddr(16 * ch + i + (odd ? 1 : 0)) - (odd ? 8 : 0), 16, psi, P.om,
+                        HQ_CHECK_OUT(saddr(16 * ch + i + (odd ? 1 : 0)) - (odd ? 8 : 0), 16, psi, pk_om(X),
                                      P.h.ntiles << (K + SETBITS + 3), 3);
                         st_cs_f4(saddr(16 * ch + i + (odd ? 1 : 0)) - (odd ? 8 : 0), u64_as_f2(odd ? r : y0),
                                  u64_as_f2(odd ? y1 : r));
@@ -721,7 +733,7 @@ apply_tcb(float2 *__restrict__ psi, const __grid_constant__ ParamsB P,
                     const uint64_t x = (uint64_t)v[2 * i] | ((uint64_t)v[2 * i + 1] << 32);
                     const float2 o = u64_as_f2(mul_f32x2(mul_f32x2(x, f1), f2));
                     if (DIAG && (P.diag & 4)) continue; // diagnostics only: no stores
-                    HQ_CHECK_OUT(saddr(16 * ch + i), 8, psi, P.om, P.h.ntiles << (K + SETBITS + 3), 4);
+                    HQ_CHECK_OUT(saddr(16 * ch + i), 8, psi, pk_om(X), P.h.ntiles << (K + SETBITS + 3), 4);
                     st_cs_f2(saddr(16 * ch + i), o);
                 }
             }
@@ -791,8 +803,11 @@ struct ParamsL {
     int ue;                // A = U * 2^ue (host scaling into the fp16 range)
     int ea;                // B = psi * 2^ea (runtime: from the amplitude bound)
     uint64_t ntiles;
-    // out-of-place output (apply+pack; om.active): amplitude offsets of the
-    // permuted pattern / set parts without the selector bits, and those bits
+};
+
+// apply+pack output of mode L (PK instantiation only): amplitude offsets of
+// the permuted pattern / set parts without the selector bits, and those bits
+struct PackL {
     OutMap om;
     uint64_t poff[64];
     uint64_t psetoff[64];
@@ -821,9 +836,11 @@ __device__ __forceinline__ uint64_t tile_base12(uint64_t t, const ParamsL &P) {
 }
 
 
+template <bool PK>      // PK: apply+pack variant (see apply_tcb)
 __global__ void __launch_bounds__(LB_THREADS, 1)
 apply_tcL(float2 *__restrict__ psi, const __grid_constant__ ParamsL P,
-          const uint32_t *__restrict__ Apack /* [2][128][64] half2: hi then lo, row = output real */) {
+          const uint32_t *__restrict__ Apack /* [2][128][64] half2: hi then lo, row = output real */,
+          const __grid_constant__ std::conditional_t<PK, PackL, NoPack> X) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -1003,6 +1020,9 @@ apply_tcL(float2 *__restrict__ psi, const __grid_constant__ ParamsL P,
         // set offsets are GF(2)-linear in the set index (disjoint bits), so
         // setoff[32 hc + j] = setoff[32 hc] + setoff[j], j a compile-time index
         const uint64_t rbh = rb + 2 * (uint64_t)P.setoff[32 * hc];
+        uint64_t sb[5];
+#pragma unroll
+        for (int b = 0; b < 5; ++b) sb[b] = 2 * (uint64_t)P.setoff[1 << b];
         // 2^-(ea + ue) as one factor when it is a normal float, else two
         const int se = -(max(-126, min(127, P.ea)) + P.ue);
         const float2 sf = pow2_factors(se);
@@ -1028,23 +1048,29 @@ apply_tcL(float2 *__restrict__ psi, const __grid_constant__ ParamsL P,
 #pragma unroll
                 for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) * sf.x * sf.y);
             }
-            if (!P.om.active) {
+            if constexpr (!PK) {
                 float *pb = psif + 2 * tw.base + rbh;
+                // set j's offset from the five single-bit offsets (linearity):
+                // five tile-invariant values instead of 32 held in registers
 #pragma unroll
                 for (int j = 0; j < 32; ++j) {
-                    HQ_CHECK_IN(pb + 2 * P.setoff[j], 4, psi, P.ntiles << 15, 6);
-                    st_cs_f1(pb + 2 * P.setoff[j], __uint_as_float(v[j]));
+                    uint64_t o = 0;
+#pragma unroll
+                    for (int b = 0; b < 5; ++b)
+                        if ((j >> b) & 1) o += sb[b];
+                    HQ_CHECK_IN(pb + o, 4, psi, P.ntiles << 15, 6);
+                    st_cs_f1(pb + o, __uint_as_float(v[j]));
                 }
             } else {                  // apply+pack (see apply_tcb)
-                const uint64_t y = om_swap(tw.base, P.om);
-                const uint32_t tsel = ((uint32_t)(y >> P.om.tsh) & P.om.tmask) | P.tpat[r];
-                const uint64_t ob = ((y & ~((uint64_t)P.om.tmask << P.om.tsh)) | P.om.add) + P.poff[r];
+                const uint64_t y = om_swap(tw.base, X.om);
+                const uint32_t tsel = ((uint32_t)(y >> X.om.tsh) & X.om.tmask) | X.tpat[r];
+                const uint64_t ob = ((y & ~((uint64_t)X.om.tmask << X.om.tsh)) | X.om.add) + X.poff[r];
 #pragma unroll
                 for (int j = 0; j < 32; ++j) {
                     const int sn = 32 * hc + j;
-                    float *dst = reinterpret_cast<float *>(P.om.dst[tsel | P.tset[sn]]);
-                    HQ_CHECK_OUT(dst + 2 * (ob + P.psetoff[sn]) + e, 4, psi, P.om, P.ntiles << 15, 7);
-                    dst[2 * (ob + P.psetoff[sn]) + e] = __uint_as_float(v[j]);
+                    float *dst = reinterpret_cast<float *>(X.om.dst[tsel | X.tset[sn]]);
+                    HQ_CHECK_OUT(dst + 2 * (ob + X.psetoff[sn]) + e, 4, psi, X.om, P.ntiles << 15, 7);
+                    dst[2 * (ob + X.psetoff[sn]) + e] = __uint_as_float(v[j]);
                 }
             }
         }
@@ -1383,12 +1409,13 @@ static int sm_count() {
 // 34q bench circuit in the sustained (power-capped) regime
 // (tools/pass_times.py, round 1): (4, 2) beats (4, 1), (8, *) and the
 // earlier cp.async kernel (3.91 s vs 4.28 s and 4.08 s).
-template <int K, bool DIAG = false>
-static int tc_launch_b(void *psi, const tc::ParamsB &P, const void *dev_payload, cudaStream_t st) {
+template <int K, bool DIAG = false, bool PK = false>
+static int tc_launch_b(void *psi, const tc::ParamsB &P, const std::conditional_t<PK, tc::PackB, tc::NoPack> &X,
+                       const void *dev_payload, cudaStream_t st) {
     constexpr int NS = 4, NP = 2;
     using C = tc::CfgB<K, NS>;
     static std::atomic<uint64_t> attr{0};
-    cudaError_t e = smem_attr_once(tc::apply_tcb<K, NS, NP, DIAG>, C::SMEM, attr);
+    cudaError_t e = smem_attr_once(tc::apply_tcb<K, NS, NP, DIAG, PK>, C::SMEM, attr);
     if (e != cudaSuccess) return (int)e;
     const int sms = sm_count();
     const uint64_t grid = P.h.ntiles < (uint64_t)sms ? P.h.ntiles : (uint64_t)sms;
@@ -1400,19 +1427,21 @@ static int tc_launch_b(void *psi, const tc::ParamsB &P, const void *dev_payload,
         const int r = tc_encode_rows_map(&map, psi, nl);
         if (r) return r;
     }
-    tc::apply_tcb<K, NS, NP, DIAG><<<(unsigned)grid, tc::bk_threads(NP), C::SMEM, st>>>(
-        reinterpret_cast<float2 *>(psi), P, reinterpret_cast<const __half *>(dev_payload), map);
+    tc::apply_tcb<K, NS, NP, DIAG, PK><<<(unsigned)grid, tc::bk_threads(NP), C::SMEM, st>>>(
+        reinterpret_cast<float2 *>(psi), P, reinterpret_cast<const __half *>(dev_payload), map, X);
     return (int)cudaGetLastError();
 }
 
-static int tc_launch_l(void *psi, const tc::ParamsL &P, const void *dev_payload, cudaStream_t st) {
+template <bool PK>
+static int tc_launch_l(void *psi, const tc::ParamsL &P, const std::conditional_t<PK, tc::PackL, tc::NoPack> &X,
+                       const void *dev_payload, cudaStream_t st) {
     static std::atomic<uint64_t> attr{0};
-    cudaError_t e = smem_attr_once(tc::apply_tcL, tc::LB_SMEM, attr);
+    cudaError_t e = smem_attr_once(tc::apply_tcL<PK>, tc::LB_SMEM, attr);
     if (e != cudaSuccess) return (int)e;
     const int sms = sm_count();
     const uint64_t grid = P.ntiles < (uint64_t)sms ? P.ntiles : (uint64_t)sms;
-    tc::apply_tcL<<<(unsigned)grid, tc::LB_THREADS, tc::LB_SMEM, st>>>(
-        reinterpret_cast<float2 *>(psi), P, reinterpret_cast<const uint32_t *>(dev_payload));
+    tc::apply_tcL<PK><<<(unsigned)grid, tc::LB_THREADS, tc::LB_SMEM, st>>>(
+        reinterpret_cast<float2 *>(psi), P, reinterpret_cast<const uint32_t *>(dev_payload), X);
     return (int)cudaGetLastError();
 }
 
@@ -1422,49 +1451,58 @@ static int tc_launch_l(void *psi, const tc::ParamsL &P, const void *dev_payload,
 // lane-pair stores, whole 32-byte sectors).
 bool tc_set_output(std::vector<char> &params, const OutSpec &o) {
     if (params.empty()) return false;
+    const char tag = params.back();
+    if (!o.active) return tag == 'B' || tag == 'L';
     OutMap m{};
-    if (o.active) {
-        m.active = 1;
-        m.npairs = o.npairs;
-        for (int i = 0; i < o.npairs; ++i) {
-            if (o.pa[i] < PACK_MIN_BIT || o.pb[i] < PACK_MIN_BIT) return false;
-            m.pa[i] = o.pa[i];
-            m.pb[i] = o.pb[i];
-        }
-        if (o.tmask && o.tsh < PACK_MIN_BIT) return false;
-        m.tsh = o.tmask ? o.tsh : 0;
-        m.tmask = o.tmask;
-        m.add = o.add;
-        for (int t = 0; t < 8; ++t) m.dst[t] = reinterpret_cast<uint64_t>(o.dst[t]);
+    m.active = 1;
+    m.npairs = o.npairs;
+    for (int i = 0; i < o.npairs; ++i) {
+        if (o.pa[i] < PACK_MIN_BIT || o.pb[i] < PACK_MIN_BIT) return false;
+        m.pa[i] = o.pa[i];
+        m.pb[i] = o.pb[i];
     }
+    if (o.tmask && o.tsh < PACK_MIN_BIT) return false;
+    m.tsh = o.tmask ? o.tsh : 0;
+    m.tmask = o.tmask;
+    m.add = o.add;
+    for (int t = 0; t < 8; ++t) m.dst[t] = reinterpret_cast<uint64_t>(o.dst[t]);
     const uint64_t strip = ~((uint64_t)m.tmask << m.tsh);
     auto split = [&](uint64_t x, uint64_t &low, uint8_t &sel) {
         const uint64_t y = om_swap(x, m);
         sel = (uint8_t)((y >> m.tsh) & m.tmask);
         low = y & strip;
     };
-    if (params.back() == 'B') {
-        tc::ParamsB &B = *reinterpret_cast<tc::ParamsB *>(params.data());
-        B.om = m;
-        if (!m.active) return true;
+    // layout of a packed block: [Params][Pack][tag], tag 'P' (mode H) / 'Q' (mode L)
+    if (tag == 'B' || tag == 'P') {
+        const tc::ParamsB B = *reinterpret_cast<const tc::ParamsB *>(params.data());
+        tc::PackB X{};
+        X.om = m;
         for (int c = 0; c < (1 << B.h.k); ++c) {
             uint64_t lo;
-            split(B.h.off[c], lo, B.tpat[c]);
-            B.poff8[c] = lo * 8;
+            split(B.h.off[c], lo, X.tpat[c]);
+            X.poff8[c] = lo * 8;
         }
         for (int n = 0; n < tc::M; ++n) {
             uint64_t lo;
-            split(B.h.setoff[n], lo, B.tset[n]);
-            B.psoff8[n] = lo * 8;
+            split(B.h.setoff[n], lo, X.tset[n]);
+            X.psoff8[n] = lo * 8;
         }
+        params.assign(sizeof(tc::ParamsB) + sizeof(tc::PackB) + 1, 0);
+        memcpy(params.data(), &B, sizeof B);
+        memcpy(params.data() + sizeof B, &X, sizeof X);
+        params.back() = 'P';
         return true;
     }
-    if (params.back() == 'L') {
-        tc::ParamsL &L = *reinterpret_cast<tc::ParamsL *>(params.data());
-        L.om = m;
-        if (!m.active) return true;
-        for (int c = 0; c < 64; ++c) split(L.off[c], L.poff[c], L.tpat[c]);
-        for (int n = 0; n < 64; ++n) split(L.setoff[n], L.psetoff[n], L.tset[n]);
+    if (tag == 'L' || tag == 'Q') {
+        const tc::ParamsL L = *reinterpret_cast<const tc::ParamsL *>(params.data());
+        tc::PackL X{};
+        X.om = m;
+        for (int c = 0; c < 64; ++c) split(L.off[c], X.poff[c], X.tpat[c]);
+        for (int n = 0; n < 64; ++n) split(L.setoff[n], X.psetoff[n], X.tset[n]);
+        params.assign(sizeof(tc::ParamsL) + sizeof(tc::PackL) + 1, 0);
+        memcpy(params.data(), &L, sizeof L);
+        memcpy(params.data() + sizeof L, &X, sizeof X);
+        params.back() = 'Q';
         return true;
     }
     return false;
@@ -1477,8 +1515,9 @@ void tc_set_amp_bound(std::vector<char> &params, double bound) {
     int ex = 0;
     if (bound > 0 && std::isfinite(bound)) std::frexp(bound, &ex);   // bound < 2^ex
     const int ea = std::max(-126, std::min(127, 14 - ex));
-    if (params.back() == 'B') reinterpret_cast<tc::ParamsB *>(params.data())->h.ea = ea;
-    else if (params.back() == 'L') reinterpret_cast<tc::ParamsL *>(params.data())->ea = ea;
+    const char tag = params.back();
+    if (tag == 'B' || tag == 'P') reinterpret_cast<tc::ParamsB *>(params.data())->h.ea = ea;
+    else if (tag == 'L' || tag == 'Q') reinterpret_cast<tc::ParamsL *>(params.data())->ea = ea;
 }
 
 // params: a tc::ParamsB (mode H) or tc::ParamsL (mode L) block followed by
@@ -1486,15 +1525,30 @@ void tc_set_amp_bound(std::vector<char> &params, double bound) {
 int tc_launch(void *psi, const void *params, size_t params_size, const void *dev_payload,
               void *stream) {
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    const char tag = reinterpret_cast<const char *>(params)[params_size - 1];
-    if (tag == 'L') return tc_launch_l(psi, *reinterpret_cast<const tc::ParamsL *>(params), dev_payload, st);
+    const char *pb = reinterpret_cast<const char *>(params);
+    const char tag = pb[params_size - 1];
+    if (tag == 'L') {
+        const tc::ParamsL &L = *reinterpret_cast<const tc::ParamsL *>(pb);
+        return tc_launch_l<false>(psi, L, tc::NoPack{}, dev_payload, st);
+    }
+    if (tag == 'Q') {
+        const tc::ParamsL &L = *reinterpret_cast<const tc::ParamsL *>(pb);
+        const tc::PackL &X = *reinterpret_cast<const tc::PackL *>(pb + sizeof(tc::ParamsL));
+        return tc_launch_l<true>(psi, L, X, dev_payload, st);
+    }
+    const tc::ParamsB &B = *reinterpret_cast<const tc::ParamsB *>(pb);
+    if (tag == 'P') {
+        const tc::PackB &X = *reinterpret_cast<const tc::PackB *>(pb + sizeof(tc::ParamsB));
+        return B.h.k == 5 ? tc_launch_b<5, false, true>(psi, B, X, dev_payload, st)
+                          : tc_launch_b<6, false, true>(psi, B, X, dev_payload, st);
+    }
     if (tag != 'B') return (int)cudaErrorInvalidValue;
-    const tc::ParamsB &B = *reinterpret_cast<const tc::ParamsB *>(params);
 #ifdef HQ_TC_DIAG_BUILD
-    if (B.diag) return B.h.k == 5 ? tc_launch_b<5, true>(psi, B, dev_payload, st)
-                                  : tc_launch_b<6, true>(psi, B, dev_payload, st);
+    if (B.diag) return B.h.k == 5 ? tc_launch_b<5, true>(psi, B, tc::NoPack{}, dev_payload, st)
+                                  : tc_launch_b<6, true>(psi, B, tc::NoPack{}, dev_payload, st);
 #endif
-    return B.h.k == 5 ? tc_launch_b<5>(psi, B, dev_payload, st) : tc_launch_b<6>(psi, B, dev_payload, st);
+    return B.h.k == 5 ? tc_launch_b<5>(psi, B, tc::NoPack{}, dev_payload, st)
+                      : tc_launch_b<6>(psi, B, tc::NoPack{}, dev_payload, st);
 }
 
 }  // namespace hq
