@@ -94,6 +94,7 @@ typedef struct hq_stats {
     uint64_t h2d_bytes;       /* host->device bytes the library copied (this rank) */
     uint64_t d2h_bytes;       /* device->host bytes the library copied (this rank) */
     uint64_t packs;           /* PERMUTEs folded into an apply pass (apply+pack)   */
+    uint64_t remaps_fused;    /* remaps done inside the preceding apply pass       */
 } hq_stats;
 
 /* ------------------------------------------------------------------ create */
@@ -161,6 +162,22 @@ hq_status hq_state_create_rank_from_buffers(int n, hq_dtype dtype, int world_siz
  * the rank bits).  Errors: HQ_ERR_ARG (not a permutation). */
 hq_status hq_state_set_layout(hq_state *s, const int32_t *pi);
 hq_status hq_state_get_layout(const hq_state *s, int32_t *pi_out);
+
+/* How a remap (global<->local qubit swap) moves data between ranks:
+ *   HQ_REMAP_FUSED (default): when the scheduler has packed the evictees on
+ *     the top local bits and the apply pass before the remap can write out
+ *     of place, that pass writes every element directly into its destination
+ *     rank's exchange buffer (peer memory: CUDA IPC in one-process-per-GPU
+ *     states, peer access in multi-device states, the other shards' buffers
+ *     for virtual shards), with a stream barrier across ranks before and
+ *     after; the exchange costs no separate transfer or HBM pass.  Used only
+ *     when every rank could map every peer (else the exchange path runs).
+ *   HQ_REMAP_EXCHANGE: always a separate exchange (grouped NCCL send/recv, or
+ *     device copies for virtual shards) after the pass.
+ * fused_available (may be NULL) receives 1 when peer buffers are mapped. */
+#define HQ_REMAP_EXCHANGE 0
+#define HQ_REMAP_FUSED 1
+hq_status hq_state_set_remap_mode(hq_state *s, int mode, int *fused_available);
 
 /* Forget the tracked amplitude bound (see the rule above): the next pass that
  * needs it recomputes it with one norm pass.  Never changes the amplitudes. */

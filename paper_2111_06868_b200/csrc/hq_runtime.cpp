@@ -8,6 +8,7 @@
 // aligned.  The logical->physical qubit map pi starts as q -> n-1-q (so the
 // physical index equals the logical index, reading C1) and changes only when
 // the distributed schedule remaps global qubits.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -125,6 +126,24 @@ struct hq_state {
     bool profiling = false;
     std::vector<ProfEvent> prof;  // pending
     ProfAcc acc[3];               // per kernel family (PATH_REG, PATH_GEN, PATH_TC)
+    // fused remap (row f1): the apply pass before a packed
+    // remap writes every element straight into its destination rank's
+    // exchange buffer (peer memory over NVLink), so the exchange needs no
+    // separate transfer.  p2p: every peer's buffers are addressable.
+    int remap_mode = HQ_REMAP_FUSED;
+    bool p2p = false;
+    std::vector<void *> peer_base[2];   // rank mode: IPC-mapped original [psi, buf] of every rank
+    uint64_t swaps = 0;                 // psi <-> buf exchanges so far (the same on every rank)
+    int *d_bar = nullptr;               // rank mode: one-int all-reduce used as a stream barrier
+    std::vector<cudaEvent_t> bar_ev;    // multi-device mode: one event per shard for barriers
+};
+
+struct Fold {
+    int consumed = 0;
+    bool fused = false;
+    bool with_perm = false;
+    const Op *rem = nullptr;
+    OutSpec tmpl;
 };
 
 struct hq_circuit {
@@ -138,7 +157,7 @@ struct hq_circuit {
     std::vector<std::vector<struct Prep>> cprep;
     std::vector<std::vector<long long>> cuoff;
     std::vector<double> cgnorm;            // spectral bound of the whole U
-    std::vector<OutSpec> pack;             // per APPLY op: apply+pack output map (active: folds op i+1)
+    std::vector<Fold> fold;                // per APPLY op: ops folded into it (apply+pack, fused remap)
     std::vector<char *> dev_U;             // per shard: all payloads
     // small single-shard states: the whole op stream in one shared-memory CTA
     SmemOp *small_ops = nullptr;
@@ -285,6 +304,138 @@ static hq_status validate_common(int n, hq_dtype dtype, int G) {
     return HQ_OK;
 }
 
+// ------------------------------------------------------------------ peer access (fused remaps)
+
+// Single process, several devices: enable peer access between every pair.
+static void setup_p2p_multi(hq_state *st) {
+    bool ok = true;
+    for (auto &a : st->sh)
+        for (auto &b : st->sh) {
+            if (a.device == b.device) continue;
+            int can = 0;
+            cudaDeviceCanAccessPeer(&can, a.device, b.device);
+            if (!can) { ok = false; continue; }
+            cudaSetDevice(a.device);
+            cudaError_t e = cudaDeviceEnablePeerAccess(b.device, 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) ok = false;
+        }
+    cudaGetLastError();
+    st->bar_ev.assign(st->sh.size(), nullptr);
+    for (size_t r = 0; r < st->sh.size(); ++r) {
+        cudaSetDevice(st->sh[r].device);
+        if (cudaEventCreateWithFlags(&st->bar_ev[r], cudaEventDisableTiming) != cudaSuccess) ok = false;
+    }
+    st->p2p = ok;
+}
+
+// One process per GPU: map every rank's two exchange buffers into this process
+// with CUDA IPC (handles of the allocations holding psi and buf, all-gathered
+// over NCCL).  Any failure on any rank (e.g. buffers from a VMM allocator,
+// which IPC cannot export) leaves fused remaps off on every rank, and the
+// remaps go through the NCCL exchange.
+using GetAddrRangeFn = CUresult (*)(CUdeviceptr *, size_t *, CUdeviceptr);
+static bool alloc_base(void *p, void **base) {
+    static GetAddrRangeFn fn = nullptr;
+    if (!fn) {
+        void *f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !f)
+            return false;
+        fn = reinterpret_cast<GetAddrRangeFn>(f);
+    }
+    CUdeviceptr b = 0;
+    size_t sz = 0;
+    if (fn(&b, &sz, reinterpret_cast<CUdeviceptr>(p)) != CUDA_SUCCESS) return false;
+    *base = reinterpret_cast<void *>(b);
+    return true;
+}
+
+static void setup_p2p_rank(hq_state *st) {
+    Shard &s = st->sh[0];
+    const int W = st->world;
+    struct Rec {
+        cudaIpcMemHandle_t h[2];
+        uint64_t off[2];
+        int ok;
+        int pad;
+    };
+    Rec mine;
+    memset(&mine, 0, sizeof mine);
+    mine.ok = 1;
+    void *ptrs[2] = {s.psi, s.buf};
+    for (int i = 0; i < 2; ++i) {
+        void *base = nullptr;
+        if (!alloc_base(ptrs[i], &base) || cudaIpcGetMemHandle(&mine.h[i], base) != cudaSuccess) {
+            mine.ok = 0;
+            continue;
+        }
+        mine.off[i] = (uint64_t)((char *)ptrs[i] - (char *)base);
+    }
+    cudaGetLastError();
+    cudaSetDevice(s.device);
+    Rec *d = nullptr;
+    std::vector<Rec> all(W);
+    bool ok = cudaMalloc((void **)&d, sizeof(Rec) * W) == cudaSuccess &&
+              cudaMemcpy(d + s.rank, &mine, sizeof mine, cudaMemcpyHostToDevice) == cudaSuccess &&
+              ncclAllGather(d + s.rank, d, sizeof(Rec), ncclChar, s.comm, s.stream) == ncclSuccess &&
+              cudaStreamSynchronize(s.stream) == cudaSuccess &&
+              cudaMemcpy(all.data(), d, sizeof(Rec) * W, cudaMemcpyDeviceToHost) == cudaSuccess;
+    if (d) cudaFree(d);
+    for (int r = 0; r < W && ok; ++r) ok = all[r].ok != 0;
+    st->peer_base[0].assign(W, nullptr);
+    st->peer_base[1].assign(W, nullptr);
+    int local_ok = ok ? 1 : 0;
+    for (int r = 0; r < W && local_ok; ++r) {
+        if (r == s.rank) {
+            st->peer_base[0][r] = s.psi;
+            st->peer_base[1][r] = s.buf;
+            continue;
+        }
+        for (int i = 0; i < 2 && local_ok; ++i) {
+            void *b = nullptr;
+            if (cudaIpcOpenMemHandle(&b, all[r].h[i], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) local_ok = 0;
+            else st->peer_base[i][r] = (char *)b + all[r].off[i];
+        }
+    }
+    cudaGetLastError();
+    // every rank must agree (a rank that could not map its peers turns fusion off everywhere)
+    int *dk = nullptr;
+    int agree = 0;
+    if (cudaMalloc((void **)&st->d_bar, sizeof(int)) == cudaSuccess &&
+        cudaMemset(st->d_bar, 0, sizeof(int)) == cudaSuccess && cudaMalloc((void **)&dk, sizeof(int)) == cudaSuccess &&
+        cudaMemcpy(dk, &local_ok, sizeof(int), cudaMemcpyHostToDevice) == cudaSuccess &&
+        ncclAllReduce(dk, dk, 1, ncclInt, ncclMin, s.comm, s.stream) == ncclSuccess &&
+        cudaStreamSynchronize(s.stream) == cudaSuccess)
+        cudaMemcpy(&agree, dk, sizeof(int), cudaMemcpyDeviceToHost);
+    if (dk) cudaFree(dk);
+    cudaGetLastError();
+    st->p2p = agree == 1;
+}
+
+static void release_p2p(hq_state *st) {
+    if (st->mode == MODE_RANK && !st->sh.empty()) {
+        cudaSetDevice(st->sh[0].device);
+        for (size_t r = 0; r < st->peer_base[0].size(); ++r) {
+            if ((int)r == st->sh[0].rank) continue;
+            for (int i = 0; i < 2; ++i)
+                if (st->peer_base[i][r]) {
+                    // the mapping was opened at the allocation base; psi/buf offsets are
+                    // recomputed from the base the handle maps
+                    void *b = nullptr;
+                    if (alloc_base(st->peer_base[i][r], &b)) cudaIpcCloseMemHandle(b);
+                }
+        }
+    }
+    for (size_t r = 0; r < st->bar_ev.size(); ++r)
+        if (st->bar_ev[r]) {
+            cudaSetDevice(st->sh[r].device);
+            cudaEventDestroy(st->bar_ev[r]);
+        }
+    if (st->d_bar) cudaFree(st->d_bar);
+    cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ create / destroy
 
 extern "C" hq_status hq_state_create(int n, hq_dtype dtype, int ngpus, hq_state **out) {
@@ -323,6 +474,7 @@ extern "C" hq_status hq_state_create(int n, hq_dtype dtype, int ngpus, hq_state 
             return set_error(HQ_ERR_NCCL, "ncclCommInitAll: %s", ncclGetErrorString(nr));
         }
         for (int r = 0; r < ngpus; ++r) st->sh[r].comm = comms[r];
+        setup_p2p_multi(st);
     }
     cudaSetDevice(cur);
     *out = st;
@@ -370,6 +522,7 @@ extern "C" hq_status hq_state_create_rank(int n, hq_dtype dtype, int world_size,
             delete st;
             return set_error(HQ_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(nr));
         }
+        setup_p2p_rank(st);
     }
     *out = st;
     return HQ_OK;
@@ -426,6 +579,7 @@ extern "C" hq_status hq_state_create_rank_from_buffers(int n, hq_dtype dtype, in
             delete st;
             return set_error(HQ_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(nr));
         }
+        setup_p2p_rank(st);
     }
     *out = st;
     return HQ_OK;
@@ -441,6 +595,7 @@ extern "C" hq_status hq_state_create_virtual(int n, hq_dtype dtype, int nshards,
     hq_state *st = new_state(n, dtype, nshards);
     if (!st) return set_error(HQ_ERR_OOM, "host allocation failed");
     st->mode = MODE_VIRTUAL;
+    st->p2p = true;                      // every shard buffer lives on this device
     st->sh.resize(nshards);
     int cur = 0;
     cudaGetDevice(&cur);
@@ -499,9 +654,19 @@ extern "C" hq_status hq_state_destroy(hq_state *st) {
         cudaEventDestroy(p.a);
         cudaEventDestroy(p.b);
     }
+    release_p2p(st);
     // virtual shards share shard 0's stream: free others first
     for (size_t i = st->sh.size(); i-- > 0;) shard_free(st->sh[i]);
     delete st;
+    return HQ_OK;
+}
+
+extern "C" hq_status hq_state_set_remap_mode(hq_state *st, int mode, int *fused_available) {
+    clear_error();
+    if (!st) return set_error(HQ_ERR_ARG, "state is NULL");
+    if (mode != HQ_REMAP_EXCHANGE && mode != HQ_REMAP_FUSED) return set_error(HQ_ERR_ARG, "bad remap mode %d", mode);
+    st->remap_mode = mode;
+    if (fused_available) *fused_available = st->p2p ? 1 : 0;
     return HQ_OK;
 }
 
@@ -700,7 +865,8 @@ static bool pack_spec(const hq_state *st, const Prep &p, const Op &perm, OutSpec
     return apply_supports_out((int)st->dtype, p.d, o);
 }
 
-static hq_status exec_apply(hq_state *st, Shard &s, const Prep &p, const void *dU, const OutSpec *pack = nullptr) {
+static hq_status exec_apply(hq_state *st, Shard &s, const Prep &p, const void *dU, const OutSpec *pack = nullptr,
+                           bool fused_remap = false) {
     CUDA_TRY(cudaSetDevice(s.device));
     ProfEvent pe{};
     hq_status rc = HQ_OK;
@@ -708,7 +874,7 @@ static hq_status exec_apply(hq_state *st, Shard &s, const Prep &p, const void *d
     OutSpec o;
     if (pack) {
         o = *pack;
-        o.dst[0] = s.buf;
+        if (!fused_remap) o.dst[0] = s.buf;      // apply+pack: this shard's own exchange buffer
     }
     if (p.path == PATH_TC) {
         if ((rc = ensure_bound(st))) return rc;
@@ -729,7 +895,7 @@ static hq_status exec_apply(hq_state *st, Shard &s, const Prep &p, const void *d
         return set_error(HQ_ERR_CUDA, "apply kernel launch failed: %s", cudaGetErrorString((cudaError_t)e));
     const uint64_t bytes = (uint64_t)2 * (st->es << st->nl);
     if ((rc = prof_end(st, s, pe, bytes, p.path))) return rc;
-    if (pack) {
+    if (pack && !fused_remap) {
         std::swap(s.psi, s.buf);
         std::swap(s.own_psi, s.own_buf);
     }
@@ -788,7 +954,7 @@ static void prepare_cond(const hq_state *st, const GateRef &g, const Op &op, int
 }
 
 static hq_status exec_prep(hq_state *st, Shard &s, const Prep &p, const void *dU, const OutSpec *pack = nullptr) {
-    if (!p.scalar) return exec_apply(st, s, p, dU, pack);
+    if (!p.scalar) return exec_apply(st, s, p, dU, pack, false);
     if (p.sre == 1.0 && p.sim == 0.0) return HQ_OK;
     CUDA_TRY(cudaSetDevice(s.device));
     int e = launch_scale_complex((int)st->dtype, s.psi, 1ull << st->nl, p.sre, p.sim, s.stream);
@@ -812,6 +978,7 @@ static hq_status exec_permute(hq_state *st, const Op &op) {
         st->stats.kernel_launches++;
         st->stats.hbm_bytes += (uint64_t)2 * (st->es << st->nl);
     }
+    st->swaps++;
     st->stats.permutes++;
     return HQ_OK;
 }
@@ -904,6 +1071,7 @@ static hq_status exec_remap(hq_state *st, const Op &op) {
         std::swap(s.psi, s.buf);
         std::swap(s.own_psi, s.own_buf);
     }
+    st->swaps++;
     st->stats.remaps++;
     return HQ_OK;
 }
@@ -931,32 +1099,182 @@ static hq_status validate_gates(const hq_state *st, const hq_gate *g, size_t ng,
     return HQ_OK;
 }
 
+// ------------------------------------------------------------------ apply+pack and fused remaps
+// How an APPLY op executes together with the ops after it:
+//   consumed 0: alone, in place;
+//   consumed 1, !fused: the PERMUTE after it folded in (apply+pack);
+//   fused: [PERMUTE +] REMAP folded in (fused remap): the pass writes every
+//   element into its destination rank's exchange buffer, peer memory over
+//   NVLink (the remap's local bits must be the top nin local bits, which the
+//   scheduler's pack guarantees).
+static bool out_supported(const hq_state *st, const Prep &p, const OutSpec &o) {
+    if (p.scalar) return false;
+    if (p.path == PATH_TC) {
+        std::vector<char> tmp = p.params;
+        return tc_set_output(tmp, o);
+    }
+    return apply_supports_out((int)st->dtype, p.d, o);
+}
+
+static Fold plan_fold(const hq_state *st, const Prep &p, const std::vector<Op> &ops, size_t i) {
+    Fold f;
+    size_t j = i + 1;
+    const Op *perm = (j < ops.size() && ops[j].kind == OP_PERMUTE) ? &ops[j] : nullptr;
+    if (perm) ++j;
+    const Op *rem = (j < ops.size() && ops[j].kind == OP_REMAP) ? &ops[j] : nullptr;
+    for (auto &sh : st->sh)
+        if (!sh.buf) return f;
+    if (rem && st->remap_mode == HQ_REMAP_FUSED && st->p2p && rem->nbits >= 1 && rem->nbits <= 3) {
+        bool top = true;
+        for (int t = 0; t < rem->nbits; ++t) top &= rem->bits[2 * t + 1] == st->nl - rem->nbits + t;
+        OutSpec o;
+        o.active = true;
+        if (perm) {
+            o.npairs = perm->nbits;
+            for (int t = 0; t < perm->nbits; ++t) {
+                o.pa[t] = perm->bits[2 * t];
+                o.pb[t] = perm->bits[2 * t + 1];
+                top &= o.pa[t] >= PACK_MIN_BIT && o.pb[t] >= PACK_MIN_BIT;
+            }
+        }
+        o.tsh = st->nl - rem->nbits;
+        o.tmask = (1u << rem->nbits) - 1;
+        for (int t = 0; t < 8; ++t) o.dst[t] = st->sh[0].buf;    // placeholders for the support check
+        if (top && out_supported(st, p, o)) {
+            f.consumed = (perm ? 1 : 0) + 1;
+            f.fused = true;
+            f.with_perm = perm != nullptr;
+            f.rem = rem;
+            f.tmpl = o;
+            return f;
+        }
+    }
+    if (perm && pack_spec(st, p, *perm, f.tmpl)) {
+        f.consumed = 1;
+        f.with_perm = true;
+    }
+    return f;
+}
+
+// the rank whose rank bits gsh[i] equal t's bits i (the others as r's)
+static int remap_peer(const Op &rem, int nl, int r, int t) {
+    int p = r;
+    for (int i = 0; i < rem.nbits; ++i) {
+        const int g = rem.bits[2 * i] - nl;
+        p = (p & ~(1 << g)) | (((t >> i) & 1) << g);
+    }
+    return p;
+}
+
+static int remap_bits(const Op &rem, int nl, int r) {
+    int t = 0;
+    for (int i = 0; i < rem.nbits; ++i) t |= ((r >> (rem.bits[2 * i] - nl)) & 1) << i;
+    return t;
+}
+
+// the current exchange buffer of rank p, as addressable from this process
+static void *peer_buf(const hq_state *st, int p) {
+    if (st->mode != MODE_RANK) return st->sh[p].buf;
+    if (p == st->sh[0].rank) return st->sh[0].buf;
+    return st->peer_base[(st->swaps & 1) ? 0 : 1][p];
+}
+
+// All shards' streams reach this point before any continues (fused remaps
+// write into peers' buffers, which must be free before and complete after).
+static hq_status peer_barrier(hq_state *st) {
+    if (st->mode == MODE_RANK) {
+        Shard &s = st->sh[0];
+        CUDA_TRY(cudaSetDevice(s.device));
+        NCCL_TRY(ncclAllReduce(st->d_bar, st->d_bar, 1, ncclInt, ncclSum, s.comm, s.stream));
+    } else if (st->mode == MODE_MULTI) {
+        for (size_t r = 0; r < st->sh.size(); ++r) {
+            CUDA_TRY(cudaSetDevice(st->sh[r].device));
+            CUDA_TRY(cudaEventRecord(st->bar_ev[r], st->sh[r].stream));
+        }
+        for (size_t r = 0; r < st->sh.size(); ++r) {
+            CUDA_TRY(cudaSetDevice(st->sh[r].device));
+            for (size_t q = 0; q < st->sh.size(); ++q)
+                if (q != r) CUDA_TRY(cudaStreamWaitEvent(st->sh[r].stream, st->bar_ev[q], 0));
+        }
+    }
+    return HQ_OK;        // virtual shards share one stream
+}
+
+// Execute an APPLY with its fold.  get(r) -> (prep, device payload) of shard r.
+template <class Get>
+static hq_status run_apply(hq_state *st, const Fold &f, Get get) {
+    hq_status rc;
+    const size_t G = st->sh.size();
+    if (!f.fused) {
+        for (size_t r = 0; r < G; ++r) {
+            auto pr = get(r);
+            if ((rc = exec_prep(st, st->sh[r], *pr.first, pr.second, f.consumed ? &f.tmpl : nullptr))) return rc;
+        }
+        if (f.consumed) {
+            st->swaps++;
+            st->stats.packs++;
+        }
+        return HQ_OK;
+    }
+    // fused remap: every shard's output map from the peer buffers as they are now
+    std::vector<OutSpec> os(G, f.tmpl);
+    for (size_t r = 0; r < G; ++r) {
+        const int rank = st->sh[r].rank;
+        os[r].add = (uint64_t)remap_bits(*f.rem, st->nl, rank) << os[r].tsh;
+        for (int t = 0; t < (1 << f.rem->nbits); ++t) os[r].dst[t] = peer_buf(st, remap_peer(*f.rem, st->nl, rank, t));
+    }
+    if ((rc = peer_barrier(st))) return rc;
+    for (size_t r = 0; r < G; ++r) {
+        auto pr = get(r);
+        if ((rc = exec_apply(st, st->sh[r], *pr.first, pr.second, &os[r], true))) return rc;
+    }
+    if ((rc = peer_barrier(st))) return rc;
+    for (auto &s : st->sh) {
+        std::swap(s.psi, s.buf);
+        std::swap(s.own_psi, s.own_buf);
+    }
+    st->swaps++;
+    st->stats.remaps++;
+    st->stats.remaps_fused++;
+    if (f.with_perm) st->stats.packs++;
+    const uint64_t chunk = (st->es << st->nl) >> f.rem->nbits;
+    st->stats.link_bytes += (uint64_t)G * (((uint64_t)1 << f.rem->nbits) - 1) * chunk;
+    return HQ_OK;
+}
+
 // Run an op stream with matrices either host-side (converted on the fly and
 // staged through the arena) or precompiled (circuit).
 static hq_status run_ops(hq_state *st, const std::vector<GateRef> &refs, const std::vector<Op> &ops) {
     Prep p;
+    std::vector<void *> dUs(st->sh.size());
     for (size_t i = 0; i < ops.size(); ++i) {
         const Op &op = ops[i];
         hq_status rc = HQ_OK;
         if (op.kind == OP_APPLY) {
             const GateRef &g = refs[op.gate];
-            const bool cond = op_conditioned(st, op);
-            if (!cond) prepare(st->dtype, g.U, g.k, op.bits, st->nl, p);
-            OutSpec pk;
-            const bool fold = !cond && i + 1 < ops.size() && pack_spec(st, p, ops[i + 1], pk);
+            if (op_conditioned(st, op)) {
+                for (size_t r = 0; r < st->sh.size(); ++r) {
+                    Shard &s = st->sh[r];
+                    prepare_cond(st, g, op, s.rank, p);
+                    void *dU = nullptr;
+                    if (!p.payload.empty() && (rc = arena_push(st, s, p.payload.data(), p.payload.size(), &dU)))
+                        return rc;
+                    if ((rc = exec_prep(st, s, p, dU))) return rc;
+                }
+                if (st->amp_bound >= 0) st->amp_bound *= spectral_bound(g.U, g.k);
+                continue;
+            }
+            prepare(st->dtype, g.U, g.k, op.bits, st->nl, p);
+            const Fold f = plan_fold(st, p, ops, i);
             for (size_t r = 0; r < st->sh.size(); ++r) {
-                Shard &s = st->sh[r];
-                if (cond) prepare_cond(st, g, op, s.rank, p);
-                void *dU = nullptr;
-                if (!p.payload.empty() && (rc = arena_push(st, s, p.payload.data(), p.payload.size(), &dU)))
+                dUs[r] = nullptr;
+                if (!p.payload.empty() && (rc = arena_push(st, st->sh[r], p.payload.data(), p.payload.size(), &dUs[r])))
                     return rc;
-                if ((rc = exec_prep(st, s, p, dU, fold ? &pk : nullptr))) return rc;
             }
-            if (fold) {
-                st->stats.packs++;
-                ++i;                       // the PERMUTE is done
-            }
-            if (st->amp_bound >= 0) st->amp_bound *= cond ? spectral_bound(g.U, g.k) : p.gnorm;
+            if ((rc = run_apply(st, f, [&](size_t r) { return std::make_pair((const Prep *)&p, (const void *)dUs[r]); })))
+                return rc;
+            i += f.consumed;
+            if (st->amp_bound >= 0) st->amp_bound *= p.gnorm;
         } else if (op.kind == OP_REMAP) {
             rc = exec_remap(st, op);
         } else {
@@ -1004,12 +1322,18 @@ static hq_status circuit_compile(hq_state *st, hq_circuit *c, const std::vector<
     c->cprep.assign(c->ops.size(), {});
     c->cuoff.assign(c->ops.size(), {});
     c->cgnorm.assign(c->ops.size(), 1.0);
-    c->pack.assign(c->ops.size(), OutSpec{});
+    c->fold.assign(c->ops.size(), Fold{});
     size_t total = 0;
     c->passes = c->remaps = c->permutes = c->packs = 0;
     for (size_t i = 0; i < c->ops.size(); ++i) {
         const Op &op = c->ops[i];
-        if (op.kind == OP_PERMUTE && i > 0 && c->pack[i - 1].active) continue;    // folded (apply+pack)
+        bool folded = false;          // consumed by an earlier APPLY's fold
+        for (size_t b = 1; b <= 2 && b <= i && !folded; ++b)
+            folded = c->ops[i - b].kind == OP_APPLY && (size_t)c->fold[i - b].consumed >= b;
+        if (folded) {
+            if (op.kind == OP_REMAP) c->remaps++;
+            continue;
+        }
         if (op.kind == OP_APPLY) {
             const GateRef &g = refs[op.gate];
             if (op_conditioned(st, op)) {
@@ -1032,8 +1356,9 @@ static hq_status circuit_compile(hq_state *st, hq_circuit *c, const std::vector<
                 c->op_uoff[i] = (long long)total;
                 total += (c->prep[i].payload.size() + 255) & ~(size_t)255;
             }
-            if (i + 1 < c->ops.size() && pack_spec(st, c->prep[i], c->ops[i + 1], c->pack[i])) c->packs++;
-            else c->pack[i] = OutSpec{};
+            c->fold[i] = plan_fold(st, c->prep[i], c->ops, i);
+            if (c->fold[i].fused) c->fold[i].rem = nullptr;     // re-pointed at run time (ops may move)
+            if (c->fold[i].with_perm) c->packs++;
             c->passes++;
         } else if (op.kind == OP_REMAP) {
             c->remaps++;
@@ -1125,18 +1450,17 @@ static hq_status circuit_run_ops(hq_state *st, hq_circuit *c) {
         hq_status rc = HQ_OK;
         if (op.kind == OP_APPLY) {
             const bool cond = !c->cprep[i].empty();
-            const OutSpec *pk = c->pack[i].active ? &c->pack[i] : nullptr;
-            for (size_t r = 0; r < st->sh.size(); ++r) {
+            auto get = [&](size_t r) {
                 const char *base = c->dev_U[st->mode == MODE_VIRTUAL ? 0 : r];
                 const long long off = cond ? c->cuoff[i][r] : c->op_uoff[i];
                 const void *dU = (base && off >= 0) ? base + off : nullptr;
-                if ((rc = exec_prep(st, st->sh[r], cond ? c->cprep[i][r] : c->prep[i], dU, pk))) return rc;
-            }
-            if (pk) {
-                st->stats.packs++;
-                ++i;                       // the folded PERMUTE
-            }
+                return std::make_pair((const Prep *)(cond ? &c->cprep[i][r] : &c->prep[i]), dU);
+            };
+            Fold f = c->fold[i];
+            if (f.fused) f.rem = &c->ops[i + f.consumed];
+            if ((rc = run_apply(st, f, get))) return rc;
             if (st->amp_bound >= 0) st->amp_bound *= cond ? c->cgnorm[i] : c->prep[i].gnorm;
+            i += f.consumed;
         } else if (op.kind == OP_REMAP) {
             rc = exec_remap(st, op);
         } else {

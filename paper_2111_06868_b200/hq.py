@@ -46,7 +46,8 @@ class hq_stats(ctypes.Structure):
     _fields_ = [("passes", ctypes.c_uint64), ("remaps", ctypes.c_uint64),
                 ("permutes", ctypes.c_uint64), ("kernel_launches", ctypes.c_uint64),
                 ("hbm_bytes", ctypes.c_uint64), ("link_bytes", ctypes.c_uint64),
-                ("h2d_bytes", ctypes.c_uint64), ("d2h_bytes", ctypes.c_uint64), ("packs", ctypes.c_uint64)]
+                ("h2d_bytes", ctypes.c_uint64), ("d2h_bytes", ctypes.c_uint64), ("packs", ctypes.c_uint64),
+                ("remaps_fused", ctypes.c_uint64)]
 
 
 _lib = None
@@ -96,6 +97,7 @@ def lib():
                                ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)],
             "hq_state_set_layout": [P, P],
             "hq_state_invalidate_bound": [P],
+            "hq_state_set_remap_mode": [P, ctypes.c_int, ctypes.POINTER(ctypes.c_int)],
             "hq_state_init_tokens": [P, ctypes.c_char_p],
             "hq_dm_superop": [P, ctypes.c_int, ctypes.c_int, P],
             "hq_dm_apply_unitary": [P, P, P, ctypes.c_int],
@@ -511,6 +513,18 @@ def hq_plan_layout(n, m, gates, dtype="c64"):
 def hq_state_set_layout(state, pi):
     v = np.ascontiguousarray(pi, dtype=np.int32)
     _check(lib().hq_state_set_layout(state.ptr, v.ctypes.data))
+
+
+REMAP_MODES = {"exchange": 0, "fused": 1}
+
+
+def hq_state_set_remap_mode(state, mode="fused"):
+    """'fused' (default): remaps folded into the preceding apply pass when
+    possible; 'exchange': always a separate exchange.  Returns whether peer
+    buffers are mapped (fused remaps possible)."""
+    avail = ctypes.c_int()
+    _check(lib().hq_state_set_remap_mode(state.ptr, REMAP_MODES[mode], ctypes.byref(avail)))
+    return bool(avail.value)
 
 
 def hq_state_invalidate_bound(state):

@@ -106,3 +106,55 @@ def test_pack_single_pass_every_tc_mode():
         want = O.simulate(n, gates, psi0)
         err = np.linalg.norm(hq.hq_get_amplitudes(s).astype(np.complex128) - want)
         assert err < 4e-6, (placement, err)
+
+
+# ---------------------------------------------------------------- fused remaps
+@pytest.mark.parametrize("kmax", [4, 6])
+@pytest.mark.parametrize("G", [2, 4, 8])
+@pytest.mark.parametrize("compiled", [False, True])
+def test_fused_remap_vs_exchange_and_oracle(kmax, G, compiled):
+    """Fused remaps (the apply pass writes each element into its destination
+    shard's exchange buffer) give bit-identical amplitudes to the separate
+    exchange path (same kernels, only the output addresses differ) and match
+    the oracle; on virtual shards every packed remap fuses."""
+    n = 20
+    gates = sycamore_circuit(n, 14, 78)
+    fused = hq.hq_fuse(gates, kmax, merged=True)
+    m = G.bit_length() - 1
+    out = {}
+    for mode in ("exchange", "fused"):
+        s = hq.hq_state_create_virtual(n, "c64", G)
+        assert hq.hq_state_set_remap_mode(s, mode)            # virtual shards: always mappable
+        pi0, _, _ = hq.hq_plan_layout(n, m, fused)
+        hq.hq_state_set_layout(s, pi0)
+        hq.hq_state_init_basis(s, 0)
+        hq.hq_stats_reset(s)
+        if compiled:
+            hq.hq_circuit_run(s, hq.hq_circuit_create(s, fused))
+        else:
+            hq.hq_apply_circuit(s, fused)
+        out[mode] = (hq.hq_get_amplitudes(s), hq.hq_stats_get(s))
+    a_x, st_x = out["exchange"]
+    a_f, st_f = out["fused"]
+    assert st_x["remaps_fused"] == 0 and st_f["remaps"] == st_x["remaps"] > 0
+    assert st_f["remaps_fused"] > 0, st_f
+    assert np.array_equal(a_x, a_f)
+    err = np.linalg.norm(a_f.astype(np.complex128) - O.simulate(n, gates))
+    assert err <= 1e-4, err
+
+
+@pytest.mark.parametrize("G", [4, 8])
+def test_fused_remap_reversible_bit_exact(G):
+    n = 20
+    gates = reversible_circuit(n, 150, 37, kmax=3)
+    fused = hq.hq_fuse(gates, 6)
+    m = G.bit_length() - 1
+    s = hq.hq_state_create_virtual(n, "c64", G)
+    hq.hq_state_set_remap_mode(s, "fused")
+    hq.hq_state_set_layout(s, hq.hq_plan_layout(n, m, fused)[0])
+    x = 0x5C3A7
+    hq.hq_state_init_basis(s, x)
+    hq.hq_apply_circuit(s, fused)
+    y = O.reversible_image(n, gates, x)
+    got = hq.hq_get_amplitudes(s)
+    assert got[y] == 1.0 and np.count_nonzero(got) == 1
