@@ -396,8 +396,13 @@ void schedule(int n, int m, const std::vector<GateRef> &g, std::vector<int> &pi,
                 ev[t] = std::get<2>(cand[t]);
                 in_window &= ev[t] >= nl - RUNWIN;
             }
+            // after an apply the pack is free (folded into that pass), and
+            // evictees on exactly the top bits let the executor fuse the whole
+            // exchange into the pass (one contiguous chunk per peer); with no
+            // apply before, evictees already in the top RUNWIN bits are used
+            // where they are (a few long runs per peer, no permute pass)
             int lb[6];
-            if (in_window) {
+            if (in_window && !after_apply) {
                 for (int t = 0; t < nin; ++t) lb[t] = ev[t];
             } else {
                 // pack: the evictees onto the top nin local bits
