@@ -95,6 +95,7 @@ typedef struct hq_stats {
     uint64_t d2h_bytes;       /* device->host bytes the library copied (this rank) */
     uint64_t packs;           /* PERMUTEs folded into an apply pass (apply+pack)   */
     uint64_t remaps_fused;    /* remaps done inside the preceding apply pass       */
+    uint64_t gathers;         /* gates applied across a rank pair (GATHER ops)     */
 } hq_stats;
 
 /* ------------------------------------------------------------------ create */
@@ -293,6 +294,13 @@ hq_status hq_kraus_sample(hq_state *s, const double *const *K, int nkraus, const
  * per-shot matrix).  HQ_ERR_RANGE if some shot has every p_i ~ 0 (state
  * unchanged).  Synchronises. */
 hq_status hq_reduced_dm_batched(hq_state *s, int nb, const int32_t *qubits, int k, double *rho_out);
+/* Sum over the first nlive shots of each shot's reduced density matrix
+ * normalised to unit trace: rho_sum = sum_s rho_s / Tr(rho_s) (2*4^k doubles),
+ * the trajectory average's numerator.  Same
+ * read pass as hq_reduced_dm_batched.  HQ_ERR_RANGE if a live shot has zero
+ * trace.  Synchronises. */
+hq_status hq_reduced_dm_batched_sum(hq_state *s, int nb, const int32_t *qubits, int k, int nlive,
+                                    double *rho_sum);
 hq_status hq_kraus_sample_batched(hq_state *s, int nb, const double *const *K, int nkraus,
                                   const int32_t *qubits, int k, const double *u, int32_t *chosen_out,
                                   double *probs_out);
@@ -395,7 +403,12 @@ hq_status hq_fuse_plan(const hq_gate *in, size_t ngates, int kmax, int32_t *grou
  *                   r applies the block its rank bits select;
  *   kind 1 REMAP  : swap global bit bits[2i] with local bit bits[2i+1],
  *                   i < nbits (all-to-all among 2^nbits ranks);
- *   kind 2 PERMUTE: local bit swap bits[2i] <-> bits[2i+1], i < nbits.
+ *   kind 2 PERMUTE: local bit swap bits[2i] <-> bits[2i+1], i < nbits;
+ *   kind 3 GATHER : gate `gate` with bits as for APPLY, exactly one of them
+ *                   global and not block-diagonal: the rank pair that differs
+ *                   in it computes the gate over peer memory (row f1), no
+ *                   remap; only with flags & HQ_SCHED_GATHER (the executor
+ *                   asks for it when peer buffers are mapped).
  * pi_out (n entries, may be NULL) receives the final logical->physical map. */
 typedef struct hq_op {
     int32_t kind;
@@ -406,9 +419,11 @@ typedef struct hq_op {
 hq_status hq_schedule(int n, int m, const hq_gate *gates, size_t ngates,
                       hq_op **ops, size_t *nops, int32_t *pi_out);
 /* The same from a given initial layout pi_in (n entries, a permutation; e.g.
- * hq_plan_layout's), as a state with that layout would execute it. */
+ * hq_plan_layout's; NULL = default), as a state with that layout would execute
+ * it; flags: HQ_SCHED_GATHER allows GATHER ops for isolated global accesses. */
+#define HQ_SCHED_GATHER 1
 hq_status hq_schedule_from(int n, int m, const hq_gate *gates, size_t ngates, const int32_t *pi_in,
-                           hq_op **ops, size_t *nops, int32_t *pi_out);
+                           int flags, hq_op **ops, size_t *nops, int32_t *pi_out);
 hq_status hq_free_ops(hq_op *ops);
 
 /* Layout planner (the GPU counterpart of the paper's "qubits are swapped to

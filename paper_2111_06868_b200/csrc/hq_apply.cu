@@ -331,6 +331,92 @@ apply_gen_warp(typename C2<R>::T *__restrict__ psi, const __grid_constant__ GenP
     }
 }
 
+// ------------------------------------------------------------------ pair gather (row f1)
+// One thread per local gather set of the k-1 local targets: reads the
+// 2^(k-1) amplitudes of the set from this rank and from its partner (peer
+// memory over NVLink), forms the full 2^k input (canonical bit k-1 = the
+// global target: this rank holds half `half`), and writes the 2^(k-1)
+// outputs of its own half into dst.  NVLink-bound (one partner shard read per
+// pass); used only for isolated global accesses.
+template <typename R, int K>
+__global__ void __launch_bounds__(128)
+apply_pair_gather(const typename C2<R>::T *__restrict__ me, const typename C2<R>::T *__restrict__ peer,
+                  typename C2<R>::T *__restrict__ dst, const __grid_constant__ GenParams P, int half,
+                  const typename C2<R>::T *__restrict__ Ud) {
+    using V = typename C2<R>::T;
+    constexpr int D = 1 << K, H = D / 2;
+    for (uint64_t o = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; o < P.nsets;
+         o += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t base = o;
+#pragma unroll
+        for (int j = 0; j < K - 1; ++j) base = insert_zero(base, P.s[j]);
+        V v[D];
+#pragma unroll
+        for (int c = 0; c < H; ++c) {
+            v[c | (half * H)] = me[base + P.off[c]];
+            v[c | ((1 - half) * H)] = peer[base + P.off[c]];
+        }
+        for (int r = 0; r < H; ++r) {
+            const int row = r | (half * H);
+            R ar = 0, ai = 0;
+#pragma unroll
+            for (int c = 0; c < D; ++c) {
+                const V u = __ldg(&Ud[row * D + c]);
+                ar = fma(u.x, v[c].x, ar);
+                ar = fma(-u.y, v[c].y, ar);
+                ai = fma(u.x, v[c].y, ai);
+                ai = fma(u.y, v[c].x, ai);
+            }
+            V w;
+            w.x = ar;
+            w.y = ai;
+            HQ_CHECK_IDX(base + P.off[r], P.nsets << (K - 1), 15);
+            dst[base + P.off[r]] = w;
+        }
+    }
+}
+
+template <typename R>
+static cudaError_t launch_pg(const void *me, const void *peer, void *dst, const GenParams &P, int K, int half,
+                             const void *dU, cudaStream_t st) {
+    using V = typename C2<R>::T;
+    uint64_t blocks = (P.nsets + 127) / 128;
+    if (blocks > 148ull * 64) blocks = 148ull * 64;
+    if (blocks == 0) blocks = 1;
+    const V *a = reinterpret_cast<const V *>(me), *b = reinterpret_cast<const V *>(peer);
+    V *o = reinterpret_cast<V *>(dst);
+    const V *u = reinterpret_cast<const V *>(dU);
+    switch (K) {
+        case 1: apply_pair_gather<R, 1><<<(unsigned)blocks, 128, 0, st>>>(a, b, o, P, half, u); break;
+        case 2: apply_pair_gather<R, 2><<<(unsigned)blocks, 128, 0, st>>>(a, b, o, P, half, u); break;
+        case 3: apply_pair_gather<R, 3><<<(unsigned)blocks, 128, 0, st>>>(a, b, o, P, half, u); break;
+        case 4: apply_pair_gather<R, 4><<<(unsigned)blocks, 128, 0, st>>>(a, b, o, P, half, u); break;
+        case 5: apply_pair_gather<R, 5><<<(unsigned)blocks, 128, 0, st>>>(a, b, o, P, half, u); break;
+        case 6: apply_pair_gather<R, 6><<<(unsigned)blocks, 128, 0, st>>>(a, b, o, P, half, u); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+int launch_pair_gather(int dtype, const void *psi_me, const void *psi_peer, void *dst, const ApplyDesc &d,
+                       int half, const void *dev_U, void *stream) {
+    // d.k = number of targets including the global one; d.p[0..k-2] local (ascending)
+    GenParams gp{};
+    const int kl = d.k - 1;
+    for (int c = 0; c < (1 << kl); ++c) {
+        uint64_t o = 0;
+        for (int i = 0; i < kl; ++i)
+            if ((c >> i) & 1) o |= 1ull << d.p[i];
+        gp.off[c] = o;
+    }
+    for (int i = 0; i < kl; ++i) gp.s[i] = d.p[i];
+    gp.nsets = 1ull << (d.n_local - kl);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const cudaError_t e = dtype == HQ_C64 ? launch_pg<float>(psi_me, psi_peer, dst, gp, d.k, half, dev_U, st)
+                                          : launch_pg<double>(psi_me, psi_peer, dst, gp, d.k, half, dev_U, st);
+    return (int)e;
+}
+
 // ------------------------------------------------------------------ dispatch
 
 namespace {

@@ -54,7 +54,7 @@ struct FusedGate {
 void fuse_build(const std::vector<GateRef> &g, int kmax, std::vector<FusedGate> &out, bool merge = false);
 
 // Distributed schedule (hq_schedule semantics).  pi: logical->physical, in/out.
-enum OpKind { OP_APPLY = 0, OP_REMAP = 1, OP_PERMUTE = 2 };
+enum OpKind { OP_APPLY = 0, OP_REMAP = 1, OP_PERMUTE = 2, OP_GATHER = 3 };
 struct Op {
     int kind;
     int gate;
@@ -64,11 +64,17 @@ struct Op {
 // APPLY ops may carry global target bits (>= n - m): the scheduler emits them
 // only for gates block-diagonal in those targets (block_diag_in), and rank r
 // applies the block selected by its rank bits to the local targets (row f1).
+// gather = true: a gate that needs exactly one global qubit local, which no
+// gate in the lookahead window needs again, runs as OP_GATHER (pair gather
+// over peer memory, no remap) instead of triggering a remap.
 void schedule(int n, int m, const std::vector<GateRef> &g, std::vector<int> &pi,
-              std::vector<Op> &ops);
+              std::vector<Op> &ops, bool gather = false);
 // Lowest physical bit a scheduler PERMUTE (pack) may move: bits 0 and 1 stay in
 // place so that every apply+pack write still fills whole 32-byte sectors.
 constexpr int PACK_MIN_BIT = 2;
+// OP_GATHER only when the global qubit's next local need is further than this
+// many gates away (or never): then bringing it in by a remap would buy nothing
+constexpr int GATHER_LOOKAHEAD = 32;
 bool block_diag_in(const double *U, int k, int umask);
 uint64_t local_need(const GateRef &gt);
 
@@ -135,6 +141,14 @@ struct KernelStatus {
 // as int.  stream is a cudaStream_t.
 int launch_apply(int dtype, void *psi, const ApplyDesc &d, const void *host_U,
                  const void *dev_U, void *stream, int *launches, const OutSpec *out = nullptr);
+// Pair gather (OP_GATHER, row f1): a gate whose canonical target k-1 is a
+// global (rank) bit, applied on the rank pair that differs in it.  Each rank
+// reads its own shard and its partner's (peer memory) and writes its half of
+// the outputs, rows with canonical bit k-1 = half, into dst (out of place).
+// d: the k-1 local targets (canonical, ascending); dev_U: canonical D x D.
+int launch_pair_gather(int dtype, const void *psi_me, const void *psi_peer, void *dst, const ApplyDesc &d,
+                       int half, const void *dev_U, void *stream);
+
 // Whether launch_apply can write this pass out of place through an OutSpec
 // (every kernel but the complex128 k = 5, 6 tile kernel).
 bool apply_supports_out(int dtype, const ApplyDesc &d, const OutSpec &o);

@@ -311,7 +311,7 @@ uint64_t local_need(const GateRef &gt) {
 // out-of-place write (apply+pack: no extra HBM pass), so every peer's data is
 // one contiguous chunk (or a few long runs).
 void schedule(int n, int m, const std::vector<GateRef> &g, std::vector<int> &pi,
-              std::vector<Op> &ops) {
+              std::vector<Op> &ops, bool gather) {
     const int nl = n - m;
     if ((int)pi.size() != n) {
         pi.resize(n);
@@ -347,6 +347,20 @@ void schedule(int n, int m, const std::vector<GateRef> &g, std::vector<int> &pi,
     const int RUNWIN = std::min(nl, 7);
     for (size_t i = 0; i < N; ++i) {
         const GateRef &gt = g[i];
+        if (gather && m > 0 && __builtin_popcountll(need[i] & globals()) == 1) {
+            // an isolated global access (row f1): the one global qubit this
+            // gate needs is not needed local again within the lookahead, so
+            // the rank pair that differs in it computes the gate over peer
+            // memory (OP_GATHER) and the global set stays
+            const int gq = __builtin_ctzll(need[i] & globals());
+            const size_t nu = next_use(gq, i + 1);
+            if (nu == std::numeric_limits<size_t>::max() || nu > i + (size_t)GATHER_LOOKAHEAD) {
+                Op ga{OP_GATHER, (int)i, gt.k, {0}};
+                for (int jj = 0; jj < gt.k; ++jj) ga.bits[jj] = pi[gt.q[jj]];
+                ops.push_back(ga);
+                continue;
+            }
+        }
         if (m > 0 && (need[i] & globals())) {
             // the segment starting at gate i; it also ends early when the
             // incoming globals would outnumber the local qubits outside it
@@ -658,11 +672,11 @@ extern "C" hq_status hq_free_gates(hq_gate *gates, size_t ngates) {
 
 extern "C" hq_status hq_schedule(int n, int m, const hq_gate *gates, size_t ngates, hq_op **ops,
                                  size_t *nops, int32_t *pi_out) {
-    return hq_schedule_from(n, m, gates, ngates, nullptr, ops, nops, pi_out);
+    return hq_schedule_from(n, m, gates, ngates, nullptr, 0, ops, nops, pi_out);
 }
 
 extern "C" hq_status hq_schedule_from(int n, int m, const hq_gate *gates, size_t ngates, const int32_t *pi_in,
-                                      hq_op **ops, size_t *nops, int32_t *pi_out) {
+                                      int flags, hq_op **ops, size_t *nops, int32_t *pi_out) {
     clear_error();
     if ((!gates && ngates) || !ops || !nops) return set_error(HQ_ERR_ARG, "NULL argument");
     if (n < 1 || n > 63 || m < 0 || m > 16) return set_error(HQ_ERR_ARG, "bad n=%d / m=%d", n, m);
@@ -680,7 +694,7 @@ extern "C" hq_status hq_schedule_from(int n, int m, const hq_gate *gates, size_t
             if (pi[q] < 0 || pi[q] >= n || seen[pi[q]]++) return set_error(HQ_ERR_ARG, "pi_in is not a permutation");
     }
     std::vector<Op> v;
-    schedule(n, m, refs, pi, v);
+    schedule(n, m, refs, pi, v, (flags & HQ_SCHED_GATHER) != 0);
     hq_op *arr = new (std::nothrow) hq_op[v.size() ? v.size() : 1];
     if (!arr) return set_error(HQ_ERR_OOM, "host allocation failed");
     for (size_t i = 0; i < v.size(); ++i) {

@@ -165,7 +165,7 @@ struct hq_circuit {
     int small_nops = 0;
     int small_dev = 0;
     std::vector<int> dev_of;               // per shard: its device (destroy must not read the state)
-    uint64_t passes = 0, remaps = 0, permutes = 0, packs = 0;
+    uint64_t passes = 0, remaps = 0, permutes = 0, packs = 0, gathers = 0;
     // CUDA graph of the whole op stream (single-shard states, profiling off):
     // captured on the first run, replayed while the capture key matches.
     cudaGraphExec_t graph = nullptr;
@@ -1181,6 +1181,17 @@ static void *peer_buf(const hq_state *st, int p) {
 
 // All shards' streams reach this point before any continues (fused remaps
 // write into peers' buffers, which must be free before and complete after).
+// the current state buffer of rank p, as addressable from this process
+static const void *peer_psi(const hq_state *st, int p) {
+    if (st->mode != MODE_RANK) return st->sh[p].psi;
+    if (p == st->sh[0].rank) return st->sh[0].psi;
+    return st->peer_base[(st->swaps & 1) ? 1 : 0][p];
+}
+
+static bool use_gather(const hq_state *st) {
+    return st->m > 0 && st->p2p && st->remap_mode == HQ_REMAP_FUSED;
+}
+
 static hq_status peer_barrier(hq_state *st) {
     if (st->mode == MODE_RANK) {
         Shard &s = st->sh[0];
@@ -1242,6 +1253,55 @@ static hq_status run_apply(hq_state *st, const Fold &f, Get get) {
     return HQ_OK;
 }
 
+// OP_GATHER (row f1): the gate's one global target stays global; the rank
+// pair that differs in it computes the gate over peer memory, each writing
+// its half into its exchange buffer (out of place: the partner reads this
+// rank's state during the pass), between two barriers.
+static void prepare_gather(hq_dtype dt, const double *U, int k, const int *phys, int nl, Prep &p) {
+    std::vector<double> Uc;
+    canonical_U64(U, k, phys, p.d, Uc, nl);     // the global bit sorts last: canonical bit k-1
+    p.gnorm = spectral_bound(Uc.data(), k);
+    const int D = 1 << k;
+    const size_t es = dt == HQ_C64 ? 8 : 16;
+    p.hostU.resize(es * D * D);
+    for (size_t i = 0; i < (size_t)2 * D * D; ++i) {
+        if (dt == HQ_C64) reinterpret_cast<float *>(p.hostU.data())[i] = (float)Uc[i];
+        else reinterpret_cast<double *>(p.hostU.data())[i] = Uc[i];
+    }
+    p.payload = p.hostU;
+    p.params.clear();
+    p.path = PATH_GEN;
+    p.scalar = false;
+}
+
+template <class GetU>
+static hq_status exec_gather(hq_state *st, const Prep &p, GetU dU_of) {
+    hq_status rc;
+    const int gsh = p.d.p[p.d.k - 1] - st->nl;
+    if (gsh < 0 || gsh >= st->m) return set_error(HQ_ERR_STATE, "internal: gather without a global target");
+    if ((rc = peer_barrier(st))) return rc;
+    for (size_t r = 0; r < st->sh.size(); ++r) {
+        Shard &s = st->sh[r];
+        CUDA_TRY(cudaSetDevice(s.device));
+        const int half = (s.rank >> gsh) & 1, partner = s.rank ^ (1 << gsh);
+        int e = launch_pair_gather((int)st->dtype, s.psi, peer_psi(st, partner), s.buf, p.d, half, dU_of(r), s.stream);
+        if (e) return set_error(HQ_ERR_CUDA, "pair gather launch: %s", cudaGetErrorString((cudaError_t)e));
+        st->stats.kernel_launches++;
+        st->stats.hbm_bytes += (uint64_t)2 * (st->es << st->nl);
+        st->stats.link_bytes += st->es << st->nl;
+    }
+    if ((rc = peer_barrier(st))) return rc;
+    for (auto &s : st->sh) {
+        std::swap(s.psi, s.buf);
+        std::swap(s.own_psi, s.own_buf);
+    }
+    st->swaps++;
+    st->stats.passes++;
+    st->stats.gathers++;
+    if (st->amp_bound >= 0) st->amp_bound *= p.gnorm;
+    return HQ_OK;
+}
+
 // Run an op stream with matrices either host-side (converted on the fly and
 // staged through the arena) or precompiled (circuit).
 static hq_status run_ops(hq_state *st, const std::vector<GateRef> &refs, const std::vector<Op> &ops) {
@@ -1275,6 +1335,14 @@ static hq_status run_ops(hq_state *st, const std::vector<GateRef> &refs, const s
                 return rc;
             i += f.consumed;
             if (st->amp_bound >= 0) st->amp_bound *= p.gnorm;
+        } else if (op.kind == OP_GATHER) {
+            const GateRef &g = refs[op.gate];
+            prepare_gather(st->dtype, g.U, g.k, op.bits, st->nl, p);
+            for (size_t r = 0; r < st->sh.size(); ++r) {
+                dUs[r] = nullptr;
+                if ((rc = arena_push(st, st->sh[r], p.payload.data(), p.payload.size(), &dUs[r]))) return rc;
+            }
+            rc = exec_gather(st, p, [&](size_t r) { return (const void *)dUs[r]; });
         } else if (op.kind == OP_REMAP) {
             rc = exec_remap(st, op);
         } else {
@@ -1304,7 +1372,7 @@ extern "C" hq_status hq_apply_circuit(hq_state *st, const hq_gate *gates, size_t
     if (rc) return rc;
     std::vector<Op> ops;
     std::vector<int> pi = st->pi;
-    schedule(st->n, st->m, refs, pi, ops);
+    schedule(st->n, st->m, refs, pi, ops, use_gather(st));
     rc = run_ops(st, refs, ops);
     if (rc) return rc;
     st->pi = pi;
@@ -1316,7 +1384,7 @@ extern "C" hq_status hq_apply_circuit(hq_state *st, const hq_gate *gates, size_t
 static hq_status circuit_compile(hq_state *st, hq_circuit *c, const std::vector<GateRef> &refs) {
     c->pi_start = st->pi;
     c->pi_end = st->pi;
-    schedule(st->n, st->m, refs, c->pi_end, c->ops);
+    schedule(st->n, st->m, refs, c->pi_end, c->ops, use_gather(st));
     c->prep.assign(c->ops.size(), Prep{});
     c->op_uoff.assign(c->ops.size(), -1);
     c->cprep.assign(c->ops.size(), {});
@@ -1324,7 +1392,7 @@ static hq_status circuit_compile(hq_state *st, hq_circuit *c, const std::vector<
     c->cgnorm.assign(c->ops.size(), 1.0);
     c->fold.assign(c->ops.size(), Fold{});
     size_t total = 0;
-    c->passes = c->remaps = c->permutes = c->packs = 0;
+    c->passes = c->remaps = c->permutes = c->packs = c->gathers = 0;
     for (size_t i = 0; i < c->ops.size(); ++i) {
         const Op &op = c->ops[i];
         bool folded = false;          // consumed by an earlier APPLY's fold
@@ -1360,6 +1428,13 @@ static hq_status circuit_compile(hq_state *st, hq_circuit *c, const std::vector<
             if (c->fold[i].fused) c->fold[i].rem = nullptr;     // re-pointed at run time (ops may move)
             if (c->fold[i].with_perm) c->packs++;
             c->passes++;
+        } else if (op.kind == OP_GATHER) {
+            const GateRef &g = refs[op.gate];
+            prepare_gather(st->dtype, g.U, g.k, op.bits, st->nl, c->prep[i]);
+            c->op_uoff[i] = (long long)total;
+            total += (c->prep[i].payload.size() + 255) & ~(size_t)255;
+            c->passes++;
+            c->gathers++;
         } else if (op.kind == OP_REMAP) {
             c->remaps++;
         } else {
@@ -1461,6 +1536,11 @@ static hq_status circuit_run_ops(hq_state *st, hq_circuit *c) {
             if ((rc = run_apply(st, f, get))) return rc;
             if (st->amp_bound >= 0) st->amp_bound *= cond ? c->cgnorm[i] : c->prep[i].gnorm;
             i += f.consumed;
+        } else if (op.kind == OP_GATHER) {
+            rc = exec_gather(st, c->prep[i], [&](size_t r) {
+                const char *base = c->dev_U[st->mode == MODE_VIRTUAL ? 0 : r];
+                return (const void *)(base + c->op_uoff[i]);
+            });
         } else if (op.kind == OP_REMAP) {
             rc = exec_remap(st, op);
         } else {
@@ -2153,6 +2233,28 @@ extern "C" hq_status hq_reduced_dm_batched(hq_state *st, int nb, const int32_t *
                 rho[2 * (b * D + a) + 1] = -acc[2 * q + 1];
             }
     }
+    return HQ_OK;
+}
+
+extern "C" hq_status hq_reduced_dm_batched_sum(hq_state *st, int nb, const int32_t *qubits, int k, int nlive,
+                                               double *rho_sum) {
+    clear_error();
+    if (!st || !rho_sum) return set_error(HQ_ERR_ARG, "NULL argument");
+    if (nb < 0 || nb > 16 || nlive < 0 || nlive > (1 << nb)) return set_error(HQ_ERR_ARG, "nlive=%d not in [0, 2^nb]", nlive);
+    if (k < 1 || k > 3) return set_error(HQ_ERR_K, "k=%d not in [1,3]", k);
+    const int D = 1 << k;
+    std::vector<double> rho((size_t)(1 << nb) * 2 * D * D);
+    hq_status rc = hq_reduced_dm_batched(st, nb, qubits, k, rho.data());
+    if (rc) return rc;
+    std::vector<double> acc((size_t)2 * D * D, 0.0);
+    for (int sh = 0; sh < nlive; ++sh) {
+        const double *r = rho.data() + (size_t)sh * 2 * D * D;
+        double tr = 0.0;
+        for (int a = 0; a < D; ++a) tr += r[2 * (a * D + a)];
+        if (!(tr > 0.0)) return set_error(HQ_ERR_RANGE, "shot %d: reduced density matrix has zero trace", sh);
+        for (int i = 0; i < 2 * D * D; ++i) acc[i] += r[i] / tr;
+    }
+    for (int i = 0; i < 2 * D * D; ++i) rho_sum[i] = acc[i];
     return HQ_OK;
 }
 

@@ -47,7 +47,7 @@ class hq_stats(ctypes.Structure):
                 ("permutes", ctypes.c_uint64), ("kernel_launches", ctypes.c_uint64),
                 ("hbm_bytes", ctypes.c_uint64), ("link_bytes", ctypes.c_uint64),
                 ("h2d_bytes", ctypes.c_uint64), ("d2h_bytes", ctypes.c_uint64), ("packs", ctypes.c_uint64),
-                ("remaps_fused", ctypes.c_uint64)]
+                ("remaps_fused", ctypes.c_uint64), ("gathers", ctypes.c_uint64)]
 
 
 _lib = None
@@ -91,7 +91,7 @@ def lib():
             "hq_schedule": [ctypes.c_int, ctypes.c_int, P, ctypes.c_size_t,
                             ctypes.POINTER(ctypes.POINTER(hq_op)), ctypes.POINTER(ctypes.c_size_t), P],
             "hq_free_ops": [P],
-            "hq_schedule_from": [ctypes.c_int, ctypes.c_int, P, ctypes.c_size_t, P,
+            "hq_schedule_from": [ctypes.c_int, ctypes.c_int, P, ctypes.c_size_t, P, ctypes.c_int,
                                  ctypes.POINTER(ctypes.POINTER(hq_op)), ctypes.POINTER(ctypes.c_size_t), P],
             "hq_plan_layout": [ctypes.c_int, ctypes.c_int, ctypes.c_int, P, ctypes.c_size_t, P,
                                ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)],
@@ -110,6 +110,7 @@ def lib():
             "hq_fuse_merged": [P, ctypes.c_size_t, ctypes.c_int, ctypes.POINTER(ctypes.POINTER(hq_gate)),
                                ctypes.POINTER(ctypes.c_size_t)],
             "hq_reduced_dm_batched": [P, ctypes.c_int, P, ctypes.c_int, P],
+            "hq_reduced_dm_batched_sum": [P, ctypes.c_int, P, ctypes.c_int, ctypes.c_int, P],
             "hq_kraus_sample_batched": [P, ctypes.c_int, P, ctypes.c_int, P, ctypes.c_int, P, P, P],
             "hq_kraus_sample": [P, P, ctypes.c_int, P, ctypes.c_int, ctypes.c_double, ctypes.POINTER(ctypes.c_int), P],
             "hq_state_get_layout": [P, P],
@@ -321,6 +322,17 @@ def hq_reduced_dm_batched(state, nb, qubits):
     return rho
 
 
+def hq_reduced_dm_batched_sum(state, nb, qubits, nlive):
+    """Sum over the first nlive shots of the trace-normalised reduced density
+    matrices (the trajectory average's numerator), computed in the library."""
+    q = np.ascontiguousarray(qubits, dtype=np.int32)
+    d = 2 ** q.size
+    rho = np.zeros((d, d), dtype=np.complex128)
+    _check(lib().hq_reduced_dm_batched_sum(state.ptr, int(nb), q.ctypes.data, int(q.size), int(nlive),
+                                           rho.ctypes.data))
+    return rho
+
+
 def hq_kraus_sample_batched(state, nb, K, qubits, u):
     """One trajectory step for each of the 2^nb shots with uniforms u (2^nb):
     returns (chosen indices int32 array, probabilities (2^nb, nkraus))."""
@@ -480,20 +492,21 @@ def hq_fuse_plan(gates, kmax):
     return group_of[:ng].copy(), ngroups.value
 
 
-def hq_schedule(n, m, gates, pi0=None):
-    """Returns (ops list of dict, final pi list); pi0: initial layout (default q -> n-1-q)."""
+def hq_schedule(n, m, gates, pi0=None, gather=False):
+    """Returns (ops list of dict, final pi list); pi0: initial layout (default
+    q -> n-1-q); gather: allow GATHER ops (isolated global accesses)."""
     arr, ng, keep = _gate_array(gates)
     ops = ctypes.POINTER(hq_op)()
     nops = ctypes.c_size_t()
     pi = np.zeros(max(n, 1), dtype=np.int32)
     p0 = None if pi0 is None else np.ascontiguousarray(pi0, dtype=np.int32)
     _check(lib().hq_schedule_from(int(n), int(m), arr, ng, None if p0 is None else p0.ctypes.data,
-                                  ctypes.byref(ops), ctypes.byref(nops), pi.ctypes.data))
+                                  1 if gather else 0, ctypes.byref(ops), ctypes.byref(nops), pi.ctypes.data))
     res = []
     try:
         for i in range(nops.value):
             o = ops[i]
-            res.append({"kind": ("apply", "remap", "permute")[o.kind], "gate": o.gate,
+            res.append({"kind": ("apply", "remap", "permute", "gather")[o.kind], "gate": o.gate,
                         "nbits": o.nbits, "bits": [o.bits[t] for t in range(12)]})
     finally:
         lib().hq_free_ops(ops)

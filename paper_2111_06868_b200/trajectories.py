@@ -174,9 +174,7 @@ def _sample_batched(n, ops, n_shots, observe, seed, init, dtype, kmax, rank, wor
         picks, r = [[] for _ in range(live)], 0
 
         def record(slot):
-            rho = hq.hq_reduced_dm_batched(s, nb, obs)[:live]
-            tr = np.einsum("sii->s", rho).real
-            acc[slot] += np.sum(rho / tr[:, None, None], axis=0)
+            acc[slot] += hq.hq_reduced_dm_batched_sum(s, nb, obs, live)
 
         for j, ((kind, _), item) in enumerate(zip(segs, compiled)):
             if kind == "U":

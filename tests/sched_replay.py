@@ -105,6 +105,14 @@ def replay_all_shards(n, m, gates, ops, psi_logical):
             k = len(g.qubits)
             for r, s in enumerate(shards):
                 apply_on_shard(s, nl, g.U, op["bits"][:k], r)
+        elif op["kind"] == "gather":
+            # the gate across rank pairs: on the whole physical vector (rank
+            # bits are the top m physical bits), then split back
+            g = gates[op["gate"]]
+            k = len(g.qubits)
+            full = np.concatenate(shards)
+            phys_apply(full, n, g.U, op["bits"][:k])
+            shards = [full[r << nl:(r + 1) << nl].copy() for r in range(G)]
         elif op["kind"] == "permute":
             pairs = [(op["bits"][2 * i], op["bits"][2 * i + 1]) for i in range(op["nbits"])]
             shards = [permute_bits(s, pairs) for s in shards]

@@ -169,6 +169,31 @@ def test_schedule_global_diagonal_gates_skip_remaps(m, kind):
     assert r_diag < r_dense, (r_diag, r_dense)
 
 
+@pytest.mark.parametrize("m", [1, 2, 3])
+@pytest.mark.parametrize("kind", ["qft", "random"])
+def test_schedule_gather_ops_replay(m, kind):
+    """Row f1, GATHER ops: with gathers allowed, isolated global accesses
+    (a global qubit not needed local again within the lookahead) run across
+    the rank pair instead of triggering a remap; the replay (the gate on the
+    whole physical vector) matches the oracle and needs no more remaps."""
+    from hq_inputs import qft_circuit
+    n = 12
+    gates = qft_circuit(n) if kind == "qft" else random_circuit(n, 40, 8, kmax=3)
+    ops_g, pi = hq.hq_schedule(n, m, gates, gather=True)
+    ops_r, _ = hq.hq_schedule(n, m, gates)
+    assert sum(o["kind"] == "remap" for o in ops_g) <= sum(o["kind"] == "remap" for o in ops_r)
+    if kind == "qft":
+        assert sum(o["kind"] == "gather" for o in ops_g) > 0
+        assert sum(o["kind"] == "remap" for o in ops_g) == 0      # H on globals gathered, phases in place
+    for o in ops_g:
+        if o["kind"] == "gather":
+            k = len(gates[o["gate"]].qubits)
+            assert sum(b >= n - m for b in o["bits"][:k]) == 1
+    psi0 = random_state(n, 4)
+    got = to_logical(n, replay_all_shards(n, m, gates, ops_g, psi0), pi)
+    assert np.max(np.abs(got - O.simulate(n, gates, psi0))) < 1e-12
+
+
 def test_schedule_phase_only_on_global_qubits():
     """A diagonal gate whose targets are all global is a per-rank phase."""
     n, m = 8, 2

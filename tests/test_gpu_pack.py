@@ -158,3 +158,53 @@ def test_fused_remap_reversible_bit_exact(G):
     y = O.reversible_image(n, gates, x)
     got = hq.hq_get_amplitudes(s)
     assert got[y] == 1.0 and np.count_nonzero(got) == 1
+
+
+# ---------------------------------------------------------------- pair gathers (row f1)
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("G", [2, 4, 8])
+@pytest.mark.parametrize("compiled", [False, True])
+def test_pair_gather_qft_no_remaps(dtype, G, compiled):
+    """QFT on virtual shards: the Hadamards on global qubits run as pair
+    gathers (each shard reads its partner's shard and writes its half), the
+    controlled phases in place (block-diagonal), so the circuit needs no remap
+    at all; matches the oracle."""
+    from hq_inputs import qft_circuit
+    n = 18
+    gates = qft_circuit(n)
+    s = hq.hq_state_create_virtual(n, dtype, G)
+    psi0 = random_state(n, 21)
+    hq.hq_set_amplitudes(s, psi0)
+    hq.hq_stats_reset(s)
+    if compiled:
+        hq.hq_circuit_run(s, hq.hq_circuit_create(s, [(tuple(g.qubits), g.U) for g in gates]))
+    else:
+        hq.hq_apply_circuit(s, gates)
+    st = hq.hq_stats_get(s)
+    assert st["gathers"] > 0 and st["remaps"] == 0, st
+    err = np.linalg.norm(hq.hq_get_amplitudes(s).astype(np.complex128) - O.simulate(n, gates, psi0))
+    assert err <= TOL[dtype], err
+    # the exchange mode (no peer gathers) gives the same result through remaps
+    s2 = hq.hq_state_create_virtual(n, dtype, G)
+    hq.hq_state_set_remap_mode(s2, "exchange")
+    hq.hq_set_amplitudes(s2, psi0)
+    hq.hq_stats_reset(s2)
+    hq.hq_apply_circuit(s2, gates)
+    assert hq.hq_stats_get(s2)["gathers"] == 0 and hq.hq_stats_get(s2)["remaps"] > 0
+    err2 = np.linalg.norm(hq.hq_get_amplitudes(s2).astype(np.complex128) - O.simulate(n, gates, psi0))
+    assert err2 <= TOL[dtype], err2
+
+
+def test_pair_gather_reversible_bit_exact():
+    """A permutation gate with one global target through a pair gather is exact."""
+    from hq_inputs import CX, X, CCX
+    n, G = 16, 4
+    gates = [Gate("X", (0,), X), Gate("CX", (0, 9), CX), Gate("CCX", (3, 1, 12), CCX), Gate("X", (1,), X)]
+    x = 0x1234
+    s = hq.hq_state_create_virtual(n, "c64", G)
+    hq.hq_state_init_basis(s, x)
+    hq.hq_apply_circuit(s, gates)
+    y = O.reversible_image(n, gates, x)
+    got = hq.hq_get_amplitudes(s)
+    assert got[y] == 1.0 and np.count_nonzero(got) == 1
+    assert hq.hq_stats_get(s)["gathers"] > 0
