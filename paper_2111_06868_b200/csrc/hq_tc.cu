@@ -791,17 +791,18 @@ constexpr int LB_PROD = L_CONV0 + NUM_CONV;
 constexpr int LB_THREADS = (LB_PROD + 1) * 32;
 constexpr int L_BARS = L_STAGES * L_STAGE + L_NR * L_RAW;
 constexpr int LB_SMEM = L_BARS + BAR_BYTES;
-constexpr int L_TMEM_COLS = 256;
+constexpr int L_TMEM_COLS = 512;                  // K = 6: A 128 + D 2 x 64; K = 5: A 64 + D 2 x 128 (from 128)
 
 struct ParamsL {
     uint64_t off[64];      // amplitude offset of canonical target pattern c
-    uint32_t setoff[64];   // amplitude offset of set n inside a tile
+    uint32_t setoff[128];  // amplitude offset of set n inside a tile (64 sets at k = 6, 128 at k = 5)
     uint64_t boff[32];     // amplitude offset of 1 KB block j of a tile (tile bits >= 7 of j << 7)
     int pos[12];           // ascending bit positions of the tile (targets + set bits)
     int nbit[12];          // tile bit i -> set-index bit (or -1)
     int cbit[12];          // tile bit i -> canonical target bit (or -1)
     int ue;                // A = U * 2^ue (host scaling into the fp16 range)
     int ea;                // B = psi * 2^ea (runtime: from the amplitude bound)
+    int k;                 // 6, or 5 (native M = 64 kernel)
     uint64_t ntiles;
 };
 
@@ -810,10 +811,19 @@ struct ParamsL {
 struct PackL {
     OutMap om;
     uint64_t poff[64];
-    uint64_t psetoff[64];
+    uint64_t psetoff[128];
     uint8_t tpat[64];
-    uint8_t tset[64];
+    uint8_t tset[128];
 };
+
+// tcgen05.ld .16x32bx2: a warp reads 16 TMEM lanes (the M = 64 accumulator
+// layout uses lanes 0-15 of each 32-lane quarter); threads 0-15 get columns
+// [c, c + 32) of lanes 0..15, threads 16-31 columns [c + 32, c + 64)
+__device__ __forceinline__ void tmem_ld16x2_32(uint32_t addr, uint32_t (&v)[32]) {
+    asm volatile("tcgen05.ld.sync.aligned.16x32bx2.x32.b32 " TC_LIST32 ", [%32], 32;"
+                 : TC_REGS32(v)
+                 : "r"(addr));
+}
 
 __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t addr) {
     // K-major SWIZZLE_128B: rows of 128 B, 8-row atoms (SBO = 1024 B), LBO unused (1)
@@ -836,7 +846,12 @@ __device__ __forceinline__ uint64_t tile_base12(uint64_t t, const ParamsL &P) {
 }
 
 
-template <bool PK>      // PK: apply+pack variant (see apply_tcb)
+// K = 6: M = 128 output reals, N = 64 sets.  K = 5 (native, no U (x) I
+// widening): M = 64 output reals, N = 128 sets, K = 64 input reals -- half
+// the tensor MACs per amplitude, which under the 1 kW cap is what sets the
+// clock.  The M = 64 A operand and accumulator occupy TMEM lanes 0-15 of
+// each 32-lane quarter (row m -> lane m % 16 + 32 (m / 16)).
+template <int K, bool PK>      // PK: apply+pack variant (see apply_tcb)
 __global__ void __launch_bounds__(LB_THREADS, 1)
 apply_tcL(float2 *__restrict__ psi, const __grid_constant__ ParamsL P,
           const uint32_t *__restrict__ Apack /* [2][128][64] half2: hi then lo, row = output real */,
@@ -882,14 +897,18 @@ apply_tcL(float2 *__restrict__ psi, const __grid_constant__ ParamsL P,
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     // A (U hi, lo as packed half2) into TMEM: warp q writes lanes 32q..32q+31
+    constexpr int ACOLS = K == 6 ? 64 : 32;           // 32-bit columns per term (K reals / 2)
     if (warp < 4) {
-        const int m = warp * 32 + lane;
+        // K = 6: lane 32q + l holds row 32q + l; K = 5: lanes 32q + l, l < 16,
+        // hold rows 16q + l (M = 64 layout), the other lanes zeros
+        const int m = K == 6 ? warp * 32 + lane : (lane < 16 ? warp * 16 + lane : -1);
 #pragma unroll 1
-        for (int ch = 0; ch < 4; ++ch) {
+        for (int ch = 0; ch < 2 * ACOLS / 32; ++ch) {
             uint32_t v[32];
-            const uint32_t *src = Apack + (ch >> 1) * (128 * 64) + m * 64 + (ch & 1) * 32;
+            const int term = ch / (ACOLS / 32), cc = ch % (ACOLS / 32);
+            const uint32_t *src = Apack + term * (128 * 64) + (m < 0 ? 0 : m) * 64 + cc * 32;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = __ldg(src + i);
+            for (int i = 0; i < 32; ++i) v[i] = m < 0 ? 0u : __ldg(src + i);
             tmem_st32(tmem + ((uint32_t)(warp * 32) << 16) + ch * 32, v);
         }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -897,7 +916,9 @@ apply_tcL(float2 *__restrict__ psi, const __grid_constant__ ParamsL P,
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t A_HI = tmem, A_LO = tmem + 64;
+    const uint32_t A_HI = tmem, A_LO = tmem + ACOLS;
+    constexpr int NSET = K == 6 ? 64 : 128;           // MMA N (sets per tile)
+    constexpr uint32_t D0 = 128;                      // accumulator d at columns [D0 + NSET d, + NSET)
     const uint64_t ntiles = P.ntiles;
     const uint64_t G = gridDim.x;
     uint64_t tmask = 0;
@@ -916,8 +937,11 @@ apply_tcL(float2 *__restrict__ psi, const __grid_constant__ ParamsL P,
             bulk_g2s(raw0 + r * L_RAW + lane * 1024, psi + tw.base + P.boff[lane], 1024, rfull(r));
         }
     } else if (warp == L_MMA) {
-        // idesc: F32 accumulate, A/B F16, both K-major, N = 64 sets, M = 128 output reals
-        const uint32_t idesc = (1u << 4) | ((uint32_t)(L_NS >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+        // idesc: F32 accumulate, A/B F16, both K-major; K = 6: M = 128 output
+        // reals, N = 64 sets; K = 5: M = 64, N = 128
+        constexpr uint32_t MM = K == 6 ? 128 : 64;
+        const uint32_t idesc = (1u << 4) | ((uint32_t)(NSET >> 3) << 17) | ((MM >> 4) << 24);
+        constexpr int NJ = K == 6 ? 8 : 4;            // K-chunks of 16 halves
         uint32_t it = 0;
         for (uint64_t t = blockIdx.x; t < ntiles; t += G, ++it) {
             const int s = it % L_STAGES;
@@ -928,18 +952,18 @@ apply_tcL(float2 *__restrict__ psi, const __grid_constant__ ParamsL P,
             mbar_wait(full_bar(s), sp);
             tc_fence_after();
             if (elect_one()) {
-                const uint32_t D = tmem + 128 + L_NS * d;
+                const uint32_t D = tmem + D0 + NSET * d;
                 const uint32_t bhi = sbase + s * L_STAGE, blo = bhi + L_HALF;
                 // K-chunk j (16 halves = 32 B): atom column j/4, +32 B inside the 128-B row;
                 // correction terms first, main terms last (accuracy, see apply_tcb)
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
+                for (int j = 0; j < NJ; ++j) {
                     const uint32_t o = (j >> 2) * L_ATOMCOL + (j & 3) * 32;
                     mma_f16(D, A_LO + 8 * j, smem_desc_sw128(bhi + o), idesc, j > 0);
                     mma_f16(D, A_HI + 8 * j, smem_desc_sw128(blo + o), idesc, 1);
                 }
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
+                for (int j = 0; j < NJ; ++j) {
                     const uint32_t o = (j >> 2) * L_ATOMCOL + (j & 3) * 32;
                     mma_f16(D, A_HI + 8 * j, smem_desc_sw128(bhi + o), idesc, 1);
                 }
@@ -973,7 +997,8 @@ apply_tcL(float2 *__restrict__ psi, const __grid_constant__ ParamsL P,
                     if (P.cbit[8 + b] >= 0) c |= 1u << P.cbit[8 + b];
                 }
             const uint32_t r8 = n & 7, ch = (c >> 2) & 7;
-            sdst[i] = (c >> 5) * L_ATOMCOL + (n >> 3) * 1024 + r8 * 128 + ((ch ^ r8) << 4) + (c & 3) * 4;
+            // atom column c / 32 spans the NSET rows (K = 5 has one atom column)
+            sdst[i] = (c >> 5) * (NSET / 8) * 1024 + (n >> 3) * 1024 + r8 * 128 + ((ch ^ r8) << 4) + (c & 3) * 4;
         }
         const float sA = __int_as_float((127 + max(-126, min(127, P.ea))) << 23);
         const uint64_t sA2 = f2_as_u64(make_float2(sA, sA));
@@ -1008,18 +1033,21 @@ apply_tcL(float2 *__restrict__ psi, const __grid_constant__ ParamsL P,
             if (lane == 0) mbar_arrive(full_bar(s));
         }
     } else {
-        // epilogue warp w (0..7): TMEM lanes 32 (w % 4).. = output reals m = 2r + e,
-        // columns (sets) [32 (w / 4), +32).  Each lane stores its own component
-        // of output r for every set: a warp's 32 lanes write re, im of 16
-        // patterns, one 4-byte store per set (a full 128-byte line when the
-        // lowest targets are bits 0..3), no re/im shuffles.
+        // epilogue warp w (0..7), TMEM lane quarter q = w % 4, column half
+        // hc = w / 4.  K = 6: lane l holds output real m = 32q + l (m = 2r + e)
+        // for the 32 sets [32 hc, +32).  K = 5: a .16x32bx2 load gives lanes
+        // l < 16 of the quarter (rows m = 16q + l % 16) to both thread halves,
+        // sets [64 hc + 32 (l / 16), +32).  Each lane stores its own real
+        // component, one 4-byte store per set (a full line per warp store when
+        // the lowest targets are the lowest bits), no re/im shuffles.
         const int q = warp & 3, hc = warp >> 2;
-        const int m = q * 32 + lane;
+        const int m = K == 6 ? q * 32 + lane : q * 16 + (lane & 15);
         const int r = m >> 1, e = m & 1;
+        const int nbase = K == 6 ? 32 * hc : 64 * hc + 32 * (lane >> 4);
         const uint64_t rb = 2 * P.off[r] + e;                  // float offset of (r, e) in a set
         // set offsets are GF(2)-linear in the set index (disjoint bits), so
-        // setoff[32 hc + j] = setoff[32 hc] + setoff[j], j a compile-time index
-        const uint64_t rbh = rb + 2 * (uint64_t)P.setoff[32 * hc];
+        // setoff[nbase + j] = setoff[nbase] + setoff[j], j a compile-time index
+        const uint64_t rbh = rb + 2 * (uint64_t)P.setoff[nbase];
         uint64_t sb[5];
 #pragma unroll
         for (int b = 0; b < 5; ++b) sb[b] = 2 * (uint64_t)P.setoff[1 << b];
@@ -1036,7 +1064,10 @@ apply_tcL(float2 *__restrict__ psi, const __grid_constant__ ParamsL P,
             wait(tfull_bar(d), dp);
             tc_fence_after();
             uint32_t v[32];
-            tmem_ld32(tmem + 128 + L_NS * d + 32 * hc + ((uint32_t)(q * 32) << 16), v);
+            if constexpr (K == 6)
+                tmem_ld32(tmem + D0 + NSET * d + 32 * hc + ((uint32_t)(q * 32) << 16), v);
+            else
+                tmem_ld16x2_32(tmem + D0 + NSET * d + 64 * hc + ((uint32_t)(q * 32) << 16), v);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             tc_fence_before();
             __syncwarp();
@@ -1067,7 +1098,7 @@ apply_tcL(float2 *__restrict__ psi, const __grid_constant__ ParamsL P,
                 const uint64_t ob = ((y & ~((uint64_t)X.om.tmask << X.om.tsh)) | X.om.add) + X.poff[r];
 #pragma unroll
                 for (int j = 0; j < 32; ++j) {
-                    const int sn = 32 * hc + j;
+                    const int sn = nbase + j;
                     float *dst = reinterpret_cast<float *>(X.om.dst[tsel | X.tset[sn]]);
                     HQ_CHECK_OUT(dst + 2 * (ob + X.psetoff[sn]) + e, 4, psi, X.om, P.ntiles << 15, 7);
                     dst[2 * (ob + X.psetoff[sn]) + e] = __uint_as_float(v[j]);
@@ -1129,43 +1160,18 @@ static void split_f16(double x, __half &hi, __half &lo) {
 
 static void tc_prepare_l(const ApplyDesc &d, const double *Ucanon, std::vector<char> &payload,
                          std::vector<char> &params) {
-    int p6[6];
-    std::vector<double> U6;
-    const int D6 = 64;
-    if (d.k == 6) {
-        for (int i = 0; i < 6; ++i) p6[i] = d.p[i];
-        U6.assign(Ucanon, Ucanon + 2 * D6 * D6);
-    } else {
-        // widen: U6 = U (x) I on the lowest non-target bit e (exact)
-        int e = 0;
-        for (;; ++e) {
-            bool t = false;
-            for (int i = 0; i < d.k; ++i) t |= d.p[i] == e;
-            if (!t) break;
-        }
-        int j = 0;
-        while (j < d.k && d.p[j] < e) ++j;
-        for (int i = 0, s = 0; i < 6; ++i) p6[i] = i == j ? e : d.p[s++];
-        const int D5 = 32;
-        U6.assign(2 * D6 * D6, 0.0);
-        auto drop = [&](int x) { return ((x >> (j + 1)) << j) | (x & ((1 << j) - 1)); };
-        for (int r = 0; r < D6; ++r)
-            for (int c = 0; c < D6; ++c) {
-                if (((r >> j) & 1) != ((c >> j) & 1)) continue;
-                U6[2 * (r * D6 + c)] = Ucanon[2 * (drop(r) * D5 + drop(c))];
-                U6[2 * (r * D6 + c) + 1] = Ucanon[2 * (drop(r) * D5 + drop(c)) + 1];
-            }
-    }
-    const int ue = u_scale_exp(U6.data(), 6);
+    // k = 6, or k = 5 on the native M = 64 kernel (no widening)
+    const int K = d.k, D = 1 << K, NSET = K == 6 ? 64 : 128, NSB = 12 - K;
+    const int ue = u_scale_exp(Ucanon, K);
     // A = interleaved real embedding (row = output real 2r+e, column kk = input
     // real 2c+f) times 2^ue, FP16 hi and lo, packed two halves (f = 0, 1) per
-    // 32-bit word: [2][128][64] words
+    // 32-bit word: [2][128 rows][64 words] (k = 5: rows < 64, words < 32)
     payload.assign(2 * 128 * 64 * sizeof(uint32_t), 0);
     __half *hi = reinterpret_cast<__half *>(payload.data());
     __half *lo = hi + 128 * 128;
-    for (int r = 0; r < D6; ++r)
-        for (int c = 0; c < D6; ++c) {
-            const double ur = U6[2 * (r * D6 + c)], ui = U6[2 * (r * D6 + c) + 1];
+    for (int r = 0; r < D; ++r)
+        for (int c = 0; c < D; ++c) {
+            const double ur = Ucanon[2 * (r * D + c)], ui = Ucanon[2 * (r * D + c) + 1];
             const double blk[2][2] = {{ur, -ui}, {ui, ur}};
             for (int e = 0; e < 2; ++e)
                 for (int f = 0; f < 2; ++f) {
@@ -1176,36 +1182,38 @@ static void tc_prepare_l(const ApplyDesc &d, const double *Ucanon, std::vector<c
     params.assign(sizeof(tc::ParamsL) + 1, 0);
     params.back() = 'L';
     tc::ParamsL &P = *reinterpret_cast<tc::ParamsL *>(params.data());
+    P.k = K;
     P.ue = ue;
     P.ea = 14;             // set per launch by the runtime (tc_set_amp_bound)
-    for (int c = 0; c < 64; ++c) {
+    for (int c = 0; c < D; ++c) {
         uint64_t o = 0;
-        for (int i = 0; i < 6; ++i)
-            if ((c >> i) & 1) o |= 1ull << p6[i];
+        for (int i = 0; i < K; ++i)
+            if ((c >> i) & 1) o |= 1ull << d.p[i];
         P.off[c] = o;
     }
-    int setbits[6], ns = 0;
-    for (int b = 0; ns < 6; ++b) {
+    int setbits[7], ns = 0;
+    for (int b = 0; ns < NSB; ++b) {
         bool t = false;
-        for (int i = 0; i < 6; ++i) t |= p6[i] == b;
+        for (int i = 0; i < K; ++i) t |= d.p[i] == b;
         if (!t) setbits[ns++] = b;
     }
-    for (int n = 0; n < 64; ++n) {
+    for (int n = 0; n < NSET; ++n) {
         uint32_t o = 0;
-        for (int i = 0; i < 6; ++i)
+        for (int i = 0; i < NSB; ++i)
             if ((n >> i) & 1) o |= 1u << setbits[i];
         P.setoff[n] = o;
     }
     int all[12];
-    for (int i = 0; i < 6; ++i) { all[i] = p6[i]; all[6 + i] = setbits[i]; }
+    for (int i = 0; i < K; ++i) all[i] = d.p[i];
+    for (int i = 0; i < NSB; ++i) all[K + i] = setbits[i];
     std::sort(all, all + 12);
     for (int i = 0; i < 12; ++i) {
         P.pos[i] = all[i];
         P.nbit[i] = P.cbit[i] = -1;
-        for (int j = 0; j < 6; ++j) {
+        for (int j = 0; j < NSB; ++j)
             if (setbits[j] == all[i]) P.nbit[i] = j;
-            if (p6[j] == all[i]) P.cbit[i] = j;
-        }
+        for (int j = 0; j < K; ++j)
+            if (d.p[j] == all[i]) P.cbit[i] = j;
     }
     // physical bits 0..6 are tile bits 0..6 (some target is below bit 7 in
     // mode L), so a tile is 32 contiguous 1 KB blocks
@@ -1432,15 +1440,15 @@ static int tc_launch_b(void *psi, const tc::ParamsB &P, const std::conditional_t
     return (int)cudaGetLastError();
 }
 
-template <bool PK>
+template <int K, bool PK>
 static int tc_launch_l(void *psi, const tc::ParamsL &P, const std::conditional_t<PK, tc::PackL, tc::NoPack> &X,
                        const void *dev_payload, cudaStream_t st) {
     static std::atomic<uint64_t> attr{0};
-    cudaError_t e = smem_attr_once(tc::apply_tcL<PK>, tc::LB_SMEM, attr);
+    cudaError_t e = smem_attr_once(tc::apply_tcL<K, PK>, tc::LB_SMEM, attr);
     if (e != cudaSuccess) return (int)e;
     const int sms = sm_count();
     const uint64_t grid = P.ntiles < (uint64_t)sms ? P.ntiles : (uint64_t)sms;
-    tc::apply_tcL<PK><<<(unsigned)grid, tc::LB_THREADS, tc::LB_SMEM, st>>>(
+    tc::apply_tcL<K, PK><<<(unsigned)grid, tc::LB_THREADS, tc::LB_SMEM, st>>>(
         reinterpret_cast<float2 *>(psi), P, reinterpret_cast<const uint32_t *>(dev_payload), X);
     return (int)cudaGetLastError();
 }
@@ -1497,8 +1505,8 @@ bool tc_set_output(std::vector<char> &params, const OutSpec &o) {
         const tc::ParamsL L = *reinterpret_cast<const tc::ParamsL *>(params.data());
         tc::PackL X{};
         X.om = m;
-        for (int c = 0; c < 64; ++c) split(L.off[c], X.poff[c], X.tpat[c]);
-        for (int n = 0; n < 64; ++n) split(L.setoff[n], X.psetoff[n], X.tset[n]);
+        for (int c = 0; c < (1 << L.k); ++c) split(L.off[c], X.poff[c], X.tpat[c]);
+        for (int n = 0; n < (L.k == 5 ? 128 : 64); ++n) split(L.setoff[n], X.psetoff[n], X.tset[n]);
         params.assign(sizeof(tc::ParamsL) + sizeof(tc::PackL) + 1, 0);
         memcpy(params.data(), &L, sizeof L);
         memcpy(params.data() + sizeof L, &X, sizeof X);
@@ -1529,12 +1537,14 @@ int tc_launch(void *psi, const void *params, size_t params_size, const void *dev
     const char tag = pb[params_size - 1];
     if (tag == 'L') {
         const tc::ParamsL &L = *reinterpret_cast<const tc::ParamsL *>(pb);
-        return tc_launch_l<false>(psi, L, tc::NoPack{}, dev_payload, st);
+        return L.k == 5 ? tc_launch_l<5, false>(psi, L, tc::NoPack{}, dev_payload, st)
+                        : tc_launch_l<6, false>(psi, L, tc::NoPack{}, dev_payload, st);
     }
     if (tag == 'Q') {
         const tc::ParamsL &L = *reinterpret_cast<const tc::ParamsL *>(pb);
         const tc::PackL &X = *reinterpret_cast<const tc::PackL *>(pb + sizeof(tc::ParamsL));
-        return tc_launch_l<true>(psi, L, X, dev_payload, st);
+        return L.k == 5 ? tc_launch_l<5, true>(psi, L, X, dev_payload, st)
+                        : tc_launch_l<6, true>(psi, L, X, dev_payload, st);
     }
     const tc::ParamsB &B = *reinterpret_cast<const tc::ParamsB *>(pb);
     if (tag == 'P') {
