@@ -164,8 +164,9 @@ hq_status hq_state_create_rank_from_buffers(int n, hq_dtype dtype, int world_siz
 hq_status hq_state_set_layout(hq_state *s, const int32_t *pi);
 hq_status hq_state_get_layout(const hq_state *s, int32_t *pi_out);
 
-/* How a remap (global<->local qubit swap) moves data between ranks:
- *   HQ_REMAP_FUSED (default): when the scheduler has packed the evictees on
+/* How a remap (global<->local qubit swap) moves data between ranks (mode =
+ * OR of the flags; default HQ_REMAP_FUSED | HQ_REMAP_GATHER):
+ *   HQ_REMAP_FUSED: when the scheduler has packed the evictees on
  *     the top local bits and the apply pass before the remap can write out
  *     of place, that pass writes every element directly into its destination
  *     rank's exchange buffer (peer memory: CUDA IPC in one-process-per-GPU
@@ -173,11 +174,15 @@ hq_status hq_state_get_layout(const hq_state *s, int32_t *pi_out);
  *     for virtual shards), with a stream barrier across ranks before and
  *     after; the exchange costs no separate transfer or HBM pass.  Used only
  *     when every rank could map every peer (else the exchange path runs).
- *   HQ_REMAP_EXCHANGE: always a separate exchange (grouped NCCL send/recv, or
- *     device copies for virtual shards) after the pass.
+ *   HQ_REMAP_GATHER: a gate whose one global target is not needed local
+ *     again within the lookahead runs as a pair gather over peer memory (each
+ *     rank of the pair reads its partner's shard) instead of a remap.
+ *   HQ_REMAP_EXCHANGE (0): always a separate exchange (grouped NCCL send/recv,
+ *     or device copies for virtual shards) after the pass, and no gathers.
  * fused_available (may be NULL) receives 1 when peer buffers are mapped. */
 #define HQ_REMAP_EXCHANGE 0
 #define HQ_REMAP_FUSED 1
+#define HQ_REMAP_GATHER 2
 hq_status hq_state_set_remap_mode(hq_state *s, int mode, int *fused_available);
 
 /* Forget the tracked amplitude bound (see the rule above): the next pass that

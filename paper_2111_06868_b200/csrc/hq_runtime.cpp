@@ -130,7 +130,7 @@ struct hq_state {
     // remap writes every element straight into its destination rank's
     // exchange buffer (peer memory over NVLink), so the exchange needs no
     // separate transfer.  p2p: every peer's buffers are addressable.
-    int remap_mode = HQ_REMAP_FUSED;
+    int remap_mode = HQ_REMAP_FUSED | HQ_REMAP_GATHER;
     bool p2p = false;
     std::vector<void *> peer_base[2];   // rank mode: IPC-mapped original [psi, buf] of every rank
     uint64_t swaps = 0;                 // psi <-> buf exchanges so far (the same on every rank)
@@ -664,7 +664,7 @@ extern "C" hq_status hq_state_destroy(hq_state *st) {
 extern "C" hq_status hq_state_set_remap_mode(hq_state *st, int mode, int *fused_available) {
     clear_error();
     if (!st) return set_error(HQ_ERR_ARG, "state is NULL");
-    if (mode != HQ_REMAP_EXCHANGE && mode != HQ_REMAP_FUSED) return set_error(HQ_ERR_ARG, "bad remap mode %d", mode);
+    if (mode & ~(HQ_REMAP_FUSED | HQ_REMAP_GATHER)) return set_error(HQ_ERR_ARG, "bad remap mode %d", mode);
     st->remap_mode = mode;
     if (fused_available) *fused_available = st->p2p ? 1 : 0;
     return HQ_OK;
@@ -1124,7 +1124,7 @@ static Fold plan_fold(const hq_state *st, const Prep &p, const std::vector<Op> &
     const Op *rem = (j < ops.size() && ops[j].kind == OP_REMAP) ? &ops[j] : nullptr;
     for (auto &sh : st->sh)
         if (!sh.buf) return f;
-    if (rem && st->remap_mode == HQ_REMAP_FUSED && st->p2p && rem->nbits >= 1 && rem->nbits <= 3) {
+    if (rem && (st->remap_mode & HQ_REMAP_FUSED) && st->p2p && rem->nbits >= 1 && rem->nbits <= 3) {
         bool top = true;
         for (int t = 0; t < rem->nbits; ++t) top &= rem->bits[2 * t + 1] == st->nl - rem->nbits + t;
         OutSpec o;
@@ -1189,7 +1189,7 @@ static const void *peer_psi(const hq_state *st, int p) {
 }
 
 static bool use_gather(const hq_state *st) {
-    return st->m > 0 && st->p2p && st->remap_mode == HQ_REMAP_FUSED;
+    return st->m > 0 && st->p2p && (st->remap_mode & HQ_REMAP_GATHER);
 }
 
 static hq_status peer_barrier(hq_state *st) {

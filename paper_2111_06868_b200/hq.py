@@ -528,13 +528,14 @@ def hq_state_set_layout(state, pi):
     _check(lib().hq_state_set_layout(state.ptr, v.ctypes.data))
 
 
-REMAP_MODES = {"exchange": 0, "fused": 1}
+REMAP_MODES = {"exchange": 0, "fused": 1, "gather": 2, "fused+gather": 3}
 
 
-def hq_state_set_remap_mode(state, mode="fused"):
-    """'fused' (default): remaps folded into the preceding apply pass when
-    possible; 'exchange': always a separate exchange.  Returns whether peer
-    buffers are mapped (fused remaps possible)."""
+def hq_state_set_remap_mode(state, mode="fused+gather"):
+    """'fused+gather' (default): remaps folded into the preceding apply pass
+    and isolated global accesses as pair gathers, when peer buffers are
+    mapped; 'fused' / 'gather' one of them; 'exchange': always a separate
+    exchange.  Returns whether peer buffers are mapped."""
     avail = ctypes.c_int()
     _check(lib().hq_state_set_remap_mode(state.ptr, REMAP_MODES[mode], ctypes.byref(avail)))
     return bool(avail.value)

@@ -17,9 +17,10 @@ pytestmark = pytest.mark.gpu
 TOL = {"c64": 1e-4, "c128": 1e-10}
 
 
-def _run(n, dtype, G, fused, planned, compiled, psi0=None, x=0):
+def _run(n, dtype, G, fused, planned, compiled, psi0=None, x=0, mode="fused+gather"):
     m = G.bit_length() - 1
     s = hq.hq_state_create_virtual(n, dtype, G)
+    hq.hq_state_set_remap_mode(s, mode)
     if planned:
         pi0, _, _ = hq.hq_plan_layout(n, m, fused, dtype)
         hq.hq_state_set_layout(s, pi0)
@@ -101,7 +102,8 @@ def test_pack_single_pass_every_tc_mode():
         g = haar_sweep_gate(n, 6, placement, 2301)
         gates = [g] + tail
         psi0 = random_state(n, 12)
-        s, st = _run(n, "c64", G, [(tuple(x.qubits), x.U) for x in gates], False, False, psi0=psi0)
+        s, st = _run(n, "c64", G, [(tuple(x.qubits), x.U) for x in gates], False, False, psi0=psi0,
+                     mode="exchange")
         assert st["remaps"] == 1 and st["packs"] == 1 and st["permutes"] == 0, (placement, st)
         want = O.simulate(n, gates, psi0)
         err = np.linalg.norm(hq.hq_get_amplitudes(s).astype(np.complex128) - want)
@@ -122,7 +124,7 @@ def test_fused_remap_vs_exchange_and_oracle(kmax, G, compiled):
     fused = hq.hq_fuse(gates, kmax, merged=True)
     m = G.bit_length() - 1
     out = {}
-    for mode in ("exchange", "fused"):
+    for mode in ("exchange", "fused"):                         # fused without gathers: same kernels
         s = hq.hq_state_create_virtual(n, "c64", G)
         assert hq.hq_state_set_remap_mode(s, mode)            # virtual shards: always mappable
         pi0, _, _ = hq.hq_plan_layout(n, m, fused)
