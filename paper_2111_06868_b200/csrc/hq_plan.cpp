@@ -464,7 +464,7 @@ void schedule(int n, int m, const std::vector<GateRef> &g, std::vector<int> &pi,
 //     with the low bits free.
 double layout_pass_cost(int dtype, int k, const int *bits) {
     double c = 1.0;
-    if (dtype == HQ_C64 && k >= 5) {
+    if (dtype == HQ_C64 && k >= 4) {      // tensor cores (k = 4 widened to 5, hq_tc.cu)
         // tensor-core pass, measured per pass on the sustained 34q circuit
         // (tools/pass_times.py): mode H with <= 1 target in bits 0..3 is the
         // baseline; 2 such targets cost 1.19x; 3 or more 1.29x, in mode L

@@ -1119,8 +1119,32 @@ apply_tcL(float2 *__restrict__ psi, const __grid_constant__ ParamsL P,
 
 // ------------------------------------------------------------------ host side
 
+// complex64 k = 5, 6 run on the tensor cores, and k = 4 too, widened to a
+// k = 5 gate (U (x) I on one more bit, exact): measured under the 1 kW cap the
+// SIMT k = 4 pass is power-bound at 0.78-0.91 of the HBM peak (64 FMA per
+// amplitude on the FP32 pipe), a k = 5 tensor-core pass runs at 0.81-0.95.
 bool tc_applicable(int dtype, const ApplyDesc &d) {
-    return dtype == HQ_C64 && (d.k == 5 || d.k == 6) && d.n_local >= d.k + tc::SETBITS + 3;
+    const int kk = d.k == 4 ? 5 : d.k;              // the widened k = 4 runs as k = 5
+    return dtype == HQ_C64 && d.k >= 4 && d.k <= 6 && d.n_local >= kk + tc::SETBITS + 3;
+}
+
+// U (x) I: a k-qubit canonical gate as a (k+1)-qubit one with the extra
+// physical bit e (not a target) as an identity factor; exact.
+static void widen_gate(const ApplyDesc &d, const double *U, int e, ApplyDesc &w, std::vector<double> &Uw) {
+    const int k = d.k, D = 1 << k, k1 = k + 1, D1 = 1 << k1;
+    int j = 0;
+    while (j < k && d.p[j] < e) ++j;                // canonical position of e
+    w = d;
+    w.k = k1;
+    for (int i = 0, s = 0; i < k1; ++i) w.p[i] = i == j ? e : d.p[s++];
+    Uw.assign((size_t)2 * D1 * D1, 0.0);
+    auto drop = [&](int x) { return ((x >> (j + 1)) << j) | (x & ((1 << j) - 1)); };
+    for (int r = 0; r < D1; ++r)
+        for (int c = 0; c < D1; ++c) {
+            if (((r >> j) & 1) != ((c >> j) & 1)) continue;
+            Uw[2 * (r * D1 + c)] = U[2 * (drop(r) * D + drop(c))];
+            Uw[2 * (r * D1 + c) + 1] = U[2 * (drop(r) * D + drop(c)) + 1];
+        }
 }
 
 // Mode L (U in TMEM, tile in shared memory) when the targets crowd the lowest
@@ -1229,8 +1253,23 @@ static void tc_prepare_l(const ApplyDesc &d, const double *Ucanon, std::vector<c
 // Build the device payload (B = real embedding of U times 2^ue, FP16 hi and
 // lo, [N][KD] each, row n = output real) and the kernel parameter block from
 // the canonical fp64 U (canonical order: U-index bit i <-> d.p[i]).
-void tc_prepare(const ApplyDesc &d, const double *Ucanon, std::vector<char> &payload,
+void tc_prepare(const ApplyDesc &d0, const double *Ucanon0, std::vector<char> &payload,
                 std::vector<char> &params) {
+    ApplyDesc d = d0;
+    const double *Ucanon = Ucanon0;
+    std::vector<double> Uw;
+    if (d0.k == 4) {
+        // widen with the lowest non-target bit >= 4 (adds no low target, so
+        // the mode rule sees the same low bits)
+        int e = 4;
+        for (;; ++e) {
+            bool t = false;
+            for (int i = 0; i < 4; ++i) t |= d0.p[i] == e;
+            if (!t) break;
+        }
+        widen_gate(d0, Ucanon0, e, d, Uw);
+        Ucanon = Uw.data();
+    }
     if (tc_use_mode_l(d)) {
         tc_prepare_l(d, Ucanon, payload, params);
         return;
