@@ -430,6 +430,16 @@ hq_status hq_schedule(int n, int m, const hq_gate *gates, size_t ngates,
 hq_status hq_schedule_from(int n, int m, const hq_gate *gates, size_t ngates, const int32_t *pi_in,
                            int flags, hq_op **ops, size_t *nops, int32_t *pi_out);
 hq_status hq_free_ops(hq_op *ops);
+/* Host-only: the transfers a REMAP op makes for `rank` of an n-qubit state on
+ * 2^m ranks, exactly as the executor issues them (grouped NCCL send/recv, or
+ * device copies): transfer i sends amplitudes [off_out[i], off_out[i] +
+ * len_out[i]) of this rank's shard to rank peer_out[i] and receives that
+ * peer's run into the same range of the exchange buffer (peer == rank: a
+ * local copy).  *count receives the number of transfers; with cap < count
+ * (or NULL arrays) only *count is written (HQ_ERR_RANGE if the arrays are
+ * given but too small).  Used by the multi-process CPU test. */
+hq_status hq_remap_plan(int n, int m, const hq_op *op, int rank, int32_t *peer_out, uint64_t *off_out,
+                        uint64_t *len_out, size_t cap, size_t *count);
 
 /* Layout planner (the GPU counterpart of the paper's "qubits are swapped to
  * fully exploit AVX instructions"): a local search over the

@@ -983,86 +983,97 @@ static hq_status exec_permute(hq_state *st, const Op &op) {
     return HQ_OK;
 }
 
-// REMAP: swap global (rank) bits g_i with local bits l_i (any local bits; the
-// scheduler keeps them in the top local bits so the data per peer is a few
-// long runs).  Element x of rank r goes to the peer p whose g-bits equal x's
-// l-bits, landing at x with its l-bits replaced by r's g-bits.  This is
-// symmetric: for each peer p (index t = p's g-bits), rank r sends the runs of
-// x whose l-bits equal t and receives p's runs into the same offsets.
-// The runs: x = pdep(rho << lmin, ~Lmask) | pdep(t, Lmask), length 2^lmin.
-static hq_status exec_remap(hq_state *st, const Op &op) {
+// REMAP: swap global (rank) bits g_i with local bits l_i.  Element x of rank
+// r goes to the peer p whose g-bits equal x's l-bits, landing at x with its
+// l-bits replaced by r's g-bits.  This is symmetric: for each peer p (index t
+// = p's g-bits), rank r sends the runs of x whose l-bits equal t and receives
+// p's runs into the same offsets.  The runs: x = pdep(rho << lmin, ~Lmask) |
+// pdep(t, Lmask), length 2^lmin amplitudes (one run per peer after a pack).
+// remap_transfers lists them for one rank; the executor and hq_remap_plan
+// (host-only, used by the gloo test) share it.
+struct Transfer {
+    int peer;
+    uint64_t off, len;      // amplitudes: send [off, off+len) of this shard, receive into the same range
+};
+
+static bool remap_transfers(int nl, int m, const Op &op, int rank, std::vector<Transfer> &out) {
+    out.clear();
     const int mp = op.nbits;
     int gsh[6], lb[6];
     uint64_t lmask = 0;
     int lmin = 64;
     for (int i = 0; i < mp; ++i) {
-        gsh[i] = op.bits[2 * i] - st->nl;               // rank bit
+        gsh[i] = op.bits[2 * i] - nl;
         lb[i] = op.bits[2 * i + 1];
-        if (lb[i] < 0 || lb[i] >= st->nl || gsh[i] < 0 || gsh[i] >= st->m)
-            return set_error(HQ_ERR_STATE, "internal: bad remap bits");
+        if (lb[i] < 0 || lb[i] >= nl || gsh[i] < 0 || gsh[i] >= m) return false;
         lmask |= 1ull << lb[i];
         lmin = std::min(lmin, lb[i]);
     }
-    const uint64_t runlen = 1ull << lmin;                     // amplitudes per run
-    const uint64_t nruns = 1ull << (st->nl - mp - lmin);      // runs per peer
-    const size_t rbytes = runlen * st->es;
-    // start (in amplitudes) of run rho of peer index t
-    auto run_start = [&](uint64_t rho, int t) {
-        uint64_t x = 0, src = rho << lmin;
-        int b = 0;
-        for (int pos = 0; pos < st->nl; ++pos) {
-            if ((lmask >> pos) & 1) {
-                int i = 0;
-                while (lb[i] != pos) ++i;
-                x |= (uint64_t)((t >> i) & 1) << pos;
-            } else {
-                x |= ((src >> b) & 1) << pos;
-                ++b;
-            }
-        }
-        return x;
-    };
-    auto bits_of = [&](int r) {
-        int t = 0;
-        for (int i = 0; i < mp; ++i) t |= ((r >> gsh[i]) & 1) << i;
-        return t;
-    };
-    auto peer_of = [&](int r, int t) {
-        int p = r;
+    const uint64_t runlen = 1ull << lmin;
+    const uint64_t nruns = 1ull << (nl - mp - lmin);
+    for (int t = 0; t < (1 << mp); ++t) {
+        int p = rank;
         for (int i = 0; i < mp; ++i) p = (p & ~(1 << gsh[i])) | (((t >> i) & 1) << gsh[i]);
-        return p;
-    };
-    if (st->mode == MODE_VIRTUAL) {
-        for (auto &s : st->sh) {
-            const int u = bits_of(s.rank);
-            for (int t = 0; t < (1 << mp); ++t) {
-                Shard &d = st->sh[peer_of(s.rank, t)];
-                for (uint64_t rho = 0; rho < nruns; ++rho) {
-                    const char *src = (const char *)s.psi + run_start(rho, t) * st->es;
-                    char *dst = (char *)d.buf + run_start(rho, u) * st->es;
-                    CUDA_TRY(cudaMemcpyAsync(dst, src, rbytes, cudaMemcpyDeviceToDevice, s.stream));
+        for (uint64_t rho = 0; rho < nruns; ++rho) {
+            uint64_t x = 0, src = rho << lmin;
+            int b = 0;
+            for (int pos = 0; pos < nl; ++pos) {
+                if ((lmask >> pos) & 1) {
+                    int i = 0;
+                    while (lb[i] != pos) ++i;
+                    x |= (uint64_t)((t >> i) & 1) << pos;
+                } else {
+                    x |= ((src >> b) & 1) << pos;
+                    ++b;
                 }
-                if (d.rank != s.rank) st->stats.link_bytes += nruns * rbytes;
+            }
+            out.push_back({p, x, runlen});
+        }
+    }
+    return true;
+}
+
+static hq_status exec_remap(hq_state *st, const Op &op) {
+    std::vector<std::vector<Transfer>> plan(st->sh.size());
+    for (size_t r = 0; r < st->sh.size(); ++r)
+        if (!remap_transfers(st->nl, st->m, op, st->sh[r].rank, plan[r]))
+            return set_error(HQ_ERR_STATE, "internal: bad remap bits");
+    if (st->mode == MODE_VIRTUAL) {
+        // shard r's run [off, off+len) lands in the peer's buffer at the run
+        // of r's g-bits: the peer's own transfer list pairs them the same way
+        // (symmetry), so copy r -> p at the offset p uses for peer r
+        // shard r's run (t, rho) lands in the peer's buffer at the run offset
+        // of (u, rho), u = r's swapped rank bits (offsets depend only on (t, rho))
+        for (size_t r = 0; r < st->sh.size(); ++r) {
+            Shard &s = st->sh[r];
+            const size_t nruns = plan[r].size() >> op.nbits;
+            int u = 0;
+            for (int i = 0; i < op.nbits; ++i) u |= ((s.rank >> (op.bits[2 * i] - st->nl)) & 1) << i;
+            for (size_t i = 0; i < plan[r].size(); ++i) {
+                const Transfer &x = plan[r][i];
+                Shard &d = st->sh[x.peer];
+                const uint64_t doff = plan[r][(size_t)u * nruns + i % nruns].off;
+                CUDA_TRY(cudaMemcpyAsync((char *)d.buf + doff * st->es, (const char *)s.psi + x.off * st->es,
+                                         x.len * st->es, cudaMemcpyDeviceToDevice, s.stream));
+                if (d.rank != s.rank) st->stats.link_bytes += x.len * st->es;
             }
         }
     } else {
         NCCL_TRY(ncclGroupStart());
-        for (auto &s : st->sh) {
+        for (size_t r = 0; r < st->sh.size(); ++r) {
+            Shard &s = st->sh[r];
             cudaSetDevice(s.device);
-            for (int t = 0; t < (1 << mp); ++t) {
-                const int p = peer_of(s.rank, t);
-                for (uint64_t rho = 0; rho < nruns; ++rho) {
-                    const uint64_t off = run_start(rho, t) * st->es;
-                    const char *src = (const char *)s.psi + off;
-                    char *dst = (char *)s.buf + off;     // from p: its runs for our g-bits land here
-                    if (p == s.rank) {
-                        CUDA_TRY(cudaMemcpyAsync(dst, src, rbytes, cudaMemcpyDeviceToDevice, s.stream));
-                    } else {
-                        NCCL_TRY(ncclSend(src, rbytes, ncclChar, p, s.comm, s.stream));
-                        NCCL_TRY(ncclRecv(dst, rbytes, ncclChar, p, s.comm, s.stream));
-                    }
+            for (const Transfer &x : plan[r]) {
+                const char *src = (const char *)s.psi + x.off * st->es;
+                char *dst = (char *)s.buf + x.off * st->es;     // from the peer: its runs for our g-bits land here
+                const size_t bytes = x.len * st->es;
+                if (x.peer == s.rank) {
+                    CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s.stream));
+                } else {
+                    NCCL_TRY(ncclSend(src, bytes, ncclChar, x.peer, s.comm, s.stream));
+                    NCCL_TRY(ncclRecv(dst, bytes, ncclChar, x.peer, s.comm, s.stream));
+                    st->stats.link_bytes += bytes;
                 }
-                if (p != s.rank) st->stats.link_bytes += nruns * rbytes;
             }
         }
         NCCL_TRY(ncclGroupEnd());
@@ -1073,6 +1084,26 @@ static hq_status exec_remap(hq_state *st, const Op &op) {
     }
     st->swaps++;
     st->stats.remaps++;
+    return HQ_OK;
+}
+
+extern "C" hq_status hq_remap_plan(int n, int m, const hq_op *op, int rank, int32_t *peer_out, uint64_t *off_out,
+                                   uint64_t *len_out, size_t cap, size_t *count) {
+    clear_error();
+    if (!op || !count) return set_error(HQ_ERR_ARG, "NULL argument");
+    if (op->kind != OP_REMAP || m < 1 || n - m < 1 || rank < 0 || rank >= (1 << m) || op->nbits < 1 || op->nbits > 6)
+        return set_error(HQ_ERR_ARG, "not a REMAP op of an n=%d, m=%d state / bad rank", n, m);
+    Op o{OP_REMAP, -1, op->nbits, {0}};
+    for (int t = 0; t < 12; ++t) o.bits[t] = op->bits[t];
+    std::vector<Transfer> v;
+    if (!remap_transfers(n - m, m, o, rank, v)) return set_error(HQ_ERR_ARG, "bad remap bits");
+    *count = v.size();
+    if (cap < v.size()) return peer_out ? set_error(HQ_ERR_RANGE, "cap %zu < %zu transfers", cap, v.size()) : HQ_OK;
+    for (size_t i = 0; i < v.size(); ++i) {
+        if (peer_out) peer_out[i] = v[i].peer;
+        if (off_out) off_out[i] = v[i].off;
+        if (len_out) len_out[i] = v[i].len;
+    }
     return HQ_OK;
 }
 

@@ -91,6 +91,8 @@ def lib():
             "hq_schedule": [ctypes.c_int, ctypes.c_int, P, ctypes.c_size_t,
                             ctypes.POINTER(ctypes.POINTER(hq_op)), ctypes.POINTER(ctypes.c_size_t), P],
             "hq_free_ops": [P],
+            "hq_remap_plan": [ctypes.c_int, ctypes.c_int, P, ctypes.c_int, P, P, P, ctypes.c_size_t,
+                              ctypes.POINTER(ctypes.c_size_t)],
             "hq_schedule_from": [ctypes.c_int, ctypes.c_int, P, ctypes.c_size_t, P, ctypes.c_int,
                                  ctypes.POINTER(ctypes.POINTER(hq_op)), ctypes.POINTER(ctypes.c_size_t), P],
             "hq_plan_layout": [ctypes.c_int, ctypes.c_int, ctypes.c_int, P, ctypes.c_size_t, P,
@@ -511,6 +513,24 @@ def hq_schedule(n, m, gates, pi0=None, gather=False):
     finally:
         lib().hq_free_ops(ops)
     return res, [int(x) for x in pi[:n]]
+
+
+def hq_remap_plan(n, m, op, rank):
+    """The library's transfer list of a REMAP op (dict from hq_schedule) for
+    `rank`: list of (peer, offset, length) in amplitudes."""
+    o = hq_op()
+    o.kind, o.gate, o.nbits = 1, -1, int(op["nbits"])
+    for t in range(12):
+        o.bits[t] = int(op["bits"][t])
+    cnt = ctypes.c_size_t()
+    _check(lib().hq_remap_plan(int(n), int(m), ctypes.byref(o), int(rank), None, None, None, 0, ctypes.byref(cnt)))
+    k = cnt.value
+    peer = np.zeros(max(k, 1), dtype=np.int32)
+    off = np.zeros(max(k, 1), dtype=np.uint64)
+    ln = np.zeros(max(k, 1), dtype=np.uint64)
+    _check(lib().hq_remap_plan(int(n), int(m), ctypes.byref(o), int(rank), peer.ctypes.data, off.ctypes.data,
+                               ln.ctypes.data, k, ctypes.byref(cnt)))
+    return [(int(peer[i]), int(off[i]), int(ln[i])) for i in range(k)]
 
 
 def hq_plan_layout(n, m, gates, dtype="c64"):

@@ -1,9 +1,9 @@
 """Multi-process check of the distributed schedule's host logic (world_size 2,
 gloo backend, CPU).  Each rank owns its shard of the physical index space and
 executes the op stream hq_schedule emits: APPLY with the oracle on the local
-shard, REMAP as the documented chunk exchange (chunk t -> peer whose swapped
-rank bits equal t, landing at the run offsets of bits(rank)) over torch.distributed
-point-to-point, PERMUTE as a local bit swap.  Rank 0 gathers the shards and
+shard, REMAP as the library's own transfer list (hq_remap_plan: the runs
+exec_remap sends and receives with NCCL) over torch.distributed point-to-point,
+PERMUTE as a local bit swap.  Rank 0 gathers the shards and
 compares the logical state with the oracle (bit-exact for a reversible
 circuit, 1e-12 for Haar gates).  This is the same exchange exec_remap issues
 through NCCL on GPUs (one send/recv pair per contiguous run)."""
@@ -36,7 +36,7 @@ def _worker(rank, world, port, n, kind, q):
         import oracle as O
         import paper_2111_06868_b200 as hq
         from hq_inputs import reversible_circuit, random_circuit, integer_state, random_state
-        from sched_replay import apply_on_shard, permute_bits, remap_runs, peer_of, bits_of, to_logical
+        from sched_replay import apply_on_shard, permute_bits, to_logical
 
         m = world.bit_length() - 1
         nl = n - m
@@ -56,29 +56,24 @@ def _worker(rank, world, port, n, kind, q):
                 pairs = [(op["bits"][2 * i], op["bits"][2 * i + 1]) for i in range(op["nbits"])]
                 shard = permute_bits(shard, pairs)
             else:
-                pairs = [(op["bits"][2 * i], op["bits"][2 * i + 1]) for i in range(op["nbits"])]
-                mp_, gsh, lmask, lmin, runlen, nruns, run_start = remap_runs(nl, pairs)
+                # the library's own transfer list (hq_remap_plan, the list
+                # exec_remap issues as NCCL send/recv), moved over gloo
                 new = np.empty_like(shard)
-                reqs = []
-                recv_bufs = []
-                for t in range(1 << mp_):
-                    p = peer_of(rank, t, gsh)
-                    for rho in range(nruns):
-                        a = run_start(rho, t)
-                        src = shard[a:a + runlen]
-                        if p == rank:
-                            new[a:a + runlen] = src
-                            continue
-                        # send my runs with l-bits t to p; receive p's runs into the same offsets
-                        send = torch.from_numpy(np.ascontiguousarray(src).view(np.float64).copy())
-                        recv = torch.empty_like(send)
-                        reqs.append(dist.isend(send, p))
-                        reqs.append(dist.irecv(recv, p))
-                        recv_bufs.append((a, recv))
+                reqs, recv_bufs = [], []
+                for p, a, ln in hq.hq_remap_plan(n, m, op, rank):
+                    src = shard[a:a + ln]
+                    if p == rank:
+                        new[a:a + ln] = src
+                        continue
+                    send = torch.from_numpy(np.ascontiguousarray(src).view(np.float64).copy())
+                    recv = torch.empty_like(send)
+                    reqs.append(dist.isend(send, p))
+                    reqs.append(dist.irecv(recv, p))
+                    recv_bufs.append((a, ln, recv))
                 for r in reqs:
                     r.wait()
-                for a, recv in recv_bufs:
-                    new[a:a + runlen] = recv.numpy().view(np.complex128)
+                for a, ln, recv in recv_bufs:
+                    new[a:a + ln] = recv.numpy().view(np.complex128)
                 shard = new
         parts = [torch.empty(2 << nl, dtype=torch.float64) for _ in range(world)]
         dist.all_gather(parts, torch.from_numpy(shard.view(np.float64).copy()))
@@ -95,12 +90,13 @@ def _worker(rank, world, port, n, kind, q):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("kind", ["reversible", "haar"])
-def test_schedule_over_gloo_world2(kind):
+def test_schedule_over_gloo_world2(kind, world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, 10, kind, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, 10, kind, q)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
