@@ -346,7 +346,7 @@ def run_hq(args):
         layout, cost0, cost1 = hq.hq_plan_layout(n, m_bits, fused, args.dtype)
         plan_ms += (time.perf_counter() - t0) * 1e3
         hq.hq_state_set_layout(state, layout)
-    fused_ok = hq.hq_state_set_remap_mode(state, "fused") if world > 1 else False
+    fused_ok = hq.hq_state_set_remap_mode(state, "fused+gather") if world > 1 else False
     circ = hq.hq_circuit_create(state, fused)
     info = hq.hq_circuit_info(circ)
     P, R = info["passes"], info["remaps"]
@@ -496,8 +496,10 @@ def run_hq(args):
         line["parity"] = parity
     if world > 1:
         line["remaps_fused_per_step"] = stats["remaps_fused"] / max(args.steps, 1)
-        line["remap_transport"] = ("fused into the apply pass (peer writes over NVLink, CUDA IPC)" if fused_ok
+        line["remap_transport"] = ("fused into the apply pass (peer writes over NVLink, CUDA IPC); "
+                                   "isolated global accesses as pair gathers" if fused_ok
                                    else "NCCL grouped send/recv")
+        line["gathers_per_step"] = stats["gathers"] / max(args.steps, 1)
     if sweep is not None:
         line["sweep"] = sweep
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
