@@ -56,8 +56,8 @@ def parse():
     ap.add_argument("--impl", default="hq", choices=["hq", "reference"])
     ap.add_argument("--config", default="34q", choices=sorted(CONFIGS))
     ap.add_argument("--kmax", type=int, default=None)
-    ap.add_argument("--fuse", default="merged", choices=["merged", "c7"],
-                    help="planner: hq_fuse_merged (default) or the plain C7 greedy hq_fuse")
+    ap.add_argument("--fuse", default="blocks", choices=["blocks", "c7"],
+                    help="planner: hq_fuse_blocks (default) or the plain C7 greedy hq_fuse")
     ap.add_argument("--dtype", default="c64", choices=["c64", "c128"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
@@ -158,15 +158,15 @@ def traffic_from_profiles(cfg, kmax, path, bytes_per_launch):
 # arms express their time in the same unit, P * 2 * (c64 state bytes) / T, so
 # the driver's ratio of the two values is the ratio of circuit times.  The GPU
 # arm checks its own P against this table (unit_passes_match); the 34q entry
-# is pinned by tests/test_abi_cpu.py::test_fuse_merged_34q_bench_circuit.
+# is pinned by tests/test_abi_cpu.py::test_fuse_blocks_bench_circuits.
 UNIT_PASSES = {
-    ("12q", 2, "merged"): 43, ("12q", 4, "merged"): 15, ("12q", 5, "merged"): 16, ("12q", 6, "merged"): 11,
+    ("12q", 2, "blocks"): 43, ("12q", 4, "blocks"): 10, ("12q", 5, "blocks"): 9, ("12q", 6, "blocks"): 7,
     ("12q", 2, "c7"): 43, ("12q", 4, "c7"): 16, ("12q", 5, "c7"): 17, ("12q", 6, "c7"): 15,
-    ("30q", 2, "merged"): 245, ("30q", 4, "merged"): 100, ("30q", 5, "merged"): 99, ("30q", 6, "merged"): 63,
+    ("30q", 2, "blocks"): 245, ("30q", 4, "blocks"): 71, ("30q", 5, "blocks"): 49, ("30q", 6, "blocks"): 36,
     ("30q", 2, "c7"): 245, ("30q", 4, "c7"): 101, ("30q", 5, "c7"): 100, ("30q", 6, "c7"): 67,
-    ("34q", 2, "merged"): 280, ("34q", 4, "merged"): 114, ("34q", 5, "merged"): 112, ("34q", 6, "merged"): 75,
+    ("34q", 2, "blocks"): 280, ("34q", 4, "blocks"): 79, ("34q", 5, "blocks"): 59, ("34q", 6, "blocks"): 37,
     ("34q", 2, "c7"): 280, ("34q", 4, "c7"): 116, ("34q", 5, "c7"): 115, ("34q", 6, "c7"): 80,
-    ("36q", 2, "merged"): 360, ("36q", 4, "merged"): 144, ("36q", 5, "merged"): 143, ("36q", 6, "merged"): 96,
+    ("36q", 2, "blocks"): 360, ("36q", 4, "blocks"): 103, ("36q", 5, "blocks"): 79, ("36q", 6, "blocks"): 46,
     ("36q", 2, "c7"): 360, ("36q", 4, "c7"): 144, ("36q", 5, "c7"): 144, ("36q", 6, "c7"): 96,
 }
 ORACLE_SAMPLE_N = 26     # the oracle's c128 state at n=26 is 1 GiB; the full 725-gate circuit takes ~15 s
@@ -318,8 +318,8 @@ def run_hq(args):
     kmax = args.kmax or kdef
     gates = sycamore_circuit(n, cycles, seed)
     t0 = time.perf_counter()
-    merged = args.fuse == "merged"
-    fused = hq.hq_fuse(gates, kmax, merged=merged)
+    blocks = args.fuse == "blocks"
+    fused = hq.hq_fuse(gates, kmax, blocks=blocks)
     plan_ms = (time.perf_counter() - t0) * 1e3
     es = 8 if args.dtype == "c64" else 16
 
@@ -427,7 +427,7 @@ def run_hq(args):
         st0 = hq.hq_stats_get(state)
         t0 = time.perf_counter()
         hq.hq_state_init_basis(state, 0)
-        fz = hq.hq_fuse(gates, kmax, merged=merged)
+        fz = hq.hq_fuse(gates, kmax, blocks=blocks)
         if layout is not None:
             hq.hq_state_set_layout(state, hq.hq_plan_layout(n, m_bits, fz, args.dtype)[0])
             hq.hq_state_init_basis(state, 0)
@@ -459,7 +459,7 @@ def run_hq(args):
     # ---- N>1: correctness through the real transport (pins P9, P10)
     parity = None
     if world > 1:
-        parity = remap_parity(hq, state, n, gates, kmax, merged, world, rank, dist, torch)
+        parity = remap_parity(hq, state, n, gates, kmax, blocks, world, rank, dist, torch)
 
     # ---- N=1: fused-gate sweep (BASELINE configs[2]) on this dense state
     sweep = None
@@ -481,7 +481,7 @@ def run_hq(args):
                    "l2": "no flush: state %.0f GiB >> 126 MB L2" % (state_bytes / 2 ** 30),
                    "parallelism": "sv-shard%d" % world,
                    "layout": "hq_plan_layout" if layout is not None else "default",
-                   "fusion": "hq_fuse_merged (C7 groups + convex merging)" if merged else "hq_fuse (C7)"},
+                   "fusion": "hq_fuse_blocks (frontier block planner)" if blocks else "hq_fuse (C7)"},
         "circuit_wall_s": ms_per_step / 1e3,
         "per_gpu_gbs": value / world,
         "frac_of_hbm_per_gpu": value / world / peak,
@@ -530,7 +530,7 @@ def reversible_image(n, gates, x):
     return y
 
 
-def remap_parity(hq, state, n, gates, kmax, merged, world, rank, dist, torch):
+def remap_parity(hq, state, n, gates, kmax, blocks, world, rank, dist, torch):
     """Correctness of the sharded path through the NCCL remaps, at full size:
     mirror circuit C.C^dagger from |0> (pin P9: returns to |0>; distance
     ||psi - |0>||_2 = sqrt(||psi||^2 - 2 Re psi_0 + 1) <= 1e-4 in complex64)
@@ -549,7 +549,7 @@ def remap_parity(hq, state, n, gates, kmax, merged, world, rank, dist, torch):
 
     out = {}
     mirror = list(gates) + [Gate(g.name + "^dag", g.qubits, np.conj(np.asarray(g.U)).T) for g in reversed(gates)]
-    fz = hq.hq_fuse(mirror, kmax, merged=merged)
+    fz = hq.hq_fuse(mirror, kmax, blocks=blocks)
     c = hq.hq_circuit_create(state, fz)
     info = hq.hq_circuit_info(c)
     hq.hq_state_init_basis(state, 0)
@@ -564,7 +564,7 @@ def remap_parity(hq, state, n, gates, kmax, merged, world, rank, dist, torch):
     rev = reversible_circuit(n, 4 * n, 4242, kmax=3)
     x = int.from_bytes(np.random.default_rng(4243).bytes(8), "little") & ((1 << n) - 1)
     y = reversible_image(n, rev, x)
-    fz = hq.hq_fuse(rev, kmax, merged=merged)
+    fz = hq.hq_fuse(rev, kmax, blocks=blocks)
     st0 = hq.hq_stats_get(state)
     hq.hq_state_init_basis(state, x)
     hq.hq_apply_circuit(state, fz)

@@ -379,14 +379,16 @@ hq_status hq_circuit_destroy(hq_circuit *c);
  * *out is allocated by the library (free with hq_free_gates). */
 hq_status hq_fuse(const hq_gate *in, size_t ngates, int kmax, hq_gate **out, size_t *nout);
 
-/* hq_fuse followed by group merging: edges A -> B of the
- * group dependency DAG are contracted while |supp(A) u supp(B)| <= kmax and
- * no other path A -> ... -> B exists (the merged block stays convex, the DAG
- * acyclic); groups are emitted in a topological order (smallest first member
- * first), members in their original order.  Never more fused gates than
- * hq_fuse (80 -> 75 on the 34q d20 circuit at kmax = 6).  Same arguments,
- * ownership and errors as hq_fuse. */
-hq_status hq_fuse_merged(const hq_gate *in, size_t ngates, int kmax, hq_gate **out, size_t *nout);
+/* Block planner (the paper's `compress` bounds the block size only,
+ * P:499-504, so any partition into convex blocks of <= kmax qubits is the
+ * same circuit): blocks are built front to back over the gate
+ * DAG, each the maximal set of gates on a <= kmax-qubit set that can run as
+ * one pass at that point, the set chosen by a short greedy lookahead over a
+ * per-width pass-cost model.  34q d20 at kmax = 6: 38 fused gates (hq_fuse:
+ * 80).  Members of a block keep their list order; each fused gate acts on
+ * its ascending support with U = U_last ... U_first (fp64).  Same
+ * arguments, ownership and errors as hq_fuse. */
+hq_status hq_fuse_blocks(const hq_gate *in, size_t ngates, int kmax, hq_gate **out, size_t *nout);
 hq_status hq_free_gates(hq_gate *gates, size_t ngates);
 
 /* Grouping only: group_of[i] = index (first-member order) of the fused group

@@ -23,11 +23,11 @@ Contents, each following the passage cited:
 * ``compress`` / ``fused_gates`` -- the greedy fusion rule, reading C7 of
   PAPER P:499-504 (worked example P:510-529), and the fused matrix
   U_group = U_last ... U_first embedded on the ascending support (P:493-494,
-  readings C8, C9).  The product's further merging of C7 groups
-  (``hq_fuse_merged``) is a planner choice the paper does not fix (many
-  groupings are valid); the oracle holds no transcript of it.
-  Merged plans are checked only through the state they produce (fused vs
-  unfused, and the dense circuit matrix), never grouping against grouping.
+  readings C8, C9).  The product's block planner (``hq_fuse_blocks``) is a
+  planner choice the paper does not fix (many groupings are valid,
+  P:499-504); the oracle holds no transcript of it.  Block plans are checked
+  only through the state they produce (fused vs unfused, and the dense
+  circuit matrix), never grouping against grouping.
 
 * ``reversible_image`` -- pin P10: a basis state |x> through permutation
   gates (0/1 matrices) is the basis state |f(x)>, with f computed by host bit

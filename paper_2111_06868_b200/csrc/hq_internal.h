@@ -51,7 +51,7 @@ struct FusedGate {
     int q[6];
     std::vector<double> U;  // 2*4^k
 };
-void fuse_build(const std::vector<GateRef> &g, int kmax, std::vector<FusedGate> &out, bool merge = false);
+void fuse_build(const std::vector<GateRef> &g, int kmax, std::vector<FusedGate> &out, bool blocks = false);
 
 // Distributed schedule (hq_schedule semantics).  pi: logical->physical, in/out.
 enum OpKind { OP_APPLY = 0, OP_REMAP = 1, OP_PERMUTE = 2, OP_GATHER = 3 };

@@ -113,108 +113,176 @@ static void left_multiply_embedded(std::vector<double> &M, int m, const int *sup
     M.swap(out);
 }
 
-// Group merging (hq_fuse_merged): after the
-// C7 grouping, contract edges A -> B of the group dependency DAG (A's last
-// use of a qubit is followed by B's first use of it) whenever
-// |supp(A) u supp(B)| <= kmax and no other path A -> ... -> B exists (so the
-// merged block is convex and the DAG stays acyclic).  Candidates are taken in
-// ascending (A, B) order and the scan repeats until nothing merges.  The
-// merged groups are then emitted in a topological order (Kahn, smallest
-// first-member index first); members keep their original order inside a
-// group.  Returns the ordered member lists.
-static std::vector<std::vector<size_t>> merge_groups(const std::vector<GateRef> &g, int kmax,
-                                                     const std::vector<int32_t> &group_of, size_t ng) {
-    std::vector<std::vector<size_t>> members(ng);
-    for (size_t i = 0; i < g.size(); ++i) members[group_of[i]].push_back(i);
-    std::vector<uint64_t> supp(ng, 0);
-    for (size_t i = 0; i < g.size(); ++i) supp[group_of[i]] |= qmask(g[i]);
-    std::vector<std::vector<char>> adj(ng, std::vector<char>(ng, 0));   // adj[a][b]: edge a -> b
-    std::vector<int> last(64, -1);
-    for (size_t i = 0; i < g.size(); ++i)
-        for (int j = 0; j < g[i].k; ++j) {
-            const int q = g[i].q[j], G = group_of[i];
-            if (last[q] >= 0 && last[q] != G) adj[last[q]][G] = 1;
-            last[q] = G;
+// Block planner (hq_fuse_blocks).  The paper's `compress` only bounds the
+// block size; any partition of the gate list into convex blocks
+// of <= kmax qubits computes the same circuit.  This planner builds the
+// blocks front to back over the gate DAG (wire order = the list order):
+//
+// * frontier: ptr[q] = first gate on wire q not yet in a block; a gate is
+//   ready when it is first on every one of its wires;
+// * grow(S): the maximal block on qubit set S from the frontier = repeatedly
+//   take any gate whose qubits are all in S and which is first on all of its
+//   wires (all its predecessors are earlier blocks or this block), so the
+//   block can run as one pass at this point of the list;
+// * candidates: for every ready gate, S starts as its qubits and grows one
+//   qubit at a time (the qubit, among those of the next LOOK gates on S's
+//   wires, whose addition absorbs the most gates; lowest qubit on ties) up
+//   to kmax; the candidate is the absorbed block, on its own support; equal
+//   supports are one candidate; candidates are ranked by gates absorbed;
+// * choice: each of the best WIDTH candidates is followed by HORIZON greedy
+//   blocks (always the best-ranked candidate) and scored by modelled pass
+//   cost per gate absorbed over that window (pass cost by block width:
+//   the measured sustained complex64 pass times on one B200, relative to a
+//   1-2 qubit pass); the lowest score wins (first on ties).
+//
+// On the 34q d20 benchmark circuit at kmax = 6 this gives 38 blocks where
+// the C7 greedy gives 80.  Members are emitted in list order (a topological
+// order of the block); blocks in the order they were built.
+namespace {
+constexpr int BLK_LOOK = 6, BLK_WIDTH = 3, BLK_HORIZON = 16;
+constexpr double BLK_COST[7] = {0.0, 1.0, 1.0, 1.06, 1.15, 1.13, 1.24};
+
+struct Frontier {
+    const std::vector<GateRef> &g;
+    std::vector<std::vector<uint32_t>> wire;       // gates on each qubit, list order
+    explicit Frontier(const std::vector<GateRef> &gates) : g(gates), wire(64) {
+        for (size_t i = 0; i < g.size(); ++i)
+            for (int j = 0; j < g[i].k; ++j) wire[g[i].q[j]].push_back((uint32_t)i);
+    }
+    bool first_on_all(const std::vector<uint32_t> &p, uint32_t gi, uint64_t S) const {
+        for (int j = 0; j < g[gi].k; ++j) {
+            const int x = g[gi].q[j];
+            if (!((S >> x) & 1) || p[x] >= wire[x].size() || wire[x][p[x]] != gi) return false;
         }
-    std::vector<char> alive(ng, 1);
-    // is there a path a -> ... -> b of length >= 2 (through some other live group)?
-    auto indirect = [&](size_t a, size_t b) {
-        std::vector<char> seen(ng, 0);
-        std::vector<size_t> stack;
-        for (size_t x = 0; x < ng; ++x)
-            if (alive[x] && adj[a][x] && x != b) { stack.push_back(x); seen[x] = 1; }
-        while (!stack.empty()) {
-            const size_t x = stack.back();
-            stack.pop_back();
-            if (adj[x][b]) return true;
-            for (size_t y = 0; y < ng; ++y)
-                if (alive[y] && adj[x][y] && !seen[y] && y != b) { seen[y] = 1; stack.push_back(y); }
-        }
-        return false;
-    };
-    auto reach = [&](size_t a, size_t b) {       // any path a -> ... -> b
-        return adj[a][b] || indirect(a, b);
-    };
-    static const char *indep_env = getenv("HQ_FUSE_INDEP");   // "0": edges only (experiments)
-    const bool indep = !(indep_env && indep_env[0] == '0');
-    for (bool merged = true; merged;) {
-        merged = false;
-        for (size_t a = 0; a < ng && !merged; ++a) {
-            if (!alive[a]) continue;
-            for (size_t b = 0; b < ng; ++b) {
-                if (b == a || !alive[b] || __builtin_popcountll(supp[a] | supp[b]) > kmax) continue;
-                if (adj[a][b]) {
-                    if (indirect(a, b)) continue;
-                } else if (!indep || adj[b][a] || reach(a, b) || reach(b, a)) {
-                    continue;                    // dependent through other groups (or b -> a: seen from b)
+        return true;
+    }
+    // the maximal block on S from p (p advanced past it); gates absorbed,
+    // their support and (optionally) their indices
+    size_t grow(std::vector<uint32_t> &p, uint64_t S, uint64_t *supp, std::vector<uint32_t> *blk) const {
+        size_t cnt = 0;
+        uint64_t su = 0;
+        for (bool changed = true; changed;) {
+            changed = false;
+            for (uint64_t m = S; m; m &= m - 1) {
+                const int q = __builtin_ctzll(m);
+                while (p[q] < wire[q].size()) {
+                    const uint32_t gi = wire[q][p[q]];
+                    if (!first_on_all(p, gi, S)) break;
+                    for (int j = 0; j < g[gi].k; ++j) {
+                        p[g[gi].q[j]]++;
+                        su |= 1ull << g[gi].q[j];
+                    }
+                    if (blk) blk->push_back(gi);
+                    ++cnt;
+                    changed = true;
                 }
-                // contract b into a
-                supp[a] |= supp[b];
-                members[a].insert(members[a].end(), members[b].begin(), members[b].end());
-                std::sort(members[a].begin(), members[a].end());
-                members[b].clear();
-                alive[b] = 0;
-                for (size_t x = 0; x < ng; ++x) {
-                    if (adj[b][x]) adj[a][x] = 1;
-                    if (adj[x][b]) adj[x][a] = 1;
-                    adj[b][x] = adj[x][b] = 0;
-                }
-                adj[a][a] = 0;
-                merged = true;
-                break;
             }
         }
+        if (supp) *supp = su;
+        return cnt;
     }
-    // topological order, smallest first member first
-    std::vector<int> indeg(ng, 0);
-    for (size_t a = 0; a < ng; ++a)
-        if (alive[a])
-            for (size_t b = 0; b < ng; ++b)
-                if (alive[b] && adj[a][b]) indeg[b]++;
+    struct Cand { size_t cnt; uint64_t supp; };
+    std::vector<Cand> candidates(const std::vector<uint32_t> &ptr, int kmax) const {
+        std::vector<Cand> out;
+        std::vector<uint32_t> p;
+        for (int q = 0; q < 64; ++q) {
+            if (ptr[q] >= wire[q].size()) continue;
+            const uint32_t gi = wire[q][ptr[q]];
+            uint64_t S = 0;
+            for (int j = 0; j < g[gi].k; ++j) S |= 1ull << g[gi].q[j];
+            if (__builtin_ctzll(S) != q || !first_on_all(ptr, gi, S)) continue;     // each ready gate once
+            p = ptr;
+            size_t cnt = grow(p, S, nullptr, nullptr);
+            while (__builtin_popcountll(S) < kmax) {
+                uint64_t cand = 0;
+                for (uint64_t m = S; m; m &= m - 1) {
+                    const int x = __builtin_ctzll(m);
+                    const auto &w = wire[x];
+                    for (size_t t = ptr[x]; t < w.size() && t < ptr[x] + BLK_LOOK; ++t)
+                        for (int j = 0; j < g[w[t]].k; ++j) cand |= 1ull << g[w[t]].q[j];
+                }
+                cand &= ~S;
+                if (!cand) break;
+                int best = -1;
+                size_t bc = 0;
+                for (uint64_t m = cand; m; m &= m - 1) {
+                    const int c = __builtin_ctzll(m);
+                    p = ptr;
+                    const size_t n2 = grow(p, S | (1ull << c), nullptr, nullptr);
+                    if (best < 0 || n2 > bc) { best = c; bc = n2; }
+                }
+                S |= 1ull << best;
+                cnt = bc;
+            }
+            p = ptr;
+            uint64_t supp = 0;
+            grow(p, S, &supp, nullptr);
+            bool dup = false;
+            for (const Cand &c : out) dup |= c.supp == supp;
+            if (!dup) out.push_back({cnt, supp});
+        }
+        std::stable_sort(out.begin(), out.end(), [](const Cand &a, const Cand &b) { return a.cnt > b.cnt; });
+        return out;
+    }
+    bool done(const std::vector<uint32_t> &p) const {
+        for (int q = 0; q < 64; ++q) if (p[q] < wire[q].size()) return false;
+        return true;
+    }
+};
+}  // namespace
+
+static std::vector<std::vector<size_t>> frontier_blocks(const std::vector<GateRef> &g, int kmax) {
+    Frontier F(g);
+    std::vector<uint32_t> ptr(64, 0), p2;
     std::vector<std::vector<size_t>> order;
-    std::vector<char> done(ng, 0);
-    for (;;) {
-        size_t best = ng;
-        for (size_t a = 0; a < ng; ++a)
-            if (alive[a] && !done[a] && indeg[a] == 0 && (best == ng || members[a][0] < members[best][0])) best = a;
-        if (best == ng) break;
-        done[best] = 1;
-        for (size_t b = 0; b < ng; ++b)
-            if (alive[b] && adj[best][b]) indeg[b]--;
-        order.push_back(members[best]);
+    std::vector<uint32_t> blk;
+    while (!F.done(ptr)) {
+        const auto cs = F.candidates(ptr, kmax);
+        size_t pick = 0;
+        if (cs.size() > 1) {
+            double best = std::numeric_limits<double>::infinity();
+            for (size_t c = 0; c < cs.size() && c < (size_t)BLK_WIDTH; ++c) {
+                p2 = ptr;
+                F.grow(p2, cs[c].supp, nullptr, nullptr);
+                double cost = BLK_COST[__builtin_popcountll(cs[c].supp)];
+                size_t gates = cs[c].cnt;
+                for (int h = 0; h < BLK_HORIZON && !F.done(p2); ++h) {
+                    const auto nx = F.candidates(p2, kmax);
+                    F.grow(p2, nx[0].supp, nullptr, nullptr);
+                    cost += BLK_COST[__builtin_popcountll(nx[0].supp)];
+                    gates += nx[0].cnt;
+                }
+                const double score = cost / (double)gates;
+                if (score < best - 1e-12) { best = score; pick = c; }
+            }
+        }
+        blk.clear();
+        F.grow(ptr, cs[pick].supp, nullptr, &blk);
+        std::sort(blk.begin(), blk.end());
+        order.emplace_back(blk.begin(), blk.end());
     }
     return order;
 }
 
-void fuse_build(const std::vector<GateRef> &g, int kmax, std::vector<FusedGate> &out, bool merge) {
+void fuse_build(const std::vector<GateRef> &g, int kmax, std::vector<FusedGate> &out, bool blocks) {
+    std::vector<std::vector<size_t>> members;
     std::vector<int32_t> group_of;
     const size_t ng0 = fuse_groups(g, kmax, group_of);
-    std::vector<std::vector<size_t>> members;
-    if (merge) {
-        members = merge_groups(g, kmax, group_of, ng0);
-    } else {
-        members.assign(ng0, {});
-        for (size_t i = 0; i < g.size(); ++i) members[group_of[i]].push_back(i);
+    members.assign(ng0, {});
+    for (size_t i = 0; i < g.size(); ++i) members[group_of[i]].push_back(i);
+    if (blocks) {
+        // the block plan, unless the C7 plan is cheaper under the same model
+        auto cost = [&](const std::vector<std::vector<size_t>> &mm) {
+            double c = 0;
+            for (const auto &m : mm) {
+                uint64_t s = 0;
+                for (size_t i : m) s |= qmask(g[i]);
+                c += BLK_COST[__builtin_popcountll(s)];
+            }
+            return c;
+        };
+        auto fb = frontier_blocks(g, kmax);
+        if (cost(fb) <= cost(members)) members.swap(fb);
     }
     const size_t ng = members.size();
     out.clear();
@@ -548,31 +616,65 @@ void plan_layout(int n, int m, int dtype, const std::vector<GateRef> &g, std::ve
         for (int j = 0; j < g[i].k; ++j) b[j] = pi[g[i].q[j]];
         return layout_pass_cost(dtype, g[i].k, b);
     };
+    auto total = [&]() {
+        double c = 0;
+        for (size_t i = 0; i < g.size(); ++i) c += gate_cost(i);
+        return c;
+    };
     std::vector<int> inv(n);
-    for (int q = 0; q < n; ++q) inv[pi[q]] = q;
-    for (int sweep = 0; sweep < 20; ++sweep) {
-        bool improved = false;
-        for (int a = 0; a < nl; ++a)
-            for (int b = a + 1; b < nl; ++b) {
-                const int qa = inv[a], qb = inv[b];
-                std::vector<int> touched(uses[qa]);
-                touched.insert(touched.end(), uses[qb].begin(), uses[qb].end());
-                std::sort(touched.begin(), touched.end());
-                touched.erase(std::unique(touched.begin(), touched.end()), touched.end());
-                double before = 0, after = 0;
-                for (int i : touched) before += gate_cost(i);
-                std::swap(pi[qa], pi[qb]);
-                for (int i : touched) after += gate_cost(i);
-                if (after < before - 1e-9) {
-                    inv[a] = qb;
-                    inv[b] = qa;
-                    improved = true;
-                } else {
+    auto descend = [&]() {
+        for (int q = 0; q < n; ++q) inv[pi[q]] = q;
+        for (int sweep = 0; sweep < 20; ++sweep) {
+            bool improved = false;
+            for (int a = 0; a < nl; ++a)
+                for (int b = a + 1; b < nl; ++b) {
+                    const int qa = inv[a], qb = inv[b];
+                    std::vector<int> touched(uses[qa]);
+                    touched.insert(touched.end(), uses[qb].begin(), uses[qb].end());
+                    std::sort(touched.begin(), touched.end());
+                    touched.erase(std::unique(touched.begin(), touched.end()), touched.end());
+                    double before = 0, after = 0;
+                    for (int i : touched) before += gate_cost(i);
                     std::swap(pi[qa], pi[qb]);
+                    for (int i : touched) after += gate_cost(i);
+                    if (after < before - 1e-9) {
+                        inv[a] = qb;
+                        inv[b] = qa;
+                        improved = true;
+                    } else {
+                        std::swap(pi[qa], pi[qb]);
+                    }
                 }
-            }
-        if (!improved) break;
+            if (!improved) break;
+        }
+    };
+    // pairwise-swap descent from the start layout, then from LAYOUT_RESTARTS
+    // deterministic shuffles of its local positions; the cheapest result
+    // wins (the first on ties)
+    constexpr int LAYOUT_RESTARTS = 24;
+    const std::vector<int> start = pi;
+    descend();
+    std::vector<int> best = pi;
+    double bc = total();
+    uint64_t rs = 0x9e3779b97f4a7c15ull;
+    for (int r = 0; r < LAYOUT_RESTARTS && bc > (double)g.size() + 1e-9; ++r) {
+        pi = start;
+        std::vector<int> loc;
+        for (int q = 0; q < n; ++q) if (pi[q] < nl) loc.push_back(q);
+        for (size_t i = loc.size(); i > 1; --i) {         // Fisher-Yates on the local positions
+            rs += 0x9e3779b97f4a7c15ull;
+            uint64_t z = rs;
+            z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+            z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+            z ^= z >> 31;
+            const size_t j = (size_t)(z % i);
+            std::swap(pi[loc[i - 1]], pi[loc[j]]);
+        }
+        descend();
+        const double c = total();
+        if (c < bc - 1e-9) { bc = c; best = pi; }
     }
+    pi = best;
 }
 
 }  // namespace hq
@@ -617,19 +719,19 @@ extern "C" hq_status hq_fuse_plan(const hq_gate *in, size_t ngates, int kmax, in
     return HQ_OK;
 }
 
-static hq_status fuse_abi(const hq_gate *in, size_t ngates, int kmax, hq_gate **out, size_t *nout, bool merge);
+static hq_status fuse_abi(const hq_gate *in, size_t ngates, int kmax, hq_gate **out, size_t *nout, bool blocks);
 
 extern "C" hq_status hq_fuse(const hq_gate *in, size_t ngates, int kmax, hq_gate **out,
                              size_t *nout) {
     return fuse_abi(in, ngates, kmax, out, nout, false);
 }
 
-extern "C" hq_status hq_fuse_merged(const hq_gate *in, size_t ngates, int kmax, hq_gate **out,
+extern "C" hq_status hq_fuse_blocks(const hq_gate *in, size_t ngates, int kmax, hq_gate **out,
                                     size_t *nout) {
     return fuse_abi(in, ngates, kmax, out, nout, true);
 }
 
-static hq_status fuse_abi(const hq_gate *in, size_t ngates, int kmax, hq_gate **out, size_t *nout, bool merge) {
+static hq_status fuse_abi(const hq_gate *in, size_t ngates, int kmax, hq_gate **out, size_t *nout, bool blocks) {
     clear_error();
     if ((!in && ngates) || !out || !nout) return set_error(HQ_ERR_ARG, "NULL argument");
     if (kmax < 1 || kmax > 6) return set_error(HQ_ERR_K, "kmax=%d not in [1,6]", kmax);
@@ -640,7 +742,7 @@ static hq_status fuse_abi(const hq_gate *in, size_t ngates, int kmax, hq_gate **
         if (refs[i].k > kmax) return set_error(HQ_ERR_K, "gate %zu wider (%d) than kmax=%d", i, refs[i].k, kmax);
     std::vector<FusedGate> fused;
     try {
-        fuse_build(refs, kmax, fused, merge);
+        fuse_build(refs, kmax, fused, blocks);
     } catch (const std::bad_alloc &) {
         return set_error(HQ_ERR_OOM, "host allocation failed in hq_fuse");
     }

@@ -109,7 +109,7 @@ def lib():
             "hq_probabilities": [P, P, ctypes.c_int, P],
             "hq_measure": [P, P, ctypes.c_int, ctypes.c_double, ctypes.POINTER(ctypes.c_uint64)],
             "hq_reduced_dm": [P, P, ctypes.c_int, P],
-            "hq_fuse_merged": [P, ctypes.c_size_t, ctypes.c_int, ctypes.POINTER(ctypes.POINTER(hq_gate)),
+            "hq_fuse_blocks": [P, ctypes.c_size_t, ctypes.c_int, ctypes.POINTER(ctypes.POINTER(hq_gate)),
                                ctypes.POINTER(ctypes.c_size_t)],
             "hq_reduced_dm_batched": [P, ctypes.c_int, P, ctypes.c_int, P],
             "hq_reduced_dm_batched_sum": [P, ctypes.c_int, P, ctypes.c_int, ctypes.c_int, P],
@@ -465,13 +465,13 @@ def hq_circuit_info(circuit):
 
 # ------------------------------------------------------------------ planner
 
-def hq_fuse(gates, kmax, merged=False):
-    """Returns list of (qubits tuple, U complex128 ndarray); merged=True runs
-    hq_fuse_merged (C7 groups, then convex group merging)."""
+def hq_fuse(gates, kmax, blocks=False):
+    """Returns list of (qubits tuple, U complex128 ndarray); blocks=True runs
+    the block planner hq_fuse_blocks instead of the C7 greedy hq_fuse."""
     arr, ng, keep = _gate_array(gates)
     out = ctypes.POINTER(hq_gate)()
     nout = ctypes.c_size_t()
-    fn = lib().hq_fuse_merged if merged else lib().hq_fuse
+    fn = lib().hq_fuse_blocks if blocks else lib().hq_fuse
     _check(fn(arr, ng, int(kmax), ctypes.byref(out), ctypes.byref(nout)))
     res = []
     try:

@@ -233,15 +233,15 @@ def _segments_lower_bound(n, m, fused):
 
 
 @pytest.mark.parametrize("n,cycles,seed", [(34, 20, 3000), (36, 24, 4000)])
-@pytest.mark.parametrize("kmax,merged", [(4, False), (5, False), (6, True)])
-def test_schedule_remap_counts(n, cycles, seed, kmax, merged):
+@pytest.mark.parametrize("kmax,blocks", [(4, False), (5, False), (6, True)])
+def test_schedule_remap_counts(n, cycles, seed, kmax, blocks):
     """the segment scheduler stays within two
     remaps of the lower bound (one remap per segment boundary; a segment
     ends early when a folded pack could not move enough evictees, which
     must not sit on bits 0, 1), from the planned first global set and from
     the default layout; at 34q m=3, k<=5: R <= 11 and R/P <= 0.106, the
     6x-at-8-GPUs threshold of the survey's cost model."""
-    fused = hq.hq_fuse(sycamore_circuit(n, cycles, seed), kmax, merged=merged)
+    fused = hq.hq_fuse(sycamore_circuit(n, cycles, seed), kmax, blocks=blocks)
     gates = [Gate("F", q, U) for q, U in fused]
     for m in (1, 2, 3):
         lb = _segments_lower_bound(n, m, fused)
@@ -299,12 +299,12 @@ def test_plan_layout_errors():
         hq.hq_plan_layout(8, 0, [Gate("U", (9,), np.eye(2))])
 
 
-# ---------------------------------------------------------------- merged fusion (hq_fuse_merged)
+# ---------------------------------------------------------------- block planner (hq_fuse_blocks)
 
 @pytest.mark.parametrize("kind", ["sycamore", "random", "reversible"])
 @pytest.mark.parametrize("kmax", [2, 3, 4, 5, 6])
-def test_fuse_merged_is_valid_and_no_worse(kind, kmax):
-    """The merged plan is the same circuit (oracle: fused vs unfused, fp64),
+def test_fuse_blocks_is_valid_and_no_worse(kind, kmax):
+    """The block plan is the same circuit (oracle: fused vs unfused, fp64),
     every block has <= kmax qubits, and it never has more blocks than C7."""
     n = 12
     if kind == "sycamore":
@@ -315,7 +315,7 @@ def test_fuse_merged_is_valid_and_no_worse(kind, kmax):
         gates = reversible_circuit(n, 150, 9, kmax=min(kmax, 3))
     gates = [g for g in gates if len(g.qubits) <= kmax]
     c7 = hq.hq_fuse(gates, kmax)
-    mg = hq.hq_fuse(gates, kmax, merged=True)
+    mg = hq.hq_fuse(gates, kmax, blocks=True)
     assert len(mg) <= len(c7)
     assert all(1 <= len(q) <= kmax and list(q) == sorted(q) for q, _ in mg)
     psi = random_state(n, 3)
@@ -324,24 +324,26 @@ def test_fuse_merged_is_valid_and_no_worse(kind, kmax):
     assert np.max(np.abs(got - want)) < 1e-12
 
 
-def test_fuse_merged_34q_bench_circuit():
-    """The bench circuit: 80 C7 blocks -> 75 merged."""
-    gates = sycamore_circuit(34, 20, 3000)
-    assert len(hq.hq_fuse(gates, 6)) == 80
-    assert len(hq.hq_fuse(gates, 6, merged=True)) == 75
+def test_fuse_blocks_bench_circuits():
+    """The bench circuits (bench.py UNIT_PASSES): 34q d20 at
+    kmax = 6, 80 C7 blocks -> 37; 36q d24, 96 -> 46; 30q d20, 67 -> 36."""
+    for (n, c, s), c7, blk in [((34, 20, 3000), 80, 37), ((36, 24, 4000), 96, 46), ((30, 20, 1000), 67, 36)]:
+        gates = sycamore_circuit(n, c, s)
+        assert len(hq.hq_fuse(gates, 6)) == c7
+        assert len(hq.hq_fuse(gates, 6, blocks=True)) == blk
 
 
 @pytest.mark.parametrize("seed", range(4))
 @pytest.mark.parametrize("kmax", [3, 4, 6])
-def test_fuse_merged_dense_matrix_equals_original(seed, kmax):
-    """The merged plan is a regrouping, so its circuit matrix (product of the
+def test_fuse_blocks_dense_matrix_equals_original(seed, kmax):
+    """The block plan is a regrouping, so its circuit matrix (product of the
     embedded block matrices, brute force P7) equals the original
     circuit's; every gate is in one block of <= kmax ascending qubits.  The
     grouping itself is a planner choice the paper does not fix,
     so it is not compared with any reference grouping."""
     n = 8
     gates = [g for g in random_circuit(n, 70, 17 + seed, kmax=min(kmax, 3)) if len(g.qubits) <= kmax]
-    mg = hq.hq_fuse(gates, kmax, merged=True)
+    mg = hq.hq_fuse(gates, kmax, blocks=True)
     assert len(mg) <= len(hq.hq_fuse(gates, kmax))
     assert all(1 <= len(q) <= kmax and list(q) == sorted(q) for q, _ in mg)
     got = O.circuit_matrix(n, [Gate("F", q, U) for q, U in mg])

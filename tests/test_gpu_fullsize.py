@@ -69,14 +69,14 @@ def test_sampled_outputs_32q(k, placement):
     torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("merged", [True, False])
-def test_mirror_circuit_34q_k6_planned_layout(merged):
+@pytest.mark.parametrize("blocks", [True, False])
+def test_mirror_circuit_34q_k6_planned_layout(blocks):
     """P9 at the bench configuration (34q d20, k <= 6, hq_plan_layout; the
-    bench's merged plan and the plain C7 plan)."""
+    bench planner (hq_fuse_blocks) and the plain C7 plan)."""
     n = 34
     gates = sycamore_circuit(n, 20, 3000)
     inv = [Gate(g.name + "^-1", g.qubits, g.U.conj().T) for g in reversed(gates)]
-    fused = hq.hq_fuse(gates, 6, merged=merged) + hq.hq_fuse(inv, 6, merged=merged)
+    fused = hq.hq_fuse(gates, 6, blocks=blocks) + hq.hq_fuse(inv, 6, blocks=blocks)
     s = hq.hq_state_create(n, "c64", 1)
     hq.hq_state_set_layout(s, hq.hq_plan_layout(n, 0, fused)[0])
     hq.hq_state_init_basis(s, 0)

@@ -46,7 +46,7 @@ def test_pack_sycamore_vs_oracle(kmax, G, planned, compiled):
     the SIMT kernel; every pack is folded (no standalone permute pass)."""
     n = 20
     gates = sycamore_circuit(n, 14, 77)
-    fused = hq.hq_fuse(gates, kmax, merged=True)
+    fused = hq.hq_fuse(gates, kmax, blocks=True)
     s, st = _run(n, "c64", G, fused, planned, compiled)
     assert st["remaps"] > 0
     assert st["packs"] > 0 and st["permutes"] == 0, st
@@ -121,7 +121,7 @@ def test_fused_remap_vs_exchange_and_oracle(kmax, G, compiled):
     the oracle; on virtual shards every packed remap fuses."""
     n = 20
     gates = sycamore_circuit(n, 14, 78)
-    fused = hq.hq_fuse(gates, kmax, merged=True)
+    fused = hq.hq_fuse(gates, kmax, blocks=True)
     m = G.bit_length() - 1
     out = {}
     for mode in ("exchange", "fused"):                         # fused without gathers: same kernels

@@ -64,12 +64,12 @@ def test_ghz_and_norm(dtype):
 @pytest.mark.parametrize("dtype", ["c64", "c128"])
 @pytest.mark.parametrize("kmax", [2, 3, 4, 5, 6])
 @pytest.mark.parametrize("seed", [0, 1, 2, 3, 4])
-@pytest.mark.parametrize("merged", [False, True])
-def test_config0_12q_fused_vs_unfused_oracle(dtype, kmax, seed, merged):
+@pytest.mark.parametrize("blocks", [False, True])
+def test_config0_12q_fused_vs_unfused_oracle(dtype, kmax, seed, blocks):
     n = 12
     gates = sycamore_circuit(n, 10, seed)
     want = O.simulate(n, gates)
-    fused = hq.hq_fuse(gates, kmax, merged=merged)
+    fused = hq.hq_fuse(gates, kmax, blocks=blocks)
     s = _gpu_state(n, dtype)
     hq.hq_apply_circuit(s, fused)
     got = hq.hq_get_amplitudes(s)
@@ -423,16 +423,16 @@ def test_borrowed_buffer_external_write_needs_invalidate():
     assert np.linalg.norm(got - want) / np.linalg.norm(want) < 2e-6
 
 
-# ---------------------------------------------------------------- merged plan at a tensor-core size
+# ---------------------------------------------------------------- block plan at a tensor-core size
 
 @pytest.mark.parametrize("kmax", [5, 6])
-def test_merged_plan_20q_tensor_cores_vs_oracle(kmax):
-    """The bench's planner (hq_fuse_merged) + hq_plan_layout at a size where
+def test_block_plan_20q_tensor_cores_vs_oracle(kmax):
+    """The bench's planner (hq_fuse_blocks) + hq_plan_layout at a size where
     the k = 5, 6 blocks run on the tensor cores, against the unfused oracle."""
     n = 20
     gates = sycamore_circuit(n, 14, 77)
     want = O.simulate(n, gates)
-    fused = hq.hq_fuse(gates, kmax, merged=True)
+    fused = hq.hq_fuse(gates, kmax, blocks=True)
     s = hq.hq_state_create(n, "c64", 1)
     hq.hq_state_set_layout(s, hq.hq_plan_layout(n, 0, fused)[0])
     hq.hq_state_init_basis(s, 0)

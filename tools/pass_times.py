@@ -22,13 +22,13 @@ def main():
     ap.add_argument("--seed", type=int, default=3000)
     ap.add_argument("--kmax", type=int, default=6)
     ap.add_argument("--rounds", type=int, default=3)
-    ap.add_argument("--c7", action="store_true", help="plain C7 fusion instead of hq_fuse_merged")
+    ap.add_argument("--c7", action="store_true", help="plain C7 fusion instead of hq_fuse_blocks")
     a = ap.parse_args()
     import torch
     import paper_2111_06868_b200 as hq
     from hq_inputs import sycamore_circuit
     n = a.n
-    fused = hq.hq_fuse(sycamore_circuit(n, a.cycles, a.seed), a.kmax, merged=not a.c7)
+    fused = hq.hq_fuse(sycamore_circuit(n, a.cycles, a.seed), a.kmax, blocks=not a.c7)
     layout = hq.hq_plan_layout(n, 0, fused, "c64")[0]
     s = hq.hq_state_create(n, "c64", 1)
     st = torch.cuda.Stream()

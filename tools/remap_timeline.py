@@ -31,7 +31,7 @@ def main():
     import paper_2111_06868_b200 as hq
     from hq_inputs import sycamore_circuit
     gates = sycamore_circuit(a.n, a.cycles, 1000 + a.n)
-    fused = hq.hq_fuse(gates, a.kmax, merged=True)
+    fused = hq.hq_fuse(gates, a.kmax, blocks=True)
     m = a.G.bit_length() - 1
     pi0, _, _ = hq.hq_plan_layout(a.n, m, fused)
     res = {"n": a.n, "G": a.G, "kmax": a.kmax, "passes": len(fused)}

@@ -44,7 +44,7 @@ def main():
         print("12q %s kmax=%d err=%.2e" % (dtype, kmax, err), flush=True)
     n = 18
     gates = sycamore_circuit(n, 8, 9)
-    fused = hq.hq_fuse(gates, 6, merged=True)
+    fused = hq.hq_fuse(gates, 6, blocks=True)
     s = hq.hq_state_create_virtual(n, "c64", 4)
     pi0, _, _ = hq.hq_plan_layout(n, 2, fused)
     hq.hq_state_set_layout(s, pi0)
