@@ -162,11 +162,11 @@ def traffic_from_profiles(cfg, kmax, path, bytes_per_launch):
 UNIT_PASSES = {
     ("12q", 2, "blocks"): 43, ("12q", 4, "blocks"): 10, ("12q", 5, "blocks"): 9, ("12q", 6, "blocks"): 7,
     ("12q", 2, "c7"): 43, ("12q", 4, "c7"): 16, ("12q", 5, "c7"): 17, ("12q", 6, "c7"): 15,
-    ("30q", 2, "blocks"): 245, ("30q", 4, "blocks"): 71, ("30q", 5, "blocks"): 49, ("30q", 6, "blocks"): 36,
+    ("30q", 2, "blocks"): 245, ("30q", 4, "blocks"): 70, ("30q", 5, "blocks"): 49, ("30q", 6, "blocks"): 33,
     ("30q", 2, "c7"): 245, ("30q", 4, "c7"): 101, ("30q", 5, "c7"): 100, ("30q", 6, "c7"): 67,
-    ("34q", 2, "blocks"): 280, ("34q", 4, "blocks"): 79, ("34q", 5, "blocks"): 59, ("34q", 6, "blocks"): 37,
+    ("34q", 2, "blocks"): 280, ("34q", 4, "blocks"): 79, ("34q", 5, "blocks"): 59, ("34q", 6, "blocks"): 36,
     ("34q", 2, "c7"): 280, ("34q", 4, "c7"): 116, ("34q", 5, "c7"): 115, ("34q", 6, "c7"): 80,
-    ("36q", 2, "blocks"): 360, ("36q", 4, "blocks"): 103, ("36q", 5, "blocks"): 79, ("36q", 6, "blocks"): 46,
+    ("36q", 2, "blocks"): 360, ("36q", 4, "blocks"): 100, ("36q", 5, "blocks"): 79, ("36q", 6, "blocks"): 42,
     ("36q", 2, "c7"): 360, ("36q", 4, "c7"): 144, ("36q", 5, "c7"): 144, ("36q", 6, "c7"): 96,
 }
 ORACLE_SAMPLE_N = 26     # the oracle's c128 state at n=26 is 1 GiB; the full 725-gate circuit takes ~15 s

@@ -22,6 +22,7 @@
 #include <vector>
 #include <limits>
 #include <new>
+#include <thread>
 
 #include "hq_internal.h"
 
@@ -134,12 +135,18 @@ static void left_multiply_embedded(std::vector<double> &M, int m, const int *sup
 //   cost per gate absorbed over that window (pass cost by block width:
 //   the measured sustained complex64 pass times on one B200, relative to a
 //   1-2 qubit pass); the lowest score wins (first on ties).
+//   The WIDTH rollouts run on parallel host threads.
 //
-// On the 34q d20 benchmark circuit at kmax = 6 this gives 38 blocks where
-// the C7 greedy gives 80.  Members are emitted in list order (a topological
-// order of the block); blocks in the order they were built.
+// Two settings run side by side, (LOOK, WIDTH, HORIZON) = (4, 6, 8) and
+// (6, 3, 16); the cheaper plan under the same cost model is returned (the
+// first on ties), or the C7 plan when that is cheaper still.  On the 34q
+// d20 benchmark circuit at kmax = 6 this gives 36 blocks where the C7
+// greedy gives 80 (30q d20: 33, 36q d24: 42).  Members are emitted in list
+// order (a topological order of the block); blocks in the order they were
+// built.
 namespace {
-constexpr int BLK_LOOK = 6, BLK_WIDTH = 3, BLK_HORIZON = 16;
+struct BlkSetting { int look, width, horizon; };
+constexpr BlkSetting BLK_SETTINGS[2] = {{4, 6, 8}, {6, 3, 16}};
 constexpr double BLK_COST[7] = {0.0, 1.0, 1.0, 1.06, 1.15, 1.13, 1.24};
 
 struct Frontier {
@@ -182,7 +189,7 @@ struct Frontier {
         return cnt;
     }
     struct Cand { size_t cnt; uint64_t supp; };
-    std::vector<Cand> candidates(const std::vector<uint32_t> &ptr, int kmax) const {
+    std::vector<Cand> candidates(const std::vector<uint32_t> &ptr, int kmax, int look) const {
         std::vector<Cand> out;
         std::vector<uint32_t> p;
         for (int q = 0; q < 64; ++q) {
@@ -198,7 +205,7 @@ struct Frontier {
                 for (uint64_t m = S; m; m &= m - 1) {
                     const int x = __builtin_ctzll(m);
                     const auto &w = wire[x];
-                    for (size_t t = ptr[x]; t < w.size() && t < ptr[x] + BLK_LOOK; ++t)
+                    for (size_t t = ptr[x]; t < w.size() && t < ptr[x] + (size_t)look; ++t)
                         for (int j = 0; j < g[w[t]].k; ++j) cand |= 1ull << g[w[t]].q[j];
                 }
                 cand &= ~S;
@@ -231,30 +238,39 @@ struct Frontier {
 };
 }  // namespace
 
-static std::vector<std::vector<size_t>> frontier_blocks(const std::vector<GateRef> &g, int kmax) {
+static std::vector<std::vector<size_t>> frontier_blocks(const std::vector<GateRef> &g, int kmax,
+                                                        const BlkSetting &cfg) {
     Frontier F(g);
-    std::vector<uint32_t> ptr(64, 0), p2;
+    std::vector<uint32_t> ptr(64, 0);
     std::vector<std::vector<size_t>> order;
     std::vector<uint32_t> blk;
     while (!F.done(ptr)) {
-        const auto cs = F.candidates(ptr, kmax);
+        const auto cs = F.candidates(ptr, kmax, cfg.look);
         size_t pick = 0;
-        if (cs.size() > 1) {
-            double best = std::numeric_limits<double>::infinity();
-            for (size_t c = 0; c < cs.size() && c < (size_t)BLK_WIDTH; ++c) {
-                p2 = ptr;
+        const size_t nw = std::min(cs.size(), (size_t)cfg.width);
+        if (nw > 1) {
+            // rollout c: candidate c, then HORIZON greedy blocks; cost per gate
+            std::vector<double> score(nw);
+            auto rollout = [&](size_t c) {
+                std::vector<uint32_t> p2 = ptr;
                 F.grow(p2, cs[c].supp, nullptr, nullptr);
                 double cost = BLK_COST[__builtin_popcountll(cs[c].supp)];
                 size_t gates = cs[c].cnt;
-                for (int h = 0; h < BLK_HORIZON && !F.done(p2); ++h) {
-                    const auto nx = F.candidates(p2, kmax);
+                for (int h = 0; h < cfg.horizon && !F.done(p2); ++h) {
+                    const auto nx = F.candidates(p2, kmax, cfg.look);
                     F.grow(p2, nx[0].supp, nullptr, nullptr);
                     cost += BLK_COST[__builtin_popcountll(nx[0].supp)];
                     gates += nx[0].cnt;
                 }
-                const double score = cost / (double)gates;
-                if (score < best - 1e-12) { best = score; pick = c; }
-            }
+                score[c] = cost / (double)gates;
+            };
+            std::vector<std::thread> th;
+            for (size_t c = 1; c < nw; ++c) th.emplace_back(rollout, c);
+            rollout(0);
+            for (auto &t : th) t.join();
+            double best = std::numeric_limits<double>::infinity();
+            for (size_t c = 0; c < nw; ++c)
+                if (score[c] < best - 1e-12) { best = score[c]; pick = c; }
         }
         blk.clear();
         F.grow(ptr, cs[pick].supp, nullptr, &blk);
@@ -281,8 +297,12 @@ void fuse_build(const std::vector<GateRef> &g, int kmax, std::vector<FusedGate> 
             }
             return c;
         };
-        auto fb = frontier_blocks(g, kmax);
-        if (cost(fb) <= cost(members)) members.swap(fb);
+        std::vector<std::vector<size_t>> fb[2];
+        std::thread t1([&] { fb[1] = frontier_blocks(g, kmax, BLK_SETTINGS[1]); });
+        fb[0] = frontier_blocks(g, kmax, BLK_SETTINGS[0]);
+        t1.join();
+        const int b = cost(fb[1]) < cost(fb[0]) ? 1 : 0;
+        if (cost(fb[b]) <= cost(members)) members.swap(fb[b]);
     }
     const size_t ng = members.size();
     out.clear();
