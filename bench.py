@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--dtype", default="c64", choices=["c64", "c128"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-other-configs", action="store_true",
+                    help="skip the configs[0] / configs[1] circuits appended to the N=1 line")
     ap.add_argument("--sweep-reps", type=int, default=5,
                     help="N=1: passes per fused-gate sweep cell on the bench state (0: no sweep)")
     ap.add_argument("--no-layout", action="store_true",
@@ -465,6 +467,9 @@ def run_hq(args):
     sweep = None
     if world == 1 and args.sweep_reps > 0:
         sweep = run_sweep(hq, torch, psi_t, stream, n, args.dtype, args.sweep_reps)
+    others = None
+    if world == 1 and args.config == "34q" and args.dtype == "c64" and not args.no_other_configs:
+        others = run_other_configs(hq, torch, stream)
 
     line = {
         "metric": "state-update GB/s", "value": value, "unit": "GB/s", "n_gpus": world,
@@ -502,6 +507,8 @@ def run_hq(args):
         line["gathers_per_step"] = stats["gathers"] / max(args.steps, 1)
     if sweep is not None:
         line["sweep"] = sweep
+    if others is not None:
+        line["other_configs"] = others
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_block(args.config, kmax, args.fuse)
     if rank == 0:
@@ -612,6 +619,47 @@ def run_sweep(hq, torch, psi_t, stream, n, dtype, reps, ks=(1, 2, 3, 4, 5, 6),
                         "median of %d passes" % (n, reps),
             "cells": cells, "min_frac_k_le_5": min(v["frac"] for key, v in cells.items() if int(key[1]) <= 5),
             "norm_after": nrm}
+
+
+def run_other_configs(hq, torch, stream, reps=5, names=("12q", "30q")):
+    """BASELINE configs[0] (12q d10, k <= 6) and configs[1] (30q d20, 2-qubit
+    fused gates) on their own PyTorch buffers beside the bench state: the
+    compiled circuit from |0> with the planned layout, 2 warm-up + `reps`
+    timed runs (CUDA events on the library's stream), median."""
+    from hq_inputs import sycamore_circuit
+    peak, _ = peaks()
+    out = {}
+    for name in names:
+        n, cycles, seed, kmax, cidx = CONFIGS[name]
+        gates = sycamore_circuit(n, cycles, seed)
+        fused = hq.hq_fuse(gates, kmax, blocks=True)
+        psi = torch.empty(2 ** n, dtype=torch.complex64, device="cuda")
+        s = hq.hq_state_create_from_buffers(n, "c64", psi.data_ptr(), stream.cuda_stream)
+        hq.hq_state_set_layout(s, hq.hq_plan_layout(n, 0, fused, "c64")[0])
+        circ = hq.hq_circuit_create(s, fused)
+        P = hq.hq_circuit_info(circ)["passes"]
+        ms = []
+        for i in range(reps + 2):
+            hq.hq_state_init_basis(s, 0)
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            hq.hq_circuit_run(s, circ)
+            b.record(stream)
+            torch.cuda.synchronize()
+            if i >= 2:
+                ms.append(a.elapsed_time(b))
+        nrm = hq.hq_norm(s)
+        t = statistics.median(ms)
+        gbs = P * 2 * 8 * 2 ** n / (t * 1e-3) / 1e9
+        out[name] = {"workload": "%s Sycamore-style d%d, seed %d, fused k<=%d (BASELINE configs[%d]), c64"
+                                 % (name, cycles, seed, kmax, cidx),
+                     "gates": len(gates), "passes": P, "circuit_ms": t, "state_update_gbs": gbs,
+                     "frac_of_hbm": gbs / peak, "norm_after": nrm}
+        del circ                  # hq_circuit_destroy (Circuit.__del__) before the state
+        s.close()
+        del psi
+    return out
 
 
 def main():
