@@ -23,6 +23,7 @@
 #include <limits>
 #include <new>
 #include <thread>
+#include <system_error>
 
 #include "hq_internal.h"
 
@@ -238,6 +239,24 @@ struct Frontier {
 };
 }  // namespace
 
+// f(0) .. f(n - 1) on host threads (f(0) on the caller's); a thread that
+// cannot be created runs its share on the caller's thread instead
+template <class F>
+static void run_parallel(size_t n, F &&f) {
+    std::vector<std::thread> th;
+    std::vector<size_t> inline_idx;
+    for (size_t i = 1; i < n; ++i) {
+        try {
+            th.emplace_back(f, i);
+        } catch (const std::system_error &) {
+            inline_idx.push_back(i);
+        }
+    }
+    f(0);
+    for (size_t i : inline_idx) f(i);
+    for (auto &t : th) t.join();
+}
+
 static std::vector<std::vector<size_t>> frontier_blocks(const std::vector<GateRef> &g, int kmax,
                                                         const BlkSetting &cfg) {
     Frontier F(g);
@@ -264,10 +283,7 @@ static std::vector<std::vector<size_t>> frontier_blocks(const std::vector<GateRe
                 }
                 score[c] = cost / (double)gates;
             };
-            std::vector<std::thread> th;
-            for (size_t c = 1; c < nw; ++c) th.emplace_back(rollout, c);
-            rollout(0);
-            for (auto &t : th) t.join();
+            run_parallel(nw, rollout);
             double best = std::numeric_limits<double>::infinity();
             for (size_t c = 0; c < nw; ++c)
                 if (score[c] < best - 1e-12) { best = score[c]; pick = c; }
@@ -298,9 +314,7 @@ void fuse_build(const std::vector<GateRef> &g, int kmax, std::vector<FusedGate> 
             return c;
         };
         std::vector<std::vector<size_t>> fb[2];
-        std::thread t1([&] { fb[1] = frontier_blocks(g, kmax, BLK_SETTINGS[1]); });
-        fb[0] = frontier_blocks(g, kmax, BLK_SETTINGS[0]);
-        t1.join();
+        run_parallel(2, [&](size_t i) { fb[i] = frontier_blocks(g, kmax, BLK_SETTINGS[i]); });
         const int b = cost(fb[1]) < cost(fb[0]) ? 1 : 0;
         if (cost(fb[b]) <= cost(members)) members.swap(fb[b]);
     }
