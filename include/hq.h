@@ -384,7 +384,8 @@ hq_status hq_fuse(const hq_gate *in, size_t ngates, int kmax, hq_gate **out, siz
  * same circuit): blocks are built front to back over the gate
  * DAG, each the maximal set of gates on a <= kmax-qubit set that can run as
  * one pass at that point, the set chosen by a short greedy lookahead over a
- * per-width pass-cost model.  34q d20 at kmax = 6: 38 fused gates (hq_fuse:
+ * per-width pass-cost model (two settings on host threads, the cheaper plan
+ * kept).  34q d20 at kmax = 6: 36 fused gates (hq_fuse:
  * 80).  Members of a block keep their list order; each fused gate acts on
  * its ascending support with U = U_last ... U_first (fp64).  Same
  * arguments, ownership and errors as hq_fuse. */

@@ -324,6 +324,32 @@ def test_fuse_blocks_is_valid_and_no_worse(kind, kmax):
     assert np.max(np.abs(got - want)) < 1e-12
 
 
+_PASS_COST = {1: 1.0, 2: 1.0, 3: 1.06, 4: 1.15, 5: 1.13, 6: 1.24}   # DESIGN.md §6 pass-cost model
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_fuse_blocks_cost_not_above_c7_and_deterministic(seed):
+    """On random circuits of random width the block plan never costs more
+    than the C7 plan under the planner's own cost model (the C7 plan is the
+    fallback), is the same circuit (oracle, fp64), and two calls return the
+    identical plan (the rollouts run on host threads; the choice must not
+    depend on their timing)."""
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(6, 15))
+    kmax = int(rng.integers(2, 7))
+    gates = random_circuit(n, 250, 100 + seed, kmax=min(kmax, 3))
+    c7 = hq.hq_fuse(gates, kmax)
+    b1 = hq.hq_fuse(gates, kmax, blocks=True)
+    b2 = hq.hq_fuse(gates, kmax, blocks=True)
+    cost = lambda f: sum(_PASS_COST[len(q)] for q, _ in f)
+    assert cost(b1) <= cost(c7) + 1e-9
+    assert [q for q, _ in b1] == [q for q, _ in b2]
+    assert all(np.array_equal(u1, u2) for (_, u1), (_, u2) in zip(b1, b2))
+    psi = random_state(n, 5)
+    got = O.simulate(n, [Gate("F", q, U) for q, U in b1], psi)
+    assert np.max(np.abs(got - O.simulate(n, gates, psi))) < 1e-12
+
+
 def test_fuse_blocks_bench_circuits():
     """The bench circuits (bench.py UNIT_PASSES): 34q d20 at
     kmax = 6, 80 C7 blocks -> 36; 36q d24, 96 -> 42; 30q d20, 67 -> 33."""
