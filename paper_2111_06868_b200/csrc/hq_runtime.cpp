@@ -21,6 +21,8 @@
 #include <memory>
 #include <mutex>
 #include <new>
+#include <chrono>
+#include <thread>
 #include <vector>
 
 #include "hq_internal.h"
@@ -93,6 +95,40 @@ struct Shard {
     // recorded on a stream of the device it was created on)
     std::vector<cudaEvent_t> ev_pool;
 };
+
+// Synchronise a shard's stream.  With an NCCL communicator (rank mode, or one
+// process driving several devices) the wait polls ncclCommGetAsyncError, so a
+// peer that died or a broken link surfaces as HQ_ERR_NCCL -- the communicator
+// is aborted -- instead of a host thread blocked forever in
+// cudaStreamSynchronize behind a collective that never completes (SURVEY §5
+// "failure detection").  Without one it is cudaStreamSynchronize.
+static hq_status sync_shard(Shard &s) {
+    if (!s.comm) {
+        CUDA_TRY(cudaStreamSynchronize(s.stream));
+        return HQ_OK;
+    }
+    for (unsigned spin = 0;; ++spin) {
+        const cudaError_t q = cudaStreamQuery(s.stream);
+        if (q == cudaSuccess) return HQ_OK;
+        if (q != cudaErrorNotReady)
+            return set_error(q == cudaErrorMemoryAllocation ? HQ_ERR_OOM : HQ_ERR_CUDA, "stream: %s",
+                             cudaGetErrorString(q));
+        ncclResult_t ar = ncclSuccess;
+        const ncclResult_t r = ncclCommGetAsyncError(s.comm, &ar);
+        if (r != ncclSuccess || (ar != ncclSuccess && ar != ncclInProgress)) {
+            ncclCommAbort(s.comm);
+            s.comm = nullptr;
+            return set_error(HQ_ERR_NCCL, "NCCL asynchronous error (communicator aborted): %s",
+                             ncclGetErrorString(r != ncclSuccess ? r : ar));
+        }
+        if (spin >= 64) std::this_thread::sleep_for(std::chrono::microseconds(20));
+    }
+}
+#define SYNC_TRY(shard)                             \
+    do {                                            \
+        const hq_status _rc = sync_shard(shard);    \
+        if (_rc) return _rc;                        \
+    } while (0)
 
 constexpr int AR_CAP = 1024;      // largest host all-reduce: 2^10 outcome probabilities
 
@@ -207,7 +243,7 @@ static hq_status arena_push(hq_state *st, Shard &s, const void *src, size_t byte
     const size_t a = (bytes + 255) & ~(size_t)255;
     if (a > s.arena.cap) return set_error(HQ_ERR_ARG, "matrix larger than staging arena");
     if (s.arena.off + a > s.arena.cap) {
-        CUDA_TRY(cudaStreamSynchronize(s.stream));
+        SYNC_TRY(s);
         s.arena.off = 0;
     }
     memcpy(s.arena.host + s.arena.off, src, bytes);
@@ -704,7 +740,7 @@ extern "C" hq_status hq_state_set_stream(hq_state *st, void *stream) {
     if (st->mode == MODE_MULTI) return set_error(HQ_ERR_STATE, "set_stream not supported for multi-device states");
     Shard &s0 = st->sh[0];
     CUDA_TRY(cudaSetDevice(s0.device));
-    if (s0.stream) CUDA_TRY(cudaStreamSynchronize(s0.stream));
+    if (s0.stream) SYNC_TRY(s0);
     if (s0.own_stream && s0.stream) cudaStreamDestroy(s0.stream);
     for (auto &s : st->sh) {
         s.stream = reinterpret_cast<cudaStream_t>(stream);
@@ -1760,7 +1796,7 @@ static hq_status io_amplitudes(hq_state *st, uint64_t first, uint64_t count, voi
             char *d = (char *)s.psi + (a - lo) * es;
             if (get) CUDA_TRY(copy_async(st->stats, h, d, (b - a) * es, cudaMemcpyDeviceToHost, s.stream));
             else CUDA_TRY(copy_async(st->stats, d, h, (b - a) * es, cudaMemcpyHostToDevice, s.stream));
-            CUDA_TRY(cudaStreamSynchronize(s.stream));
+            SYNC_TRY(s);
             continue;
         }
         // general: gather/scatter through a device temp in slices
@@ -1831,7 +1867,7 @@ extern "C" hq_status hq_norm(hq_state *st, double *out) {
     for (size_t i = 0; i < st->sh.size(); ++i) {
         Shard &s = st->sh[i];
         CUDA_TRY(cudaSetDevice(s.device));
-        CUDA_TRY(cudaStreamSynchronize(s.stream));
+        SYNC_TRY(s);
         double acc = 0.0;
         for (int b = 0; b < nbs[i]; ++b) acc += s.h_part[b];
         total += acc;
@@ -1842,7 +1878,7 @@ extern "C" hq_status hq_norm(hq_state *st, double *out) {
         CUDA_TRY(copy_async(st->stats, s.d_part, s.h_part, sizeof(double), cudaMemcpyHostToDevice, s.stream));
         NCCL_TRY(ncclAllReduce(s.d_part, s.d_part, 1, ncclDouble, ncclSum, s.comm, s.stream));
         CUDA_TRY(copy_async(st->stats, s.h_part, s.d_part, sizeof(double), cudaMemcpyDeviceToHost, s.stream));
-        CUDA_TRY(cudaStreamSynchronize(s.stream));
+        SYNC_TRY(s);
         total = s.h_part[0];
     }
     *out = sqrt(total);
@@ -1929,7 +1965,7 @@ static hq_status allreduce_host(hq_state *st, double *v, int count) {
     CUDA_TRY(copy_async(st->stats, s.d_ar, s.h_ar, sizeof(double) * count, cudaMemcpyHostToDevice, s.stream));
     NCCL_TRY(ncclAllReduce(s.d_ar, s.d_ar, count, ncclDouble, ncclSum, s.comm, s.stream));
     CUDA_TRY(copy_async(st->stats, s.h_ar, s.d_ar, sizeof(double) * count, cudaMemcpyDeviceToHost, s.stream));
-    CUDA_TRY(cudaStreamSynchronize(s.stream));
+    SYNC_TRY(s);
     memcpy(v, s.h_ar, sizeof(double) * count);
     return HQ_OK;
 }
@@ -1963,7 +1999,7 @@ extern "C" hq_status hq_project(hq_state *st, const int32_t *qubits, const int32
         st->stats.kernel_launches++;
         st->stats.hbm_bytes += (uint64_t)2 * (st->es << st->nl);
         CUDA_TRY(copy_async(st->stats, s.h_part, s.d_part, sizeof(double) * nb, cudaMemcpyDeviceToHost, s.stream));
-        CUDA_TRY(cudaStreamSynchronize(s.stream));
+        SYNC_TRY(s);
         double acc = 0.0;
         for (int b = 0; b < nb; ++b) acc += s.h_part[b];
         total += acc;
@@ -2119,7 +2155,7 @@ extern "C" hq_status hq_reduced_dm(hq_state *st, const int32_t *qubits, int k, d
         st->stats.kernel_launches++;
         st->stats.hbm_bytes += st->es << st->nl;
         CUDA_TRY(copy_async(st->stats, s.h_red, s.d_red, sizeof(double) * 2 * E * nb, cudaMemcpyDeviceToHost, s.stream));
-        CUDA_TRY(cudaStreamSynchronize(s.stream));
+        SYNC_TRY(s);
         for (int b = 0; b < nb; ++b)
             for (int x = 0; x < 2 * E; ++x) acc[x] += s.h_red[(size_t)b * 2 * E + x];
     }
@@ -2250,7 +2286,7 @@ extern "C" hq_status hq_reduced_dm_batched(hq_state *st, int nb, const int32_t *
     st->stats.kernel_launches++;
     st->stats.hbm_bytes += st->es << st->nl;
     CUDA_TRY(copy_async(st->stats, s.h_red, s.d_red, sizeof(double) * 2 * E * nblk * S, cudaMemcpyDeviceToHost, s.stream));
-    CUDA_TRY(cudaStreamSynchronize(s.stream));
+    SYNC_TRY(s);
     for (int sh = 0; sh < S; ++sh) {
         double acc[2 * 36] = {0};
         for (int b = 0; b < nblk; ++b)
@@ -2461,7 +2497,7 @@ extern "C" hq_status hq_dm_trace(hq_state *st, double *re, double *im) {
         if (e) return set_error(HQ_ERR_CUDA, "dm_trace launch: %s", cudaGetErrorString((cudaError_t)e));
         st->stats.kernel_launches++;
         CUDA_TRY(copy_async(st->stats, s.h_part, s.d_part, sizeof(double) * 2 * nb, cudaMemcpyDeviceToHost, s.stream));
-        CUDA_TRY(cudaStreamSynchronize(s.stream));
+        SYNC_TRY(s);
         for (int b = 0; b < nb; ++b) { t[0] += s.h_part[2 * b]; t[1] += s.h_part[2 * b + 1]; }
     }
     hq_status rc = allreduce_host(st, t, 2);
@@ -2480,7 +2516,7 @@ extern "C" hq_status hq_sync(hq_state *st) {
     if (!st) return set_error(HQ_ERR_ARG, "state is NULL");
     for (auto &s : st->sh) {
         CUDA_TRY(cudaSetDevice(s.device));
-        CUDA_TRY(cudaStreamSynchronize(s.stream));
+        SYNC_TRY(s);
     }
     return HQ_OK;
 }
