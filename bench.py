@@ -559,6 +559,7 @@ def remap_parity(hq, state, n, gates, kmax, blocks, world, rank, dist, torch):
     fz = hq.hq_fuse(mirror, kmax, blocks=blocks)
     c = hq.hq_circuit_create(state, fz)
     info = hq.hq_circuit_info(c)
+    s_begin = hq.hq_stats_get(state)
     hq.hq_state_init_basis(state, 0)
     hq.hq_circuit_run(state, c)
     nrm = hq.hq_norm(state)
@@ -580,7 +581,12 @@ def remap_parity(hq, state, n, gates, kmax, blocks, world, rank, dist, torch):
     nrm = hq.hq_norm(state)
     out["reversible_exact"] = bool(ay == 1.0 and owners == 1.0 and nrm == 1.0)
     out["reversible_remaps"] = st1["remaps"] - st0["remaps"]
-    out["transport"] = "NCCL grouped send/recv between %d ranks" % world
+    s_end = hq.hq_stats_get(state)
+    fused = s_end["remaps_fused"] - s_begin["remaps_fused"]
+    total = s_end["remaps"] - s_begin["remaps"]
+    out["remaps_fused"], out["remaps_total"] = fused, total
+    out["transport"] = ("%d of %d remaps fused into the apply pass (peer writes), the rest NCCL grouped "
+                        "send/recv, between %d ranks" % (fused, total, world))
     return out
 
 
