@@ -584,9 +584,7 @@ double layout_pass_cost(int dtype, int k, const int *bits) {
             b0 |= bits[j] == 0;
             b1 |= bits[j] == 1;
         }
-        static const char *old_model = getenv("HQ_LAYOUT_V4");   // "1": the round-1 v4 model (experiments)
-        if (old_model && old_model[0] == '1') c += lo ? 0.06 + 0.02 * lo : 0.0;
-        else if (lo >= 4 || (b0 && b1 && lo >= 3)) c += 0.29;   // mode L
+        if (lo >= 4 || (b0 && b1 && lo >= 3)) c += 0.29;        // mode L
         else if (lo == 3) c += 0.29;   // mode H, 0.65-0.79 of peak
         else if (lo == 2) c += 0.19;   // mode H, incl. bits {0,1} (0.75-0.86)
     } else {

@@ -1524,8 +1524,6 @@ static hq_status circuit_compile(hq_state *st, hq_circuit *c, const std::vector<
         const int maxnl = std::min(10, st->dtype == HQ_C64 ? SMEM_CIRCUIT_MAX_NL_C64 : SMEM_CIRCUIT_MAX_NL_C128);
         bool ok = st->sh.size() == 1 && st->m == 0 && st->nl <= maxnl && c->ops.size() >= 2 && c->remaps == 0 &&
                   c->permutes == 0;
-        static const char *off = getenv("HQ_SMEM_CIRCUIT");   // "0": per-pass kernels (experiments)
-        if (off && off[0] == '0') ok = false;
         if (ok) {
             std::vector<SmemOp> ops;
             std::vector<char> mats;
