@@ -29,6 +29,8 @@ def main():
     ap.add_argument("--kmax", type=int, default=6)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--dtype", default="c64")
+    ap.add_argument("--fuse", default="blocks", choices=["blocks", "c7"],
+                    help="planner: hq_fuse_blocks (default) or the C7 greedy hq_fuse")
     a = ap.parse_args()
     import numpy as np
     import torch
@@ -48,7 +50,7 @@ def main():
             q = g.qubits[0]
             gates.append(Gate("D", (q, q + N), S1))
     t0 = time.perf_counter()
-    fused = hq.hq_fuse(gates, a.kmax)
+    fused = hq.hq_fuse(gates, a.kmax, blocks=a.fuse == "blocks")
     layout, _, _ = hq.hq_plan_layout(2 * N, 0, fused, a.dtype)
     plan_ms = (time.perf_counter() - t0) * 1e3
     s = hq.hq_state_create(2 * N, a.dtype, 1)
@@ -76,7 +78,7 @@ def main():
                       "unit": "GB/s", "frac_of_hbm": gbs / peak, "ms_per_circuit": t,
                       "config": {"N": N, "vec_qubits": 2 * N, "cycles": a.cycles, "p_depol": a.p,
                                  "kmax": a.kmax, "pure_gates": len(pure), "super_gates": len(gates),
-                                 "passes": len(fused), "dtype": a.dtype},
+                                 "passes": len(fused), "fusion": a.fuse, "dtype": a.dtype},
                       "plan_ms": plan_ms, "trace": [tr.real, tr.imag]}))
 
 

@@ -30,7 +30,7 @@ def main():
     from hq_inputs import sycamore_circuit
     with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
         peak = float(json.load(f)["hbm_gbs"])
-    fused = hq.hq_fuse(sycamore_circuit(a.n, a.cycles, a.seed), a.kmax)
+    fused = hq.hq_fuse(sycamore_circuit(a.n, a.cycles, a.seed), a.kmax, blocks=True)
     s = hq.hq_state_create(a.n, a.dtype, 1)
     st = torch.cuda.Stream()
     hq.hq_state_set_stream(s, st.cuda_stream)
