@@ -119,3 +119,34 @@ def test_reversible_34q_all_k_bit_exact():
     hq.hq_apply_circuit(s, gates)
     assert hq.hq_get_amplitudes(s, y, 1)[0] == 1.0
     assert hq.hq_norm(s) == 1.0
+
+
+@pytest.mark.parametrize("G", [2, 8])
+def test_block_plan_mirror_30q_virtual_shards_fused_remaps(G):
+    """P9 through the distributed path at size: the 30q d20 circuit and its
+    inverse, block plan k <= 6, planned layout with its first global set, on G
+    virtual shards with fused remaps (the apply pass before each remap writes
+    into the peer shards' buffers) -- |psi - |0>| <= 1e-4, and the remaps did
+    fuse."""
+    n = 30
+    m = G.bit_length() - 1
+    gates = sycamore_circuit(n, 20, 1000)
+    inv = [Gate(g.name + "^-1", g.qubits, g.U.conj().T) for g in reversed(gates)]
+    fused = hq.hq_fuse(gates, 6, blocks=True) + hq.hq_fuse(inv, 6, blocks=True)
+    s = hq.hq_state_create_virtual(n, "c64", G)
+    assert hq.hq_state_set_remap_mode(s, "fused+gather")
+    hq.hq_state_set_layout(s, hq.hq_plan_layout(n, m, fused)[0])
+    hq.hq_state_init_basis(s, 0)
+    hq.hq_stats_reset(s)
+    c = hq.hq_circuit_create(s, fused)
+    hq.hq_circuit_run(s, c)
+    st = hq.hq_stats_get(s)
+    a0 = hq.hq_get_amplitudes(s, 0, 1)[0]
+    nrm = hq.hq_norm(s)
+    dist = np.sqrt(max(nrm ** 2 - abs(a0) ** 2, 0.0) + abs(a0 - 1) ** 2)
+    print("30q mirror on %d virtual shards: passes=%d remaps=%d fused=%d |psi - |0>| = %.3e"
+          % (G, len(fused), st["remaps"], st["remaps_fused"], dist))
+    assert st["remaps"] > 0 and st["remaps_fused"] == st["remaps"]
+    assert dist <= 1e-4
+    del c
+    s.close()
