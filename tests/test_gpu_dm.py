@@ -69,6 +69,37 @@ def test_noisy_circuit_density_matrix(dtype, shards):
     assert abs(tr - 1) < (1e-5 if dtype == "c64" else 1e-12)
 
 
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_super_circuit_block_plan_vs_oracle(dtype):
+    """The bench_dm.py path: a noisy Sycamore-style circuit as a regular gate
+    list on vec(rho) (every gate U (x) conj(U) on (q, q + N), a depolarising
+    superoperator after each single-qubit gate), fused by the block planner
+    and run with hq_apply_circuit, against the oracle's Kraus maps on rho."""
+    from hq_inputs import sycamore_circuit
+    N = 6
+    pure = sycamore_circuit(N, 6, 5001)
+    depol = _depolarizing(0.02)
+    S1 = hq.hq_dm_superop(depol)
+    gates = []
+    rho = np.zeros((2 ** N, 2 ** N), dtype=complex)
+    rho[0, 0] = 1.0
+    for g in pure:
+        gates.append(Gate("S", tuple(g.qubits) + tuple(q + N for q in g.qubits), np.kron(g.U, g.U.conj())))
+        rho = O.dm_apply_kraus(rho, [g.U], list(g.qubits))
+        if len(g.qubits) == 1:
+            q = g.qubits[0]
+            gates.append(Gate("D", (q, q + N), S1))
+            rho = O.dm_apply_kraus(rho, depol, [q])
+    fused = hq.hq_fuse(gates, 6, blocks=True)
+    assert len(fused) <= len(hq.hq_fuse(gates, 6))
+    s = hq.hq_state_create(2 * N, dtype, 1)
+    hq.hq_state_init_basis(s, 0)
+    hq.hq_apply_circuit(s, fused)
+    got = hq.hq_get_amplitudes(s).astype(np.complex128)
+    assert np.linalg.norm(got - O.dm_vec(rho)) <= TOL[dtype]
+    assert abs(hq.hq_dm_trace(s) - 1) < (1e-5 if dtype == "c64" else 1e-12)
+
+
 def test_dm_errors():
     s = hq.hq_state_create(7, "c64", 1)
     with pytest.raises(hq.HQError) as e:
