@@ -9,6 +9,9 @@ of `reps` after warm-up; fp32 (no TF32) and TF32-allowed matmul.  Not a
 product path; it puts the hand-written kernel next to the library call a
 user would otherwise write.
 
+Also the general placement through torch.tensordot (the paper's einsum
+engine idea), which adds two transposing copies to the GEMM.
+
     python tools/cublas_baseline.py [--n 32] [--reps 5]
 """
 import argparse
@@ -76,6 +79,26 @@ def main():
         res["speedup_vs_cublas_fp32"] = res["cublas_fp32_ms"] / ours
         rows.append(res)
         print(json.dumps(res), flush=True)
+    # a general placement as the paper's tensordot engine would do it in
+    # PyTorch: move the target axes last, one GEMM, move them back
+    # (two transposing copies + the GEMM)
+    qubits = [2, 9, 15, 20, 26, n - 2]
+    ours = timed(lambda: hq.hq_apply_matrix(s, U, qubits), a.reps, st)
+    T = psi.view(*([2] * n))
+    Uk = Ut.view(*([2] * (2 * k)))
+
+    def tensordot():
+        r = torch.tensordot(T, Uk, dims=(qubits, list(range(k, 2 * k))))   # target axes appended last
+        return torch.movedim(r, list(range(n - k, n)), qubits).contiguous()
+
+    res = {"placement": "spread %s" % qubits, "n": n, "k": k, "hq_ms": ours,
+           "hq_frac_of_hbm": nbytes / (ours * 1e-3) / 1e9 / peak}
+    for tf32 in (False, True):
+        torch.backends.cuda.matmul.allow_tf32 = tf32
+        res["torch_tensordot_%s_ms" % ("tf32" if tf32 else "fp32")] = timed(tensordot, a.reps, st)
+    torch.backends.cuda.matmul.allow_tf32 = False
+    res["speedup_vs_tensordot_fp32"] = res["torch_tensordot_fp32_ms"] / ours
+    print(json.dumps(res), flush=True)
     s.close()
 
 
