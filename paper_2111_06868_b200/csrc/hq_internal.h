@@ -3,6 +3,8 @@
 #pragma once
 
 #include <atomic>
+#include <exception>
+#include <new>
 #include <cstdint>
 #include <cstddef>
 #include <string>
@@ -16,6 +18,22 @@ namespace hq {
 
 // ------------------------------------------------------------------ errors
 hq_status set_error(hq_status st, const char *fmt, ...);
+
+// Every C ABI entry point runs inside this guard: an exception (a host
+// allocation failure in a std container, or anything else) never crosses the
+// extern "C" boundary; it becomes an hq_status with a message.
+#define HQ_ABI_BEGIN try {
+#define HQ_ABI_END                                                                   \
+    }                                                                                \
+    catch (const std::bad_alloc &) {                                                 \
+        return ::hq::set_error(HQ_ERR_OOM, "host allocation failed");                \
+    }                                                                                \
+    catch (const std::exception &e_) {                                               \
+        return ::hq::set_error(HQ_ERR_STATE, "internal error: %s", e_.what());       \
+    }                                                                                \
+    catch (...) {                                                                    \
+        return ::hq::set_error(HQ_ERR_STATE, "internal error");                      \
+    }
 void clear_error();
 
 // ------------------------------------------------------------------ launch helpers

@@ -24,6 +24,7 @@
 #include <new>
 #include <thread>
 #include <system_error>
+#include <exception>
 
 #include "hq_internal.h"
 
@@ -240,21 +241,33 @@ struct Frontier {
 }  // namespace
 
 // f(0) .. f(n - 1) on host threads (f(0) on the caller's); a thread that
-// cannot be created runs its share on the caller's thread instead
+// cannot be created runs its share on the caller's thread instead.  An
+// exception thrown by any f(i) (std::bad_alloc) is rethrown on the caller's
+// thread after every thread has joined.
 template <class F>
 static void run_parallel(size_t n, F &&f) {
+    std::vector<std::exception_ptr> err(n);
+    auto guarded = [&](size_t i) {
+        try {
+            f(i);
+        } catch (...) {
+            err[i] = std::current_exception();
+        }
+    };
     std::vector<std::thread> th;
     std::vector<size_t> inline_idx;
     for (size_t i = 1; i < n; ++i) {
         try {
-            th.emplace_back(f, i);
+            th.emplace_back(guarded, i);
         } catch (const std::system_error &) {
             inline_idx.push_back(i);
         }
     }
-    f(0);
-    for (size_t i : inline_idx) f(i);
+    guarded(0);
+    for (size_t i : inline_idx) guarded(i);
     for (auto &t : th) t.join();
+    for (auto &e : err)
+        if (e) std::rethrow_exception(e);
 }
 
 static std::vector<std::vector<size_t>> frontier_blocks(const std::vector<GateRef> &g, int kmax,
@@ -737,6 +750,7 @@ static hq_status to_refs(const hq_gate *in, size_t ng, int n, std::vector<GateRe
 
 extern "C" hq_status hq_fuse_plan(const hq_gate *in, size_t ngates, int kmax, int32_t *group_of,
                                   size_t *ngroups) {
+    HQ_ABI_BEGIN
     clear_error();
     if ((!in && ngates) || !ngroups || (!group_of && ngates)) return set_error(HQ_ERR_ARG, "NULL argument");
     if (kmax < 1 || kmax > 6) return set_error(HQ_ERR_K, "kmax=%d not in [1,6]", kmax);
@@ -749,18 +763,23 @@ extern "C" hq_status hq_fuse_plan(const hq_gate *in, size_t ngates, int kmax, in
     *ngroups = fuse_groups(refs, kmax, go);
     if (ngates) std::memcpy(group_of, go.data(), sizeof(int32_t) * ngates);
     return HQ_OK;
+    HQ_ABI_END
 }
 
 static hq_status fuse_abi(const hq_gate *in, size_t ngates, int kmax, hq_gate **out, size_t *nout, bool blocks);
 
 extern "C" hq_status hq_fuse(const hq_gate *in, size_t ngates, int kmax, hq_gate **out,
                              size_t *nout) {
+    HQ_ABI_BEGIN
     return fuse_abi(in, ngates, kmax, out, nout, false);
+    HQ_ABI_END
 }
 
 extern "C" hq_status hq_fuse_blocks(const hq_gate *in, size_t ngates, int kmax, hq_gate **out,
                                     size_t *nout) {
+    HQ_ABI_BEGIN
     return fuse_abi(in, ngates, kmax, out, nout, true);
+    HQ_ABI_END
 }
 
 static hq_status fuse_abi(const hq_gate *in, size_t ngates, int kmax, hq_gate **out, size_t *nout, bool blocks) {
@@ -798,19 +817,24 @@ static hq_status fuse_abi(const hq_gate *in, size_t ngates, int kmax, hq_gate **
 }
 
 extern "C" hq_status hq_free_gates(hq_gate *gates, size_t ngates) {
+    HQ_ABI_BEGIN
     if (!gates) return HQ_OK;
     for (size_t i = 0; i < ngates; ++i) delete[] gates[i].U;
     delete[] gates;
     return HQ_OK;
+    HQ_ABI_END
 }
 
 extern "C" hq_status hq_schedule(int n, int m, const hq_gate *gates, size_t ngates, hq_op **ops,
                                  size_t *nops, int32_t *pi_out) {
+    HQ_ABI_BEGIN
     return hq_schedule_from(n, m, gates, ngates, nullptr, 0, ops, nops, pi_out);
+    HQ_ABI_END
 }
 
 extern "C" hq_status hq_schedule_from(int n, int m, const hq_gate *gates, size_t ngates, const int32_t *pi_in,
                                       int flags, hq_op **ops, size_t *nops, int32_t *pi_out) {
+    HQ_ABI_BEGIN
     clear_error();
     if ((!gates && ngates) || !ops || !nops) return set_error(HQ_ERR_ARG, "NULL argument");
     if (n < 1 || n > 63 || m < 0 || m > 16) return set_error(HQ_ERR_ARG, "bad n=%d / m=%d", n, m);
@@ -841,10 +865,12 @@ extern "C" hq_status hq_schedule_from(int n, int m, const hq_gate *gates, size_t
     *nops = v.size();
     if (pi_out) for (int q = 0; q < n; ++q) pi_out[q] = pi[q];
     return HQ_OK;
+    HQ_ABI_END
 }
 
 extern "C" hq_status hq_plan_layout(int n, int m, int dtype, const hq_gate *gates, size_t ngates,
                                    int32_t *pi_out, double *cost_before, double *cost_after) {
+    HQ_ABI_BEGIN
     clear_error();
     if ((!gates && ngates) || !pi_out) return set_error(HQ_ERR_ARG, "NULL argument");
     if (n < 1 || n > 63 || m < 0 || m > 16 || (m > 0 && n - m < 6))
@@ -868,9 +894,12 @@ extern "C" hq_status hq_plan_layout(int n, int m, int dtype, const hq_gate *gate
     if (cost_after) *cost_after = total(pi);
     for (int q = 0; q < n; ++q) pi_out[q] = pi[q];
     return HQ_OK;
+    HQ_ABI_END
 }
 
 extern "C" hq_status hq_free_ops(hq_op *ops) {
+    HQ_ABI_BEGIN
     delete[] ops;
     return HQ_OK;
+    HQ_ABI_END
 }

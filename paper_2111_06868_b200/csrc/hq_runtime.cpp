@@ -475,6 +475,7 @@ static void release_p2p(hq_state *st) {
 // ------------------------------------------------------------------ create / destroy
 
 extern "C" hq_status hq_state_create(int n, hq_dtype dtype, int ngpus, hq_state **out) {
+    HQ_ABI_BEGIN
     clear_error();
     if (!out) return set_error(HQ_ERR_ARG, "out is NULL");
     *out = nullptr;
@@ -515,9 +516,11 @@ extern "C" hq_status hq_state_create(int n, hq_dtype dtype, int ngpus, hq_state 
     cudaSetDevice(cur);
     *out = st;
     return HQ_OK;
+    HQ_ABI_END
 }
 
 extern "C" hq_status hq_nccl_unique_id(void *out128) {
+    HQ_ABI_BEGIN
     clear_error();
     if (!out128) return set_error(HQ_ERR_ARG, "out is NULL");
     static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
@@ -525,10 +528,12 @@ extern "C" hq_status hq_nccl_unique_id(void *out128) {
     NCCL_TRY(ncclGetUniqueId(&id));
     memcpy(out128, &id, sizeof id);
     return HQ_OK;
+    HQ_ABI_END
 }
 
 extern "C" hq_status hq_state_create_rank(int n, hq_dtype dtype, int world_size, int rank,
                                           int device, const void *nccl_id, hq_state **out) {
+    HQ_ABI_BEGIN
     clear_error();
     if (!out) return set_error(HQ_ERR_ARG, "out is NULL");
     *out = nullptr;
@@ -562,11 +567,13 @@ extern "C" hq_status hq_state_create_rank(int n, hq_dtype dtype, int world_size,
     }
     *out = st;
     return HQ_OK;
+    HQ_ABI_END
 }
 
 extern "C" hq_status hq_state_create_rank_from_buffers(int n, hq_dtype dtype, int world_size, int rank,
                                                        const void *nccl_id, void *psi_device, void *buf_device,
                                                        void *stream, hq_state **out) {
+    HQ_ABI_BEGIN
     clear_error();
     if (!out || !psi_device) return set_error(HQ_ERR_ARG, "NULL argument");
     *out = nullptr;
@@ -619,9 +626,11 @@ extern "C" hq_status hq_state_create_rank_from_buffers(int n, hq_dtype dtype, in
     }
     *out = st;
     return HQ_OK;
+    HQ_ABI_END
 }
 
 extern "C" hq_status hq_state_create_virtual(int n, hq_dtype dtype, int nshards, hq_state **out) {
+    HQ_ABI_BEGIN
     clear_error();
     if (!out) return set_error(HQ_ERR_ARG, "out is NULL");
     *out = nullptr;
@@ -648,10 +657,12 @@ extern "C" hq_status hq_state_create_virtual(int n, hq_dtype dtype, int nshards,
     }
     *out = st;
     return HQ_OK;
+    HQ_ABI_END
 }
 
 extern "C" hq_status hq_state_create_from_buffers(int n, hq_dtype dtype, void *psi_device,
                                                   void *stream, hq_state **out) {
+    HQ_ABI_BEGIN
     clear_error();
     if (!out || !psi_device) return set_error(HQ_ERR_ARG, "NULL argument");
     *out = nullptr;
@@ -680,9 +691,11 @@ extern "C" hq_status hq_state_create_from_buffers(int n, hq_dtype dtype, void *p
     }
     *out = st;
     return HQ_OK;
+    HQ_ABI_END
 }
 
 extern "C" hq_status hq_state_destroy(hq_state *st) {
+    HQ_ABI_BEGIN
     clear_error();
     if (!st) return HQ_OK;
     for (auto &p : st->prof) {
@@ -695,25 +708,31 @@ extern "C" hq_status hq_state_destroy(hq_state *st) {
     for (size_t i = st->sh.size(); i-- > 0;) shard_free(st->sh[i]);
     delete st;
     return HQ_OK;
+    HQ_ABI_END
 }
 
 extern "C" hq_status hq_state_set_remap_mode(hq_state *st, int mode, int *fused_available) {
+    HQ_ABI_BEGIN
     clear_error();
     if (!st) return set_error(HQ_ERR_ARG, "state is NULL");
     if (mode & ~(HQ_REMAP_FUSED | HQ_REMAP_GATHER)) return set_error(HQ_ERR_ARG, "bad remap mode %d", mode);
     st->remap_mode = mode;
     if (fused_available) *fused_available = st->p2p ? 1 : 0;
     return HQ_OK;
+    HQ_ABI_END
 }
 
 extern "C" hq_status hq_state_invalidate_bound(hq_state *st) {
+    HQ_ABI_BEGIN
     clear_error();
     if (!st) return set_error(HQ_ERR_ARG, "state is NULL");
     st->amp_bound = -1.0;
     return HQ_OK;
+    HQ_ABI_END
 }
 
 extern "C" hq_status hq_state_set_layout(hq_state *st, const int32_t *pi) {
+    HQ_ABI_BEGIN
     clear_error();
     if (!st || !pi) return set_error(HQ_ERR_ARG, "NULL argument");
     std::vector<int> seen(st->n, 0), v(st->n);
@@ -725,16 +744,20 @@ extern "C" hq_status hq_state_set_layout(hq_state *st, const int32_t *pi) {
     st->pi = v;
     st->pi_init = v;
     return HQ_OK;
+    HQ_ABI_END
 }
 
 extern "C" hq_status hq_state_get_layout(const hq_state *st, int32_t *pi_out) {
+    HQ_ABI_BEGIN
     clear_error();
     if (!st || !pi_out) return set_error(HQ_ERR_ARG, "NULL argument");
     for (int q = 0; q < st->n; ++q) pi_out[q] = st->pi[q];
     return HQ_OK;
+    HQ_ABI_END
 }
 
 extern "C" hq_status hq_state_set_stream(hq_state *st, void *stream) {
+    HQ_ABI_BEGIN
     clear_error();
     if (!st) return set_error(HQ_ERR_ARG, "state is NULL");
     if (st->mode == MODE_MULTI) return set_error(HQ_ERR_STATE, "set_stream not supported for multi-device states");
@@ -747,10 +770,12 @@ extern "C" hq_status hq_state_set_stream(hq_state *st, void *stream) {
         s.own_stream = false;
     }
     return HQ_OK;
+    HQ_ABI_END
 }
 
 extern "C" hq_status hq_state_info(const hq_state *st, int *n, int *dtype, int *world,
                                    int *local_shards, int *first_rank) {
+    HQ_ABI_BEGIN
     clear_error();
     if (!st) return set_error(HQ_ERR_ARG, "state is NULL");
     if (n) *n = st->n;
@@ -759,6 +784,7 @@ extern "C" hq_status hq_state_info(const hq_state *st, int *n, int *dtype, int *
     if (local_shards) *local_shards = (int)st->sh.size();
     if (first_rank) *first_rank = st->sh[0].rank;
     return HQ_OK;
+    HQ_ABI_END
 }
 
 // ------------------------------------------------------------------ executor
@@ -1125,6 +1151,7 @@ static hq_status exec_remap(hq_state *st, const Op &op) {
 
 extern "C" hq_status hq_remap_plan(int n, int m, const hq_op *op, int rank, int32_t *peer_out, uint64_t *off_out,
                                    uint64_t *len_out, size_t cap, size_t *count) {
+    HQ_ABI_BEGIN
     clear_error();
     if (!op || !count) return set_error(HQ_ERR_ARG, "NULL argument");
     if (op->kind != OP_REMAP || m < 1 || n - m < 1 || rank < 0 || rank >= (1 << m) || op->nbits < 1 || op->nbits > 6)
@@ -1141,6 +1168,7 @@ extern "C" hq_status hq_remap_plan(int n, int m, const hq_op *op, int rank, int3
         if (len_out) len_out[i] = v[i].len;
     }
     return HQ_OK;
+    HQ_ABI_END
 }
 
 static hq_status validate_gates(const hq_state *st, const hq_gate *g, size_t ng,
@@ -1421,6 +1449,7 @@ static hq_status run_ops(hq_state *st, const std::vector<GateRef> &refs, const s
 }
 
 extern "C" hq_status hq_apply_matrix(hq_state *st, const double *U, const int32_t *qubits, int k) {
+    HQ_ABI_BEGIN
     clear_error();
     if (!st || !U || !qubits) return set_error(HQ_ERR_ARG, "NULL argument");
     if (k < 1 || k > 6) return set_error(HQ_ERR_K, "k=%d not in [1,6]", k);
@@ -1429,9 +1458,11 @@ extern "C" hq_status hq_apply_matrix(hq_state *st, const double *U, const int32_
     for (int j = 0; j < 6; ++j) g.qubits[j] = j < k ? qubits[j] : -1;
     g.U = U;
     return hq_apply_circuit(st, &g, 1);
+    HQ_ABI_END
 }
 
 extern "C" hq_status hq_apply_circuit(hq_state *st, const hq_gate *gates, size_t ng) {
+    HQ_ABI_BEGIN
     clear_error();
     if (!st || (!gates && ng)) return set_error(HQ_ERR_ARG, "NULL argument");
     std::vector<GateRef> refs;
@@ -1444,6 +1475,7 @@ extern "C" hq_status hq_apply_circuit(hq_state *st, const hq_gate *gates, size_t
     if (rc) return rc;
     st->pi = pi;
     return HQ_OK;
+    HQ_ABI_END
 }
 
 // ------------------------------------------------------------------ circuits
@@ -1567,6 +1599,7 @@ static hq_status circuit_compile(hq_state *st, hq_circuit *c, const std::vector<
 }
 
 extern "C" hq_status hq_circuit_create(hq_state *st, const hq_gate *gates, size_t ng, hq_circuit **out) {
+    HQ_ABI_BEGIN
     clear_error();
     if (!st || !out || (!gates && ng)) return set_error(HQ_ERR_ARG, "NULL argument");
     *out = nullptr;
@@ -1582,6 +1615,7 @@ extern "C" hq_status hq_circuit_create(hq_state *st, const hq_gate *gates, size_
     }
     *out = c;
     return HQ_OK;
+    HQ_ABI_END
 }
 
 static hq_status circuit_run_ops(hq_state *st, hq_circuit *c) {
@@ -1617,6 +1651,7 @@ static hq_status circuit_run_ops(hq_state *st, hq_circuit *c) {
 }
 
 extern "C" hq_status hq_circuit_run(hq_state *st, hq_circuit *c) {
+    HQ_ABI_BEGIN
     clear_error();
     if (!st || !c) return set_error(HQ_ERR_ARG, "NULL argument");
     if (c->owner != st) return set_error(HQ_ERR_STATE, "circuit was compiled for another state");
@@ -1704,19 +1739,23 @@ extern "C" hq_status hq_circuit_run(hq_state *st, hq_circuit *c) {
     st->stats.hbm_bytes += c->passes * (uint64_t)2 * (st->es << st->nl);
     st->pi = c->pi_end;
     return HQ_OK;
+    HQ_ABI_END
 }
 
 extern "C" hq_status hq_circuit_info(const hq_circuit *c, uint64_t *passes, uint64_t *remaps,
                                      uint64_t *permutes) {
+    HQ_ABI_BEGIN
     clear_error();
     if (!c) return set_error(HQ_ERR_ARG, "NULL circuit");
     if (passes) *passes = c->passes;
     if (remaps) *remaps = c->remaps;
     if (permutes) *permutes = c->permutes;      // standalone PERMUTE passes (folded ones excluded)
     return HQ_OK;
+    HQ_ABI_END
 }
 
 extern "C" hq_status hq_circuit_destroy(hq_circuit *c) {
+    HQ_ABI_BEGIN
     if (!c) return HQ_OK;
     if (c->graph) cudaGraphExecDestroy(c->graph);
     if (c->small_ops || c->small_mats) {
@@ -1734,6 +1773,7 @@ extern "C" hq_status hq_circuit_destroy(hq_circuit *c) {
     delete c;
     cudaGetLastError();
     return HQ_OK;
+    HQ_ABI_END
 }
 
 // ------------------------------------------------------------------ state I/O
@@ -1752,6 +1792,7 @@ static uint64_t phys_of(const hq_state *st, uint64_t i) {
 }
 
 extern "C" hq_status hq_state_init_basis(hq_state *st, uint64_t x) {
+    HQ_ABI_BEGIN
     clear_error();
     if (!st) return set_error(HQ_ERR_ARG, "state is NULL");
     if (st->n < 64 && x >= (1ull << st->n)) return set_error(HQ_ERR_RANGE, "basis index out of range");
@@ -1767,6 +1808,7 @@ extern "C" hq_status hq_state_init_basis(hq_state *st, uint64_t x) {
         st->stats.kernel_launches += idx >= 0 ? 1 : 0;
     }
     return HQ_OK;
+    HQ_ABI_END
 }
 
 static hq_status range_check(const hq_state *st, uint64_t first, uint64_t count) {
@@ -1834,19 +1876,24 @@ static hq_status io_amplitudes(hq_state *st, uint64_t first, uint64_t count, voi
 }
 
 extern "C" hq_status hq_get_amplitudes(hq_state *st, uint64_t first, uint64_t count, void *host_out) {
+    HQ_ABI_BEGIN
     clear_error();
     if (!st || (!host_out && count)) return set_error(HQ_ERR_ARG, "NULL argument");
     return io_amplitudes(st, first, count, host_out, true);
+    HQ_ABI_END
 }
 
 extern "C" hq_status hq_set_amplitudes(hq_state *st, uint64_t first, uint64_t count, const void *host_in) {
+    HQ_ABI_BEGIN
     clear_error();
     if (!st || (!host_in && count)) return set_error(HQ_ERR_ARG, "NULL argument");
     st->amp_bound = -1.0;    // recomputed (hq_norm) before the next pass that needs it
     return io_amplitudes(st, first, count, const_cast<void *>(host_in), false);
+    HQ_ABI_END
 }
 
 extern "C" hq_status hq_norm(hq_state *st, double *out) {
+    HQ_ABI_BEGIN
     clear_error();
     if (!st || !out) return set_error(HQ_ERR_ARG, "NULL argument");
     double total = 0.0;
@@ -1882,6 +1929,7 @@ extern "C" hq_status hq_norm(hq_state *st, double *out) {
     *out = sqrt(total);
     st->amp_bound = *out * (1.0 + 1e-6) + 1e-300;
     return HQ_OK;
+    HQ_ABI_END
 }
 
 static hq_status ensure_bound(hq_state *st) {
@@ -1903,6 +1951,7 @@ static hq_status validate_targets(const hq_state *st, const int32_t *qubits, int
 }
 
 extern "C" hq_status hq_state_init_tokens(hq_state *st, const char *tokens) {
+    HQ_ABI_BEGIN
     clear_error();
     if (!st || !tokens) return set_error(HQ_ERR_ARG, "NULL argument");
     const size_t len = strlen(tokens);
@@ -1946,6 +1995,7 @@ extern "C" hq_status hq_state_init_tokens(hq_state *st, const char *tokens) {
     }
     st->amp_bound = 1.0 + 1e-12;
     return HQ_OK;
+    HQ_ABI_END
 }
 
 // Sum `count` host doubles over the ranks (rank mode): one ncclAllReduce
@@ -1970,6 +2020,7 @@ static hq_status allreduce_host(hq_state *st, double *v, int count) {
 
 extern "C" hq_status hq_project(hq_state *st, const int32_t *qubits, const int32_t *bits, int nq,
                                 int renormalize, double *norm_out) {
+    HQ_ABI_BEGIN
     clear_error();
     if (!st || !bits) return set_error(HQ_ERR_ARG, "NULL argument");
     hq_status rc = validate_targets(st, qubits, nq, st->n);
@@ -2016,9 +2067,11 @@ extern "C" hq_status hq_project(hq_state *st, const int32_t *qubits, const int32
     }
     st->amp_bound = 1.0 + 1e-6;
     return HQ_OK;
+    HQ_ABI_END
 }
 
 extern "C" hq_status hq_probabilities(hq_state *st, const int32_t *qubits, int nq, double *probs_out) {
+    HQ_ABI_BEGIN
     clear_error();
     if (!st || !probs_out) return set_error(HQ_ERR_ARG, "NULL argument");
     hq_status rc = validate_targets(st, qubits, nq, 10);
@@ -2064,9 +2117,11 @@ extern "C" hq_status hq_probabilities(hq_state *st, const int32_t *qubits, int n
     if ((rc = allreduce_host(st, probs.data(), nout))) return rc;
     for (int x = 0; x < nout; ++x) probs_out[x] = probs[x];
     return HQ_OK;
+    HQ_ABI_END
 }
 
 extern "C" hq_status hq_measure(hq_state *st, const int32_t *qubits, int nq, double u, uint64_t *outcome_out) {
+    HQ_ABI_BEGIN
     clear_error();
     if (!st || !outcome_out) return set_error(HQ_ERR_ARG, "NULL argument");
     if (!(u >= 0.0 && u < 1.0)) return set_error(HQ_ERR_ARG, "u=%g not in [0,1)", u);
@@ -2091,6 +2146,7 @@ extern "C" hq_status hq_measure(hq_state *st, const int32_t *qubits, int nq, dou
     if ((rc = hq_project(st, qubits, bits.data(), nq, 1, &nrm))) return rc;
     *outcome_out = (uint64_t)x;
     return HQ_OK;
+    HQ_ABI_END
 }
 
 // ------------------------------------------------------------------ f3: reduced density matrices, trajectories
@@ -2119,6 +2175,7 @@ static hq_status ensure_local(hq_state *st, const int32_t *qubits, int k) {
 }
 
 extern "C" hq_status hq_reduced_dm(hq_state *st, const int32_t *qubits, int k, double *rho_out) {
+    HQ_ABI_BEGIN
     clear_error();
     if (!st || !rho_out) return set_error(HQ_ERR_ARG, "NULL argument");
     if (k < 1 || k > 3) return set_error(HQ_ERR_K, "k=%d not in [1,3]", k);
@@ -2166,10 +2223,12 @@ extern "C" hq_status hq_reduced_dm(hq_state *st, const int32_t *qubits, int k, d
             rho_out[2 * (b * D + a) + 1] = -acc[2 * e + 1];
         }
     return HQ_OK;
+    HQ_ABI_END
 }
 
 extern "C" hq_status hq_kraus_sample(hq_state *st, const double *const *K, int nkraus, const int32_t *qubits,
                                      int k, double u, int *chosen_out, double *probs_out) {
+    HQ_ABI_BEGIN
     clear_error();
     if (!st || !K || !chosen_out || nkraus < 1) return set_error(HQ_ERR_ARG, "NULL argument or no Kraus operators");
     if (!(u >= 0.0 && u < 1.0)) return set_error(HQ_ERR_ARG, "u=%g not in [0,1)", u);
@@ -2221,6 +2280,7 @@ extern "C" hq_status hq_kraus_sample(hq_state *st, const double *const *K, int n
     st->amp_bound = 1.0 + 1e-3;       // ||K_x psi|| / sqrt(p_x) = 1 up to the rounding of p_x
     *chosen_out = x;
     return HQ_OK;
+    HQ_ABI_END
 }
 
 // Batched trajectories: 2^nb shots in one state, shot = logical qubits
@@ -2258,6 +2318,7 @@ static RdmParams rdm_params(const hq_state *st, const int32_t *qubits, int k) {
 }
 
 extern "C" hq_status hq_reduced_dm_batched(hq_state *st, int nb, const int32_t *qubits, int k, double *rho_out) {
+    HQ_ABI_BEGIN
     clear_error();
     if (!st || !rho_out) return set_error(HQ_ERR_ARG, "NULL argument");
     hq_status rc = batch_check(st, nb, qubits, k);
@@ -2299,10 +2360,12 @@ extern "C" hq_status hq_reduced_dm_batched(hq_state *st, int nb, const int32_t *
             }
     }
     return HQ_OK;
+    HQ_ABI_END
 }
 
 extern "C" hq_status hq_reduced_dm_batched_sum(hq_state *st, int nb, const int32_t *qubits, int k, int nlive,
                                                double *rho_sum) {
+    HQ_ABI_BEGIN
     clear_error();
     if (!st || !rho_sum) return set_error(HQ_ERR_ARG, "NULL argument");
     if (nb < 0 || nb > 16 || nlive < 0 || nlive > (1 << nb)) return set_error(HQ_ERR_ARG, "nlive=%d not in [0, 2^nb]", nlive);
@@ -2321,6 +2384,7 @@ extern "C" hq_status hq_reduced_dm_batched_sum(hq_state *st, int nb, const int32
     }
     for (int i = 0; i < 2 * D * D; ++i) rho_sum[i] = acc[i];
     return HQ_OK;
+    HQ_ABI_END
 }
 
 // p_i = Re Tr(K_i rho K_i^H) for one shot
@@ -2343,6 +2407,7 @@ static double branch_weight(const double *A, const double *rho, int D) {
 extern "C" hq_status hq_kraus_sample_batched(hq_state *st, int nb, const double *const *K, int nkraus,
                                              const int32_t *qubits, int k, const double *u, int32_t *chosen_out,
                                              double *probs_out) {
+    HQ_ABI_BEGIN
     clear_error();
     if (!st || !K || !u || !chosen_out || nkraus < 1) return set_error(HQ_ERR_ARG, "NULL argument or no Kraus operators");
     hq_status rc = batch_check(st, nb, qubits, k);
@@ -2401,11 +2466,13 @@ extern "C" hq_status hq_kraus_sample_batched(hq_state *st, int nb, const double 
     st->stats.hbm_bytes += (uint64_t)2 * (st->es << st->nl);
     st->amp_bound = 1.0 + 1e-3;
     return HQ_OK;
+    HQ_ABI_END
 }
 
 // ------------------------------------------------------------------ f2: density matrices
 
 extern "C" hq_status hq_dm_superop(const double *const *K, int nkraus, int k, double *S_out) {
+    HQ_ABI_BEGIN
     clear_error();
     if (!K || !S_out || nkraus < 1) return set_error(HQ_ERR_ARG, "NULL argument or no Kraus operators");
     if (k < 1 || k > 3) return set_error(HQ_ERR_K, "k=%d not in [1,3] (superoperator has 2k <= 6 targets)", k);
@@ -2427,6 +2494,7 @@ extern "C" hq_status hq_dm_superop(const double *const *K, int nkraus, int k, do
                     }
     }
     return HQ_OK;
+    HQ_ABI_END
 }
 
 static hq_status dm_check(const hq_state *st, const int32_t *qubits, int k) {
@@ -2443,6 +2511,7 @@ static hq_status dm_check(const hq_state *st, const int32_t *qubits, int k) {
 
 extern "C" hq_status hq_dm_apply_kraus(hq_state *st, const double *const *K, int nkraus,
                                        const int32_t *qubits, int k) {
+    HQ_ABI_BEGIN
     clear_error();
     if (!st) return set_error(HQ_ERR_ARG, "state is NULL");
     hq_status rc = dm_check(st, qubits, k);
@@ -2454,9 +2523,11 @@ extern "C" hq_status hq_dm_apply_kraus(hq_state *st, const double *const *K, int
     int32_t q2[6];
     for (int j = 0; j < k; ++j) { q2[j] = qubits[j]; q2[k + j] = qubits[j] + N; }
     return hq_apply_matrix(st, S.data(), q2, 2 * k);
+    HQ_ABI_END
 }
 
 extern "C" hq_status hq_dm_apply_unitary(hq_state *st, const double *U, const int32_t *qubits, int k) {
+    HQ_ABI_BEGIN
     clear_error();
     if (!st || !U) return set_error(HQ_ERR_ARG, "NULL argument");
     hq_status rc = dm_check(st, qubits, k);
@@ -2477,9 +2548,11 @@ extern "C" hq_status hq_dm_apply_unitary(hq_state *st, const double *U, const in
     g[0].U = U;
     g[1].U = Uc.data();
     return hq_apply_circuit(st, g, 2);
+    HQ_ABI_END
 }
 
 extern "C" hq_status hq_dm_trace(hq_state *st, double *re, double *im) {
+    HQ_ABI_BEGIN
     clear_error();
     if (!st || !re || !im) return set_error(HQ_ERR_ARG, "NULL argument");
     if (st->n % 2) return set_error(HQ_ERR_STATE, "density-matrix calls need an even number of qubits");
@@ -2503,6 +2576,7 @@ extern "C" hq_status hq_dm_trace(hq_state *st, double *re, double *im) {
     *re = t[0];
     *im = t[1];
     return HQ_OK;
+    HQ_ABI_END
 }
 
 // ------------------------------------------------------------------ diagnostics
@@ -2510,6 +2584,7 @@ extern "C" hq_status hq_dm_trace(hq_state *st, double *re, double *im) {
 extern "C" const char *hq_last_error(void) { return g_err.c_str(); }
 
 extern "C" hq_status hq_sync(hq_state *st) {
+    HQ_ABI_BEGIN
     clear_error();
     if (!st) return set_error(HQ_ERR_ARG, "state is NULL");
     for (auto &s : st->sh) {
@@ -2517,31 +2592,39 @@ extern "C" hq_status hq_sync(hq_state *st) {
         SYNC_TRY(s);
     }
     return HQ_OK;
+    HQ_ABI_END
 }
 
 extern "C" hq_status hq_stats_get(const hq_state *st, hq_stats *out) {
+    HQ_ABI_BEGIN
     clear_error();
     if (!st || !out) return set_error(HQ_ERR_ARG, "NULL argument");
     *out = st->stats;
     return HQ_OK;
+    HQ_ABI_END
 }
 
 extern "C" hq_status hq_stats_reset(hq_state *st) {
+    HQ_ABI_BEGIN
     clear_error();
     if (!st) return set_error(HQ_ERR_ARG, "state is NULL");
     st->stats = hq_stats{};
     return HQ_OK;
+    HQ_ABI_END
 }
 
 extern "C" hq_status hq_profile_enable(hq_state *st, int on) {
+    HQ_ABI_BEGIN
     clear_error();
     if (!st) return set_error(HQ_ERR_ARG, "state is NULL");
     st->profiling = on != 0;
     return HQ_OK;
+    HQ_ABI_END
 }
 
 extern "C" hq_status hq_kernel_times(hq_state *st, int path, uint64_t *count, double *total_ms,
                                      double *max_ms, uint64_t *bytes) {
+    HQ_ABI_BEGIN
     clear_error();
     if (!st) return set_error(HQ_ERR_ARG, "state is NULL");
     if (path < -1 || path > 2) return set_error(HQ_ERR_ARG, "path %d not in [-1, 2]", path);
@@ -2572,6 +2655,7 @@ extern "C" hq_status hq_kernel_times(hq_state *st, int path, uint64_t *count, do
     if (max_ms) *max_ms = r.max;
     if (bytes) *bytes = r.bytes;
     return HQ_OK;
+    HQ_ABI_END
 }
 
 extern "C" const char *hq_version(void) { return "hq-b200 0.1 (sm_100a)"; }
