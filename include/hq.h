@@ -7,8 +7,10 @@
  *   set of target qubits -- the "matrix-vector multiplication of quantum
  *   states ... similar syntax of numpy.dot" of PAPER.md P:87-91, implemented
  *   there as the C++/AVX core of P:641-656 (SPEC.md S:238-246 apply_matrix,
- *   S:274-282 simulate_statevector).  Gates are fused on the host by the
- *   greedy planner of P:499-504 (utils.compress) before they reach the GPU.
+ *   S:274-282 simulate_statevector).  Gates are fused on the host into
+ *   blocks of <= kmax qubits (P:499-504 utils.compress: hq_fuse, the greedy
+ *   rule of the paper's example, or hq_fuse_blocks, the block planner) before
+ *   they reach the GPU.
  *
  * Conventions:
  *   - Amplitude index: qubit q is bit n-1-q (qubit 0 = most significant bit).
