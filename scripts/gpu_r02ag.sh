@@ -1,0 +1,8 @@
+#!/bin/bash
+set -u
+export HQ_NO_BUILD=1
+OUT=gpurun_out/r02ag
+mkdir -p $OUT
+python tools/norm_timing.py 34 > $OUT/norm.json 2>&1
+python tools/norm_timing.py 32 >> $OUT/norm.json 2>&1
+timeout 2400 python -m pytest tests -m gpu -q --timeout 900 -p no:cacheprovider > $OUT/gputests.log 2>&1; echo "tests rc=$?" >> $OUT/gputests.log
