@@ -2000,6 +2000,20 @@ extern "C" hq_status hq_state_init_tokens(hq_state *st, const char *tokens) {
 
 // Sum `count` host doubles over the ranks (rank mode): one ncclAllReduce
 // through a persistent device scratch (allocated on first use).
+// Grow a shard's reduction scratch (device + pinned host) to >= cap doubles.
+static hq_status ensure_red(Shard &s, size_t cap) {
+    if (s.red_cap >= cap) return HQ_OK;
+    if (s.d_red) cudaFree(s.d_red);
+    if (s.h_red) cudaFreeHost(s.h_red);
+    s.d_red = nullptr;
+    s.h_red = nullptr;
+    s.red_cap = 0;
+    CUDA_TRY(cudaMalloc((void **)&s.d_red, sizeof(double) * cap));
+    CUDA_TRY(cudaMallocHost((void **)&s.h_red, sizeof(double) * cap));
+    s.red_cap = cap;
+    return HQ_OK;
+}
+
 static hq_status allreduce_host(hq_state *st, double *v, int count) {
     if (st->mode != MODE_RANK) return HQ_OK;
     if (count > AR_CAP) return set_error(HQ_ERR_ARG, "internal: all-reduce of %d > %d doubles", count, AR_CAP);
@@ -2085,18 +2099,16 @@ extern "C" hq_status hq_probabilities(hq_state *st, const int32_t *qubits, int n
             if (st->pi[qubits[j]] < st->nl) loc[nloc++] = j;
         P.nq = nloc;
         for (int t = 0; t < nloc; ++t) P.pos[t] = st->pi[qubits[loc[t]]];
-        const int nb_max = 148 * 2;
-        double *dh = nullptr;
+        const int nb_max = 148 * 8;
         CUDA_TRY(cudaSetDevice(s.device));
-        CUDA_TRY(cudaMalloc((void **)&dh, sizeof(double) * (size_t)nb_max << nloc));
+        if ((rc = ensure_red(s, (size_t)nb_max << nloc))) return rc;     // persistent scratch
         int nb = 0;
-        int e = launch_probabilities((int)st->dtype, s.psi, 1ull << st->nl, P, dh, nb_max, s.stream, &nb);
-        if (e) { cudaFree(dh); return set_error(HQ_ERR_CUDA, "probabilities launch: %s", cudaGetErrorString((cudaError_t)e)); }
-        std::vector<double> h((size_t)nb << nloc);
-        cudaError_t ce = copy_async(st->stats, h.data(), dh, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, s.stream);
-        if (!ce) ce = cudaStreamSynchronize(s.stream);
-        cudaFree(dh);
-        if (ce) return set_error(HQ_ERR_CUDA, "probabilities copy: %s", cudaGetErrorString(ce));
+        int e = launch_probabilities((int)st->dtype, s.psi, 1ull << st->nl, P, s.d_red, nb_max, s.stream, &nb);
+        if (e) return set_error(HQ_ERR_CUDA, "probabilities launch: %s", cudaGetErrorString((cudaError_t)e));
+        CUDA_TRY(copy_async(st->stats, s.h_red, s.d_red, sizeof(double) * ((size_t)nb << nloc),
+                            cudaMemcpyDeviceToHost, s.stream));
+        SYNC_TRY(s);
+        const double *h = s.h_red;
         st->stats.kernel_launches++;
         st->stats.hbm_bytes += st->es << st->nl;
         // local outcome y (bits of the local measured qubits) -> full outcome x
@@ -2199,11 +2211,7 @@ extern "C" hq_status hq_reduced_dm(hq_state *st, const int32_t *qubits, int k, d
     std::vector<double> acc(2 * E, 0.0);
     for (auto &s : st->sh) {
         CUDA_TRY(cudaSetDevice(s.device));
-        if (!s.d_red) {
-            CUDA_TRY(cudaMalloc((void **)&s.d_red, sizeof(double) * RDM_MAX_BLOCKS * RDM_MAX_ENTRIES));
-            CUDA_TRY(cudaMallocHost((void **)&s.h_red, sizeof(double) * RDM_MAX_BLOCKS * RDM_MAX_ENTRIES));
-            s.red_cap = (size_t)RDM_MAX_BLOCKS * RDM_MAX_ENTRIES;
-        }
+        if ((rc = ensure_red(s, (size_t)RDM_MAX_BLOCKS * RDM_MAX_ENTRIES))) return rc;
         int nb = 0;
         int e = launch_reduced_dm((int)st->dtype, s.psi, 1ull << st->nl, P, s.d_red, s.stream, &nb);
         if (e) return set_error(HQ_ERR_CUDA, "reduced_dm launch: %s", cudaGetErrorString((cudaError_t)e));
@@ -2328,16 +2336,7 @@ extern "C" hq_status hq_reduced_dm_batched(hq_state *st, int nb, const int32_t *
     Shard &s = st->sh[0];
     CUDA_TRY(cudaSetDevice(s.device));
     const size_t cap = (size_t)std::max(RDM_MAX_BLOCKS, S * 4) * RDM_MAX_ENTRIES;
-    if (s.red_cap < cap) {
-        if (s.d_red) cudaFree(s.d_red);
-        if (s.h_red) cudaFreeHost(s.h_red);
-        s.d_red = nullptr;
-        s.h_red = nullptr;
-        s.red_cap = 0;
-        CUDA_TRY(cudaMalloc((void **)&s.d_red, sizeof(double) * cap));
-        CUDA_TRY(cudaMallocHost((void **)&s.h_red, sizeof(double) * cap));
-        s.red_cap = cap;
-    }
+    if ((rc = ensure_red(s, cap))) return rc;
     int nblk = 0;
     int e = launch_reduced_dm_batched((int)st->dtype, s.psi, 1ull << (st->n - nb), S, P, s.d_red,
                                       (int)(cap / (2 * E)), s.stream, &nblk);

@@ -1,0 +1,7 @@
+#!/bin/bash
+set -u
+export HQ_NO_BUILD=1
+OUT=gpurun_out/r02ai
+mkdir -p $OUT
+python tools/stateops_timing.py 32 > $OUT/ops.json 2>&1
+timeout 2400 python -m pytest tests -m gpu -q --timeout 900 -p no:cacheprovider > $OUT/gputests.log 2>&1; echo "tests rc=$?" >> $OUT/gputests.log
