@@ -239,29 +239,45 @@ __global__ void __launch_bounds__(256) reduced_dm_kernel(const V *__restrict__ p
     double acc[2 * E];
 #pragma unroll
     for (int e = 0; e < 2 * E; ++e) acc[e] = 0.0;
-    for (uint64_t o = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; o < nsets;
-         o += (uint64_t)gridDim.x * blockDim.x) {
-        uint64_t base = o;
+    auto base_of = [&](uint64_t o) {
 #pragma unroll
         for (int i = 0; i < K; ++i) {
             const int s = P.pos[i];
-            base = ((base >> s) << (s + 1)) | (base & ((1ull << s) - 1));
+            o = ((o >> s) << (s + 1)) | (o & ((1ull << s) - 1));
         }
-        double re[D], im[D];
-#pragma unroll
-        for (int a = 0; a < D; ++a) {
-            const V v = psi[base + P.off[a]];
-            re[a] = (double)v.x;
-            im[a] = (double)v.y;
-        }
+        return o;
+    };
+    auto accumulate = [&](const V (&v)[D]) {
         int e = 0;
 #pragma unroll
         for (int a = 0; a < D; ++a)
 #pragma unroll
             for (int b = a; b < D; ++b, ++e) {
-                acc[2 * e] += re[a] * re[b] + im[a] * im[b];
-                acc[2 * e + 1] += im[a] * re[b] - re[a] * im[b];
+                const double ra = v[a].x, ia = v[a].y, rb = v[b].x, ib = v[b].y;
+                acc[2 * e] += ra * rb + ia * ib;
+                acc[2 * e + 1] += ia * rb - ra * ib;
             }
+    };
+    // two gather sets per iteration: 2 * 2^K independent loads in flight
+    const uint64_t S = (uint64_t)gridDim.x * blockDim.x;
+    uint64_t o = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; o + S < nsets; o += 2 * S) {
+        const uint64_t b0 = base_of(o), b1 = base_of(o + S);
+        V v0[D], v1[D];
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            v0[a] = __ldcs(psi + b0 + P.off[a]);
+            v1[a] = __ldcs(psi + b1 + P.off[a]);
+        }
+        accumulate(v0);
+        accumulate(v1);
+    }
+    if (o < nsets) {
+        const uint64_t b0 = base_of(o);
+        V v0[D];
+#pragma unroll
+        for (int a = 0; a < D; ++a) v0[a] = psi[b0 + P.off[a]];
+        accumulate(v0);
     }
     __shared__ double red[8][2 * E];
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
