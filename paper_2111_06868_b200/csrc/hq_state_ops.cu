@@ -35,22 +35,65 @@ __global__ void __launch_bounds__(256) init_tokens_kernel(V *__restrict__ psi, u
     }
 }
 
+// Zero the amplitudes outside (i & mask) == val and sum |psi|^2 of the kept
+// ones in fp64 per block (keep_all: keep everything).  16-byte vectors (two
+// complex64 amplitudes or one complex128), four per thread per iteration
+// (round 1's one 8-byte element per iteration ran at ~1 TB/s).
 template <typename V>
 __global__ void __launch_bounds__(256) project_kernel(V *__restrict__ psi, uint64_t n_amps,
                                                       uint64_t mask, uint64_t val, int keep_all,
                                                       double *__restrict__ part) {
+    constexpr int PER = sizeof(V) == 8 ? 2 : 1;
+    float4 *v4 = reinterpret_cast<float4 *>(psi);
+    const uint64_t nv = n_amps / PER, S = (uint64_t)gridDim.x * blockDim.x;
     double acc = 0.0;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_amps;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        if (keep_all || (i & mask) == val) {
-            const V v = psi[i];
-            acc += (double)v.x * (double)v.x + (double)v.y * (double)v.y;
+    auto kept = [&](uint64_t i) { return keep_all || (i & mask) == val; };
+    // vectors whose amplitudes are all projected out are written (zeros)
+    // without being read; the others are read, summed, and written only when
+    // one of their two amplitudes goes
+    auto dead = [&](uint64_t j) { return PER == 2 ? !kept(2 * j) && !kept(2 * j + 1) : !kept(j); };
+    auto sum = [&](uint64_t j, float4 &w) -> bool {
+        if constexpr (PER == 2) {
+            bool dirty = false;
+            if (kept(2 * j)) acc += (double)w.x * w.x + (double)w.y * w.y;
+            else { w.x = w.y = 0.f; dirty = true; }
+            if (kept(2 * j + 1)) acc += (double)w.z * w.z + (double)w.w * w.w;
+            else { w.z = w.w = 0.f; dirty = true; }
+            return dirty;
         } else {
-            V z;
-            z.x = 0;
-            z.y = 0;
-            psi[i] = z;
+            const double2 d = *reinterpret_cast<const double2 *>(&w);
+            acc += d.x * d.x + d.y * d.y;
+            return false;
         }
+    };
+    const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+    uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; j + 3 * S < nv; j += 4 * S) {
+        float4 w[4];
+        bool d[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {            // all loads first
+            d[u] = dead(j + u * S);
+            if (!d[u]) w[u] = v4[j + u * S];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (d[u]) v4[j + u * S] = zero;
+            else if (sum(j + u * S, w[u])) v4[j + u * S] = w[u];
+        }
+    }
+    for (; j < nv; j += S) {
+        if (dead(j)) {
+            v4[j] = zero;
+            continue;
+        }
+        float4 w = v4[j];
+        if (sum(j, w)) v4[j] = w;
+    }
+    if (PER == 2 && (n_amps & 1) && blockIdx.x == 0 && threadIdx.x == 0) {   // a lone amplitude (n = 0)
+        const uint64_t i = n_amps - 1;
+        if (keep_all || (i & mask) == val) acc += (double)psi[i].x * psi[i].x + (double)psi[i].y * psi[i].y;
+        else psi[i].x = psi[i].y = 0;
     }
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     __shared__ double red[8];
@@ -63,14 +106,40 @@ __global__ void __launch_bounds__(256) project_kernel(V *__restrict__ psi, uint6
     }
 }
 
+// psi *= s: 16-byte vectors, four per thread per iteration; complex64
+// scales in FP32 (the factor's rounding is below the storage precision)
 template <typename V>
 __global__ void __launch_bounds__(256) scale_kernel(V *__restrict__ psi, uint64_t n_amps, double s) {
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_amps;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        V v = psi[i];
-        v.x = (decltype(v.x))(v.x * s);
-        v.y = (decltype(v.y))(v.y * s);
-        psi[i] = v;
+    constexpr int PER = sizeof(V) == 8 ? 2 : 1;
+    float4 *v4 = reinterpret_cast<float4 *>(psi);
+    const uint64_t nv = n_amps / PER, S = (uint64_t)gridDim.x * blockDim.x;
+    const float sf = (float)s;
+    auto scale = [&](float4 w) {
+        if constexpr (PER == 2) {
+            w.x *= sf;
+            w.y *= sf;
+            w.z *= sf;
+            w.w *= sf;
+        } else {
+            double2 d = *reinterpret_cast<double2 *>(&w);
+            d.x *= s;
+            d.y *= s;
+            w = *reinterpret_cast<float4 *>(&d);
+        }
+        return w;
+    };
+    uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; j + 3 * S < nv; j += 4 * S) {
+        float4 w[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) w[u] = v4[j + u * S];          // all loads first
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v4[j + u * S] = scale(w[u]);
+    }
+    for (; j < nv; j += S) v4[j] = scale(v4[j]);
+    if (PER == 2 && (n_amps & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        psi[n_amps - 1].x *= sf;
+        psi[n_amps - 1].y *= sf;
     }
 }
 

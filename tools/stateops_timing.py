@@ -34,4 +34,11 @@ for nq, where in ((1, "high"), (1, "low"), (4, "high"), (4, "low"), (10, "high")
     rows["probabilities_%d_%s" % (nq, where)] = t(lambda: hq.hq_probabilities(s, qs))
 for k in (1, 2):
     rows["reduced_dm_%d" % k] = t(lambda: hq.hq_reduced_dm(s, list(range(k))))
+rows["measure_1"] = t(lambda: hq.hq_measure(s, [0], 0.3))
+rows["probabilities_1_high_after"] = t(lambda: hq.hq_probabilities(s, [0]))
+rows["project_1_keep"] = t(lambda: hq.hq_project(s, [0], [0], renormalize=True))
+rows["project_1_renorm"] = t(lambda: hq.hq_project(s, [n - 1], [0], renormalize=True))
+rows["init_tokens_plus"] = t(lambda: hq.hq_state_init_tokens(s, "+"))
+K = [np.sqrt(0.9) * np.eye(2), np.sqrt(0.1) * np.array([[0, 1], [1, 0]], dtype=complex)]
+rows["kraus_sample_1"] = t(lambda: hq.hq_kraus_sample(s, K, [3], 0.4))
 print(json.dumps({"n": n, "ms": rows, "read_gbs": {k: state_gb / (v * 1e-3) for k, v in rows.items()}}))
