@@ -22,10 +22,14 @@ e2e    = the same metric through the public API with host inputs: per step
 sweep  = (N=1) the fused-gate sweep of BASELINE configs[2] on the bench's own
          dense state: one Haar k-qubit gate per k=1..6 at the low / spread /
          random0 placements, median of 5 passes, as a fraction of the HBM peak.
+other_configs = (N=1, 34q) BASELINE configs[0] (12q d10) and configs[1] (30q
+         d20, 2-qubit fused gates) on their own buffers, circuit time.
+The planner is hq_fuse_blocks (--fuse c7 for the paper's greedy rule).
 For N>1 the same circuit is strong-scaled: the state is sharded on the top
-log2 N qubits and remaps run as NCCL exchanges; the line then carries a
-parity object computed through that transport (mirror circuit C.C^dagger
-distance from |0>, pin P9; reversible circuit |x> -> |f(x)> bit-exact, P10).
+log2 N qubits and remaps run fused into the preceding apply pass (peer writes
+over NVLink, CUDA IPC) or as NCCL exchanges; the line then carries a parity
+object computed through that transport (mirror circuit C.C^dagger distance
+from |0>, pin P9; reversible circuit |x> -> |f(x)> bit-exact, P10).
 """
 import argparse
 import json
